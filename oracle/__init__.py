@@ -1,0 +1,185 @@
+"""ctypes front-end of the CPU oracle (oracle/oracle.cpp).
+
+TEST INFRASTRUCTURE ONLY: tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+``--impl reference`` leg are the only callers.  The product package never imports this module.
+The oracle follows SURVEY.md §8c O1-O13 (and DESIGN.md "Readings"); see oracle.cpp for the
+per-function citations.  Parity pinned: every function here is pinned by tests/test_oracle_*.py
+(closed forms, brute force, scipy, paper examples) — no function is "parity unpinned".
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.cpp")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with g++ (no FMA contraction: fp64 evaluated exactly as written)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = ["g++", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c++17", "-shared", "-fPIC",
+               "-o", _LIB + ".tmp", _SRC]
+        subprocess.check_call(cmd)
+        os.replace(_LIB + ".tmp", _LIB)
+    return _LIB
+
+
+class Grid(C.Structure):
+    _fields_ = [("voxel_size", C.c_double), ("truncation", C.c_double), ("weighting", C.c_int32),
+                ("weight_range_floor", C.c_double), ("carve", C.c_int32), ("site_threshold", C.c_double)]
+
+
+class Sensor(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("width", C.c_int32), ("height", C.c_int32),
+                ("fx", C.c_float), ("fy", C.c_float), ("cx", C.c_float), ("cy", C.c_float),
+                ("min_range", C.c_float), ("max_range", C.c_float)]
+
+
+class Stats(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("rays_in", "rays_used", "skipped_invalid", "skipped_range",
+                                         "skipped_domain", "voxel_updates", "new_blocks", "total_blocks")]
+
+    def asdict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+def lib():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            L = C.CDLL(_LIB)
+            P = C.c_void_p
+            L.orc_new.restype = P
+            L.orc_new.argtypes = [C.POINTER(Grid), P]
+            L.orc_free.argtypes = [P]
+            L.orc_integrate.restype = C.c_int32
+            L.orc_integrate.argtypes = [P, P, C.c_int64, P, C.POINTER(Sensor), C.POINTER(Stats)]
+            L.orc_num_blocks.restype = C.c_int64
+            L.orc_num_blocks.argtypes = [P]
+            L.orc_export.argtypes = [P, P, P, P]
+            L.orc_ray_voxels.restype = C.c_int64
+            L.orc_ray_voxels.argtypes = [P, P, C.c_double, C.c_double, C.c_int32, P, C.c_int64]
+            L.orc_esdf.restype = C.c_int32
+            L.orc_esdf.argtypes = [P, P, P, C.c_int64, C.c_double, C.c_double, C.c_int32, P, P]
+            L.orc_query.restype = C.c_int32
+            L.orc_query.argtypes = [P, P, C.c_int64, C.c_double, P, P, C.c_int64, P, P]
+            _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def grid_struct(grid: dict) -> Grid:
+    return Grid(float(grid["voxel_size"]), float(grid["truncation"]), int(grid.get("weighting", 0)),
+                float(grid.get("weight_range_floor", 0.1)), int(grid.get("carve", 1)),
+                float(grid.get("site_threshold", grid["voxel_size"])))
+
+
+def sensor_struct(sensor: dict) -> Sensor:
+    return Sensor(int(sensor["kind"]), int(sensor.get("width", 0)), int(sensor.get("height", 0)),
+                  float(sensor.get("fx", 0)), float(sensor.get("fy", 0)), float(sensor.get("cx", 0)),
+                  float(sensor.get("cy", 0)), float(sensor.get("min_range", 0.0)),
+                  float(sensor.get("max_range", 3.0e38)))
+
+
+class OracleSubmap:
+    """One submap's TSDF as plain fp64 sums (O7-O8)."""
+
+    def __init__(self, grid: dict, T_world_submap=None):
+        self.grid = dict(grid)
+        self._g = grid_struct(grid)
+        T = np.ascontiguousarray(np.eye(4) if T_world_submap is None else T_world_submap, dtype=np.float64)
+        self.T_ws = T
+        self._h = lib().orc_new(C.byref(self._g), _p(T))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib().orc_free(h)
+            self._h = None
+
+    def integrate(self, data, T_world_sensor, sensor: dict) -> dict:
+        d = np.ascontiguousarray(np.asarray(data, dtype=np.float32))
+        n = d.size if sensor["kind"] == 1 else d.size // 3
+        T = np.ascontiguousarray(T_world_sensor, dtype=np.float64)
+        st = Stats()
+        sm = sensor_struct(sensor)
+        rc = lib().orc_integrate(self._h, _p(d), n, _p(T), C.byref(sm), C.byref(st))
+        assert rc == 0
+        return st.asdict()
+
+    def num_blocks(self) -> int:
+        return int(lib().orc_num_blocks(self._h))
+
+    def export(self):
+        """(bxyz int32 [nb,3], D fp64 [nb,512], W fp64 [nb,512]) in lexicographic (bx,by,bz) order."""
+        nb = self.num_blocks()
+        b = np.zeros((nb, 3), np.int32)
+        D = np.zeros((nb, 512), np.float64)
+        W = np.zeros((nb, 512), np.float64)
+        if nb:
+            lib().orc_export(self._h, _p(b), _p(D), _p(W))
+        return b, D, W
+
+
+def ray_voxels(o, p, voxel_size: float, truncation: float, carve: int = 1) -> np.ndarray:
+    """Ordered voxel list [n,3] of one ray (O3-O4); None when outside the key domain."""
+    o = np.ascontiguousarray(o, dtype=np.float64)
+    p = np.ascontiguousarray(p, dtype=np.float64)
+    cap = 1 << 16
+    out = np.zeros((cap, 3), np.int32)
+    n = lib().orc_ray_voxels(_p(o), _p(p), voxel_size, truncation, carve, _p(out), cap)
+    if n < 0:
+        return None
+    assert n <= cap
+    return out[:n].copy()
+
+
+def esdf(bxyz, D, W, voxel_size: float, site_threshold: float, brute: bool = False):
+    """(E fp64 [nb,512], d2 int64 [nb,512] with -1 = no site) per O10-O12."""
+    b = np.ascontiguousarray(bxyz, dtype=np.int32)
+    Dd = np.ascontiguousarray(D, dtype=np.float64)
+    Wd = np.ascontiguousarray(W, dtype=np.float64)
+    nb = b.shape[0]
+    E = np.zeros((nb, 512), np.float64)
+    d2 = np.zeros((nb, 512), np.int64)
+    if nb:
+        rc = lib().orc_esdf(_p(b), _p(Dd), _p(Wd), nb, voxel_size, site_threshold, int(brute), _p(E), _p(d2))
+        assert rc == 0
+    return E, d2
+
+
+def query(bxyz, E, voxel_size: float, T_world_submap, pts):
+    """(value fp64 [m], status uint8 [m]) per O13."""
+    b = np.ascontiguousarray(bxyz, dtype=np.int32)
+    Ed = np.ascontiguousarray(E, dtype=np.float64)
+    T = np.ascontiguousarray(T_world_submap, dtype=np.float64)
+    x = np.ascontiguousarray(pts, dtype=np.float32)
+    m = x.shape[0]
+    out = np.zeros(m, np.float64)
+    st = np.zeros(m, np.uint8)
+    rc = lib().orc_query(_p(b), _p(Ed), b.shape[0], voxel_size, _p(T), _p(x), m, _p(out), _p(st))
+    assert rc == 0
+    return out, st
+
+
+def build_submap(cfg: dict, submap: int = 0, frames=None) -> tuple[OracleSubmap, list]:
+    """Integrate (a subset of) one config submap's frames through the oracle."""
+    sm = cfg["submaps"][submap]
+    o = OracleSubmap(cfg["grid"], sm["T_world_submap"])
+    stats = []
+    for k in (sm["frames"] if frames is None else frames):
+        fr = cfg["frames"][k]
+        stats.append(o.integrate(fr["data"].cpu().numpy(), fr["T_world_sensor"], cfg["sensor"]))
+    return o, stats

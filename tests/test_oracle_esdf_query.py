@@ -1,0 +1,133 @@
+"""Pins of the oracle's ESDF and query (O13).
+
+References: a literal brute-force minimum over sites, scipy.ndimage.distance_transform_edt (a library
+exact EDT), single-site and plane-of-sites closed forms, the voxel-centre identity of trilinear
+interpolation and exactness of trilinear interpolation on affine fields.
+"""
+import numpy as np
+import pytest
+from scipy import ndimage
+
+
+def _random_tsdf(rng, nb_side=(3, 3, 2), fill=0.8, p_obs=0.9, tau=0.3):
+    blocks = [(x, y, z) for x in range(nb_side[0]) for y in range(nb_side[1]) for z in range(nb_side[2])
+              if rng.random() < fill]
+    b = np.array(blocks, np.int32) - np.array([1, 1, 0], np.int32)
+    nb = len(blocks)
+    W = (rng.random((nb, 512)) < p_obs).astype(np.float64) * rng.uniform(0.5, 3, (nb, 512))
+    D = rng.uniform(-tau, tau, (nb, 512)) * (W > 0)
+    return b, D, W
+
+
+def _dense(b, vals, fill):
+    lo = b.min(0) * 8
+    hi = b.max(0) * 8 + 8
+    G = np.full(tuple(hi - lo), fill, dtype=vals.dtype)
+    l = np.arange(512)
+    for i in range(b.shape[0]):
+        G[8 * b[i, 0] - lo[0] + l % 8, 8 * b[i, 1] - lo[1] + (l // 8) % 8, 8 * b[i, 2] - lo[2] + l // 64] = vals[i]
+    return G, lo
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_separable_equals_brute_force_and_scipy(orc, seed):
+    rng = np.random.default_rng(seed)
+    b, D, W = _random_tsdf(rng)
+    s, thr = 0.1, 0.02
+    E_sep, d2_sep = orc.esdf(b, D, W, s, thr, brute=False)
+    E_bf, d2_bf = orc.esdf(b, D, W, s, thr, brute=True)
+    assert np.array_equal(d2_sep, d2_bf)
+    # scipy: distance to the nearest zero of ~site over the dense AABB (unallocated -> not a site)
+    site = (W > 0) & (np.abs(D) <= thr)
+    G, lo = _dense(b, site, False)
+    ref = ndimage.distance_transform_edt(~G)
+    l = np.arange(512)
+    for i in range(b.shape[0]):
+        r = ref[8 * b[i, 0] - lo[0] + l % 8, 8 * b[i, 1] - lo[1] + (l // 8) % 8, 8 * b[i, 2] - lo[2] + l // 64]
+        assert np.array_equal(np.rint(r * r).astype(np.int64), d2_sep[i])
+    obs = W > 0
+    assert np.isnan(E_sep[~obs]).all()
+    assert np.allclose(np.abs(E_sep[obs]), s * np.sqrt(d2_sep[obs]), rtol=0, atol=1e-12)
+    assert (np.sign(E_sep[obs & (D < 0) & (d2_sep > 0)]) < 0).all()
+    assert (E_sep[obs & (D >= 0)] >= 0).all()
+
+
+def test_single_site_and_plane(orc):
+    s = 0.05
+    b = np.array([[x, y, z] for x in range(-1, 2) for y in range(-1, 2) for z in range(0, 2)], np.int32)
+    nb = len(b)
+    W = np.ones((nb, 512))
+    D = np.full((nb, 512), 0.2)
+    # single site at voxel (3, -5, 9)
+    l = np.arange(512)
+    vx = 8 * b[:, 0:1] + l % 8
+    vy = 8 * b[:, 1:2] + (l // 8) % 8
+    vz = 8 * b[:, 2:3] + l // 64
+    Ds = D.copy()
+    Ds[(vx == 3) & (vy == -5) & (vz == 9)] = 0.0
+    E, d2 = orc.esdf(b, Ds, W, s, 0.01)
+    assert np.allclose(E, s * np.sqrt((vx - 3) ** 2 + (vy + 5) ** 2 + (vz - 9) ** 2), atol=1e-12)
+    # plane of sites at layer z = 6, negative below
+    Dp = np.where(vz == 6, 0.0, np.where(vz < 6, -0.2, 0.2))
+    E, d2 = orc.esdf(b, Dp, W, s, 0.01)
+    assert np.allclose(E, np.sign(vz - 6) * s * np.abs(vz - 6), atol=1e-12)
+
+
+def test_empty_site_set_and_unobserved(orc):
+    b = np.array([[0, 0, 0], [1, 0, 0]], np.int32)
+    W = np.ones((2, 512))
+    W[1, :10] = 0
+    D = np.full((2, 512), 0.3)
+    E, d2 = orc.esdf(b, D, W, 0.1, 0.1)
+    assert np.isposinf(E[W > 0]).all() and np.isnan(E[W == 0]).all()
+    assert (d2 == -1).all()
+
+
+def _affine_blocks(a, s):
+    b = np.array([[x, y, z] for x in range(-1, 2) for y in range(-1, 2) for z in range(-1, 2)], np.int32)
+    l = np.arange(512)
+    vx = 8 * b[:, 0:1] + l % 8
+    vy = 8 * b[:, 1:2] + (l // 8) % 8
+    vz = 8 * b[:, 2:3] + l // 64
+    c = np.stack([(vx + 0.5) * s, (vy + 0.5) * s, (vz + 0.5) * s], -1)
+    E = c @ a[:3] + a[3]
+    return b, E
+
+
+def test_query_voxel_centre_identity_and_affine_exactness(orc):
+    s = 0.25                                  # dyadic: voxel centres are exact, f = 0 exactly
+    a = np.array([0.3, -1.1, 0.7, 0.05])
+    b, E = _affine_blocks(a, s)
+    rng = np.random.default_rng(0)
+    # at a voxel centre the interpolation returns the stored value exactly
+    v = rng.integers(-7, 7, (200, 3))
+    pts = ((v + 0.5) * s).astype(np.float32)
+    val, st = orc.query(b, E, s, np.eye(4), pts)
+    assert (st == 0).all()
+    l = (v % 8)[:, 0] + 8 * (v % 8)[:, 1] + 64 * (v % 8)[:, 2]
+    blk = {tuple(k): i for i, k in enumerate(b.tolist())}
+    ref = np.array([E[blk[tuple((vv // 8).tolist())], ll] for vv, ll in zip(v, l)])
+    assert np.array_equal(val, ref)
+    # trilinear interpolation is exact on an affine field
+    x = rng.uniform(-7 * s, 7 * s, (500, 3)).astype(np.float32)
+    val, st = orc.query(b, E, s, np.eye(4), x)
+    assert (st == 0).all()
+    assert np.allclose(val, x.astype(np.float64) @ a[:3] + a[3], atol=1e-9)
+
+
+def test_query_status_and_pose(orc):
+    s = 0.25
+    a = np.array([0.0, 0.0, 1.0, 0.0])
+    b, E = _affine_blocks(a, s)
+    E = E.copy()
+    E[13, 0] = np.nan                        # one unobserved voxel in block (0,0,0) at local 0
+    T = np.eye(4)
+    T[:3, 3] = [1.0, -2.0, 0.5]
+    # a point whose 8-corner stencil includes the unobserved voxel (0,0,0) but whose own voxel is (0,0,0)
+    # -> UNKNOWN;  a point whose own voxel is observed but whose stencil touches (0,0,0) -> NEAREST
+    pts_s = np.array([[0.1, 0.1, 0.1], [0.3, 0.3, 0.3], [10.0, 10.0, 10.0], [0.6, 0.6, 0.6]])
+    pts_w = (pts_s + T[:3, 3]).astype(np.float32)
+    val, st = orc.query(b, E, s, T, pts_w)
+    assert st.tolist() == [2, 1, 2, 0]
+    assert np.isnan(val[0]) and np.isnan(val[2])
+    assert val[1] == pytest.approx(E[13, 1 + 8 + 64])
