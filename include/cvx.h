@@ -1,0 +1,184 @@
+/* cvx.h — C-ABI of the B200-native coVoxSLAM submap builder (libcvx.so, sm_100a).
+ *
+ * The four calls of the problem statement (BASELINE.json north_star; §III.C-E):
+ *   cvx_create_submap        — a submap = pose + block-hashed voxel volume
+ *   cvx_integrate_pointcloud — raycast every point into the TSDF
+ *   cvx_finalize_esdf        — exact Euclidean signed distance field
+ *   cvx_query_distance       — trilinear distance look-ups
+ * plus a batched integrate (same semantics as calling integrate once per frame: fusion is a sum with
+ * no weight cap, "commutative and distributive"; reading R6), reset/stats, and the
+ * inspection hooks the parity tests and the multi-GPU gather use (export/import/pack).
+ *
+ * Citations: P:Lnn = PAPER.md line nn, S:Lnn = SPEC.md line nn, O1..O13 / Q1..Q24 = the readings in
+ * SURVEY.md §8c, restated in DESIGN.md.
+ *
+ * Conventions (all calls)
+ *  - Every call returns cvx_status; 0 = CVX_OK.  On error cvx_last_error() returns a thread-local
+ *    message.  Host-detectable errors (bad arguments, wrong state) return synchronously and leave the
+ *    submap unchanged.
+ *  - Buffers: pointers documented "device" must be CUDA device pointers on the submap's device (e.g.
+ *    torch CUDA tensors' data_ptr()); "host" pointers are ordinary host memory.  The CALLER owns every
+ *    buffer it passes; the library owns all submap state (hash table, block pool, ESDF, scratch) and
+ *    frees it in cvx_destroy_submap.
+ *  - Streams: `stream` is a cudaStream_t (NULL = legacy default stream).  Calls enqueue work on it and
+ *    return without a host synchronisation unless documented "synchronising".
+ *  - Device-side failures (block pool or hash table full, ray outside the 21-bit key domain) set a
+ *    sticky flag; the next synchronising call returns CVX_E_CAPACITY / CVX_E_RANGE.  Dropped work is
+ *    counted in the stats.
+ *  - A submap is not thread-safe; distinct submaps may be used concurrently from different threads.
+ */
+#ifndef CVX_H_
+#define CVX_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t cvx_status;
+#define CVX_OK 0
+#define CVX_E_INVALID (-1)  /* bad argument (null pointer, bad size, non-orthonormal rotation, ...)  */
+#define CVX_E_OOM (-2)      /* device allocation failed                                            */
+#define CVX_E_CAPACITY (-3) /* block pool (max_blocks) or hash table overflowed           */
+#define CVX_E_STATE (-4)    /* integrate after finalize, query before finalize            */
+#define CVX_E_CUDA (-5)     /* CUDA runtime error (no device, launch failure, ...)                 */
+#define CVX_E_RANGE (-6)    /* a ray left the 21-bit block-key domain or spans >= 2^15 voxels (O3)  */
+
+/* Voxel grid of one submap.  Blocks of 8^3 voxels (Q17), hashed by 3-D block index
+ * (P:L78-85).  voxel_size, truncation, site_threshold, weight_range_floor are metres. */
+typedef struct {
+  double voxel_size;         /* s > 0                                                              */
+  int32_t block_side;        /* must be 8                                                          */
+  double truncation;         /* tau >= 2*s: sdf clamp and extent behind the point */
+  int32_t weighting;         /* 0 constant w = 1, 1 inverse square w = 1/max(L, floor)^2 (Q5) */
+  double weight_range_floor; /* floor of L in the inverse-square weight (default 0.1 m)     */
+  int32_t carve;             /* 1: update o -> p + tau*u (default); 0: band p +- tau*u (Q2) */
+  double site_threshold;     /* ESDF site: observed and |D| <= site_threshold (O10, Q14; default s) */
+  int64_t max_blocks;        /* block pool capacity; the hash table holds >= 2*max_blocks entries   */
+} cvx_grid_config;
+
+/* Sensor model of the incoming frames. */
+typedef struct {
+  int32_t kind;             /* 0 unorganised points [n][3]; 1 pinhole depth [height][width];
+                               2 organised LiDAR points [height=rings][width=cols][3]               */
+  int32_t width, height;    /* organisation; for kind 1 n must equal width*height                   */
+  float fx, fy, cx, cy;     /* pinhole intrinsics (kind 1): p_c = (z(u-cx)/fx, z(v-cy)/fy, z) (O2)   */
+  float min_range, max_range; /* inclusive range filter on the ray length L (Q10)                   */
+} cvx_sensor_model;
+
+typedef struct cvx_submap cvx_submap; /* opaque; owns all device state of one submap */
+
+/* Cumulative counters of a submap since create/reset. */
+typedef struct {
+  int64_t rays_in;          /* points / pixels received                                            */
+  int64_t rays_used;        /* rays traversed                                                      */
+  int64_t skipped_invalid;  /* non-finite point, or depth <= 0 / non-finite                */
+  int64_t skipped_range;    /* outside [min_range, max_range] (Q10)                                */
+  int64_t skipped_domain;   /* outside the fixed-point / 21-bit key domain (O3) -> CVX_E_RANGE      */
+  int64_t voxel_updates;    /* sum over used rays of the traversed voxel count (COUNT)  */
+  int64_t new_blocks;       /* blocks allocated (ALLOCATE)                                  */
+  int64_t total_blocks;     /* blocks in the submap                                                */
+} cvx_integrate_stats;
+
+/* Create an empty submap on CUDA device `device` with pose T_world_submap (host, fp64 4x4 row-major,
+ * rotation orthonormal within 1e-6, last row 0 0 0 1).  Allocates and zeroes the block pool
+ * (16 B TSDF sums + 4 B ESDF per voxel) and the hash table.  Synchronising.
+ * Errors: CVX_E_INVALID (config/pose), CVX_E_OOM, CVX_E_CUDA. */
+cvx_status cvx_create_submap(const cvx_grid_config* config, const double* T_world_submap, int device,
+                             cvx_submap** out);
+
+/* Free all device state of the submap (synchronises the device first).  NULL is a no-op. */
+cvx_status cvx_destroy_submap(cvx_submap* submap);
+
+/* Return the submap to the freshly-created state without reallocating: zeroes the used blocks, clears
+ * the hash table, AABB, counters and the finalized flag.  Stream-ordered. */
+cvx_status cvx_reset_submap(cvx_submap* submap, void* stream);
+
+/* Integrate one frame.  `data` (device, fp32): kind 0/2 points [n][3] in the
+ * sensor frame, kind 1 depth [height][width] metres (n = width*height).  T_world_sensor: host fp64 4x4
+ * row-major.  Every used ray updates every voxel it traverses from the sensor origin to tau behind the
+ * point (carve) with the projective sdf d = clamp((p - c_v).u, -tau, tau) and weight w (O4-O6); the TSDF
+ * is the weighted average D = sum(w d)/sum(w), W = sum(w) (O8).  n = 0 is a no-op.
+ * `stats` (nullable, host): if given the call synchronises `stream` and returns the cumulative counters.
+ * Errors: CVX_E_INVALID, CVX_E_STATE (after finalize), CVX_E_CUDA; with stats also CVX_E_CAPACITY /
+ * CVX_E_RANGE from the sticky flags. */
+cvx_status cvx_integrate_pointcloud(cvx_submap* submap, const float* data, int64_t n,
+                                    const double* T_world_sensor, const cvx_sensor_model* sensor,
+                                    void* stream, cvx_integrate_stats* stats);
+
+/* Integrate n_frames frames of n_per_frame points each in one pass: `data` (device) holds the frames
+ * back to back, T_world_sensor (host) holds n_frames row-major 4x4 poses.  The result is identical,
+ * bit for bit, to n_frames calls of cvx_integrate_pointcloud (the fused sums are exact fixed-point
+ * integers, R6).  Same errors. */
+cvx_status cvx_integrate_batch(cvx_submap* submap, const float* data, int64_t n_per_frame,
+                               int32_t n_frames, const double* T_world_sensor,
+                               const cvx_sensor_model* sensor, void* stream, cvx_integrate_stats* stats);
+
+/* Cumulative counters (synchronising). Returns the sticky device errors. */
+cvx_status cvx_get_stats(const cvx_submap* submap, cvx_integrate_stats* out);
+
+/* Number of allocated blocks (synchronising).  Returns the sticky device errors. */
+cvx_status cvx_get_block_count(const cvx_submap* submap, int64_t* out);
+
+/* Allocated-block AABB in block coordinates, lo/hi inclusive (host int32[3] each; synchronising).
+ * Empty submap: lo > hi. */
+cvx_status cvx_get_aabb(const cvx_submap* submap, int32_t* lo, int32_t* hi);
+
+/* Exact ESDF over the allocated blocks (O10-O12): sites S = {v : W(v) > 0 and
+ * |D(v)| <= site_threshold}; E(v) = sign(D(v)) * s * sqrt(min_{u in S} |v - u|^2) for observed v,
+ * NaN for unobserved v, +inf for every observed v if S is empty.  Marks the submap finalized (no more
+ * integration).  Synchronising (reads the block count / AABB to size the dense EDT domain).
+ * Errors: CVX_E_STATE (already finalized), CVX_E_CAPACITY / CVX_E_RANGE (sticky), CVX_E_OOM. */
+cvx_status cvx_finalize_esdf(cvx_submap* submap, void* stream);
+
+/* Distance queries (O13).  points_world (device fp32 [m][3], world frame) ->
+ * out_distance (device fp32 [m]) and out_status (device uint8 [m]: 0 OK trilinear over the 8 voxel
+ * centres around x, 1 NEAREST = value of the voxel containing x, 2 UNKNOWN = NaN).
+ * Errors: CVX_E_STATE before finalize, CVX_E_INVALID. */
+cvx_status cvx_query_distance(const cvx_submap* submap, const float* points_world, int64_t m,
+                              float* out_distance, uint8_t* out_status, void* stream);
+
+/* Export every allocated block in slot order (synchronising): bxyz (device int32 [nb][3] block coords),
+ * D, W (device fp32 [nb][512], local index lx + 8 ly + 64 lz; D = sum(w d)/sum(w), 0 if W = 0), E
+ * (device fp32 [nb][512] or NULL; valid after finalize).  capacity_blocks bounds nb; *n_out = nb.
+ * Any of bxyz/D/W/E may be NULL to skip it.  Errors: CVX_E_CAPACITY if nb > capacity_blocks. */
+cvx_status cvx_export_blocks(const cvx_submap* submap, int32_t* bxyz, float* D, float* W, float* E,
+                             int64_t capacity_blocks, int64_t* n_out, void* stream);
+
+/* Import TSDF blocks (device bxyz int32 [n][3], D, W fp32 [n][512]) into a non-finalized submap,
+ * replacing the content of those blocks (used for stage-isolated ESDF parity and the ESDF stress
+ * config).  Stream-ordered. */
+cvx_status cvx_import_tsdf_blocks(cvx_submap* submap, const int32_t* bxyz, const float* D,
+                                  const float* W, int64_t n_blocks, void* stream);
+
+/* Pack the finalized ESDF for the multi-GPU gather (synchronising): dst (device) receives a
+ * 256-byte header {u32 magic 'CVXE', i32 version 1, i64 n_blocks, f64 voxel_size, f64 T_world_submap[16],
+ * zero padding} followed by n_blocks records {i32 bx, by, bz, slot; f32 E[512]} (2064 B each).
+ * *used = bytes written.  Errors: CVX_E_STATE before finalize, CVX_E_CAPACITY if dst_bytes too small. */
+cvx_status cvx_pack_esdf(const cvx_submap* submap, void* dst, int64_t dst_bytes, int64_t* used,
+                         void* stream);
+
+/* Bytes cvx_pack_esdf needs (synchronising). */
+cvx_status cvx_packed_size(const cvx_submap* submap, int64_t* bytes);
+
+/* Per-kernel timing of this submap's launches with CUDA events recorded on the launching stream
+ * (off by default; enabling synchronises the device and clears earlier records).  Used by bench.py
+ * for the roofline of the dominant kernel. */
+cvx_status cvx_profile_enable(cvx_submap* submap, int32_t enable);
+
+/* Synchronising: writes a JSON object {"kernel": {"ms": total_ms, "n": launches}, ...} of the records
+ * since the last report into buf (host, buflen bytes) and clears them.  CVX_E_CAPACITY if too small. */
+cvx_status cvx_profile_report(cvx_submap* submap, char* buf, int64_t buflen);
+
+/* Thread-local message of the last failing call on this thread ("" if none). */
+const char* cvx_last_error(void);
+
+/* Library build string (arch, version). */
+const char* cvx_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CVX_H_ */

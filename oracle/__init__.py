@@ -105,8 +105,11 @@ class OracleSubmap:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
-            lib().orc_free(h)
+        if h and _lib is not None:
+            try:
+                _lib.orc_free(h)
+            except Exception:
+                pass
             self._h = None
 
     def integrate(self, data, T_world_sensor, sensor: dict) -> dict:

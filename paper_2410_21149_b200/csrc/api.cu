@@ -1,0 +1,422 @@
+// api.cu — the C-ABI entry points of libcvx (include/cvx.h): argument checks, error codes, the
+// thread-local last error, device selection, stream-ordered launches.  No compute happens here;
+// every step of the path runs in the kernels of integrate.cu / esdf.cu / query.cu.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "submap.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+cvx_status fail(cvx_status code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+cvx_status cuda_fail(cudaError_t e, const char* where) {
+  cudaGetLastError();  // clear the non-sticky error
+  return fail(e == cudaErrorMemoryAllocation ? CVX_E_OOM : CVX_E_CUDA,
+              std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(int dev) {
+    err = cudaGetDevice(&prev);
+    if (err == cudaSuccess && prev != dev) err = cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+bool valid_pose(const double* T) {
+  if (!T) return false;
+  for (int i = 0; i < 16; ++i) if (!std::isfinite(T[i])) return false;
+  if (T[12] != 0.0 || T[13] != 0.0 || T[14] != 0.0 || T[15] != 1.0) return false;
+  for (int i = 0; i < 3; ++i)         // R^T R = I within 1e-6
+    for (int j = 0; j < 3; ++j) {
+      double d = 0;
+      for (int k = 0; k < 3; ++k) d += T[4 * k + i] * T[4 * k + j];
+      if (std::fabs(d - (i == j ? 1.0 : 0.0)) > 1e-6) return false;
+    }
+  return true;
+}
+
+cvx_status check_sensor(const cvx_sensor_model* s, int64_t n_per_frame) {
+  if (!s) return fail(CVX_E_INVALID, "sensor model is NULL");
+  if (s->kind < 0 || s->kind > 2) return fail(CVX_E_INVALID, "sensor kind must be 0, 1 or 2");
+  if (!(s->min_range >= 0.0f) || !(s->max_range >= s->min_range))
+    return fail(CVX_E_INVALID, "need 0 <= min_range <= max_range");
+  if (s->kind == 1) {
+    if (s->width <= 0 || s->height <= 0 || (int64_t)s->width * s->height != n_per_frame)
+      return fail(CVX_E_INVALID, "pinhole depth: n must equal width*height");
+    if (!(s->fx != 0.0f) || !(s->fy != 0.0f) || !std::isfinite(s->fx) || !std::isfinite(s->fy) ||
+        !std::isfinite(s->cx) || !std::isfinite(s->cy))
+      return fail(CVX_E_INVALID, "pinhole intrinsics must be finite with fx, fy != 0");
+  }
+  if (s->kind == 2 && s->width > 0 && s->height > 0 && (int64_t)s->width * s->height != n_per_frame)
+    return fail(CVX_E_INVALID, "organised LiDAR: n must equal width*height");
+  return CVX_OK;
+}
+
+cvx_status read_counters(const cvx_submap* sm, cudaStream_t st, cvx::Counters* out) {
+  cudaError_t e = cudaMemcpyAsync(sm->ctr_host, sm->ctr, sizeof(cvx::Counters), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "reading submap counters");
+  *out = *sm->ctr_host;
+  return CVX_OK;
+}
+
+cvx_status sticky(const cvx::Counters& c) {
+  if (c.err & (cvx::kErrCapacity | cvx::kErrHashFull))
+    return fail(CVX_E_CAPACITY, (c.err & cvx::kErrCapacity) ? "block pool overflow (max_blocks too small)"
+                                                            : "hash table full");
+  if (c.err & cvx::kErrRange) return fail(CVX_E_RANGE, "a ray or block left the 21-bit key / fixed-point domain");
+  return CVX_OK;
+}
+
+void fill_stats(const cvx::Counters& c, int max_blocks, cvx_integrate_stats* s) {
+  s->rays_in = (int64_t)c.rays_in;
+  s->rays_used = (int64_t)c.rays_used;
+  s->skipped_invalid = (int64_t)c.skipped_invalid;
+  s->skipped_range = (int64_t)c.skipped_range;
+  s->skipped_domain = (int64_t)c.skipped_domain;
+  s->voxel_updates = (int64_t)c.voxel_updates;
+  s->new_blocks = (int64_t)c.new_blocks;
+  s->total_blocks = c.n_blocks < max_blocks ? c.n_blocks : max_blocks;
+}
+
+void free_all(cvx_submap* sm) {
+  if (sm->hash.keys) cudaFree(sm->hash.keys);
+  if (sm->hash.vals) cudaFree(sm->hash.vals);
+  if (sm->pool.sums) cudaFree(sm->pool.sums);
+  if (sm->pool.esdf) cudaFree(sm->pool.esdf);
+  if (sm->pool.coords) cudaFree(sm->pool.coords);
+  if (sm->ctr) cudaFree(sm->ctr);
+  if (sm->ctr_host) cudaFreeHost(sm->ctr_host);
+  if (sm->frame_T) cudaFree(sm->frame_T);
+  if (sm->rays) cudaFree(sm->rays);
+  if (sm->edt) cudaFree(sm->edt);
+  if (sm->block_grid) cudaFree(sm->block_grid);
+  delete sm->prof;
+  sm->prof = nullptr;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* cvx_last_error(void) { return g_last_error.c_str(); }
+
+const char* cvx_version(void) { return "libcvx 0.1 (sm_100a; coVoxSLAM submap TSDF+ESDF, arXiv 2410.21149)"; }
+
+cvx_status cvx_create_submap(const cvx_grid_config* cfg, const double* T_world_submap, int device,
+                             cvx_submap** out) {
+  g_last_error.clear();
+  if (!cfg || !out) return fail(CVX_E_INVALID, "config and out must be non-NULL");
+  *out = nullptr;
+  if (!(cfg->voxel_size > 0) || !std::isfinite(cfg->voxel_size)) return fail(CVX_E_INVALID, "voxel_size must be > 0");
+  if (cfg->block_side != 8) return fail(CVX_E_INVALID, "block_side must be 8");
+  if (!(cfg->truncation > 0) || !std::isfinite(cfg->truncation)) return fail(CVX_E_INVALID, "truncation must be > 0");
+  if (cfg->weighting != 0 && cfg->weighting != 1) return fail(CVX_E_INVALID, "weighting must be 0 or 1");
+  if (cfg->weighting == 1 && !(cfg->weight_range_floor > 0)) return fail(CVX_E_INVALID, "weight_range_floor must be > 0");
+  if (cfg->carve != 0 && cfg->carve != 1) return fail(CVX_E_INVALID, "carve must be 0 or 1");
+  if (!(cfg->site_threshold >= 0) || !std::isfinite(cfg->site_threshold)) return fail(CVX_E_INVALID, "site_threshold must be >= 0");
+  if (cfg->max_blocks < 1 || cfg->max_blocks >= (1ll << 23)) return fail(CVX_E_INVALID, "max_blocks must be in [1, 2^23)");
+  if (!valid_pose(T_world_submap)) return fail(CVX_E_INVALID, "T_world_submap must be a finite rigid 4x4 (orthonormal within 1e-6)");
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+  if (device < 0 || device >= ndev) return fail(CVX_E_INVALID, "device index out of range");
+  DeviceGuard g(device);
+  if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+
+  cvx_submap* sm = new cvx_submap();
+  sm->prof = new cvx::Prof();
+  sm->cfg = *cfg;
+  std::memcpy(sm->T_ws, T_world_submap, sizeof(sm->T_ws));
+  sm->device = device;
+  int log2cap = 10;
+  while ((1ll << log2cap) < 2 * cfg->max_blocks) ++log2cap;
+  const size_t cap = (size_t)1 << log2cap;
+  const size_t nb = (size_t)cfg->max_blocks;
+  sm->hash.mask = (unsigned)(cap - 1);
+  sm->hash.log2cap = log2cap;
+  sm->pool.max_blocks = (int)nb;
+  if ((e = cudaMalloc(&sm->hash.keys, cap * 8)) != cudaSuccess ||
+      (e = cudaMalloc(&sm->hash.vals, cap * 4)) != cudaSuccess ||
+      (e = cudaMalloc(&sm->pool.sums, nb * cvx::kBlockVox * 16)) != cudaSuccess ||
+      (e = cudaMalloc(&sm->pool.esdf, nb * cvx::kBlockVox * 4)) != cudaSuccess ||
+      (e = cudaMalloc(&sm->pool.coords, nb * 16)) != cudaSuccess ||
+      (e = cudaMalloc(&sm->ctr, sizeof(cvx::Counters))) != cudaSuccess ||
+      (e = cudaMallocHost(&sm->ctr_host, sizeof(cvx::Counters))) != cudaSuccess ||
+      (e = cudaMalloc(&sm->frame_T, sizeof(double) * 12 * cvx::kMaxBatch)) != cudaSuccess) {
+    free_all(sm);
+    delete sm;
+    return cuda_fail(e, "allocating submap");
+  }
+  // zero-initialised pool (a3 zero-init happens once here; reset re-zeroes only the used blocks)
+  cudaMemset(sm->ctr, 0, sizeof(cvx::Counters));
+  cudaMemset(sm->pool.sums, 0, nb * cvx::kBlockVox * 16);
+  cudaMemset(sm->pool.esdf, 0, nb * cvx::kBlockVox * 4);
+  e = cvx::launch_reset(sm, 0);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    free_all(sm);
+    delete sm;
+    return cuda_fail(e, "initialising submap");
+  }
+  *out = sm;
+  return CVX_OK;
+}
+
+cvx_status cvx_destroy_submap(cvx_submap* sm) {
+  g_last_error.clear();
+  if (!sm) return CVX_OK;
+  DeviceGuard g(sm->device);
+  cudaDeviceSynchronize();
+  free_all(sm);
+  delete sm;
+  return CVX_OK;
+}
+
+cvx_status cvx_reset_submap(cvx_submap* sm, void* stream) {
+  g_last_error.clear();
+  if (!sm) return fail(CVX_E_INVALID, "submap is NULL");
+  DeviceGuard g(sm->device);
+  cudaError_t e = cvx::launch_reset(sm, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "reset");
+  sm->finalized = false;
+  return CVX_OK;
+}
+
+cvx_status cvx_integrate_batch(cvx_submap* sm, const float* data, int64_t n_per_frame, int32_t n_frames,
+                               const double* T_world_sensor, const cvx_sensor_model* sensor, void* stream,
+                               cvx_integrate_stats* stats) {
+  g_last_error.clear();
+  if (!sm) return fail(CVX_E_INVALID, "submap is NULL");
+  if (sm->finalized) return fail(CVX_E_STATE, "submap is finalized (S:L443): integrate rejected");
+  if (n_per_frame < 0 || n_frames < 0) return fail(CVX_E_INVALID, "negative sizes");
+  cvx_status rc = check_sensor(sensor, n_per_frame);
+  if (rc != CVX_OK) return rc;
+  if (n_per_frame > 0 && n_frames > 0) {
+    if (!data) return fail(CVX_E_INVALID, "data is NULL");
+    if (!T_world_sensor) return fail(CVX_E_INVALID, "T_world_sensor is NULL");
+    for (int f = 0; f < n_frames; ++f)
+      if (!valid_pose(T_world_sensor + 16 * f)) return fail(CVX_E_INVALID, "T_world_sensor must be a finite rigid 4x4");
+    if (n_per_frame >= (1ll << 31)) return fail(CVX_E_INVALID, "n_per_frame must be < 2^31");
+  }
+  DeviceGuard g(sm->device);
+  if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t per_launch = std::max<int64_t>(1, std::min<int64_t>(cvx::kMaxBatch, ((1ll << 31) - 1) / std::max<int64_t>(1, n_per_frame)));
+  for (int64_t f0 = 0; f0 < n_frames && n_per_frame > 0; f0 += per_launch) {
+    const int nf = (int)std::min<int64_t>(per_launch, n_frames - f0);
+    const int64_t elems = sensor->kind == 1 ? n_per_frame : 3 * n_per_frame;
+    cudaError_t e = cvx::launch_integrate(sm, data + f0 * elems, n_per_frame, nf, T_world_sensor + 16 * f0, *sensor, st);
+    if (e != cudaSuccess) return cuda_fail(e, "integrate");
+  }
+  if (stats) {
+    cvx::Counters c;
+    if ((rc = read_counters(sm, st, &c)) != CVX_OK) return rc;
+    fill_stats(c, sm->pool.max_blocks, stats);
+    return sticky(c);
+  }
+  return CVX_OK;
+}
+
+cvx_status cvx_integrate_pointcloud(cvx_submap* sm, const float* data, int64_t n, const double* T_world_sensor,
+                                    const cvx_sensor_model* sensor, void* stream, cvx_integrate_stats* stats) {
+  return cvx_integrate_batch(sm, data, n, 1, T_world_sensor, sensor, stream, stats);
+}
+
+cvx_status cvx_get_stats(const cvx_submap* sm, cvx_integrate_stats* out) {
+  g_last_error.clear();
+  if (!sm || !out) return fail(CVX_E_INVALID, "NULL argument");
+  DeviceGuard g(sm->device);
+  cvx::Counters c;
+  cvx_status rc = read_counters(sm, 0, &c);
+  if (rc != CVX_OK) return rc;
+  fill_stats(c, sm->pool.max_blocks, out);
+  return sticky(c);
+}
+
+cvx_status cvx_get_block_count(const cvx_submap* sm, int64_t* out) {
+  g_last_error.clear();
+  if (!sm || !out) return fail(CVX_E_INVALID, "NULL argument");
+  DeviceGuard g(sm->device);
+  cvx::Counters c;
+  cvx_status rc = read_counters(sm, 0, &c);
+  if (rc != CVX_OK) return rc;
+  *out = c.n_blocks < sm->pool.max_blocks ? c.n_blocks : sm->pool.max_blocks;
+  return sticky(c);
+}
+
+cvx_status cvx_get_aabb(const cvx_submap* sm, int32_t* lo, int32_t* hi) {
+  g_last_error.clear();
+  if (!sm || !lo || !hi) return fail(CVX_E_INVALID, "NULL argument");
+  DeviceGuard g(sm->device);
+  cvx::Counters c;
+  cvx_status rc = read_counters(sm, 0, &c);
+  if (rc != CVX_OK) return rc;
+  for (int a = 0; a < 3; ++a) { lo[a] = c.aabb_lo[a]; hi[a] = c.aabb_hi[a]; }
+  return CVX_OK;
+}
+
+cvx_status cvx_finalize_esdf(cvx_submap* sm, void* stream) {
+  g_last_error.clear();
+  if (!sm) return fail(CVX_E_INVALID, "submap is NULL");
+  if (sm->finalized) return fail(CVX_E_STATE, "submap already finalized");
+  DeviceGuard g(sm->device);
+  if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+  cudaStream_t st = (cudaStream_t)stream;
+  cvx::Counters c;
+  cvx_status rc = read_counters(sm, st, &c);
+  if (rc != CVX_OK) return rc;
+  if ((rc = sticky(c)) != CVX_OK) return rc;
+  const int nb = c.n_blocks < sm->pool.max_blocks ? c.n_blocks : sm->pool.max_blocks;
+  if (nb > 0) {
+    for (int a = 0; a < 3; ++a)
+      if ((int64_t)8 * ((int64_t)c.aabb_hi[a] - c.aabb_lo[a] + 1) > 65528)
+        return fail(CVX_E_RANGE, "submap AABB exceeds 65528 voxels along an axis (dense EDT domain)");
+    cudaError_t e = cvx::launch_finalize(sm, nb, c.aabb_lo, c.aabb_hi, st);
+    if (e != cudaSuccess) return cuda_fail(e, "finalize_esdf");
+  }
+  sm->finalized = true;
+  return CVX_OK;
+}
+
+cvx_status cvx_query_distance(const cvx_submap* sm, const float* pts, int64_t m, float* out, uint8_t* status,
+                              void* stream) {
+  g_last_error.clear();
+  if (!sm) return fail(CVX_E_INVALID, "submap is NULL");
+  if (!sm->finalized) return fail(CVX_E_STATE, "query before finalize_esdf");
+  if (m < 0) return fail(CVX_E_INVALID, "m < 0");
+  if (m > 0 && (!pts || !out || !status)) return fail(CVX_E_INVALID, "NULL buffer");
+  DeviceGuard g(sm->device);
+  cudaError_t e = cvx::launch_query(sm, pts, m, out, status, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "query_distance");
+  return CVX_OK;
+}
+
+cvx_status cvx_export_blocks(const cvx_submap* sm, int32_t* bxyz, float* D, float* W, float* E,
+                             int64_t capacity_blocks, int64_t* n_out, void* stream) {
+  g_last_error.clear();
+  if (!sm || !n_out) return fail(CVX_E_INVALID, "NULL argument");
+  DeviceGuard g(sm->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  cvx::Counters c;
+  cvx_status rc = read_counters(sm, st, &c);
+  if (rc != CVX_OK) return rc;
+  const int nb = c.n_blocks < sm->pool.max_blocks ? c.n_blocks : sm->pool.max_blocks;
+  *n_out = nb;
+  if (nb > capacity_blocks) return fail(CVX_E_CAPACITY, "export buffer smaller than the block count");
+  cudaError_t e = cvx::launch_export(sm, nb, bxyz, D, W, E, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "export_blocks");
+  return sticky(c);
+}
+
+cvx_status cvx_import_tsdf_blocks(cvx_submap* sm, const int32_t* bxyz, const float* D, const float* W,
+                                  int64_t n, void* stream) {
+  g_last_error.clear();
+  if (!sm) return fail(CVX_E_INVALID, "submap is NULL");
+  if (sm->finalized) return fail(CVX_E_STATE, "submap is finalized");
+  if (n < 0) return fail(CVX_E_INVALID, "n < 0");
+  if (n > 0 && (!bxyz || !D || !W)) return fail(CVX_E_INVALID, "NULL buffer");
+  DeviceGuard g(sm->device);
+  cudaError_t e = cvx::launch_import(sm, bxyz, D, W, n, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "import_tsdf_blocks");
+  return CVX_OK;
+}
+
+cvx_status cvx_packed_size(const cvx_submap* sm, int64_t* bytes) {
+  int64_t nb = 0;
+  cvx_status rc = cvx_get_block_count(sm, &nb);
+  if (rc != CVX_OK && rc != CVX_E_CAPACITY && rc != CVX_E_RANGE) return rc;
+  if (!bytes) return fail(CVX_E_INVALID, "NULL argument");
+  *bytes = 256 + nb * (16 + 4 * cvx::kBlockVox);
+  return CVX_OK;
+}
+
+cvx_status cvx_pack_esdf(const cvx_submap* sm, void* dst, int64_t dst_bytes, int64_t* used, void* stream) {
+  g_last_error.clear();
+  if (!sm || !dst || !used) return fail(CVX_E_INVALID, "NULL argument");
+  if (!sm->finalized) return fail(CVX_E_STATE, "pack before finalize_esdf");
+  DeviceGuard g(sm->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  cvx::Counters c;
+  cvx_status rc = read_counters(sm, st, &c);
+  if (rc != CVX_OK) return rc;
+  const int nb = c.n_blocks < sm->pool.max_blocks ? c.n_blocks : sm->pool.max_blocks;
+  const int64_t need = 256 + (int64_t)nb * (16 + 4 * cvx::kBlockVox);
+  *used = need;
+  if (dst_bytes < need) return fail(CVX_E_CAPACITY, "pack buffer too small");
+  unsigned char hdr[256];
+  std::memset(hdr, 0, sizeof(hdr));
+  const uint32_t magic = 0x45585643u;  // "CVXE"
+  const int32_t version = 1;
+  const int64_t n64 = nb;
+  std::memcpy(hdr, &magic, 4);
+  std::memcpy(hdr + 4, &version, 4);
+  std::memcpy(hdr + 8, &n64, 8);
+  std::memcpy(hdr + 16, &sm->cfg.voxel_size, 8);
+  std::memcpy(hdr + 24, sm->T_ws, 128);
+  cudaError_t e = cudaMemcpyAsync(dst, hdr, sizeof(hdr), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cvx::launch_pack(sm, nb, (unsigned char*)dst + 256, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "pack_esdf");
+  return CVX_OK;
+}
+
+cvx_status cvx_profile_enable(cvx_submap* sm, int32_t enable) {
+  g_last_error.clear();
+  if (!sm) return fail(CVX_E_INVALID, "submap is NULL");
+  DeviceGuard g(sm->device);
+  cudaDeviceSynchronize();
+  sm->prof->recycle();
+  sm->prof->on = enable != 0;
+  return CVX_OK;
+}
+
+cvx_status cvx_profile_report(cvx_submap* sm, char* buf, int64_t buflen) {
+  g_last_error.clear();
+  if (!sm || !buf || buflen <= 0) return fail(CVX_E_INVALID, "NULL argument");
+  DeviceGuard g(sm->device);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return cuda_fail(e, "profile_report");
+  std::vector<std::pair<std::string, std::pair<double, long long>>> acc;
+  for (auto& r : sm->prof->recs) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, r.a, r.b) != cudaSuccess) { cudaGetLastError(); continue; }
+    size_t k = 0;
+    while (k < acc.size() && acc[k].first != r.name) ++k;
+    if (k == acc.size()) acc.push_back({r.name, {0.0, 0}});
+    acc[k].second.first += ms;
+    acc[k].second.second += 1;
+  }
+  sm->prof->recycle();
+  std::string js = "{";
+  for (size_t k = 0; k < acc.size(); ++k) {
+    char item[256];
+    std::snprintf(item, sizeof(item), "%s\"%s\": {\"ms\": %.6f, \"n\": %lld}", k ? ", " : "", acc[k].first.c_str(),
+                  acc[k].second.first, acc[k].second.second);
+    js += item;
+  }
+  js += "}";
+  if ((int64_t)js.size() + 1 > buflen) return fail(CVX_E_CAPACITY, "report buffer too small");
+  std::memcpy(buf, js.c_str(), js.size() + 1);
+  return CVX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,121 @@
+// cvx_internal.cuh — device-side state and helpers of libcvx (sm_100a).  Not part of the C-ABI.
+//
+// HBM layout of one submap:
+//   keys  u64 [cap]          open-addressing hash table of packed 21-bit block keys
+//   vals  i32 [cap]          slot of the key (PENDING while the inserter publishes it)
+//   sums  i64x2 [max_blocks*512]  per voxel (sum w*d, sum w) in fixed point 2^-32 (O8 as exact sums)
+//   esdf  f32 [max_blocks*512]    E per voxel (after finalize)
+//   coords i32x4 [max_blocks]     slot -> block coordinates
+//   ctr   Counters                pool bump index, AABB, sticky errors, stats
+// Voxel local index inside a block: lx + 8 ly + 64 lz (O9); slot s owns voxels [s*512, s*512+512).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace cvx {
+
+constexpr int kBlockSide = 8;
+constexpr int kBlockVox = 512;
+constexpr unsigned long long kEmptyKey = ~0ull;
+constexpr int kPending = -1;   // vals[] while the inserting thread publishes the slot
+constexpr int kFailed = -2;    // pool overflow: updates to this block are dropped (CVX_E_CAPACITY)
+constexpr double kFxScale = 4294967296.0;  // 2^32: fixed-point scale of the TSDF sums
+
+enum ErrBits : unsigned { kErrCapacity = 1u, kErrHashFull = 2u, kErrRange = 4u };
+
+struct Counters {
+  int n_blocks;            // bump index of the block pool (may overshoot max_blocks on overflow)
+  unsigned err;            // sticky ErrBits
+  int aabb_lo[3];          // block coordinates
+  int aabb_hi[3];
+  int n_rays;              // compacted rays of the current integrate call
+  int pad;
+  unsigned long long rays_in, rays_used, skipped_invalid, skipped_range, skipped_domain, voxel_updates,
+      new_blocks;
+};
+
+struct HashView {
+  unsigned long long* keys;
+  int* vals;
+  unsigned mask;           // cap - 1
+  int log2cap;
+};
+
+struct PoolView {
+  long long* sums;         // [max_blocks*512][2]
+  float* esdf;             // [max_blocks*512]
+  int4* coords;            // [max_blocks]
+  int max_blocks;
+};
+
+// 21-bit two's-complement fields per axis; never equals kEmptyKey.
+__host__ __device__ inline unsigned long long pack_key(int bx, int by, int bz) {
+  const unsigned long long m = (1ull << 21) - 1;
+  return ((unsigned long long)(bx & (int)m) << 42) | ((unsigned long long)(by & (int)m) << 21) |
+         (unsigned long long)(bz & (int)m);
+}
+
+__device__ inline unsigned hash_slot(unsigned long long key, const HashView& h) {
+  return (unsigned)((key * 0x9E3779B97F4A7C15ull) >> (64 - h.log2cap));
+}
+
+__device__ inline int ld_volatile(const int* p) { return *(const volatile int*)p; }
+__device__ inline unsigned long long ld_volatile(const unsigned long long* p) {
+  return *(const volatile unsigned long long*)p;
+}
+
+// Find-only probe: slot, or -1 if absent.  Table must be quiescent (no concurrent inserts).
+__device__ inline int hash_find(const HashView& h, unsigned long long key) {
+  unsigned i = hash_slot(key, h);
+  for (unsigned p = 0; p <= h.mask; ++p) {
+    unsigned long long k = h.keys[i];
+    if (k == key) return h.vals[i];
+    if (k == kEmptyKey) return -1;
+    i = (i + 1) & h.mask;
+  }
+  return -1;
+}
+
+// ASH-style activate: insert-if-absent and return the block's pool slot.  The winner of the
+// key CAS claims a slot by bumping the pool index, records the block coordinates and AABB,
+// then publishes the slot; concurrent finders of the same key wait for the publication.
+__device__ inline int hash_activate(const HashView& h, const PoolView& pool, Counters* ctr,
+                                    unsigned long long key, int bx, int by, int bz) {
+  unsigned i = hash_slot(key, h);
+  for (unsigned p = 0; p <= h.mask; ++p) {
+    unsigned long long k = ld_volatile(&h.keys[i]);
+    if (k == kEmptyKey) {
+      unsigned long long old = atomicCAS(&h.keys[i], kEmptyKey, key);
+      if (old == kEmptyKey) {
+        int slot = atomicAdd(&ctr->n_blocks, 1);
+        if (slot >= pool.max_blocks) {
+          atomicOr(&ctr->err, (unsigned)kErrCapacity);
+          slot = kFailed;
+        } else {
+          pool.coords[slot] = make_int4(bx, by, bz, 0);
+          atomicMin(&ctr->aabb_lo[0], bx); atomicMin(&ctr->aabb_lo[1], by); atomicMin(&ctr->aabb_lo[2], bz);
+          atomicMax(&ctr->aabb_hi[0], bx); atomicMax(&ctr->aabb_hi[1], by); atomicMax(&ctr->aabb_hi[2], bz);
+          atomicAdd(&ctr->new_blocks, 1ull);
+        }
+        __threadfence();
+        *(volatile int*)&h.vals[i] = slot;
+        return slot;
+      }
+      k = old;
+    }
+    if (k == key) {
+      int v;
+      while ((v = ld_volatile(&h.vals[i])) == kPending) { __nanosleep(32); }
+      return v;
+    }
+    i = (i + 1) & h.mask;
+  }
+  atomicOr(&ctr->err, (unsigned)kErrHashFull);
+  return kFailed;
+}
+
+// Floor division / modulo by 8 on int32 voxel coordinates (S:L200-207 floor semantics).
+__host__ __device__ inline int bdiv(int v) { return v >> 3; }
+__host__ __device__ inline int bmod(int v) { return v & 7; }
+
+}  // namespace cvx

@@ -1,0 +1,91 @@
+// submap.h — host-side definition of the opaque cvx_submap and the internal launch entry points.
+#pragma once
+#include <cstdint>
+#include <vector>
+#include <cuda_runtime.h>
+
+#include "../../include/cvx.h"
+#include "cvx_internal.cuh"
+
+namespace cvx {
+// Optional per-kernel CUDA-event timing (cvx_profile_enable / cvx_profile_report): events are
+// recorded on the launching stream around every kernel of the submap.
+struct ProfRec { const char* name; cudaEvent_t a, b; };
+struct Prof {
+  bool on = false;
+  std::vector<ProfRec> recs;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t ev() {
+    if (!pool.empty()) { cudaEvent_t e = pool.back(); pool.pop_back(); return e; }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
+  int begin(const char* name, cudaStream_t st) {
+    if (!on) return -1;
+    ProfRec r{name, ev(), ev()};
+    cudaEventRecord(r.a, st);
+    recs.push_back(r);
+    return (int)recs.size() - 1;
+  }
+  void end(int i, cudaStream_t st) { if (i >= 0) cudaEventRecord(recs[i].b, st); }
+  void recycle() { for (auto& r : recs) { pool.push_back(r.a); pool.push_back(r.b); } recs.clear(); }
+  ~Prof() { recycle(); for (auto e : pool) cudaEventDestroy(e); }
+};
+}  // namespace cvx
+
+struct cvx_submap {
+  cvx_grid_config cfg{};
+  double T_ws[16] = {};    // world <- submap
+  int device = 0;
+  bool finalized = false;
+
+  // hash table + pool (HBM, see cvx_internal.cuh)
+  cvx::HashView hash{};
+  cvx::PoolView pool{};
+  cvx::Counters* ctr = nullptr;       // device
+  cvx::Counters* ctr_host = nullptr;  // pinned mirror for synchronising reads
+
+  // integrate scratch (grow-only)
+  double* frame_T = nullptr;  // device [kMaxBatch][12]: R_SC (row-major) then t_SC, per frame
+  void* rays = nullptr;       // device RayRec [ray_cap]
+  int64_t ray_cap = 0;
+
+  // ESDF scratch (grow-only)
+  void* edt = nullptr;        // device: g2 u32 | meta u32 | g1 u16 over the dense AABB
+  int64_t edt_bytes = 0;
+  int* block_grid = nullptr;  // device int32 [nbz][nby][nbx]
+  int64_t block_grid_cap = 0;
+
+  cvx::Prof* prof = nullptr;  // owned
+};
+
+// RAII timing scope around one kernel launch
+struct ProfScope {
+  cvx::Prof* p; int i; cudaStream_t st;
+  ProfScope(const cvx_submap* sm, const char* name, cudaStream_t s) : p(sm->prof), i(-1), st(s) {
+    if (p) i = p->begin(name, s);
+  }
+  ~ProfScope() { if (p) p->end(i, st); }
+};
+
+namespace cvx {
+
+constexpr int kMaxBatch = 128;   // frames per integrate launch
+
+// integrate.cu
+cudaError_t launch_reset(cvx_submap* sm, cudaStream_t st);
+cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_frame, int n_frames,
+                             const double* T_world_sensor, const cvx_sensor_model& sensor, cudaStream_t st);
+// esdf.cu
+cudaError_t launch_finalize(cvx_submap* sm, int n_blocks, const int lo[3], const int hi[3], cudaStream_t st);
+// query.cu
+cudaError_t launch_query(const cvx_submap* sm, const float* pts, int64_t m, float* out, uint8_t* status,
+                         cudaStream_t st);
+cudaError_t launch_export(const cvx_submap* sm, int n_blocks, int32_t* bxyz, float* D, float* W, float* E,
+                          cudaStream_t st);
+cudaError_t launch_import(cvx_submap* sm, const int32_t* bxyz, const float* D, const float* W, int64_t n,
+                          cudaStream_t st);
+cudaError_t launch_pack(const cvx_submap* sm, int n_blocks, void* dst_records, cudaStream_t st);
+
+}  // namespace cvx

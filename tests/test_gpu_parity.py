@@ -1,0 +1,234 @@
+"""GPU parity: libcvx (through the C-ABI) vs the CPU oracle on the same seeded inputs.
+
+Bar (BASELINE.json north_star): block sets and observed sets bit-exact; |dD| <= 1e-4 m,
+|dW| <= 1e-3 * max(1, W); |dE| <= 1e-4 m with identical NaN / +inf patterns; query values within
+1e-4 m and identical statuses.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from helpers import (TOL_E, assert_esdf_parity, assert_tsdf_parity, gpu_build, gpu_export_sorted,
+                     oracle_build, sort_blocks)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tiny():
+    return synth.make_config("tiny")
+
+
+def _cum_stats(stats_list):
+    keys = ("rays_in", "rays_used", "skipped_invalid", "skipped_range", "skipped_domain", "voxel_updates")
+    return {k: sum(s[k] for s in stats_list) for k in keys}
+
+
+def test_tiny_tsdf_parity_and_counts(tiny, orc):
+    frames = list(range(10))
+    sm, st = gpu_build(tiny, frames, finalize=False)
+    o = orc.OracleSubmap(tiny["grid"], tiny["submaps"][0]["T_world_submap"])
+    ost = [o.integrate(tiny["frames"][k]["data"].numpy(), tiny["frames"][k]["T_world_sensor"], tiny["sensor"])
+           for k in frames]
+    rep = assert_tsdf_parity(gpu_export_sorted(sm), o.export())
+    cum = _cum_stats(ost)
+    for k, v in cum.items():
+        assert st[k] == v, (k, st[k], v)
+    assert st["total_blocks"] == o.num_blocks() == rep["blocks"]
+    # COUNT closed form == what the walk deposits: sum of W over voxels (constant weights)
+    _, _, W, _ = gpu_export_sorted(sm)
+    assert W.astype(np.float64).sum() == st["voxel_updates"]
+
+
+def test_batch_equals_sequential_bitexact_and_deterministic(tiny):
+    frames = list(range(10))
+    a, _ = gpu_build(tiny, frames, batch=False, finalize=False)
+    b, _ = gpu_build(tiny, frames, batch=True, finalize=False)
+    c, _ = gpu_build(tiny, list(reversed(frames)), batch=True, finalize=False)
+    ea, eb, ec = gpu_export_sorted(a), gpu_export_sorted(b), gpu_export_sorted(c)
+    for x, y in ((ea, eb), (ea, ec)):
+        assert np.array_equal(x[0], y[0])
+        assert np.array_equal(x[1].view(np.uint32), y[1].view(np.uint32))   # D bitwise
+        assert np.array_equal(x[2].view(np.uint32), y[2].view(np.uint32))   # W bitwise
+
+
+@pytest.mark.parametrize("weighting,carve", [(1, 1), (0, 0), (1, 0)])
+def test_tiny_modes_parity(tiny, orc, weighting, carve):
+    g = dict(tiny["grid"], weighting=weighting, carve=carve)
+    frames = [0, 3, 7]
+    sm, _ = gpu_build(tiny, frames, grid=g, finalize=False)
+    o, _ = oracle_build(tiny, frames, grid=g)
+    assert_tsdf_parity(gpu_export_sorted(sm), o.export())
+
+
+def test_lidar_subset_parity(orc):
+    cfg = synth.make_config("lidar", frames=[0, 60])
+    sm, st = gpu_build(cfg, [0, 60], finalize=False)
+    o, _ = oracle_build(cfg, [0, 60])
+    rep = assert_tsdf_parity(gpu_export_sorted(sm), o.export())
+    assert rep["blocks"] > 5000
+
+
+def test_rgbd_subset_parity(orc):
+    cfg = synth.make_config("rgbd", frames=[0, 37])
+    sm, _ = gpu_build(cfg, [0, 37], grid=dict(cfg["grid"], weighting=1), finalize=False)
+    o, _ = oracle_build(cfg, [0, 37], grid=dict(cfg["grid"], weighting=1))
+    assert_tsdf_parity(gpu_export_sorted(sm), o.export())
+
+
+def test_pose_composition_nontrivial_submap_pose(tiny, orc):
+    T = synth.pose(synth.rot_zyx(0.7, 0.1, -0.2), [0.3, -1.7, 0.25])
+    sm, _ = gpu_build(tiny, [0, 5, 9], T_ws=T, finalize=False)
+    o, _ = oracle_build(tiny, [0, 5, 9], T_ws=T)
+    assert_tsdf_parity(gpu_export_sorted(sm), o.export())
+
+
+# ------------------------------------------------------------------------------------------ ESDF
+def test_tiny_esdf_stage_isolated_and_end_to_end(tiny, orc):
+    frames = list(range(10))
+    sm, _ = gpu_build(tiny, frames)
+    b, D, W, E = gpu_export_sorted(sm)
+    g = tiny["grid"]
+    # stage-isolated: the oracle EDT on the GPU's exported TSDF (identical site sets)
+    Eo, _ = orc.esdf(b, D.astype(np.float64), W.astype(np.float64), g["voxel_size"], g["site_threshold"])
+    assert_esdf_parity(E, Eo, W > 0)
+    # brute force agrees too (tiny config: O(|O| |S|))
+    Eb, _ = orc.esdf(b, D.astype(np.float64), W.astype(np.float64), g["voxel_size"], g["site_threshold"], brute=True)
+    assert_esdf_parity(E, Eb, W > 0)
+    # end-to-end: oracle TSDF -> oracle ESDF; voxels beyond tolerance come only from site-threshold ties
+    o, _ = oracle_build(tiny, frames)
+    bo, Do, Wo = o.export()
+    Eoe, _ = orc.esdf(bo, Do, Wo, g["voxel_size"], g["site_threshold"])
+    fin = np.isfinite(Eoe)
+    bad = (np.abs(E.astype(np.float64) - Eoe)[fin] > TOL_E).sum()
+    assert bad <= 0.001 * fin.sum(), bad
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_esdf_import_random_tsdf(orc, seed):
+    """Stage-isolated ESDF on imported random TSDFs: holes, ragged AABB, negative coordinates."""
+    from paper_2410_21149_b200 import Submap
+    rng = np.random.default_rng(seed)
+    blocks = [(x, y, z) for x in range(-2, 3) for y in range(-1, 3) for z in range(-1, 2) if rng.random() < 0.7]
+    b = np.array(blocks, np.int32)
+    nb = len(b)
+    W = ((rng.random((nb, 512)) < 0.85) * rng.uniform(0.5, 4, (nb, 512))).astype(np.float32)
+    D = (rng.uniform(-0.3, 0.3, (nb, 512)) * (W > 0)).astype(np.float32)
+    grid = dict(voxel_size=0.1, truncation=0.3, site_threshold=0.01, max_blocks=4096)
+    sm = Submap(grid)
+    dev = torch.device("cuda", 0)
+    sm.import_tsdf(torch.from_numpy(b).to(dev), torch.from_numpy(D).to(dev), torch.from_numpy(W).to(dev))
+    sm.finalize_esdf()
+    bg, Dg, Wg, Eg = gpu_export_sorted(sm)
+    bs, Ds, Ws = sort_blocks(b, D, W)
+    assert np.array_equal(bg, bs)
+    Eo, _ = orc.esdf(bg, Dg.astype(np.float64), Wg.astype(np.float64), 0.1, 0.01)
+    assert_esdf_parity(Eg, Eo, Wg > 0)
+
+
+def test_esdf_no_sites_and_single_site(orc):
+    from paper_2410_21149_b200 import Submap
+    dev = torch.device("cuda", 0)
+    b = torch.tensor([[0, 0, 0], [3, -1, 2]], dtype=torch.int32, device=dev)
+    W = torch.ones((2, 512), device=dev)
+    W[1, :7] = 0
+    D = torch.full((2, 512), 0.25, device=dev)
+    sm = Submap(dict(voxel_size=0.05, truncation=0.3, site_threshold=0.05, max_blocks=64))
+    sm.import_tsdf(b, D, W)
+    sm.finalize_esdf()
+    _, _, Wg, Eg = gpu_export_sorted(sm)
+    assert np.isposinf(Eg[Wg > 0]).all() and np.isnan(Eg[Wg == 0]).all()
+    D2 = D.clone()
+    D2[1, 100] = 0.0
+    D2[0, :] = -0.25
+    sm2 = Submap(dict(voxel_size=0.05, truncation=0.3, site_threshold=0.05, max_blocks=64))
+    sm2.import_tsdf(b, D2, W)
+    sm2.finalize_esdf()
+    bg, Dg, Wg, Eg = gpu_export_sorted(sm2)
+    Eo, _ = orc.esdf(bg, Dg.astype(np.float64), Wg.astype(np.float64), 0.05, 0.05, brute=True)
+    assert_esdf_parity(Eg, Eo, Wg > 0)
+    assert (Eg[bg[:, 0] == 0] < 0).all()
+
+
+# ------------------------------------------------------------------------------------------ query
+def test_query_parity(tiny, orc):
+    T = synth.pose(synth.rot_zyx(0.3), [0.5, 0.25, -0.1])
+    sm, _ = gpu_build(tiny, list(range(10)), T_ws=T)
+    b, D, W, E = gpu_export_sorted(sm)
+    lo, hi = sm.aabb()
+    rng = np.random.default_rng(0)
+    s = tiny["grid"]["voxel_size"]
+    xs = rng.uniform(lo * 8 * s - 0.5, (hi + 1) * 8 * s + 0.5, (20000, 3))
+    xw = (xs @ T[:3, :3].T + T[:3, 3]).astype(np.float32)
+    dist, st = sm.query(torch.from_numpy(xw).cuda())
+    dist, st = dist.cpu().numpy(), st.cpu().numpy()
+    vo, so = orc.query(b, E.astype(np.float64), s, T, xw)
+    assert np.array_equal(st, so)
+    ok = so != 2
+    assert np.allclose(dist[ok], vo[ok], atol=1e-4, rtol=0)
+    assert np.isnan(dist[~ok]).all()
+    assert (so == 0).sum() > 1000 and (so == 1).sum() > 10 and (so == 2).sum() > 100
+
+
+# ------------------------------------------------------------------------------------------ edges
+def test_edge_cases_and_errors(tiny):
+    from paper_2410_21149_b200 import CvxError, Submap
+    dev = torch.device("cuda", 0)
+    sm = Submap(tiny["grid"])
+    # empty frame: no-op; all-invalid frame counted
+    st = sm.integrate(torch.zeros((0, 3), device=dev), np.eye(4), dict(kind=0, min_range=0.1, max_range=5.0), stats=True)
+    assert st["rays_in"] == 0 and st["total_blocks"] == 0
+    bad = torch.full((33, 3), float("nan"), device=dev)
+    st = sm.integrate(bad, np.eye(4), dict(kind=0, min_range=0.1, max_range=5.0), stats=True)
+    assert st["skipped_invalid"] == 33 and st["total_blocks"] == 0
+    with pytest.raises(CvxError) as ei:
+        sm.query(torch.zeros((4, 3), device=dev))
+    assert ei.value.code == -4                 # query before finalize
+    sm.finalize_esdf()                          # empty submap finalizes
+    with pytest.raises(CvxError) as ei:
+        sm.integrate(torch.zeros((1, 3), device=dev), np.eye(4), dict(kind=0))
+    assert ei.value.code == -4                 # integrate after finalize
+    d, s = sm.query(torch.zeros((4, 3), device=dev))
+    assert (s.cpu().numpy() == 2).all()
+    # capacity overflow -> CVX_E_CAPACITY at the next synchronising call
+    small = Submap(dict(tiny["grid"], max_blocks=4))
+    small.integrate(tiny["frames"][0]["data"].to(dev), tiny["frames"][0]["T_world_sensor"], tiny["sensor"])
+    with pytest.raises(CvxError) as ei:
+        small.finalize_esdf()
+    assert ei.value.code == -3
+    # ray beyond the 21-bit key domain -> CVX_E_RANGE, ray skipped and counted
+    far = Submap(dict(voxel_size=0.001, truncation=0.003, max_blocks=1024))
+    pts = torch.tensor([[1.0, 0.0, 0.0], [9000.0, 0.0, 0.0]], device=dev)
+    with pytest.raises(CvxError) as ei:
+        far.integrate(pts, np.eye(4), dict(kind=0, min_range=0.0, max_range=1e6), stats=True)
+    assert ei.value.code == -6
+    # invalid arguments are rejected synchronously
+    with pytest.raises(CvxError):
+        Submap(dict(tiny["grid"], block_side=16))
+    T = np.eye(4)
+    T[0, 0] = 2.0
+    with pytest.raises(CvxError):
+        Submap(tiny["grid"], T)
+
+
+def test_reset_and_pack_roundtrip(tiny):
+    from paper_2410_21149_b200 import Submap, unpack
+    sm, _ = gpu_build(tiny, [0, 1, 2])
+    b, D, W, E = gpu_export_sorted(sm)
+    payload = unpack(sm.pack())
+    pb, pE = sort_blocks(payload["bxyz"], payload["E"])
+    assert np.array_equal(pb, b) and np.array_equal(pE.view(np.uint32), E.view(np.uint32))
+    assert np.allclose(payload["T_world_submap"], sm.T_ws)
+    # reset -> identical rebuild
+    sm.reset()
+    assert sm.block_count() == 0
+    dev = torch.device("cuda", 0)
+    for k in (0, 1, 2):
+        sm.integrate(tiny["frames"][k]["data"].to(dev), tiny["frames"][k]["T_world_sensor"], tiny["sensor"])
+    sm.finalize_esdf()
+    b2, D2, W2, E2 = gpu_export_sorted(sm)
+    assert np.array_equal(b2, b) and np.array_equal(D2.view(np.uint32), D.view(np.uint32))
+    assert np.array_equal(E2.view(np.uint32), E.view(np.uint32))
