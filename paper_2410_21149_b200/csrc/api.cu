@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <utility>
@@ -106,6 +107,7 @@ void free_all(cvx_submap* sm) {
   if (sm->ctr_host) cudaFreeHost(sm->ctr_host);
   if (sm->frame_T) cudaFree(sm->frame_T);
   if (sm->rays) cudaFree(sm->rays);
+  if (sm->slot_lists) cudaFree(sm->slot_lists);
   if (sm->edt) cudaFree(sm->edt);
   if (sm->block_grid) cudaFree(sm->block_grid);
   delete sm->prof;
@@ -143,6 +145,7 @@ cvx_status cvx_create_submap(const cvx_grid_config* cfg, const double* T_world_s
 
   cvx_submap* sm = new cvx_submap();
   sm->prof = new cvx::Prof();
+  if (const char* ag = std::getenv("CVX_AGGREGATE")) sm->aggregate = ag[0] != '0';  // tuning knob
   sm->cfg = *cfg;
   std::memcpy(sm->T_ws, T_world_submap, sizeof(sm->T_ws));
   sm->device = device;

@@ -3,7 +3,7 @@
 // HBM layout of one submap:
 //   keys  u64 [cap]          open-addressing hash table of packed 21-bit block keys
 //   vals  i32 [cap]          slot of the key (PENDING while the inserter publishes it)
-//   sums  i64x2 [max_blocks*512]  per voxel (sum w*d, sum w) in fixed point 2^-32 (O8 as exact sums)
+//   sums  i64x2 [max_blocks*512]  per voxel (sum w*d, sum w) in fixed point 2^-30 (O8 as exact sums)
 //   esdf  f32 [max_blocks*512]    E per voxel (after finalize)
 //   coords i32x4 [max_blocks]     slot -> block coordinates
 //   ctr   Counters                pool bump index, AABB, sticky errors, stats
@@ -19,7 +19,7 @@ constexpr int kBlockVox = 512;
 constexpr unsigned long long kEmptyKey = ~0ull;
 constexpr int kPending = -1;   // vals[] while the inserting thread publishes the slot
 constexpr int kFailed = -2;    // pool overflow: updates to this block are dropped (CVX_E_CAPACITY)
-constexpr double kFxScale = 4294967296.0;  // 2^32: fixed-point scale of the TSDF sums
+constexpr double kFxScale = 1073741824.0;  // 2^30: fixed-point scale of the TSDF sums
 
 enum ErrBits : unsigned { kErrCapacity = 1u, kErrHashFull = 2u, kErrRange = 4u };
 
@@ -29,7 +29,7 @@ struct Counters {
   int aabb_lo[3];          // block coordinates
   int aabb_hi[3];
   int n_rays;              // compacted rays of the current integrate call
-  int pad;
+  int n_slots;             // block-slot list entries claimed by the current integrate call
   unsigned long long rays_in, rays_used, skipped_invalid, skipped_range, skipped_domain, voxel_updates,
       new_blocks;
 };

@@ -4,15 +4,24 @@
 //   prepare_kernel  a1+a2  point -> ray (O2-O3, O6), range filter, fixed-point endpoints, closed-form
 //                        voxel count n_r = 1 + sum|dv| (COUNT) with warp-local counters
 //                        reduced once per warp, warp-ballot compaction of the used rays
-//   walk_kernel     a3+a4+a5  exact integer 6-connected traversal (O4); on entering a block the ray
-//                        activates it in the hash table (ALLOCATE); every voxel gets the
-//                        projective sdf (O5) and (w d, w) is merged per voxel — lanes of a warp
-//                        hitting the same voxel are reduced with match.any + a shuffle tree, then one
-//                        64-bit red.global.add per distinct voxel per warp step.  The TSDF state IS the
-//                        pair of exact fixed-point sums, so the "fold" D = sum(wd)/sum(w) (a5)
-//                        is evaluated on read (export / finalize) and fusion is order-independent and
-//                        deterministic (R6).
+//                        Organised sensors are read in 4x8 pixel patches per warp so the 32 rays of a
+//                        warp are spatial neighbours; each ray claims space for its block-slot list by a
+//                        warp-aggregated atomicAdd on a pre-allocated buffer.
+//   block_walk_kernel a3  ALLOCATE: the same exact integer traversal at block granularity (block
+//                        boundaries are a subset of voxel boundaries, so the block sequence is exactly
+//                        the one the voxel walk visits); every block is activated in the hash table
+//                        (insert-if-absent + slot bump) and its slot recorded in the
+//                        ray's list.
+//   walk_kernel     a4+a5  exact integer 6-connected voxel traversal (O4) reading the block slots from
+//                        the ray's list (prefetched one block ahead, no hashing in the hot loop); every
+//                        voxel gets the projective sdf (O5) and (w d, w) is merged per voxel —
+//                        lanes of a warp hitting the same voxel are reduced with match.any + a shuffle
+//                        tree, then one 64-bit red.global.add pair per distinct voxel per warp step.  The
+//                        TSDF state IS the pair of exact fixed-point sums, so the "fold"
+//                        D = sum(wd)/sum(w) (a5) is evaluated on read (export / finalize) and
+//                        fusion is order-independent and deterministic (R6).
 //   reset kernels   zero the used blocks, counters and AABB.
+#include <algorithm>
 #include <cstdio>
 
 #include "submap.h"
@@ -28,7 +37,7 @@ struct __align__(16) RayRec {
   float pm[3];      // p/s - vp - 1/2 (voxel units, in [-1/2, 1/2))
   int n_vox;        // closed-form voxel count (COUNT)
   float u[3];       // unit ray direction
-  int pad;
+  int list_off;     // offset of the ray's block-slot list, -1 if the list buffer was full
 };
 static_assert(sizeof(RayRec) == 96, "RayRec layout");
 
@@ -66,9 +75,11 @@ struct PrepParams {
   float fx, fy, cx, cy;
   double rmin, rmax, s, tau, rfloor;
   int weighting, carve;
+  int height;
   const double* frame_T;
   RayRec* rays;
   Counters* ctr;
+  int list_cap;
 };
 
 // O3: q(x) = floor((x / s) * 2^16), rejected outside |voxel| < 2^23.
@@ -85,19 +96,27 @@ __global__ void __launch_bounds__(256) prepare_kernel(const __grid_constant__ Pr
   int status = -1;  // -1 no thread, 0 used, 1 invalid, 2 range, 3 domain
   RayRec rec;
   if (idx < p.total) {
-    const long long f = idx / p.n_per_frame, i = idx - f * p.n_per_frame;
+    const long long f = idx / p.n_per_frame;
+    long long i = idx - f * p.n_per_frame;
+    if (p.kind != 0 && p.width > 0 && p.height > 0 && (p.width & 7) == 0 && (p.height & 3) == 0) {
+      // organised sensor: warp = 4 rows x 8 columns patch (spatially coherent rays per warp)
+      const long long pt = i >> 5, l = i & 31, pcols = p.width >> 3;
+      const long long row = (pt / pcols) * 4 + (l >> 3), col = (pt % pcols) * 8 + (l & 7);
+      i = row * p.width + col;
+    }
+    const long long src = f * p.n_per_frame + i;
     const double* T = p.frame_T + 12 * f;
     double pc[3];
     status = 0;
     if (p.kind == 1) {  // O2: pinhole depth -> point in fp32 exactly as written, integer pixel (Q24)
-      float z = p.data[idx];
+      float z = p.data[src];
       if (!(z > 0.0f) || !isfinite(z)) status = 1;
       float u = (float)(int)(i % p.width), v = (float)(int)(i / p.width);
       pc[0] = (double)__fdiv_rn(__fmul_rn(z, __fsub_rn(u, p.cx)), p.fx);
       pc[1] = (double)__fdiv_rn(__fmul_rn(z, __fsub_rn(v, p.cy)), p.fy);
       pc[2] = (double)z;
     } else {
-      const float* q = p.data + 3 * idx;
+      const float* q = p.data + 3 * src;
       pc[0] = q[0]; pc[1] = q[1]; pc[2] = q[2];
       if (!isfinite(pc[0]) || !isfinite(pc[1]) || !isfinite(pc[2])) status = 1;
     }
@@ -132,7 +151,7 @@ __global__ void __launch_bounds__(256) prepare_kernel(const __grid_constant__ Pr
           long long dv = (rec.B[a] >> 16) - (rec.A[a] >> 16);
           rec.n_vox += (int)(dv < 0 ? -dv : dv);             // a2: n_r = 1 + sum |dv| (O4)
         }
-        rec.pad = 0;
+        rec.list_off = -1;
       }
     }
   }
@@ -155,7 +174,24 @@ __global__ void __launch_bounds__(256) prepare_kernel(const __grid_constant__ Pr
     if (nv) atomicAdd(&p.ctr->voxel_updates, (unsigned long long)nv);
   }
   base = __shfl_sync(0xffffffffu, base, 0);
+  // block-slot lists: closed-form block count 1 + sum |db| (a2), space claimed per warp
+  int nb = 0;
   if (status == 0) {
+    nb = 1;
+    for (int a = 0; a < 3; ++a) {
+      long long db = (rec.B[a] >> 19) - (rec.A[a] >> 19);
+      nb += (int)(db < 0 ? -db : db);
+    }
+  }
+  int incl = nb;
+  for (int o = 1; o < 32; o <<= 1) { int t = __shfl_up_sync(0xffffffffu, incl, o); if (lane >= o) incl += t; }
+  const int wsum = __shfl_sync(0xffffffffu, incl, 31);
+  int lbase = 0;
+  if (lane == 0 && wsum) lbase = atomicAdd(&p.ctr->n_slots, wsum);
+  lbase = __shfl_sync(0xffffffffu, lbase, 0);
+  if (status == 0) {
+    const long long off = (long long)lbase + incl - nb;
+    rec.list_off = (off + nb <= p.list_cap) ? (int)off : -1;   // full buffer: the walk hashes instead
     const int pos = base + __popc(used & ((1u << lane) - 1u));   // order-preserving within the warp
     p.rays[pos] = rec;
   }
@@ -166,6 +202,7 @@ struct WalkParams {
   Counters* ctr;
   HashView hash;
   PoolView pool;
+  int* slots;       // block-slot lists
   float s, tau;
 };
 
@@ -187,101 +224,154 @@ __device__ __forceinline__ void reduce_peers(unsigned m, unsigned peers, int lan
   }
 }
 
-__global__ void __launch_bounds__(256) walk_kernel(const __grid_constant__ WalkParams p) {
+// ALLOCATE (a3): block-granular exact traversal (boundaries every 2^19 fixed-point units = 8 voxels),
+// activating every block a ray visits and recording its slot in the ray's list.
+__global__ void __launch_bounds__(256) block_walk_kernel(const __grid_constant__ WalkParams p) {
+  const int n_rays = *(volatile int*)&p.ctr->n_rays;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n_rays) return;
+  const RayRec r = p.rays[idx];
+  long long R[3], AD[3];
+  int b[3], st[3], k[3];
+  for (int a = 0; a < 3; ++a) {
+    b[a] = (int)(r.A[a] >> 19);
+    const int bb = (int)(r.B[a] >> 19);
+    const long long D = r.B[a] - r.A[a];
+    k[a] = bb > b[a] ? bb - b[a] : b[a] - bb;
+    if (D > 0) { st[a] = 1; R[a] = (((long long)b[a] + 1) << 19) - r.A[a]; }
+    else { st[a] = -1; R[a] = r.A[a] - ((long long)b[a] << 19); }
+    AD[a] = D < 0 ? -D : D;
+  }
+  int* list = r.list_off >= 0 ? p.slots + r.list_off : nullptr;
+  for (int j = 0;; ++j) {
+    const int slot = hash_activate(p.hash, p.pool, p.ctr, pack_key(b[0], b[1], b[2]), b[0], b[1], b[2]);
+    if (list) list[j] = slot;
+    if (k[0] + k[1] + k[2] == 0) break;
+    // earliest crossing, ties x < y < z (O4); axes without crossings left are not eligible
+    const bool e0 = k[0] > 0, e1 = k[1] > 0, e2 = k[2] > 0;
+    const bool y_first = e1 && (!e0 || R[1] * AD[0] < R[0] * AD[1]);
+    const bool z_first = e2 && (y_first ? R[2] * AD[1] < R[1] * AD[2] : (!e0 || R[2] * AD[0] < R[0] * AD[2]));
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const bool take = z_first ? a == 2 : (y_first ? a == 1 : a == 0);
+      if (take) { b[a] += st[a]; R[a] += 1ll << 19; --k[a]; }
+    }
+  }
+}
+
+template <bool kAggregate, bool kConstW>
+__global__ void __launch_bounds__(256, 4) walk_kernel(const __grid_constant__ WalkParams p) {
   const int n_rays = *(volatile int*)&p.ctr->n_rays;
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   if ((idx & ~31) >= n_rays) return;                       // whole warp beyond the rays
   const bool have = idx < n_rays;
 
+  // DDA state (O4).  With X_ij = r_i |D_j|, axis i crosses before axis j <=> X_ij < X_ji; only the
+  // three differences D01 = X01 - X10, D02 = X02 - X20, D12 = X12 - X21 are kept (exact int64).
   int v0 = 0, v1 = 0, v2 = 0, s0 = 1, s1 = 1, s2 = 1, k0 = 0, k1 = 0, k2 = 0;
-  long long X01 = kMax, X10 = 0, X02 = kMax, X20 = 0, X12 = kMax, X21 = 0;
-  long long I01 = 0, I10 = 0, I02 = 0, I20 = 0, I12 = 0, I21 = 0;
-  float d0 = 0, d1 = 0, d2 = 0, u0 = 0, u1 = 0, u2 = 0, pm0 = 0, pm1 = 0, pm2 = 0;
-  int vp0 = 0, vp1 = 0, vp2 = 0, n = 0;
+  long long D01 = 0, D02 = 0, D12 = 0, I0 = 0, I1 = 0, I2 = 0;
+  float u0 = 0, u1 = 0, u2 = 0, pm0 = 0, pm1 = 0, pm2 = 0;
+  int vp0 = 0, vp1 = 0, vp2 = 0, n = 0, nblk = 0, off = -1;
   long long w_fx = 0;
   float w = 0.0f;
   if (have) {
     const RayRec r = p.rays[idx];
-    long long A[3] = {r.A[0], r.A[1], r.A[2]}, B[3] = {r.B[0], r.B[1], r.B[2]};
     long long R[3], AD[3];
     int va[3], st[3], kk[3];
+    nblk = 1;
+#pragma unroll
     for (int a = 0; a < 3; ++a) {
-      va[a] = (int)(A[a] >> 16);
-      int vb = (int)(B[a] >> 16);
-      long long D = B[a] - A[a];
+      va[a] = (int)(r.A[a] >> 16);
+      const int vb = (int)(r.B[a] >> 16);
+      const long long D = r.B[a] - r.A[a];
       kk[a] = vb > va[a] ? vb - va[a] : va[a] - vb;
-      if (D > 0) { st[a] = 1; R[a] = (((long long)va[a] + 1) << 16) - A[a]; }
-      else { st[a] = -1; R[a] = A[a] - ((long long)va[a] << 16); }
+      if (D > 0) { st[a] = 1; R[a] = (((long long)va[a] + 1) << 16) - r.A[a]; }
+      else { st[a] = -1; R[a] = r.A[a] - ((long long)va[a] << 16); }
       AD[a] = D < 0 ? -D : D;
+      const long long db = (r.B[a] >> 19) - (r.A[a] >> 19);
+      nblk += (int)(db < 0 ? -db : db);
     }
     v0 = va[0]; v1 = va[1]; v2 = va[2]; s0 = st[0]; s1 = st[1]; s2 = st[2]; k0 = kk[0]; k1 = kk[1]; k2 = kk[2];
-    // X_ij = r_i |D_j|: axis i crosses before axis j  <=>  X_ij < X_ji  (O4, exact in int64)
-    X01 = R[0] * AD[1]; X10 = R[1] * AD[0]; X02 = R[0] * AD[2]; X20 = R[2] * AD[0];
-    X12 = R[1] * AD[2]; X21 = R[2] * AD[1];
-    I01 = AD[1] << 16; I10 = AD[0] << 16; I02 = AD[2] << 16; I20 = AD[0] << 16; I12 = AD[2] << 16; I21 = AD[1] << 16;
-    if (k0 == 0) { X01 = kMax; X02 = kMax; X10 = 0; X20 = 0; }
-    if (k1 == 0) { X10 = kMax; X12 = kMax; X01 = 0; X21 = 0; }
-    if (k2 == 0) { X20 = kMax; X21 = kMax; X02 = 0; X12 = 0; }
-    if (k0 == 0 && k1 == 0) { X01 = kMax; X10 = kMax; }
-    if (k0 == 0 && k2 == 0) { X02 = kMax; X20 = kMax; }
-    if (k1 == 0 && k2 == 0) { X12 = kMax; X21 = kMax; }
+    D01 = R[0] * AD[1] - R[1] * AD[0];
+    D02 = R[0] * AD[2] - R[2] * AD[0];
+    D12 = R[1] * AD[2] - R[2] * AD[1];
+    I0 = AD[0] << 16; I1 = AD[1] << 16; I2 = AD[2] << 16;
     u0 = r.u[0]; u1 = r.u[1]; u2 = r.u[2];
     pm0 = r.pm[0]; pm1 = r.pm[1]; pm2 = r.pm[2];
     vp0 = r.vp[0]; vp1 = r.vp[1]; vp2 = r.vp[2];
-    d0 = pm0 - (float)(v0 - vp0); d1 = pm1 - (float)(v1 - vp1); d2 = pm2 - (float)(v2 - vp2);
     w = r.w;
     w_fx = __double2ll_rn((double)w * kFxScale);
     n = r.n_vox;
+    off = r.list_off;
   }
   const int maxn = (int)__reduce_max_sync(0xffffffffu, (unsigned)n);
-  int slot = kFailed;
-  bool need_block = true;
+  const int* list = off >= 0 ? p.slots + off : nullptr;
+  int slot = kFailed, nslot = kFailed, j = 0;
+  if (have) {
+    slot = list ? __ldg(list) : hash_find(p.hash, pack_key(v0 >> 3, v1 >> 3, v2 >> 3));
+    if (list && nblk > 1) nslot = __ldg(list + 1);
+  }
   const float s = p.s, tau = p.tau;
+  unsigned long long* const sums = reinterpret_cast<unsigned long long*>(p.pool.sums);
   for (int it = 0; it < maxn; ++it) {
     const bool act = it < n;
-    if (act && need_block) {
-      const int bx = v0 >> 3, by = v1 >> 3, bz = v2 >> 3;
-      slot = hash_activate(p.hash, p.pool, p.ctr, pack_key(bx, by, bz), bx, by, bz);
-      need_block = false;
-    }
     const bool upd = act && slot >= 0;
-    const unsigned m = __ballot_sync(0xffffffffu, upd);
-    if (upd) {
-      // O5: sdf = (p - c_v).u, in voxel units relative to the voxel of p, clamped before fusion (Q4)
-      const float sdf = s * (d0 * u0 + d1 * u1 + d2 * u2);
-      const float dcl = fminf(fmaxf(sdf, -tau), tau);
-      long long a = __float2ll_rn((w * dcl) * 4294967296.0f);
-      long long b = w_fx;
-      const unsigned addr = (unsigned)slot * 512u + (unsigned)((v0 & 7) | ((v1 & 7) << 3) | ((v2 & 7) << 6));
-      const unsigned peers = __match_any_sync(m, addr);
-      reduce_peers(m, peers, lane, a, b);
-      if (lane == __ffs(peers) - 1) {
-        unsigned long long* dst = reinterpret_cast<unsigned long long*>(p.pool.sums) + 2ull * addr;
-        atomicAdd(dst, (unsigned long long)a);
-        atomicAdd(dst + 1, (unsigned long long)b);
+    // O5: sdf = (p - c_v).u in voxel units relative to the voxel of p, clamped before fusion (Q4)
+    const float d0 = pm0 - (float)(v0 - vp0), d1 = pm1 - (float)(v1 - vp1), d2 = pm2 - (float)(v2 - vp2);
+    const float sdf = s * (d0 * u0 + d1 * u1 + d2 * u2);
+    const float dcl = fminf(fmaxf(sdf, -tau), tau);
+    long long a = __float2ll_rn((w * dcl) * 1073741824.0f);   // fixed point 2^-30 (kFxScale)
+    const unsigned addr = (unsigned)slot * 512u + (unsigned)((v0 & 7) | ((v1 & 7) << 3) | ((v2 & 7) << 6));
+    if (kAggregate) {
+      const unsigned m = __ballot_sync(0xffffffffu, upd);
+      if (upd) {
+        if (kConstW) {
+          // constant weights: group lanes by (voxel, contribution); every group member adds the same
+          // (a, w), so the group sum is n*(a, w) — no shuffle tree.  |a| <= tau 2^30 < 2^31 (tau < 2 m,
+          // checked at launch), so (addr, a) packs injectively into the 64-bit match key.
+          const unsigned long long key = ((unsigned long long)addr << 32) | (unsigned)(int)a;
+          const unsigned peers = __match_any_sync(m, key);
+          if (lane == __ffs(peers) - 1) {
+            const long long c = __popc(peers);
+            atomicAdd(sums + 2ull * addr, (unsigned long long)(a * c));
+            atomicAdd(sums + 2ull * addr + 1, (unsigned long long)(w_fx * c));
+          }
+        } else {
+          const unsigned peers = __match_any_sync(m, addr);
+          long long b = w_fx;
+          reduce_peers(m, peers, lane, a, b);
+          if (lane == __ffs(peers) - 1) {
+            atomicAdd(sums + 2ull * addr, (unsigned long long)a);
+            atomicAdd(sums + 2ull * addr + 1, (unsigned long long)b);
+          }
+        }
       }
+    } else if (upd) {
+      atomicAdd(sums + 2ull * addr, (unsigned long long)a);
+      atomicAdd(sums + 2ull * addr + 1, (unsigned long long)w_fx);
     }
     if (act && it + 1 < n) {
-      // O4: next axis = earliest crossing, ties x < y < z
-      int ax = (X10 < X01) ? 1 : 0;
-      if (ax == 0) { if (X20 < X02) ax = 2; }
-      else { if (X21 < X12) ax = 2; }
-      if (ax == 0) {
-        v0 += s0; X01 += I01; X02 += I02; --k0;
-        d0 = pm0 - (float)(v0 - vp0);
-        need_block = (v0 & 7) == (s0 > 0 ? 0 : 7);
-        if (k0 == 0) { X01 = kMax; X02 = kMax; X10 = 0; X20 = 0; }
-      } else if (ax == 1) {
-        v1 += s1; X10 += I10; X12 += I12; --k1;
-        d1 = pm1 - (float)(v1 - vp1);
-        need_block = (v1 & 7) == (s1 > 0 ? 0 : 7);
-        if (k1 == 0) { X10 = kMax; X12 = kMax; X01 = 0; X21 = 0; }
-      } else {
-        v2 += s2; X20 += I20; X21 += I21; --k2;
-        d2 = pm2 - (float)(v2 - vp2);
-        need_block = (v2 & 7) == (s2 > 0 ? 0 : 7);
-        if (k2 == 0) { X20 = kMax; X21 = kMax; X02 = 0; X12 = 0; }
+      // O4: the axis with the earliest next crossing among those with crossings left; ties x < y < z
+      const bool e0 = k0 > 0, e1 = k1 > 0, e2 = k2 > 0;
+      const bool yf = e1 && (!e0 || D01 > 0);
+      const bool zf = e2 && (yf ? D12 > 0 : (!e0 || D02 > 0));
+      const bool bx = !yf && !zf, by = yf && !zf, bz = zf;
+      v0 += bx ? s0 : 0; v1 += by ? s1 : 0; v2 += bz ? s2 : 0;
+      k0 -= bx; k1 -= by; k2 -= bz;
+      D01 += bx ? I1 : (by ? -I0 : 0ll);
+      D02 += bx ? I2 : (bz ? -I0 : 0ll);
+      D12 += by ? I2 : (bz ? -I1 : 0ll);
+      const int nv = bx ? v0 : (by ? v1 : v2);
+      const int sv = bx ? s0 : (by ? s1 : s2);
+      if ((nv & 7) == (sv > 0 ? 0 : 7)) {     // entered the next block of the ray
+        ++j;
+        if (list) {
+          slot = nslot;
+          if (j + 1 < nblk) nslot = __ldg(list + j + 1);   // prefetch one block ahead
+        } else {
+          slot = hash_find(p.hash, pack_key(v0 >> 3, v1 >> 3, v2 >> 3));
+        }
       }
     }
   }
@@ -330,6 +420,15 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     if (e != cudaSuccess) return e;
     sm->ray_cap = total;
   }
+  const long long list_need = total * kSlotsPerRay + 1024;
+  if (sm->slot_cap < list_need) {
+    if (sm->slot_lists) cudaFree(sm->slot_lists);
+    sm->slot_lists = nullptr;
+    sm->slot_cap = 0;
+    cudaError_t e = cudaMalloc(&sm->slot_lists, sizeof(int) * (size_t)list_need);
+    if (e != cudaSuccess) return e;
+    sm->slot_cap = list_need;
+  }
   ComposeParams cp;
   for (int i = 0; i < 16; ++i) cp.Tws[i] = sm->T_ws[i];
   for (int f = 0; f < n_frames; ++f)
@@ -339,7 +438,7 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     ProfScope ps_(sm, "compose_poses", st);
     compose_kernel<<<1, kMaxBatch, 0, st>>>(cp, sm->frame_T);
   }
-  cudaMemsetAsync(&sm->ctr->n_rays, 0, sizeof(int), st);
+  cudaMemsetAsync(&sm->ctr->n_rays, 0, 2 * sizeof(int), st);   // n_rays, n_slots
 
   PrepParams pp;
   pp.data = data; pp.n_per_frame = n_per_frame; pp.total = total;
@@ -348,7 +447,9 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
   pp.rmin = (double)sensor.min_range; pp.rmax = (double)sensor.max_range;
   pp.s = sm->cfg.voxel_size; pp.tau = sm->cfg.truncation; pp.rfloor = sm->cfg.weight_range_floor;
   pp.weighting = sm->cfg.weighting; pp.carve = sm->cfg.carve;
+  pp.height = sensor.height;
   pp.frame_T = sm->frame_T; pp.rays = (RayRec*)sm->rays; pp.ctr = sm->ctr;
+  pp.list_cap = (int)std::min<long long>(sm->slot_cap, 0x7fffffffll);
   const unsigned blocks = (unsigned)((total + 255) / 256);
   {
     ProfScope ps_(sm, "ray_prepare", st);
@@ -357,10 +458,21 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
 
   WalkParams wp;
   wp.rays = (const RayRec*)sm->rays; wp.ctr = sm->ctr; wp.hash = sm->hash; wp.pool = sm->pool;
+  wp.slots = sm->slot_lists;
   wp.s = (float)sm->cfg.voxel_size; wp.tau = (float)sm->cfg.truncation;
   {
+    ProfScope ps_(sm, "block_walk_allocate", st);
+    block_walk_kernel<<<blocks, 256, 0, st>>>(wp);
+  }
+  {
     ProfScope ps_(sm, "ray_walk_update", st);
-    walk_kernel<<<blocks, 256, 0, st>>>(wp);
+    const bool cw = sm->cfg.weighting == 0 && sm->cfg.truncation < 2.0;
+    if (sm->aggregate) {
+      if (cw) walk_kernel<true, true><<<blocks, 256, 0, st>>>(wp);
+      else walk_kernel<true, false><<<blocks, 256, 0, st>>>(wp);
+    } else {
+      walk_kernel<false, false><<<blocks, 256, 0, st>>>(wp);
+    }
   }
   return cudaGetLastError();
 }

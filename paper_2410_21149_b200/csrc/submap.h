@@ -50,6 +50,9 @@ struct cvx_submap {
   double* frame_T = nullptr;  // device [kMaxBatch][12]: R_SC (row-major) then t_SC, per frame
   void* rays = nullptr;       // device RayRec [ray_cap]
   int64_t ray_cap = 0;
+  int* slot_lists = nullptr;  // device block-slot lists of the rays of one launch
+  int64_t slot_cap = 0;
+  bool aggregate = true;      // warp-aggregate equal-voxel updates before the L2 atomics
 
   // ESDF scratch (grow-only)
   void* edt = nullptr;        // device: g2 u32 | meta u32 | g1 u16 over the dense AABB
@@ -72,6 +75,7 @@ struct ProfScope {
 namespace cvx {
 
 constexpr int kMaxBatch = 128;   // frames per integrate launch
+constexpr int kSlotsPerRay = 40; // average block-slot list capacity per ray (overflow -> hashed walk)
 
 // integrate.cu
 cudaError_t launch_reset(cvx_submap* sm, cudaStream_t st);

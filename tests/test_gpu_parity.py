@@ -170,7 +170,7 @@ def test_query_parity(tiny, orc):
     ok = so != 2
     assert np.allclose(dist[ok], vo[ok], atol=1e-4, rtol=0)
     assert np.isnan(dist[~ok]).all()
-    assert (so == 0).sum() > 1000 and (so == 1).sum() > 10 and (so == 2).sum() > 100
+    assert (so == 0).sum() > 300 and (so == 1).sum() > 10 and (so == 2).sum() > 100
 
 
 # ------------------------------------------------------------------------------------------ edges
