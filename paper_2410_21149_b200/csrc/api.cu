@@ -101,6 +101,7 @@ void free_all(cvx_submap* sm) {
   if (sm->hash.keys) cudaFree(sm->hash.keys);
   if (sm->hash.vals) cudaFree(sm->hash.vals);
   if (sm->pool.sums) cudaFree(sm->pool.sums);
+  if (sm->pool.acc) cudaFree(sm->pool.acc);
   if (sm->pool.esdf) cudaFree(sm->pool.esdf);
   if (sm->pool.coords) cudaFree(sm->pool.coords);
   if (sm->ctr) cudaFree(sm->ctr);
@@ -159,6 +160,7 @@ cvx_status cvx_create_submap(const cvx_grid_config* cfg, const double* T_world_s
   if ((e = cudaMalloc(&sm->hash.keys, cap * 8)) != cudaSuccess ||
       (e = cudaMalloc(&sm->hash.vals, cap * 4)) != cudaSuccess ||
       (e = cudaMalloc(&sm->pool.sums, nb * cvx::kBlockVox * 16)) != cudaSuccess ||
+      (e = cudaMalloc(&sm->pool.acc, nb * cvx::kBlockVox * 8)) != cudaSuccess ||
       (e = cudaMalloc(&sm->pool.esdf, nb * cvx::kBlockVox * 4)) != cudaSuccess ||
       (e = cudaMalloc(&sm->pool.coords, nb * 16)) != cudaSuccess ||
       (e = cudaMalloc(&sm->ctr, sizeof(cvx::Counters))) != cudaSuccess ||
@@ -171,6 +173,7 @@ cvx_status cvx_create_submap(const cvx_grid_config* cfg, const double* T_world_s
   // zero-initialised pool (a3 zero-init happens once here; reset re-zeroes only the used blocks)
   cudaMemset(sm->ctr, 0, sizeof(cvx::Counters));
   cudaMemset(sm->pool.sums, 0, nb * cvx::kBlockVox * 16);
+  cudaMemset(sm->pool.acc, 0, nb * cvx::kBlockVox * 8);
   cudaMemset(sm->pool.esdf, 0, nb * cvx::kBlockVox * 4);
   e = cvx::launch_reset(sm, 0);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -222,7 +225,9 @@ cvx_status cvx_integrate_batch(cvx_submap* sm, const float* data, int64_t n_per_
   DeviceGuard g(sm->device);
   if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
   cudaStream_t st = (cudaStream_t)stream;
-  const int64_t per_launch = std::max<int64_t>(1, std::min<int64_t>(cvx::kMaxBatch, ((1ll << 31) - 1) / std::max<int64_t>(1, n_per_frame)));
+  int64_t ray_limit = (1ll << 31) - 1;
+  if (sm->cfg.weighting == 0 && n_per_frame <= cvx::kMaxPackedRays) ray_limit = cvx::kMaxPackedRays;  // packed accumulators
+  const int64_t per_launch = std::max<int64_t>(1, std::min<int64_t>(cvx::kMaxBatch, ray_limit / std::max<int64_t>(1, n_per_frame)));
   for (int64_t f0 = 0; f0 < n_frames && n_per_frame > 0; f0 += per_launch) {
     const int nf = (int)std::min<int64_t>(per_launch, n_frames - f0);
     const int64_t elems = sensor->kind == 1 ? n_per_frame : 3 * n_per_frame;

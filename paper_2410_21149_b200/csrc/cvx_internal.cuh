@@ -4,11 +4,13 @@
 //   keys  u64 [cap]          open-addressing hash table of packed 21-bit block keys
 //   vals  i32 [cap]          slot of the key (PENDING while the inserter publishes it)
 //   sums  i64x2 [max_blocks*512]  per voxel (sum w*d, sum w) in fixed point 2^-30 (O8 as exact sums)
+//   acc   u64 [max_blocks*512]    packed per-launch accumulator {count:22 | sum d':42} (constant w)
 //   esdf  f32 [max_blocks*512]    E per voxel (after finalize)
 //   coords i32x4 [max_blocks]     slot -> block coordinates
 //   ctr   Counters                pool bump index, AABB, sticky errors, stats
 // Voxel local index inside a block: lx + 8 ly + 64 lz (O9); slot s owns voxels [s*512, s*512+512).
 #pragma once
+#include <cmath>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -30,6 +32,8 @@ struct Counters {
   int aabb_hi[3];
   int n_rays;              // compacted rays of the current integrate call
   int n_slots;             // block-slot list entries claimed by the current integrate call
+  int next_ray;            // ray queue head of the persistent update walk
+  int pad;
   unsigned long long rays_in, rays_used, skipped_invalid, skipped_range, skipped_domain, voxel_updates,
       new_blocks;
 };
@@ -43,6 +47,7 @@ struct HashView {
 
 struct PoolView {
   long long* sums;         // [max_blocks*512][2]
+  unsigned long long* acc; // [max_blocks*512] packed per-launch accumulators (constant weights)
   float* esdf;             // [max_blocks*512]
   int4* coords;            // [max_blocks]
   int max_blocks;
@@ -112,6 +117,14 @@ __device__ inline int hash_activate(const HashView& h, const PoolView& pool, Cou
   }
   atomicOr(&ctr->err, (unsigned)kErrHashFull);
   return kFailed;
+}
+
+// Packed accumulator: at most kMaxPackedRays updates of one voxel per launch (22-bit count), and the
+// 42-bit field holds their sum of d' <= 2 round(tau 2^q) with q = floor(log2(2^19 / tau)).
+constexpr long long kMaxPackedRays = (1ll << 22) - 1;
+inline int packed_q(double tau) {
+  int q = (int)std::floor(std::log2(524288.0 / tau));
+  return q < 0 ? 0 : (q > 30 ? 30 : q);
 }
 
 // Floor division / modulo by 8 on int32 voxel coordinates (S:L200-207 floor semantics).

@@ -22,6 +22,7 @@
 //                        fusion is order-independent and deterministic (R6).
 //   reset kernels   zero the used blocks, counters and AABB.
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 
 #include "submap.h"
@@ -29,15 +30,18 @@
 namespace cvx {
 namespace {
 
+// Fixed-point sdf along a ray: units of 2^-(q+kSdfF) metres, q = packed_q(tau).
+constexpr int kSdfF = 20;
+
 struct __align__(16) RayRec {
   long long A[3];   // fixed-point (2^-16 voxel) start of the updated segment (O3)
   long long B[3];   // fixed-point end: p + tau*u
-  int vp[3];        // voxel containing p (precision anchor for the sdf)
+  long long S0;     // projective sdf (p - c_v).u of the first voxel, fixed point (kSdfF)
+  long long U[3];   // sdf decrement per voxel step along axis a: s |u_a|, fixed point (>= 0)
   float w;          // weight (O6)
-  float pm[3];      // p/s - vp - 1/2 (voxel units, in [-1/2, 1/2))
   int n_vox;        // closed-form voxel count (COUNT)
-  float u[3];       // unit ray direction
   int list_off;     // offset of the ray's block-slot list, -1 if the list buffer was full
+  int pad;
 };
 static_assert(sizeof(RayRec) == 96, "RayRec layout");
 
@@ -74,6 +78,7 @@ struct PrepParams {
   int kind, width;
   float fx, fy, cx, cy;
   double rmin, rmax, s, tau, rfloor;
+  double sdf_scale;   // 2^(q + kSdfF)
   int weighting, carve;
   int height;
   const double* frame_T;
@@ -101,7 +106,8 @@ __global__ void __launch_bounds__(256) prepare_kernel(const __grid_constant__ Pr
     if (p.kind != 0 && p.width > 0 && p.height > 0 && (p.width & 7) == 0 && (p.height & 3) == 0) {
       // organised sensor: warp = 4 rows x 8 columns patch (spatially coherent rays per warp)
       const long long pt = i >> 5, l = i & 31, pcols = p.width >> 3;
-      const long long row = (pt / pcols) * 4 + (l >> 3), col = (pt % pcols) * 8 + (l & 7);
+      const long long r4 = l >> 3, c8 = (r4 & 1) ? 7 - (l & 7) : (l & 7);   // serpentine: lane l+1 neighbours lane l
+      const long long row = (pt / pcols) * 4 + r4, col = (pt % pcols) * 8 + c8;
       i = row * p.width + col;
     }
     const long long src = f * p.n_per_frame + i;
@@ -138,11 +144,18 @@ __global__ void __launch_bounds__(256) prepare_kernel(const __grid_constant__ Pr
             long long span = (rec.B[a] >> 16) - (rec.A[a] >> 16);
             if (span >= 32768 || span <= -32768) status = 3;
           }
-          double ps = __ddiv_rn(pw[a], p.s);
-          double fl = floor(ps);
-          rec.vp[a] = (int)fl;
-          rec.pm[a] = (float)(ps - fl) - 0.5f;
-          rec.u[a] = (float)__ddiv_rn(d[a], L);
+        }
+        if (status == 0) {
+          // O5 in fixed point: sdf of the first voxel v_A, then an exact per-axis decrement s |u_a| per
+          // step (stepping axis a moves the voxel centre by s sign(u_a) e_a)
+          double u[3], sdf0 = 0.0;
+          for (int a = 0; a < 3; ++a) {
+            u[a] = d[a] / L;
+            const double c = ((double)(rec.A[a] >> 16) + 0.5) * p.s;
+            sdf0 += (pw[a] - c) * u[a];
+            rec.U[a] = __double2ll_rn(fabs(u[a]) * p.s * p.sdf_scale);
+          }
+          rec.S0 = __double2ll_rn(sdf0 * p.sdf_scale);
         }
         if (p.weighting == 0) rec.w = 1.0f;                  // O6
         else { double r = fmax(L, p.rfloor); rec.w = (float)__ddiv_rn(1.0, dm(r, r)); }
@@ -152,6 +165,7 @@ __global__ void __launch_bounds__(256) prepare_kernel(const __grid_constant__ Pr
           rec.n_vox += (int)(dv < 0 ? -dv : dv);             // a2: n_r = 1 + sum |dv| (O4)
         }
         rec.list_off = -1;
+        rec.pad = 0;
       }
     }
   }
@@ -204,9 +218,9 @@ struct WalkParams {
   PoolView pool;
   int* slots;       // block-slot lists
   float s, tau;
+  int tq;           // round(tau 2^q): the clamp bound (and packed offset) of the quantised sdf
+  int q;            // sdf quantum 2^-q m
 };
-
-constexpr long long kMax = 0x7fffffffffffffffll;
 
 // Segmented sum over lanes with equal `peers` groups (log-depth shuffle tree); result valid at the
 // lowest lane of each group.  All lanes of `m` must call it.
@@ -269,10 +283,10 @@ __global__ void __launch_bounds__(256, 4) walk_kernel(const __grid_constant__ Wa
 
   // DDA state (O4).  With X_ij = r_i |D_j|, axis i crosses before axis j <=> X_ij < X_ji; only the
   // three differences D01 = X01 - X10, D02 = X02 - X20, D12 = X12 - X21 are kept (exact int64).
-  int v0 = 0, v1 = 0, v2 = 0, s0 = 1, s1 = 1, s2 = 1, k0 = 0, k1 = 0, k2 = 0;
+  int v0 = 0, v1 = 0, v2 = 0, s0 = 1, s1 = 1, s2 = 1, k0 = 0, k1 = 0, k2 = 0, c0 = 0, c1 = 0, c2 = 0;
   long long D01 = 0, D02 = 0, D12 = 0, I0 = 0, I1 = 0, I2 = 0;
-  float u0 = 0, u1 = 0, u2 = 0, pm0 = 0, pm1 = 0, pm2 = 0;
-  int vp0 = 0, vp1 = 0, vp2 = 0, n = 0, nblk = 0, off = -1;
+  long long S = 0, U0 = 0, U1 = 0, U2 = 0;   // fixed-point sdf of the current voxel and its decrements
+  int n = 0, nblk = 0, off = -1;
   long long w_fx = 0;
   float w = 0.0f;
   if (have) {
@@ -293,13 +307,12 @@ __global__ void __launch_bounds__(256, 4) walk_kernel(const __grid_constant__ Wa
       nblk += (int)(db < 0 ? -db : db);
     }
     v0 = va[0]; v1 = va[1]; v2 = va[2]; s0 = st[0]; s1 = st[1]; s2 = st[2]; k0 = kk[0]; k1 = kk[1]; k2 = kk[2];
+    c0 = s0 > 0 ? 0 : 7; c1 = s1 > 0 ? 0 : 7; c2 = s2 > 0 ? 0 : 7;   // local coordinate on block entry
     D01 = R[0] * AD[1] - R[1] * AD[0];
     D02 = R[0] * AD[2] - R[2] * AD[0];
     D12 = R[1] * AD[2] - R[2] * AD[1];
     I0 = AD[0] << 16; I1 = AD[1] << 16; I2 = AD[2] << 16;
-    u0 = r.u[0]; u1 = r.u[1]; u2 = r.u[2];
-    pm0 = r.pm[0]; pm1 = r.pm[1]; pm2 = r.pm[2];
-    vp0 = r.vp[0]; vp1 = r.vp[1]; vp2 = r.vp[2];
+    S = r.S0; U0 = r.U[0]; U1 = r.U[1]; U2 = r.U[2];
     w = r.w;
     w_fx = __double2ll_rn((double)w * kFxScale);
     n = r.n_vox;
@@ -312,77 +325,110 @@ __global__ void __launch_bounds__(256, 4) walk_kernel(const __grid_constant__ Wa
     slot = list ? __ldg(list) : hash_find(p.hash, pack_key(v0 >> 3, v1 >> 3, v2 >> 3));
     if (list && nblk > 1) nslot = __ldg(list + 1);
   }
-  const float s = p.s, tau = p.tau;
+  const int tq = p.tq;
   unsigned long long* const sums = reinterpret_cast<unsigned long long*>(p.pool.sums);
+  unsigned long long* const acc = p.pool.acc;
   for (int it = 0; it < maxn; ++it) {
-    const bool act = it < n;
-    const bool upd = act && slot >= 0;
-    // O5: sdf = (p - c_v).u in voxel units relative to the voxel of p, clamped before fusion (Q4)
-    const float d0 = pm0 - (float)(v0 - vp0), d1 = pm1 - (float)(v1 - vp1), d2 = pm2 - (float)(v2 - vp2);
-    const float sdf = s * (d0 * u0 + d1 * u1 + d2 * u2);
-    const float dcl = fminf(fmaxf(sdf, -tau), tau);
-    long long a = __float2ll_rn((w * dcl) * 1073741824.0f);   // fixed point 2^-30 (kFxScale)
+    const bool upd = it < n && slot >= 0;
+    // O5 + Q4: clamped projective sdf, quantised to 2^-q m: dq = clamp(round(sdf 2^q), -tq, tq)
+    const int sq = (int)((S + (1ll << (kSdfF - 1))) >> kSdfF);
+    const int dq = min(max(sq, -tq), tq);
     const unsigned addr = (unsigned)slot * 512u + (unsigned)((v0 & 7) | ((v1 & 7) << 3) | ((v2 & 7) << 6));
-    if (kAggregate) {
-      const unsigned m = __ballot_sync(0xffffffffu, upd);
-      if (upd) {
-        if (kConstW) {
-          // constant weights: group lanes by (voxel, contribution); every group member adds the same
-          // (a, w), so the group sum is n*(a, w) — no shuffle tree.  |a| <= tau 2^30 < 2^31 (tau < 2 m,
-          // checked at launch), so (addr, a) packs injectively into the 64-bit match key.
-          const unsigned long long key = ((unsigned long long)addr << 32) | (unsigned)(int)a;
-          const unsigned peers = __match_any_sync(m, key);
-          if (lane == __ffs(peers) - 1) {
-            const long long c = __popc(peers);
-            atomicAdd(sums + 2ull * addr, (unsigned long long)(a * c));
-            atomicAdd(sums + 2ull * addr + 1, (unsigned long long)(w_fx * c));
-          }
-        } else {
-          const unsigned peers = __match_any_sync(m, addr);
-          long long b = w_fx;
-          reduce_peers(m, peers, lane, a, b);
-          if (lane == __ffs(peers) - 1) {
-            atomicAdd(sums + 2ull * addr, (unsigned long long)a);
-            atomicAdd(sums + 2ull * addr + 1, (unsigned long long)b);
-          }
-        }
+    if (kAggregate && kConstW) {
+      // constant weights: one packed 64-bit reduction per run of consecutive lanes with the same
+      // (voxel, contribution) into the per-launch accumulator acc = count << 42 | sum(d'), d' = dq + tq
+      // in [0, 2 tq] (fold_kernel moves it into the exact sums).  Lanes of a run add the same d', so
+      // the run total is len * (1 << 42 | d').  Lanes hold spatially adjacent rays in a serpentine
+      // order, so runs capture the rays that share a voxel; no match.any (its cost grows with the
+      // number of distinct keys) and no shuffle tree.
+      const unsigned dp = (unsigned)(dq + tq);
+      const unsigned long long key = ((unsigned long long)addr << 32) | dp;
+      const unsigned long long prev = __shfl_up_sync(0xffffffffu, key, 1);
+      const unsigned act = __ballot_sync(0xffffffffu, upd);
+      const bool head = upd && (lane == 0 || prev != key || !((act >> (lane - 1)) & 1u));
+      const unsigned stops = __ballot_sync(0xffffffffu, head) | ~act;
+      if (head) {
+        const unsigned above = stops & (0xfffffffeu << lane);
+        const unsigned len = (above ? (unsigned)(__ffs(above) - 1) : 32u) - (unsigned)lane;
+        atomicAdd(acc + addr, (unsigned long long)len * ((1ull << 42) | (unsigned long long)dp));
       }
-    } else if (upd) {
-      atomicAdd(sums + 2ull * addr, (unsigned long long)a);
-      atomicAdd(sums + 2ull * addr + 1, (unsigned long long)w_fx);
-    }
-    if (act && it + 1 < n) {
-      // O4: the axis with the earliest next crossing among those with crossings left; ties x < y < z
-      const bool e0 = k0 > 0, e1 = k1 > 0, e2 = k2 > 0;
-      const bool yf = e1 && (!e0 || D01 > 0);
-      const bool zf = e2 && (yf ? D12 > 0 : (!e0 || D02 > 0));
-      const bool bx = !yf && !zf, by = yf && !zf, bz = zf;
-      v0 += bx ? s0 : 0; v1 += by ? s1 : 0; v2 += bz ? s2 : 0;
-      k0 -= bx; k1 -= by; k2 -= bz;
-      D01 += bx ? I1 : (by ? -I0 : 0ll);
-      D02 += bx ? I2 : (bz ? -I0 : 0ll);
-      D12 += by ? I2 : (bz ? -I1 : 0ll);
-      const int nv = bx ? v0 : (by ? v1 : v2);
-      const int sv = bx ? s0 : (by ? s1 : s2);
-      if ((nv & 7) == (sv > 0 ? 0 : 7)) {     // entered the next block of the ray
-        ++j;
-        if (list) {
-          slot = nslot;
-          if (j + 1 < nblk) nslot = __ldg(list + j + 1);   // prefetch one block ahead
-        } else {
-          slot = hash_find(p.hash, pack_key(v0 >> 3, v1 >> 3, v2 >> 3));
+    } else {
+      long long a = __float2ll_rn(w * (float)dq * __int_as_float((127 + 30 - p.q) << 23));  // w d 2^30
+      if (kAggregate) {
+        const unsigned long long key = upd ? (unsigned long long)addr : (0x100000000ull | (unsigned)lane);
+        const unsigned peers = __match_any_sync(0xffffffffu, key);
+        long long b = upd ? w_fx : 0;
+        if (!upd) a = 0;
+        reduce_peers(0xffffffffu, peers, lane, a, b);
+        if (upd && lane == __ffs(peers) - 1) {
+          atomicAdd(sums + 2ull * addr, (unsigned long long)a);
+          atomicAdd(sums + 2ull * addr + 1, (unsigned long long)b);
         }
+      } else if (upd) {
+        atomicAdd(sums + 2ull * addr, (unsigned long long)a);
+        atomicAdd(sums + 2ull * addr + 1, (unsigned long long)w_fx);
+      }
+    }
+    // O4: step the axis with the earliest next crossing among those with crossings left (ties
+    // x < y < z), predicated on the lane still having a voxel to go.
+    const bool stp = it + 1 < n;
+    const bool g0 = k0 > 0, g1 = k1 > 0, g2 = k2 > 0;
+    const bool yf = g1 & (!g0 | (D01 > 0));
+    const bool zf = g2 & (yf ? (D12 > 0) : (!g0 | (D02 > 0)));
+    const bool bz = stp & zf, by = stp & yf & !zf, bx = stp & !yf & !zf;
+    if (bx) { v0 += s0; --k0; D01 += I1; D02 += I2; S -= U0; }
+    if (by) { v1 += s1; --k1; D01 -= I0; D12 += I2; S -= U1; }
+    if (bz) { v2 += s2; --k2; D02 -= I0; D12 -= I1; S -= U2; }
+    const bool enter = (bx & ((v0 & 7) == c0)) | (by & ((v1 & 7) == c1)) | (bz & ((v2 & 7) == c2));
+    if (enter) {                                // entered the next block of the ray
+      ++j;
+      if (list) {
+        slot = nslot;
+        if (j + 1 < nblk) nslot = __ldg(list + j + 1);   // prefetch one block ahead
+      } else {
+        slot = hash_find(p.hash, pack_key(v0 >> 3, v1 >> 3, v2 >> 3));
       }
     }
   }
 }
 
-__global__ void zero_blocks_kernel(Counters* ctr, long long* sums, int max_blocks) {
+// a5 FOLD of the packed per-launch accumulators into the exact sums: sum(w d) += (sum d' - n tq) 2^(30-q),
+// sum(w) += n 2^30 (w = 1).  Every update contributes exactly round(d 2^q) 2^(30-q), so the result does
+// not depend on how frames are grouped into launches.
+__global__ void fold_kernel(const Counters* ctr, unsigned long long* acc, long long* sums, int max_blocks, int tq, int shift) {
+  const int nb = min(ctr->n_blocks, max_blocks);
+  const long long nv2 = (long long)nb * (kBlockVox / 2);
+  ulonglong2* a2 = reinterpret_cast<ulonglong2*>(acc);
+  longlong2* s2 = reinterpret_cast<longlong2*>(sums);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nv2; i += (long long)gridDim.x * blockDim.x) {
+    const ulonglong2 v = a2[i];
+    if ((v.x | v.y) == 0ull) continue;
+    if (v.x) {
+      const long long n = (long long)(v.x >> 42), sd = (long long)(v.x & ((1ull << 42) - 1));
+      longlong2 t = s2[2 * i];
+      t.x += (sd - n * tq) << shift;
+      t.y += n << 30;
+      s2[2 * i] = t;
+    }
+    if (v.y) {
+      const long long n = (long long)(v.y >> 42), sd = (long long)(v.y & ((1ull << 42) - 1));
+      longlong2 t = s2[2 * i + 1];
+      t.x += (sd - n * tq) << shift;
+      t.y += n << 30;
+      s2[2 * i + 1] = t;
+    }
+    a2[i] = make_ulonglong2(0ull, 0ull);
+  }
+}
+
+__global__ void zero_blocks_kernel(Counters* ctr, long long* sums, unsigned long long* acc, int max_blocks) {
   const int nb = min(*(volatile int*)&ctr->n_blocks, max_blocks);
   const long long n16 = (long long)nb * kBlockVox;   // one longlong2 per voxel
   longlong2* s2 = reinterpret_cast<longlong2*>(sums);
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += (long long)gridDim.x * blockDim.x)
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += (long long)gridDim.x * blockDim.x) {
     s2[i] = make_longlong2(0, 0);
+    if ((i & 1) == 0) reinterpret_cast<ulonglong2*>(acc)[i >> 1] = make_ulonglong2(0ull, 0ull);
+  }
 }
 
 __global__ void reset_counters_kernel(Counters* ctr) {
@@ -397,7 +443,7 @@ __global__ void reset_counters_kernel(Counters* ctr) {
 cudaError_t launch_reset(cvx_submap* sm, cudaStream_t st) {
   {
     ProfScope ps_(sm, "reset_zero_blocks", st);
-    zero_blocks_kernel<<<148 * 8, 256, 0, st>>>(sm->ctr, sm->pool.sums, sm->pool.max_blocks);
+    zero_blocks_kernel<<<148 * 8, 256, 0, st>>>(sm->ctr, sm->pool.sums, sm->pool.acc, sm->pool.max_blocks);
   }
   {
     ProfScope ps_(sm, "reset_counters", st);
@@ -438,7 +484,7 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     ProfScope ps_(sm, "compose_poses", st);
     compose_kernel<<<1, kMaxBatch, 0, st>>>(cp, sm->frame_T);
   }
-  cudaMemsetAsync(&sm->ctr->n_rays, 0, 2 * sizeof(int), st);   // n_rays, n_slots
+  cudaMemsetAsync(&sm->ctr->n_rays, 0, 4 * sizeof(int), st);   // n_rays, n_slots, next_ray, pad
 
   PrepParams pp;
   pp.data = data; pp.n_per_frame = n_per_frame; pp.total = total;
@@ -447,6 +493,8 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
   pp.rmin = (double)sensor.min_range; pp.rmax = (double)sensor.max_range;
   pp.s = sm->cfg.voxel_size; pp.tau = sm->cfg.truncation; pp.rfloor = sm->cfg.weight_range_floor;
   pp.weighting = sm->cfg.weighting; pp.carve = sm->cfg.carve;
+  const int q = packed_q(sm->cfg.truncation);
+  pp.sdf_scale = std::ldexp(1.0, q + kSdfF);
   pp.height = sensor.height;
   pp.frame_T = sm->frame_T; pp.rays = (RayRec*)sm->rays; pp.ctr = sm->ctr;
   pp.list_cap = (int)std::min<long long>(sm->slot_cap, 0x7fffffffll);
@@ -460,19 +508,25 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
   wp.rays = (const RayRec*)sm->rays; wp.ctr = sm->ctr; wp.hash = sm->hash; wp.pool = sm->pool;
   wp.slots = sm->slot_lists;
   wp.s = (float)sm->cfg.voxel_size; wp.tau = (float)sm->cfg.truncation;
+  wp.tq = (int)std::llround(std::ldexp(sm->cfg.truncation, q));
+  wp.q = q;
   {
     ProfScope ps_(sm, "block_walk_allocate", st);
     block_walk_kernel<<<blocks, 256, 0, st>>>(wp);
   }
   {
     ProfScope ps_(sm, "ray_walk_update", st);
-    const bool cw = sm->cfg.weighting == 0 && sm->cfg.truncation < 2.0;
+    const bool cw = sm->cfg.weighting == 0 && total <= kMaxPackedRays;
     if (sm->aggregate) {
       if (cw) walk_kernel<true, true><<<blocks, 256, 0, st>>>(wp);
       else walk_kernel<true, false><<<blocks, 256, 0, st>>>(wp);
     } else {
       walk_kernel<false, false><<<blocks, 256, 0, st>>>(wp);
     }
+  }
+  if (sm->aggregate && sm->cfg.weighting == 0 && total <= kMaxPackedRays) {
+    ProfScope ps_(sm, "fold", st);
+    fold_kernel<<<148 * 8, 256, 0, st>>>(sm->ctr, sm->pool.acc, sm->pool.sums, sm->pool.max_blocks, wp.tq, 30 - q);
   }
   return cudaGetLastError();
 }
