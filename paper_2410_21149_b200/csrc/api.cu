@@ -165,7 +165,7 @@ cvx_status cvx_create_submap(const cvx_grid_config* cfg, const double* T_world_s
       (e = cudaMalloc(&sm->pool.coords, nb * 16)) != cudaSuccess ||
       (e = cudaMalloc(&sm->ctr, sizeof(cvx::Counters))) != cudaSuccess ||
       (e = cudaMallocHost(&sm->ctr_host, sizeof(cvx::Counters))) != cudaSuccess ||
-      (e = cudaMalloc(&sm->frame_T, sizeof(double) * 12 * cvx::kMaxBatch)) != cudaSuccess) {
+      (e = cudaMalloc(&sm->frame_T, sizeof(double) * 16 * cvx::kMaxBatch)) != cudaSuccess) {
     free_all(sm);
     delete sm;
     return cuda_fail(e, "allocating submap");

@@ -48,12 +48,25 @@ static_assert(sizeof(RayRec) == 96, "RayRec layout");
 struct ComposeParams {
   double Tws[16];
   double Twc[kMaxBatch][16];
+  double s;
   int n;
 };
+
+// per-frame record written by compose_kernel: R_SC (9), t_SC (3), fixed-point origin q(t_SC) (3 int64
+// bit patterns), origin-in-domain flag
+constexpr int kFrameRec = 16;
 
 __device__ __forceinline__ double dm(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double da(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double ds(double a, double b) { return __dsub_rn(a, b); }
+
+// O3: q(x) = floor((x / s) * 2^16), rejected outside |voxel| < 2^23.
+__device__ __forceinline__ bool quantise(double x, double s, long long* q) {
+  double a = dm(__ddiv_rn(x, s), 65536.0);
+  if (!(fabs(a) < 549755813888.0)) return false;
+  *q = (long long)floor(a);
+  return true;
+}
 
 // O1: R_SC[i][j] = ((Rws[0][i] Rwc[0][j] + Rws[1][i] Rwc[1][j]) + Rws[2][i] Rwc[2][j]),
 // t_SC[i] = ((Rws[0][i](twc0-tws0) + Rws[1][i](twc1-tws1)) + Rws[2][i](twc2-tws2)).
@@ -62,13 +75,18 @@ __global__ void compose_kernel(const __grid_constant__ ComposeParams p, double* 
   if (f >= p.n) return;
   const double* W = p.Tws;
   const double* C = p.Twc[f];
-  double* o = out + 12 * f;
+  double* o = out + kFrameRec * f;
+  bool ok = true;
   for (int i = 0; i < 3; ++i) {
     for (int j = 0; j < 3; ++j)
       o[3 * i + j] = da(da(dm(W[0 * 4 + i], C[0 * 4 + j]), dm(W[1 * 4 + i], C[1 * 4 + j])), dm(W[2 * 4 + i], C[2 * 4 + j]));
     o[9 + i] = da(da(dm(W[0 * 4 + i], ds(C[3], W[3])), dm(W[1 * 4 + i], ds(C[7], W[7]))),
                   dm(W[2 * 4 + i], ds(C[11], W[11])));
+    long long q = 0;
+    ok = quantise(o[9 + i], p.s, &q) && ok;     // O3: the carve start A = q(o) is shared by the frame
+    o[12 + i] = __longlong_as_double(q);
   }
+  o[15] = ok ? 1.0 : 0.0;
 }
 
 struct PrepParams {
@@ -87,14 +105,6 @@ struct PrepParams {
   int list_cap;
 };
 
-// O3: q(x) = floor((x / s) * 2^16), rejected outside |voxel| < 2^23.
-__device__ __forceinline__ bool quantise(double x, double s, long long* q) {
-  double a = dm(__ddiv_rn(x, s), 65536.0);
-  if (!(fabs(a) < 549755813888.0)) return false;
-  *q = (long long)floor(a);
-  return true;
-}
-
 __global__ void __launch_bounds__(256) prepare_kernel(const __grid_constant__ PrepParams p) {
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
@@ -111,7 +121,7 @@ __global__ void __launch_bounds__(256) prepare_kernel(const __grid_constant__ Pr
       i = row * p.width + col;
     }
     const long long src = f * p.n_per_frame + i;
-    const double* T = p.frame_T + 12 * f;
+    const double* T = p.frame_T + kFrameRec * f;
     double pc[3];
     status = 0;
     if (p.kind == 1) {  // O2: pinhole depth -> point in fp32 exactly as written, integer pixel (Q24)
@@ -135,11 +145,14 @@ __global__ void __launch_bounds__(256) prepare_kernel(const __grid_constant__ Pr
       double L = __dsqrt_rn(da(da(dm(d[0], d[0]), dm(d[1], d[1])), dm(d[2], d[2])));
       if (!(L >= p.rmin && L <= p.rmax) || !(L > 0.0)) status = 2;  // Q10
       if (status == 0) {
+        if (p.carve && T[15] == 0.0) status = 3;
         for (int a = 0; a < 3 && status == 0; ++a) {
           double ext = __ddiv_rn(dm(p.tau, d[a]), L);
           double e = da(pw[a], ext);                         // tau behind the point
-          double st = p.carve ? T[9 + a] : ds(pw[a], ext);   // from the optical centre (Q2)
-          if (!quantise(st, p.s, &rec.A[a]) || !quantise(e, p.s, &rec.B[a])) status = 3;
+          bool okA = true;
+          if (p.carve) rec.A[a] = __double_as_longlong(T[12 + a]);   // from the optical centre (Q2)
+          else okA = quantise(ds(pw[a], ext), p.s, &rec.A[a]);
+          if (!okA || !quantise(e, p.s, &rec.B[a])) status = 3;
           else {
             long long span = (rec.B[a] >> 16) - (rec.A[a] >> 16);
             if (span >= 32768 || span <= -32768) status = 3;
@@ -149,8 +162,9 @@ __global__ void __launch_bounds__(256) prepare_kernel(const __grid_constant__ Pr
           // O5 in fixed point: sdf of the first voxel v_A, then an exact per-axis decrement s |u_a| per
           // step (stepping axis a moves the voxel centre by s sign(u_a) e_a)
           double u[3], sdf0 = 0.0;
+          const double inv_l = __drcp_rn(L);
           for (int a = 0; a < 3; ++a) {
-            u[a] = d[a] / L;
+            u[a] = d[a] * inv_l;
             const double c = ((double)(rec.A[a] >> 16) + 0.5) * p.s;
             sdf0 += (pw[a] - c) * u[a];
             rec.U[a] = __double2ll_rn(fabs(u[a]) * p.s * p.sdf_scale);
@@ -158,7 +172,7 @@ __global__ void __launch_bounds__(256) prepare_kernel(const __grid_constant__ Pr
           rec.S0 = __double2ll_rn(sdf0 * p.sdf_scale);
         }
         if (p.weighting == 0) rec.w = 1.0f;                  // O6
-        else { double r = fmax(L, p.rfloor); rec.w = (float)__ddiv_rn(1.0, dm(r, r)); }
+        else { const float r = (float)fmax(L, p.rfloor); rec.w = __frcp_rn(r * r); }
         rec.n_vox = 1;
         for (int a = 0; a < 3; ++a) {
           long long dv = (rec.B[a] >> 16) - (rec.A[a] >> 16);
@@ -169,27 +183,15 @@ __global__ void __launch_bounds__(256) prepare_kernel(const __grid_constant__ Pr
       }
     }
   }
-  // warp-local counters, one atomic per warp ("each thread or block maintains its local
-  // counter, and the results are combined at the end")
+  // Local counters combined hierarchically ("each thread or block maintains its local
+  // counter, and the results are combined at the end"): warp ballots/reductions, a shared-memory scan
+  // over the CTA's warps, then ONE 64-bit atomicAdd per CTA claims both the compacted ray positions
+  // and the block-slot list space — no hot global counter per warp.
+  __shared__ unsigned long long s_base;
+  __shared__ unsigned s_w[8][7];   // per warp: used, slots, in, invalid, range, domain, voxels
+  const int warp = threadIdx.x >> 5;
   const unsigned used = __ballot_sync(0xffffffffu, status == 0);
-  const unsigned n_in = __popc(__ballot_sync(0xffffffffu, status >= 0));
-  const unsigned n_inv = __popc(__ballot_sync(0xffffffffu, status == 1));
-  const unsigned n_rng = __popc(__ballot_sync(0xffffffffu, status == 2));
-  const unsigned n_dom = __popc(__ballot_sync(0xffffffffu, status == 3));
-  const unsigned nv = __reduce_add_sync(0xffffffffu, status == 0 ? (unsigned)rec.n_vox : 0u);
-  int base = 0;
-  if (lane == 0) {
-    if (used) base = atomicAdd(&p.ctr->n_rays, __popc(used));
-    if (n_in) atomicAdd(&p.ctr->rays_in, (unsigned long long)n_in);
-    if (used) atomicAdd(&p.ctr->rays_used, (unsigned long long)__popc(used));
-    if (n_inv) atomicAdd(&p.ctr->skipped_invalid, (unsigned long long)n_inv);
-    if (n_rng) atomicAdd(&p.ctr->skipped_range, (unsigned long long)n_rng);
-    if (n_dom) { atomicAdd(&p.ctr->skipped_domain, (unsigned long long)n_dom); atomicOr(&p.ctr->err, (unsigned)kErrRange); }
-    if (nv) atomicAdd(&p.ctr->voxel_updates, (unsigned long long)nv);
-  }
-  base = __shfl_sync(0xffffffffu, base, 0);
-  // block-slot lists: closed-form block count 1 + sum |db| (a2), space claimed per warp
-  int nb = 0;
+  int nb = 0;                      // block-slot list length: closed form 1 + sum |db| (a2)
   if (status == 0) {
     nb = 1;
     for (int a = 0; a < 3; ++a) {
@@ -199,14 +201,40 @@ __global__ void __launch_bounds__(256) prepare_kernel(const __grid_constant__ Pr
   }
   int incl = nb;
   for (int o = 1; o < 32; o <<= 1) { int t = __shfl_up_sync(0xffffffffu, incl, o); if (lane >= o) incl += t; }
-  const int wsum = __shfl_sync(0xffffffffu, incl, 31);
-  int lbase = 0;
-  if (lane == 0 && wsum) lbase = atomicAdd(&p.ctr->n_slots, wsum);
-  lbase = __shfl_sync(0xffffffffu, lbase, 0);
+  const unsigned nv = __reduce_add_sync(0xffffffffu, status == 0 ? (unsigned)rec.n_vox : 0u);
+  const unsigned n_in = __popc(__ballot_sync(0xffffffffu, status >= 0));
+  const unsigned n_inv = __popc(__ballot_sync(0xffffffffu, status == 1));
+  const unsigned n_rng = __popc(__ballot_sync(0xffffffffu, status == 2));
+  const unsigned n_dom = __popc(__ballot_sync(0xffffffffu, status == 3));
+  if (lane == 31) {
+    s_w[warp][0] = __popc(used); s_w[warp][1] = (unsigned)incl; s_w[warp][2] = n_in; s_w[warp][3] = n_inv;
+    s_w[warp][4] = n_rng; s_w[warp][5] = n_dom; s_w[warp][6] = nv;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long c[7] = {0, 0, 0, 0, 0, 0, 0};
+    const int nw = blockDim.x >> 5;
+    for (int w = 0; w < nw; ++w)
+      for (int t = 0; t < 7; ++t) {
+        const unsigned x = s_w[w][t];
+        if (t < 2) s_w[w][t] = (unsigned)c[t];   // exclusive prefix of rays / slots
+        c[t] += x;
+      }
+    unsigned long long base = 0;
+    if (c[0] | c[1]) base = atomicAdd(reinterpret_cast<unsigned long long*>(&p.ctr->n_rays), (c[1] << 32) | c[0]);
+    s_base = base;
+    if (c[2]) atomicAdd(&p.ctr->rays_in, c[2]);
+    if (c[0]) atomicAdd(&p.ctr->rays_used, c[0]);
+    if (c[3]) atomicAdd(&p.ctr->skipped_invalid, c[3]);
+    if (c[4]) atomicAdd(&p.ctr->skipped_range, c[4]);
+    if (c[5]) { atomicAdd(&p.ctr->skipped_domain, c[5]); atomicOr(&p.ctr->err, (unsigned)kErrRange); }
+    if (c[6]) atomicAdd(&p.ctr->voxel_updates, c[6]);
+  }
+  __syncthreads();
   if (status == 0) {
-    const long long off = (long long)lbase + incl - nb;
+    const long long off = (long long)(unsigned)(s_base >> 32) + s_w[warp][1] + incl - nb;
     rec.list_off = (off + nb <= p.list_cap) ? (int)off : -1;   // full buffer: the walk hashes instead
-    const int pos = base + __popc(used & ((1u << lane) - 1u));   // order-preserving within the warp
+    const int pos = (int)(unsigned)(s_base & 0xffffffffu) + (int)s_w[warp][0] + __popc(used & ((1u << lane) - 1u));
     p.rays[pos] = rec;
   }
 }
@@ -239,36 +267,56 @@ __device__ __forceinline__ void reduce_peers(unsigned m, unsigned peers, int lan
 }
 
 // ALLOCATE (a3): block-granular exact traversal (boundaries every 2^19 fixed-point units = 8 voxels),
-// activating every block a ray visits and recording its slot in the ray's list.
+// activating every block a ray visits and recording its slot in the ray's list.  The loop is
+// warp-uniform; in each step only the first lane of every run of equal keys among adjacent lanes
+// (adjacent rays) probes the hash table and the slot is shuffled to the rest of the run.
 __global__ void __launch_bounds__(256) block_walk_kernel(const __grid_constant__ WalkParams p) {
   const int n_rays = *(volatile int*)&p.ctr->n_rays;
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= n_rays) return;
-  const RayRec r = p.rays[idx];
-  long long R[3], AD[3];
-  int b[3], st[3], k[3];
-  for (int a = 0; a < 3; ++a) {
-    b[a] = (int)(r.A[a] >> 19);
-    const int bb = (int)(r.B[a] >> 19);
-    const long long D = r.B[a] - r.A[a];
-    k[a] = bb > b[a] ? bb - b[a] : b[a] - bb;
-    if (D > 0) { st[a] = 1; R[a] = (((long long)b[a] + 1) << 19) - r.A[a]; }
-    else { st[a] = -1; R[a] = r.A[a] - ((long long)b[a] << 19); }
-    AD[a] = D < 0 ? -D : D;
-  }
-  int* list = r.list_off >= 0 ? p.slots + r.list_off : nullptr;
-  for (int j = 0;; ++j) {
-    const int slot = hash_activate(p.hash, p.pool, p.ctr, pack_key(b[0], b[1], b[2]), b[0], b[1], b[2]);
-    if (list) list[j] = slot;
-    if (k[0] + k[1] + k[2] == 0) break;
-    // earliest crossing, ties x < y < z (O4); axes without crossings left are not eligible
-    const bool e0 = k[0] > 0, e1 = k[1] > 0, e2 = k[2] > 0;
-    const bool y_first = e1 && (!e0 || R[1] * AD[0] < R[0] * AD[1]);
-    const bool z_first = e2 && (y_first ? R[2] * AD[1] < R[1] * AD[2] : (!e0 || R[2] * AD[0] < R[0] * AD[2]));
+  const int lane = threadIdx.x & 31;
+  if ((idx & ~31) >= n_rays) return;
+  const bool have = idx < n_rays;
+  long long R[3] = {0, 0, 0}, AD[3] = {0, 0, 0};
+  int b[3] = {0, 0, 0}, st[3] = {1, 1, 1}, k[3] = {0, 0, 0};
+  int nb = 0;
+  int* list = nullptr;
+  if (have) {
+    const RayRec r = p.rays[idx];
+    nb = 1;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      const bool take = z_first ? a == 2 : (y_first ? a == 1 : a == 0);
-      if (take) { b[a] += st[a]; R[a] += 1ll << 19; --k[a]; }
+      b[a] = (int)(r.A[a] >> 19);
+      const int bb = (int)(r.B[a] >> 19);
+      const long long D = r.B[a] - r.A[a];
+      k[a] = bb > b[a] ? bb - b[a] : b[a] - bb;
+      if (D > 0) { st[a] = 1; R[a] = (((long long)b[a] + 1) << 19) - r.A[a]; }
+      else { st[a] = -1; R[a] = r.A[a] - ((long long)b[a] << 19); }
+      AD[a] = D < 0 ? -D : D;
+      nb += k[a];
+    }
+    list = r.list_off >= 0 ? p.slots + r.list_off : nullptr;
+  }
+  const int maxnb = (int)__reduce_max_sync(0xffffffffu, (unsigned)nb);
+  for (int j = 0; j < maxnb; ++j) {
+    const bool act = j < nb;
+    const unsigned long long key = act ? pack_key(b[0], b[1], b[2]) : ((1ull << 63) | (unsigned)lane);
+    const unsigned long long prev = __shfl_up_sync(0xffffffffu, key, 1);
+    const bool head = act && (lane == 0 || prev != key);
+    int slot = kFailed;
+    if (head) slot = hash_activate(p.hash, p.pool, p.ctr, key, b[0], b[1], b[2]);
+    const unsigned heads = __ballot_sync(0xffffffffu, head) & (0xffffffffu >> (31 - lane));
+    slot = __shfl_sync(0xffffffffu, slot, heads ? 31 - __clz(heads) : lane);
+    if (act && list) list[j] = slot;
+    if (act && j + 1 < nb) {
+      // earliest crossing, ties x < y < z (O4); axes without crossings left are not eligible
+      const bool e0 = k[0] > 0, e1 = k[1] > 0, e2 = k[2] > 0;
+      const bool y_first = e1 && (!e0 || R[1] * AD[0] < R[0] * AD[1]);
+      const bool z_first = e2 && (y_first ? R[2] * AD[1] < R[1] * AD[2] : (!e0 || R[2] * AD[0] < R[0] * AD[2]));
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const bool take = z_first ? a == 2 : (y_first ? a == 1 : a == 0);
+        if (take) { b[a] += st[a]; R[a] += 1ll << 19; --k[a]; }
+      }
     }
   }
 }
@@ -480,6 +528,7 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
   for (int f = 0; f < n_frames; ++f)
     for (int i = 0; i < 16; ++i) cp.Twc[f][i] = T_world_sensor[16 * f + i];
   cp.n = n_frames;
+  cp.s = sm->cfg.voxel_size;
   {
     ProfScope ps_(sm, "compose_poses", st);
     compose_kernel<<<1, kMaxBatch, 0, st>>>(cp, sm->frame_T);

@@ -47,7 +47,7 @@ struct cvx_submap {
   cvx::Counters* ctr_host = nullptr;  // pinned mirror for synchronising reads
 
   // integrate scratch (grow-only)
-  double* frame_T = nullptr;  // device [kMaxBatch][12]: R_SC (row-major) then t_SC, per frame
+  double* frame_T = nullptr;  // device [kMaxBatch][16]: R_SC, t_SC, q(t_SC), flag per frame
   void* rays = nullptr;       // device RayRec [ray_cap]
   int64_t ray_cap = 0;
   int* slot_lists = nullptr;  // device block-slot lists of the rays of one launch
