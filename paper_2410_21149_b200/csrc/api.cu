@@ -98,8 +98,7 @@ void fill_stats(const cvx::Counters& c, int max_blocks, cvx_integrate_stats* s) 
 }
 
 void free_all(cvx_submap* sm) {
-  if (sm->hash.keys) cudaFree(sm->hash.keys);
-  if (sm->hash.vals) cudaFree(sm->hash.vals);
+  if (sm->hash.e) cudaFree(sm->hash.e);
   if (sm->pool.sums) cudaFree(sm->pool.sums);
   if (sm->pool.acc) cudaFree(sm->pool.acc);
   if (sm->pool.esdf) cudaFree(sm->pool.esdf);
@@ -157,8 +156,7 @@ cvx_status cvx_create_submap(const cvx_grid_config* cfg, const double* T_world_s
   sm->hash.mask = (unsigned)(cap - 1);
   sm->hash.log2cap = log2cap;
   sm->pool.max_blocks = (int)nb;
-  if ((e = cudaMalloc(&sm->hash.keys, cap * 8)) != cudaSuccess ||
-      (e = cudaMalloc(&sm->hash.vals, cap * 4)) != cudaSuccess ||
+  if ((e = cudaMalloc(&sm->hash.e, cap * sizeof(cvx::HashEntry))) != cudaSuccess ||
       (e = cudaMalloc(&sm->pool.sums, nb * cvx::kBlockVox * 16)) != cudaSuccess ||
       (e = cudaMalloc(&sm->pool.acc, nb * cvx::kBlockVox * 8)) != cudaSuccess ||
       (e = cudaMalloc(&sm->pool.esdf, nb * cvx::kBlockVox * 4)) != cudaSuccess ||

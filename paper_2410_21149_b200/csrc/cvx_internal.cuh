@@ -1,8 +1,8 @@
 // cvx_internal.cuh — device-side state and helpers of libcvx (sm_100a).  Not part of the C-ABI.
 //
 // HBM layout of one submap:
-//   keys  u64 [cap]          open-addressing hash table of packed 21-bit block keys
-//   vals  i32 [cap]          slot of the key (PENDING while the inserter publishes it)
+//   table {u64 key, i32 slot, pad} [cap]  open-addressing hash table of packed 21-bit block keys
+//                            (P:L78-85); slot is PENDING while the inserter publishes it
 //   sums  i64x2 [max_blocks*512]  per voxel (sum w*d, sum w) in fixed point 2^-30 (O8 as exact sums)
 //   acc   u64 [max_blocks*512]    packed per-launch accumulator {count:22 | sum d':42} (constant w)
 //   esdf  f32 [max_blocks*512]    E per voxel (after finalize)
@@ -38,9 +38,15 @@ struct Counters {
       new_blocks;
 };
 
+// One 16-byte entry per table slot so a probe is a single 128-bit load: {key, slot, pad}.
+struct __align__(16) HashEntry {
+  unsigned long long key;
+  int val;
+  int pad;
+};
+
 struct HashView {
-  unsigned long long* keys;
-  int* vals;
+  HashEntry* e;
   unsigned mask;           // cap - 1
   int log2cap;
 };
@@ -65,17 +71,16 @@ __device__ inline unsigned hash_slot(unsigned long long key, const HashView& h) 
 }
 
 __device__ inline int ld_volatile(const int* p) { return *(const volatile int*)p; }
-__device__ inline unsigned long long ld_volatile(const unsigned long long* p) {
-  return *(const volatile unsigned long long*)p;
-}
+
+__device__ __forceinline__ longlong2 ld_entry(const HashEntry* p) { return *reinterpret_cast<const longlong2*>(p); }
 
 // Find-only probe: slot, or -1 if absent.  Table must be quiescent (no concurrent inserts).
 __device__ inline int hash_find(const HashView& h, unsigned long long key) {
   unsigned i = hash_slot(key, h);
   for (unsigned p = 0; p <= h.mask; ++p) {
-    unsigned long long k = h.keys[i];
-    if (k == key) return h.vals[i];
-    if (k == kEmptyKey) return -1;
+    const longlong2 en = ld_entry(h.e + i);
+    if ((unsigned long long)en.x == key) return (int)(en.y & 0xffffffffll);
+    if ((unsigned long long)en.x == kEmptyKey) return -1;
     i = (i + 1) & h.mask;
   }
   return -1;
@@ -84,13 +89,21 @@ __device__ inline int hash_find(const HashView& h, unsigned long long key) {
 // ASH-style activate: insert-if-absent and return the block's pool slot.  The winner of the
 // key CAS claims a slot by bumping the pool index, records the block coordinates and AABB,
 // then publishes the slot; concurrent finders of the same key wait for the publication.
+// Keys only ever change EMPTY -> key, so the probe is a plain (L1-cacheable) 128-bit load of the
+// {key, slot} entry: a stale EMPTY is corrected by the CAS, a stale PENDING by the volatile re-reads.
 __device__ inline int hash_activate(const HashView& h, const PoolView& pool, Counters* ctr,
                                     unsigned long long key, int bx, int by, int bz) {
   unsigned i = hash_slot(key, h);
   for (unsigned p = 0; p <= h.mask; ++p) {
-    unsigned long long k = ld_volatile(&h.keys[i]);
+    const longlong2 en = ld_entry(h.e + i);
+    unsigned long long k = (unsigned long long)en.x;
+    if (k == key) {
+      int v = (int)(en.y & 0xffffffffll);
+      while (v == kPending) { __nanosleep(32); v = ld_volatile(&h.e[i].val); }
+      return v;
+    }
     if (k == kEmptyKey) {
-      unsigned long long old = atomicCAS(&h.keys[i], kEmptyKey, key);
+      unsigned long long old = atomicCAS(&h.e[i].key, kEmptyKey, key);
       if (old == kEmptyKey) {
         int slot = atomicAdd(&ctr->n_blocks, 1);
         if (slot >= pool.max_blocks) {
@@ -103,15 +116,14 @@ __device__ inline int hash_activate(const HashView& h, const PoolView& pool, Cou
           atomicAdd(&ctr->new_blocks, 1ull);
         }
         __threadfence();
-        *(volatile int*)&h.vals[i] = slot;
+        *(volatile int*)&h.e[i].val = slot;
         return slot;
       }
-      k = old;
-    }
-    if (k == key) {
-      int v;
-      while ((v = ld_volatile(&h.vals[i])) == kPending) { __nanosleep(32); }
-      return v;
+      if (old == key) {
+        int v;
+        while ((v = ld_volatile(&h.e[i].val)) == kPending) { __nanosleep(32); }
+        return v;
+      }
     }
     i = (i + 1) & h.mask;
   }

@@ -497,8 +497,7 @@ cudaError_t launch_reset(cvx_submap* sm, cudaStream_t st) {
     ProfScope ps_(sm, "reset_counters", st);
     reset_counters_kernel<<<1, 1, 0, st>>>(sm->ctr);
   }
-  cudaMemsetAsync(sm->hash.keys, 0xff, sizeof(unsigned long long) * ((size_t)sm->hash.mask + 1), st);
-  cudaMemsetAsync(sm->hash.vals, 0xff, sizeof(int) * ((size_t)sm->hash.mask + 1), st);
+  cudaMemsetAsync(sm->hash.e, 0xff, sizeof(HashEntry) * ((size_t)sm->hash.mask + 1), st);   // EMPTY / PENDING
   return cudaGetLastError();
 }
 
