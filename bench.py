@@ -58,7 +58,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + ",".join(self.FIELDS),
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
@@ -175,7 +175,7 @@ def cpu_baseline_sample(cfg, data, poses, n=3):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="cvx", choices=["cvx", "reference"])
     ap.add_argument("--batch", type=int, default=40, help="scans per integrate_batch call")
@@ -225,16 +225,9 @@ def main():
     def gather():
         if pg is None:
             return
-        payload = sm.pack()
-        n = torch.tensor([payload.numel()], device=dev, dtype=torch.int64)
-        sizes = [torch.zeros_like(n) for _ in range(world)]
-        pg.all_gather(sizes, n)
-        mx = int(max(x.item() for x in sizes))
-        buf = torch.zeros(mx, dtype=torch.uint8, device=dev)
-        buf[:payload.numel()] = payload
-        out = torch.empty(world * mx, dtype=torch.uint8, device=dev)
-        pg.all_gather_into_tensor(out, buf)
-        gather_bytes[0] = world * mx
+        from paper_2410_21149_b200.parallel import gather_packed
+        parts = gather_packed(sm.pack())
+        gather_bytes[0] = sum(p.numel() for p in parts)
 
     def step(src=None):
         sm.reset()
@@ -349,16 +342,16 @@ def main():
         roofline = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
                     "frac": ach / hbm, "traffic": None, "peak_source": hbm_src, "launches_per_step": n_l}
     else:
-        # ray_walk_update: bound by issue (ALU) + L2 atomics; algorithmic ops per voxel update = 24
-        # (DESIGN.md), peak = 148 SM x 128 lanes x SM clock.
+        # ray_walk_update: bound by issue (ALU); algorithmic lane-ops per voxel update = 13,
+        # peak = 148 SM x 128 lanes x SM clock.
         clk_mhz = (clk.summary().get("sm_mhz") or 1965.0)
         peak_tops = 148 * 128 * clk_mhz * 1e6 / 1e12
         avg_ms = walk["ms"] / walk["n"]
         upd_launch = updates_per_step / (walk["n"] / K)
-        ach = 24 * upd_launch / (avg_ms / 1e3) / 1e12
+        ach = 13 * upd_launch / (avg_ms / 1e3) / 1e12
         roofline = {"kernel": dom, "bound": "alu", "achieved": ach, "peak": peak_tops, "unit": "Tops/s",
                     "frac": ach / peak_tops, "traffic": None,
-                    "updates_per_s": upd_launch / (avg_ms / 1e3), "ops_per_update": 24,
+                    "updates_per_s": upd_launch / (avg_ms / 1e3), "ops_per_update": 13,
                     "peak_source": f"148 SM x 128 lanes x {clk_mhz:.0f} MHz (median under load)"}
     line = {
         "metric": METRIC, "value": value, "unit": "scans/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
