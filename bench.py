@@ -153,7 +153,7 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline_sample(cfg, data, poses, n=3):
+def cpu_baseline_sample(cfg, data, poses, n=12):
     """The oracle as it stands, single-threaded, on the first n scans of the same workload."""
     import oracle
     g = cfg["grid"]

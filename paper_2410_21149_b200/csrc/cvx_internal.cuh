@@ -91,11 +91,12 @@ __device__ inline int hash_find(const HashView& h, unsigned long long key) {
 // then publishes the slot; concurrent finders of the same key wait for the publication.
 // Keys only ever change EMPTY -> key, so the probe is a plain (L1-cacheable) 128-bit load of the
 // {key, slot} entry: a stale EMPTY is corrected by the CAS, a stale PENDING by the volatile re-reads.
-__device__ inline int hash_activate(const HashView& h, const PoolView& pool, Counters* ctr,
-                                    unsigned long long key, int bx, int by, int bz) {
+// `first` = the entry at hash_slot(key), already loaded by the caller (prefetched ahead of use).
+__device__ inline int hash_activate_pf(const HashView& h, const PoolView& pool, Counters* ctr,
+                                       unsigned long long key, int bx, int by, int bz, longlong2 first) {
   unsigned i = hash_slot(key, h);
   for (unsigned p = 0; p <= h.mask; ++p) {
-    const longlong2 en = ld_entry(h.e + i);
+    const longlong2 en = p == 0 ? first : ld_entry(h.e + i);
     unsigned long long k = (unsigned long long)en.x;
     if (k == key) {
       int v = (int)(en.y & 0xffffffffll);
@@ -129,6 +130,11 @@ __device__ inline int hash_activate(const HashView& h, const PoolView& pool, Cou
   }
   atomicOr(&ctr->err, (unsigned)kErrHashFull);
   return kFailed;
+}
+
+__device__ inline int hash_activate(const HashView& h, const PoolView& pool, Counters* ctr,
+                                    unsigned long long key, int bx, int by, int bz) {
+  return hash_activate_pf(h, pool, ctr, key, bx, by, bz, ld_entry(h.e + hash_slot(key, h)));
 }
 
 // Packed accumulator: at most kMaxPackedRays updates of one voxel per launch (22-bit count), and the

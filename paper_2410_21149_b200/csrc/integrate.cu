@@ -267,57 +267,63 @@ __device__ __forceinline__ void reduce_peers(unsigned m, unsigned peers, int lan
 }
 
 // ALLOCATE (a3): block-granular exact traversal (boundaries every 2^19 fixed-point units = 8 voxels),
-// activating every block a ray visits and recording its slot in the ray's list.  The loop is
-// warp-uniform; in each step only the first lane of every run of equal keys among adjacent lanes
-// (adjacent rays) probes the hash table and the slot is shuffled to the rest of the run.
+// activating every block a ray visits and recording its slot in the ray's list.  Same predicated
+// difference-form DDA as the voxel walk.  The loop is warp-uniform; in each step only the first lane
+// of every run of equal keys among adjacent lanes (adjacent rays) probes the hash table and the slot
+// is shuffled to the rest of the run.
 __global__ void __launch_bounds__(256) block_walk_kernel(const __grid_constant__ WalkParams p) {
   const int n_rays = *(volatile int*)&p.ctr->n_rays;
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   if ((idx & ~31) >= n_rays) return;
   const bool have = idx < n_rays;
-  long long R[3] = {0, 0, 0}, AD[3] = {0, 0, 0};
-  int b[3] = {0, 0, 0}, st[3] = {1, 1, 1}, k[3] = {0, 0, 0};
-  int nb = 0;
+  int b0 = 0, b1 = 0, b2 = 0, s0 = 1, s1 = 1, s2 = 1, k0 = 0, k1 = 0, k2 = 0, nb = 0;
+  long long D01 = 0, D02 = 0, D12 = 0, I0 = 0, I1 = 0, I2 = 0;
   int* list = nullptr;
   if (have) {
     const RayRec r = p.rays[idx];
-    nb = 1;
+    long long R[3], AD[3];
+    int bb[3], st[3], kk[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      b[a] = (int)(r.A[a] >> 19);
-      const int bb = (int)(r.B[a] >> 19);
+      bb[a] = (int)(r.A[a] >> 19);
+      const int be = (int)(r.B[a] >> 19);
       const long long D = r.B[a] - r.A[a];
-      k[a] = bb > b[a] ? bb - b[a] : b[a] - bb;
-      if (D > 0) { st[a] = 1; R[a] = (((long long)b[a] + 1) << 19) - r.A[a]; }
-      else { st[a] = -1; R[a] = r.A[a] - ((long long)b[a] << 19); }
+      kk[a] = be > bb[a] ? be - bb[a] : bb[a] - be;
+      if (D > 0) { st[a] = 1; R[a] = (((long long)bb[a] + 1) << 19) - r.A[a]; }
+      else { st[a] = -1; R[a] = r.A[a] - ((long long)bb[a] << 19); }
       AD[a] = D < 0 ? -D : D;
-      nb += k[a];
     }
+    b0 = bb[0]; b1 = bb[1]; b2 = bb[2]; s0 = st[0]; s1 = st[1]; s2 = st[2]; k0 = kk[0]; k1 = kk[1]; k2 = kk[2];
+    nb = 1 + k0 + k1 + k2;
+    D01 = R[0] * AD[1] - R[1] * AD[0];
+    D02 = R[0] * AD[2] - R[2] * AD[0];
+    D12 = R[1] * AD[2] - R[2] * AD[1];
+    I0 = AD[0] << 19; I1 = AD[1] << 19; I2 = AD[2] << 19;
     list = r.list_off >= 0 ? p.slots + r.list_off : nullptr;
   }
   const int maxnb = (int)__reduce_max_sync(0xffffffffu, (unsigned)nb);
   for (int j = 0; j < maxnb; ++j) {
     const bool act = j < nb;
-    const unsigned long long key = act ? pack_key(b[0], b[1], b[2]) : ((1ull << 63) | (unsigned)lane);
+    const unsigned long long key = act ? pack_key(b0, b1, b2) : ((1ull << 63) | (unsigned)lane);
     const unsigned long long prev = __shfl_up_sync(0xffffffffu, key, 1);
-    const bool head = act && (lane == 0 || prev != key);
+    const unsigned actm = __ballot_sync(0xffffffffu, act);
+    const unsigned same = __ballot_sync(0xffffffffu, act && prev == key) & (actm << 1);
+    const unsigned heads = actm & ~same;
     int slot = kFailed;
-    if (head) slot = hash_activate(p.hash, p.pool, p.ctr, key, b[0], b[1], b[2]);
-    const unsigned heads = __ballot_sync(0xffffffffu, head) & (0xffffffffu >> (31 - lane));
-    slot = __shfl_sync(0xffffffffu, slot, heads ? 31 - __clz(heads) : lane);
+    if ((heads >> lane) & 1u) slot = hash_activate(p.hash, p.pool, p.ctr, key, b0, b1, b2);
+    const unsigned hb = heads & (0xffffffffu >> (31 - lane));
+    slot = __shfl_sync(0xffffffffu, slot, hb ? 31 - __clz(hb) : lane);
     if (act && list) list[j] = slot;
-    if (act && j + 1 < nb) {
-      // earliest crossing, ties x < y < z (O4); axes without crossings left are not eligible
-      const bool e0 = k[0] > 0, e1 = k[1] > 0, e2 = k[2] > 0;
-      const bool y_first = e1 && (!e0 || R[1] * AD[0] < R[0] * AD[1]);
-      const bool z_first = e2 && (y_first ? R[2] * AD[1] < R[1] * AD[2] : (!e0 || R[2] * AD[0] < R[0] * AD[2]));
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        const bool take = z_first ? a == 2 : (y_first ? a == 1 : a == 0);
-        if (take) { b[a] += st[a]; R[a] += 1ll << 19; --k[a]; }
-      }
-    }
+    // O4 at block granularity: earliest crossing among axes with crossings left, ties x < y < z
+    const bool stp = j + 1 < nb;
+    const bool g0 = k0 > 0, g1 = k1 > 0, g2 = k2 > 0;
+    const bool yf = g1 & (!g0 | (D01 > 0));
+    const bool zf = g2 & (yf ? (D12 > 0) : (!g0 | (D02 > 0)));
+    const bool bz = stp & zf, by = stp & yf & !zf, bx = stp & !yf & !zf;
+    if (bx) { b0 += s0; --k0; D01 += I1; D02 += I2; }
+    if (by) { b1 += s1; --k1; D01 -= I0; D12 += I2; }
+    if (bz) { b2 += s2; --k2; D02 -= I0; D12 -= I1; }
   }
 }
 
