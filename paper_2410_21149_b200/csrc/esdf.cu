@@ -157,69 +157,79 @@ __global__ void __launch_bounds__(256) pass_line_kernel(const __grid_constant__ 
       return v == kNone16 ? kInfF : (long long)v * v;
     }
   };
-  // forward: build the envelope (Meijster phase 2 with a linked stack)
+  // forward: build the envelope (Meijster phase 2 with a linked stack).  The line is read in chunks
+  // of 8 independent loads so each thread keeps 8 requests in flight (the pass is latency-bound).
   int top = -1, t_top = 0;
   long long f_top = 0;
-  for (int q = 0; q < m; ++q) {
-    const long long fq = f_at(q);
-    if (fq >= kInfF) continue;
-    while (top >= 0) {
-      const long long a = (long long)(t_top - top), b = (long long)(t_top - q);
-      if (a * a + f_top > b * b + fq) {                 // q beats top already at top's start: pop
-        const unsigned mt = p.meta[base + (long long)top * stride];
-        const int pr = (int)(mt & 0xffffu);
-        if (pr == 0xffff) { top = -1; break; }
-        top = pr;
-        t_top = (int)(p.meta[base + (long long)top * stride] >> 16);
-        f_top = f_at(top);
-      } else {
-        break;
-      }
-    }
-    int tq;
-    if (top < 0) {
-      tq = 0;
-    } else {
-      const long long num = (long long)q * q - (long long)top * top + fq - f_top;
-      const long long sep = floordiv(num, 2ll * (q - top));   // last position where top is <= q
-      if (sep + 1 >= m) continue;                             // q never wins inside the line
-      tq = (int)(sep + 1);
-    }
-    p.meta[base + (long long)q * stride] = ((unsigned)tq << 16) | (unsigned)(top < 0 ? 0xffff : top);
-    top = q; t_top = tq; f_top = fq;
-  }
-  // backward: read the envelope from the right
-  int cur_slot = -1, cur_bz = -1;
-  const int bx = x >> 3;
-  for (int q = m - 1; q >= 0; --q) {
-    long long d2 = kInfF;
-    if (top >= 0) {
-      const long long dq = (long long)(q - top);
-      d2 = dq * dq + f_top;
-    }
-    if (!kZ) {
-      p.gout[base + (long long)q * stride] = d2 >= kInfF ? kInf32 : (unsigned)d2;
-    } else {
-      const int bz = q >> 3;
-      if (bz != cur_bz) {
-        cur_bz = bz;
-        cur_slot = p.grid[((long long)bz * p.nby + (o2 >> 3)) * p.nbx + bx];
-      }
-      if (cur_slot >= 0) {
-        const long long vi = (long long)cur_slot * kBlockVox + (x & 7) + 8 * (o2 & 7) + 64 * (q & 7);
-        const float ph = p.esdf[vi];
-        if (!isnan(ph)) {
-          float e;
-          if (d2 >= kInfF) e = __int_as_float(0x7f800000);             // S empty -> +inf (O11)
-          else e = copysignf((float)((double)p.s * sqrt((double)d2)), ph);
-          p.esdf[vi] = e;
+  for (int q0 = 0; q0 < m; q0 += 8) {
+    long long fv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) fv[u] = q0 + u < m ? f_at(q0 + u) : kInfF;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int q = q0 + u;
+      const long long fq = fv[u];
+      if (fq >= kInfF) continue;
+      while (top >= 0) {
+        const long long a = (long long)(t_top - top), b = (long long)(t_top - q);
+        if (a * a + f_top > b * b + fq) {                 // q beats top already at top's start: pop
+          const unsigned mt = p.meta[base + (long long)top * stride];
+          const int pr = (int)(mt & 0xffffu);
+          if (pr == 0xffff) { top = -1; break; }
+          top = pr;
+          t_top = (int)(p.meta[base + (long long)top * stride] >> 16);
+          f_top = f_at(top);
+        } else {
+          break;
         }
       }
+      int tq;
+      if (top < 0) {
+        tq = 0;
+      } else {
+        const long long num = (long long)q * q - (long long)top * top + fq - f_top;
+        const long long sep = floordiv(num, 2ll * (q - top));   // last position where top is <= q
+        if (sep + 1 >= m) continue;                             // q never wins inside the line
+        tq = (int)(sep + 1);
+      }
+      p.meta[base + (long long)q * stride] = ((unsigned)tq << 16) | (unsigned)(top < 0 ? 0xffff : top);
+      top = q; t_top = tq; f_top = fq;
     }
-    if (top >= 0 && q == t_top) {
-      const int pr = (int)(p.meta[base + (long long)top * stride] & 0xffffu);
-      if (pr == 0xffff) { top = -1; }
-      else { top = pr; t_top = (int)(p.meta[base + (long long)top * stride] >> 16); f_top = f_at(top); }
+  }
+  // backward: read the envelope from the right, one 8-voxel chunk (= one block along the line) at a
+  // time; pass z prefetches the chunk's sign/observed placeholders before evaluating it.
+  const int bx = x >> 3;
+  for (int q0 = m - 8; q0 >= 0; q0 -= 8) {
+    int slot = -1;
+    float ph[8];
+    if (kZ) {
+      slot = p.grid[((long long)(q0 >> 3) * p.nby + (o2 >> 3)) * p.nbx + bx];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        ph[u] = slot >= 0 ? p.esdf[(long long)slot * kBlockVox + (x & 7) + 8 * (o2 & 7) + 64 * u]
+                          : __int_as_float(0x7fc00000);
+    }
+#pragma unroll
+    for (int u = 7; u >= 0; --u) {
+      const int q = q0 + u;
+      long long d2 = kInfF;
+      if (top >= 0) {
+        const long long dq = (long long)(q - top);
+        d2 = dq * dq + f_top;
+      }
+      if (!kZ) {
+        p.gout[base + (long long)q * stride] = d2 >= kInfF ? kInf32 : (unsigned)d2;
+      } else if (!isnan(ph[u])) {
+        float e;
+        if (d2 >= kInfF) e = __int_as_float(0x7f800000);             // S empty -> +inf (O11)
+        else e = copysignf((float)((double)p.s * sqrt((double)d2)), ph[u]);
+        p.esdf[(long long)slot * kBlockVox + (x & 7) + 8 * (o2 & 7) + 64 * u] = e;
+      }
+      if (top >= 0 && q == t_top) {
+        const int pr = (int)(p.meta[base + (long long)top * stride] & 0xffffu);
+        if (pr == 0xffff) { top = -1; }
+        else { top = pr; t_top = (int)(p.meta[base + (long long)top * stride] >> 16); f_top = f_at(top); }
+      }
     }
   }
 }
