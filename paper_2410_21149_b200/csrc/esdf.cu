@@ -24,12 +24,17 @@ constexpr unsigned kNone16 = 0xffffu;
 constexpr unsigned kInf32 = 0xffffffffu;
 constexpr long long kInfF = 1ll << 62;
 
+// slot of every block of the AABB (-1 = not allocated) and, per (bx, by) column, whether any block of
+// the column is allocated (pass z skips empty columns: they hold no voxel to write)
 __global__ void block_grid_kernel(const Counters* ctr, const int4* coords, int max_blocks, int* grid,
-                                  int lx, int ly, int lz, int nbx, int nby) {
+                                  unsigned char* colmask, unsigned char* rowmask, int lx, int ly, int lz, int nbx,
+                                  int nby) {
   const int nb = min(ctr->n_blocks, max_blocks);
   for (int sIdx = blockIdx.x * blockDim.x + threadIdx.x; sIdx < nb; sIdx += gridDim.x * blockDim.x) {
     int4 c = coords[sIdx];
     grid[((long long)(c.z - lz) * nby + (c.y - ly)) * nbx + (c.x - lx)] = sIdx;
+    colmask[(long long)(c.y - ly) * nbx + (c.x - lx)] = 1;
+    rowmask[(long long)(c.z - lz) * nby + (c.y - ly)] = 1;
   }
 }
 
@@ -37,6 +42,7 @@ struct XParams {
   const long long* sums;
   float* esdf;
   const int* grid;
+  const unsigned char* rowmask;   // (by, bz) block rows with allocated blocks
   unsigned short* g1;
   int nx, ny, nz, nbx, nby;
   double site_thr;
@@ -53,6 +59,11 @@ __global__ void __launch_bounds__(128) pass_x_kernel(const __grid_constant__ XPa
   const int kNeg = -(1 << 30), kPos = 1 << 30;
   for (long long row = (long long)blockIdx.x * 4 + warp; row < rows; row += (long long)gridDim.x * 4) {
     const int y = (int)(row % p.ny), z = (int)(row / p.ny);
+    if (!p.rowmask[(long long)(z >> 3) * p.nby + (y >> 3)]) {   // no block in this row: no site, no voxel
+      unsigned short* out = p.g1 + row * p.nx;
+      for (int x = lane; x < p.nx; x += 32) out[x] = (unsigned short)kNone16;
+      continue;
+    }
     const int* grow = p.grid + ((long long)(z >> 3) * p.nby + (y >> 3)) * p.nbx;
     const int lyz = 8 * (y & 7) + 64 * (z & 7);
     // 1) sites of the row -> one 32-bit mask per chunk; E placeholder (sign of D, NaN if unobserved)
@@ -129,6 +140,7 @@ struct LineParams {
   unsigned* meta;           // per-voxel stack links {start t: hi 16, prev: lo 16}
   float* esdf;              // pass z output (ESDF blocks)
   const int* grid;
+  const unsigned char* colmask;   // (bx, by) columns with allocated blocks
   int nx, ny, nz, nbx, nby;
   float s;
 };
@@ -148,6 +160,7 @@ __global__ void __launch_bounds__(256) pass_line_kernel(const __grid_constant__ 
   const int m = kZ ? p.nz : p.ny;
   const long long stride = kZ ? (long long)p.nx * p.ny : (long long)p.nx;
   const long long base = kZ ? (long long)o2 * p.nx + x : (long long)o2 * p.nx * p.ny + x;
+  if (kZ && !p.colmask[(long long)(o2 >> 3) * p.nbx + (x >> 3)]) return;   // no allocated voxel in this line
   auto f_at = [&](int q) -> long long {
     if (kZ) {
       unsigned v = static_cast<const unsigned*>(p.fin)[base + q * stride];
@@ -249,7 +262,7 @@ cudaError_t launch_finalize(cvx_submap* sm, int n_blocks, const int lo[3], const
     if ((e = cudaMalloc(&sm->block_grid, sizeof(int) * (size_t)nblk)) != cudaSuccess) return e;
     sm->block_grid_cap = nblk;
   }
-  const long long need = nvox * (2 + 4 + 4) + 256;
+  const long long need = nvox * (2 + 4 + 4) + (long long)nbx * nby + (long long)nby * nbz + 256;
   if (sm->edt_bytes < need) {
     if (sm->edt) cudaFree(sm->edt);
     sm->edt = nullptr; sm->edt_bytes = 0;
@@ -260,14 +273,17 @@ cudaError_t launch_finalize(cvx_submap* sm, int n_blocks, const int lo[3], const
   unsigned* meta = g2 + nvox;
   unsigned short* g1 = reinterpret_cast<unsigned short*>(meta + nvox);
 
+  unsigned char* colmask = reinterpret_cast<unsigned char*>(g1 + nvox);
   cudaMemsetAsync(sm->block_grid, 0xff, sizeof(int) * (size_t)nblk, st);
+  unsigned char* rowmask = colmask + (size_t)nbx * nby;
+  cudaMemsetAsync(colmask, 0, (size_t)nbx * nby + (size_t)nby * nbz, st);
   {
     ProfScope ps_(sm, "esdf_block_grid", st);
     block_grid_kernel<<<148 * 4, 256, 0, st>>>(sm->ctr, sm->pool.coords, sm->pool.max_blocks, sm->block_grid,
-                                               lo[0], lo[1], lo[2], nbx, nby);
+                                               colmask, rowmask, lo[0], lo[1], lo[2], nbx, nby);
   }
   XParams xp;
-  xp.sums = sm->pool.sums; xp.esdf = sm->pool.esdf; xp.grid = sm->block_grid; xp.g1 = g1;
+  xp.sums = sm->pool.sums; xp.esdf = sm->pool.esdf; xp.grid = sm->block_grid; xp.g1 = g1; xp.rowmask = rowmask;
   xp.nx = nx; xp.ny = ny; xp.nz = nz; xp.nbx = nbx; xp.nby = nby; xp.site_thr = sm->cfg.site_threshold;
   const int nch = (nx + 31) / 32;
   const size_t smem = (size_t)4 * 3 * nch * sizeof(unsigned);
@@ -280,7 +296,7 @@ cudaError_t launch_finalize(cvx_submap* sm, int n_blocks, const int lo[3], const
   }
 
   LineParams lp;
-  lp.fin = g1; lp.gout = g2; lp.meta = meta; lp.esdf = sm->pool.esdf; lp.grid = sm->block_grid;
+  lp.fin = g1; lp.gout = g2; lp.meta = meta; lp.esdf = sm->pool.esdf; lp.grid = sm->block_grid; lp.colmask = colmask;
   lp.nx = nx; lp.ny = ny; lp.nz = nz; lp.nbx = nbx; lp.nby = nby; lp.s = (float)sm->cfg.voxel_size;
   long long nl = (long long)nx * nz;
   {
