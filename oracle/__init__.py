@@ -70,6 +70,8 @@ def lib():
             L.orc_ray_voxels.argtypes = [P, P, C.c_double, C.c_double, C.c_int32, P, C.c_int64]
             L.orc_esdf.restype = C.c_int32
             L.orc_esdf.argtypes = [P, P, P, C.c_int64, C.c_double, C.c_double, C.c_int32, P, P]
+            L.orc_esdf_sample.restype = C.c_int32
+            L.orc_esdf_sample.argtypes = [P, P, P, C.c_int64, C.c_double, P, C.c_int64, P]
             L.orc_query.restype = C.c_int32
             L.orc_query.argtypes = [P, P, C.c_int64, C.c_double, P, P, C.c_int64, P, P]
             _lib = L
@@ -161,6 +163,18 @@ def esdf(bxyz, D, W, voxel_size: float, site_threshold: float, brute: bool = Fal
         rc = lib().orc_esdf(_p(b), _p(Dd), _p(Wd), nb, voxel_size, site_threshold, int(brute), _p(E), _p(d2))
         assert rc == 0
     return E, d2
+
+
+def esdf_sample(bxyz, D, W, site_threshold: float, voxels):
+    """Brute-force squared distance (voxel units) of each sample voxel [m,3] to the nearest site; -1 = none."""
+    b = np.ascontiguousarray(bxyz, dtype=np.int32)
+    Dd = np.ascontiguousarray(D, dtype=np.float64)
+    Wd = np.ascontiguousarray(W, dtype=np.float64)
+    v = np.ascontiguousarray(voxels, dtype=np.int64)
+    out = np.zeros(v.shape[0], np.int64)
+    rc = lib().orc_esdf_sample(_p(b), _p(Dd), _p(Wd), b.shape[0], site_threshold, _p(v), v.shape[0], _p(out))
+    assert rc == 0
+    return out
 
 
 def query(bxyz, E, voxel_size: float, T_world_submap, pts):

@@ -394,6 +394,30 @@ int32_t orc_esdf(const int32_t* bxyz, const double* D, const double* W, int64_t 
   return 0;
 }
 
+// Brute force O11 at sample voxels (full-size parity): d2 of each sample voxel (int64 [m][3] voxel
+// coordinates) to the nearest site of the given TSDF, literally min over all sites; -1 if no site.
+int32_t orc_esdf_sample(const int32_t* bxyz, const double* D, const double* W, int64_t nb, double site_threshold,
+                        const int64_t* vox, int64_t m, int64_t* d2_out) {
+  std::vector<V3> sites;
+  for (int64_t b = 0; b < nb; ++b)
+    for (int l = 0; l < kBV; ++l) {
+      double w = W[b * kBV + l], d = D[b * kBV + l];
+      if (w > 0 && std::fabs(d) <= site_threshold)
+        sites.push_back({8 * (int64_t)bxyz[3 * b] + l % 8, 8 * (int64_t)bxyz[3 * b + 1] + (l / 8) % 8,
+                         8 * (int64_t)bxyz[3 * b + 2] + l / 64});
+    }
+  for (int64_t i = 0; i < m; ++i) {
+    int64_t best = -1;
+    for (const V3& s : sites) {
+      int64_t dx = vox[3 * i] - s.x, dy = vox[3 * i + 1] - s.y, dz = vox[3 * i + 2] - s.z;
+      int64_t dd = dx * dx + dy * dy + dz * dz;
+      if (best < 0 || dd < best) best = dd;
+    }
+    d2_out[i] = best;
+  }
+  return 0;
+}
+
 // ---------------------------------------------------------------------------------------- query
 // O13 (S:L486 trilinear over 8 ESDF voxels; S:L491 identity at a voxel centre):
 //   x_s = T_WS^-1 x ; g = x_s/s - 1/2 ; i0 = floor(g) ; f = g - i0.

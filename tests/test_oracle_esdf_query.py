@@ -131,3 +131,14 @@ def test_query_status_and_pose(orc):
     assert st.tolist() == [2, 1, 2, 0]
     assert np.isnan(val[0]) and np.isnan(val[2])
     assert val[1] == pytest.approx(E[13, 1 + 8 + 64])
+
+
+def test_esdf_sample_equals_full_transform(orc):
+    rng = np.random.default_rng(9)
+    b, D, W = _random_tsdf(rng)
+    E, d2 = orc.esdf(b, D, W, 0.1, 0.02, brute=True)
+    l = np.arange(512)
+    vox = np.stack([8 * b[:, 0:1] + l % 8, 8 * b[:, 1:2] + (l // 8) % 8, 8 * b[:, 2:3] + l // 64], -1).reshape(-1, 3)
+    pick = rng.choice(vox.shape[0], 300, replace=False)
+    s = orc.esdf_sample(b, D, W, 0.02, vox[pick])
+    assert np.array_equal(s, d2.reshape(-1)[pick])
