@@ -171,6 +171,31 @@ def cpu_baseline_sample(cfg, data, poses, n=12):
             "seconds": t2 - t0}
 
 
+NCU_FILES = {"ray_walk_update": "ncu_walk.txt", "block_walk_allocate": "ncu_block_walk.txt",
+             "ray_prepare": "ncu_prepare.txt", "esdf_pass_x": "ncu_esdf_pass_x.txt",
+             "esdf_pass_y": "ncu_esdf_pass_y.txt", "esdf_pass_z": "ncu_esdf_pass_z.txt", "fold": "ncu_fold.txt"}
+
+
+def ncu_traffic(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from the newest committed
+    `ncu --set full` capture under profiles/ (None if there is none)."""
+    prof = os.path.join(ROOT, "profiles")
+    if kernel not in NCU_FILES or not os.path.isdir(prof):
+        return None
+    for tag in sorted(os.listdir(prof), reverse=True):
+        f = os.path.join(prof, tag, NCU_FILES[kernel])
+        if not os.path.exists(f):
+            continue
+        tot = 0.0
+        for line in open(f):
+            parts = line.split()
+            if parts and parts[0] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(parts[1], 1)
+                tot += float(parts[2]) * scale
+        return {"bytes_per_launch": tot, "source": f"profiles/{tag}/{NCU_FILES[kernel]}"}
+    return None
+
+
 # ------------------------------------------------------------------------------------ product arm
 def main():
     ap = argparse.ArgumentParser()
@@ -353,6 +378,7 @@ def main():
                     "frac": ach / peak_tops, "traffic": None,
                     "updates_per_s": upd_launch / (avg_ms / 1e3), "ops_per_update": 13,
                     "peak_source": f"148 SM x 128 lanes x {clk_mhz:.0f} MHz (median under load)"}
+    roofline["traffic"] = ncu_traffic(dom)
     line = {
         "metric": METRIC, "value": value, "unit": "scans/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,

@@ -1,0 +1,24 @@
+#!/bin/bash
+# One GPU session of evidence for profiles/: default bench line, ncu launch list of our kernels, and one
+# `ncu --set full` capture per hot kernel.  usage: tools/capture_round.sh <tag> [what...]
+T=${1:-r1}; shift
+mkdir -p gpurun_out/$T
+cap() {  # <regex on the base function name> <name> <skip>
+  timeout 900 ncu --set full --clock-control none --import-source on -k "regex:$1" -s $3 -c 1 -o gpurun_out/$T/$2 \
+    python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > gpurun_out/$T/$2.log 2>&1; echo "ncu $2 rc=$?"
+}
+WHAT=${@:-bench launches walk block_walk prepare fold esdf_pass_x esdf_pass_y esdf_pass_z query}
+for w in $WHAT; do case $w in
+  bench) timeout 600 python bench.py > gpurun_out/$T/bench.json 2> gpurun_out/$T/bench.err; echo "bench rc=$?";;
+  launches) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base mangled \
+      -k regex:_ZN3cvx --csv --log-file gpurun_out/$T/launches.csv python bench.py --steps 1 --warmup 1 \
+      --no-cpu-baseline --no-e2e > gpurun_out/$T/launches_bench.json 2>&1; echo "launches rc=$?";;
+  walk) cap "^walk_kernel" walk 6;;
+  block_walk) cap "^block_walk_kernel" block_walk 6;;
+  prepare) cap "^prepare_kernel" prepare 6;;
+  fold) cap "^fold_kernel" fold 6;;
+  esdf_pass_x) cap "^pass_x_kernel" esdf_pass_x 1;;
+  esdf_pass_y) cap "^pass_line_kernel" esdf_pass_y 2;;
+  esdf_pass_z) cap "^pass_line_kernel" esdf_pass_z 3;;
+  query) cap "^query_kernel" query 0;;
+esac; done

@@ -1,0 +1,75 @@
+"""Write profiles/<tag>/ from a gpurun_out/<tag>/ capture (tools/capture_round.sh): the bench line, the
+ncu launch list, per-kernel ncu summaries and a markdown digest.  usage: python tools/make_profile_md.py r1"""
+import json
+import os
+import shutil
+import subprocess
+import sys
+
+tag = sys.argv[1]
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+src = os.path.join(ROOT, "gpurun_out", tag)
+dst = os.path.join(ROOT, "profiles", tag)
+os.makedirs(dst, exist_ok=True)
+bench = json.loads(open(os.path.join(src, "bench.json")).read().strip().splitlines()[-1])
+json.dump(bench, open(os.path.join(dst, "bench.json"), "w"), indent=1)
+shutil.copy(os.path.join(src, "launches.csv"), os.path.join(dst, "launches.csv"))
+shares = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "launch_shares.py"), os.path.join(src, "launches.csv"),
+                         os.path.join(src, "bench.json")], capture_output=True, text=True).stdout
+kern = ["walk", "block_walk", "prepare", "fold", "esdf_pass_x", "esdf_pass_y", "esdf_pass_z", "query"]
+summ = {}
+for k in kern:
+    rep = os.path.join(src, k + ".ncu-rep")
+    if os.path.exists(rep):
+        out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"), rep, "12"],
+                             capture_output=True, text=True).stdout
+        open(os.path.join(dst, f"ncu_{k}.txt"), "w").write(out)
+        summ[k] = out
+if os.path.exists(os.path.join(src, "walk.ncu-rep")):
+    shutil.copy(os.path.join(src, "walk.ncu-rep"), os.path.join(dst, "walk.ncu-rep"))
+
+
+def metric(txt, name):
+    for line in txt.splitlines():
+        if line.startswith(name):
+            return line[40:].split()[-1]
+    return "-"
+
+
+rows = []
+for k, t in summ.items():
+    rows.append(f"| {k} | {metric(t, 'Duration')} {'ms' if 'Duration                                 ms' in t else 'us'} | "
+                f"{metric(t, 'DRAM Throughput')} % | {metric(t, 'Issue Slots Busy')} % | {metric(t, 'Avg. Active Threads Per Warp')} | "
+                f"{metric(t, 'Achieved Occupancy')} % | {metric(t, 'dram__bytes_read.sum')} / {metric(t, 'dram__bytes_write.sum')} MB |")
+b = bench
+md = f"""# Profile {tag} — bench line, launch list and ncu captures
+
+Produced by `tools/capture_round.sh {tag}` on one B200 (gpurun) and `tools/make_profile_md.py {tag}`.
+ncu numbers come from separate profiled runs (`--clock-control none`, serialised, cold caches);
+the bench numbers come from an unprofiled run with CUDA events.
+
+## Bench (`bench.py`, N = 1, configs[1]: 200 OS1-64 scans, 0.2 m voxels)
+
+* value **{b['value']:.0f} scans/s** ({b['ms_per_step']:.2f} ms per submap step); e2e (host buffers) {b['e2e']['value']:.0f} scans/s
+* ESDF {b['esdf_mvox_per_s']:.0f} Mvox/s allocated ({b['esdf_dense_mvox_per_s']:.0f} Mvox/s over the dense AABB {b['aabb_voxels']})
+* voxel updates per step {b['voxel_updates_per_step']:.3e}, blocks {b['blocks']}
+* roofline (dominant kernel `{b['roofline']['kernel']}`): bound {b['roofline']['bound']}, achieved {b['roofline']['achieved']:.2f} of {b['roofline']['peak']:.1f} {b['roofline']['unit']} (frac {b['roofline']['frac']:.3f}); {b['roofline'].get('updates_per_s', 0):.3e} voxel updates/s
+* clocks {b['clocks']}
+* cpu_baseline (oracle, {b['cpu_baseline']['cores']} core): {b['cpu_baseline']['value']:.2f} scans/s — {b['cpu_baseline']['sample']}
+
+## Kernel shares: ncu launch list vs bench CUDA events
+
+```
+{shares}```
+
+## ncu (`--set full`) per kernel, one launch each
+
+| kernel | duration | DRAM thr | issue busy | active thr/warp | achieved occ | DRAM read / write |
+|---|---|---|---|---|---|---|
+""" + "\n".join(rows) + """
+
+Per-kernel stall breakdowns and the hottest SASS lines: `ncu_<kernel>.txt`. The dominant kernel's
+full report is `walk.ncu-rep` (open with `ncu -i`).
+"""
+open(os.path.join(dst, "summary.md"), "w").write(md)
+print(md)
