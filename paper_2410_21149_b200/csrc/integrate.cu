@@ -24,6 +24,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <type_traits>
 
 #include "submap.h"
 
@@ -327,8 +328,15 @@ __global__ void __launch_bounds__(256) block_walk_kernel(const __grid_constant__
   }
 }
 
-template <bool kAggregate, bool kConstW>
+// k32: the crossing-order differences fit 32 bits.  With r_i = rho_i + m_i 2^16 (m_i crossings done),
+// E_ij = X_ij - X_ji = C_ij + 2^16 F_ij with C_ij = rho_i a_j - rho_j a_i and F_ij = m_i a_j - m_j a_i, so
+// E_ij > 0  <=>  H_ij = F_ij - floor(-C_ij / 2^16) > 0; H_ij moves by a_j / -a_i per step like E_ij by
+// 2^16 a_j / -2^16 a_i, and |H_ij| <= 3 max(a) while both axes have crossings left.  Exact whenever
+// every |D_a| < 2^28 (spans < 2^12 voxels), which the launch checks from the sensor's max range.
+template <bool kAggregate, bool kConstW, bool k32>
 __global__ void __launch_bounds__(256, 4) walk_kernel(const __grid_constant__ WalkParams p) {
+  using DT = typename std::conditional<k32, unsigned, unsigned long long>::type;
+  using ST = typename std::conditional<k32, int, long long>::type;
   const int n_rays = *(volatile int*)&p.ctr->n_rays;
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
@@ -338,7 +346,7 @@ __global__ void __launch_bounds__(256, 4) walk_kernel(const __grid_constant__ Wa
   // DDA state (O4).  With X_ij = r_i |D_j|, axis i crosses before axis j <=> X_ij < X_ji; only the
   // three differences D01 = X01 - X10, D02 = X02 - X20, D12 = X12 - X21 are kept (exact int64).
   int v0 = 0, v1 = 0, v2 = 0, s0 = 1, s1 = 1, s2 = 1, k0 = 0, k1 = 0, k2 = 0, c0 = 0, c1 = 0, c2 = 0;
-  long long D01 = 0, D02 = 0, D12 = 0, I0 = 0, I1 = 0, I2 = 0;
+  DT D01 = 0, D02 = 0, D12 = 0, I0 = 0, I1 = 0, I2 = 0;   // wrap-around arithmetic, compared signed
   long long S = 0, U0 = 0, U1 = 0, U2 = 0;   // fixed-point sdf of the current voxel and its decrements
   int n = 0, nblk = 0, off = -1;
   long long w_fx = 0;
@@ -362,10 +370,16 @@ __global__ void __launch_bounds__(256, 4) walk_kernel(const __grid_constant__ Wa
     }
     v0 = va[0]; v1 = va[1]; v2 = va[2]; s0 = st[0]; s1 = st[1]; s2 = st[2]; k0 = kk[0]; k1 = kk[1]; k2 = kk[2];
     c0 = s0 > 0 ? 0 : 7; c1 = s1 > 0 ? 0 : 7; c2 = s2 > 0 ? 0 : 7;   // local coordinate on block entry
-    D01 = R[0] * AD[1] - R[1] * AD[0];
-    D02 = R[0] * AD[2] - R[2] * AD[0];
-    D12 = R[1] * AD[2] - R[2] * AD[1];
-    I0 = AD[0] << 16; I1 = AD[1] << 16; I2 = AD[2] << 16;
+    const long long C01 = R[0] * AD[1] - R[1] * AD[0];
+    const long long C02 = R[0] * AD[2] - R[2] * AD[0];
+    const long long C12 = R[1] * AD[2] - R[2] * AD[1];
+    if (k32) {
+      D01 = (DT)(-((-C01) >> 16)); D02 = (DT)(-((-C02) >> 16)); D12 = (DT)(-((-C12) >> 16));
+      I0 = (DT)AD[0]; I1 = (DT)AD[1]; I2 = (DT)AD[2];
+    } else {
+      D01 = (DT)C01; D02 = (DT)C02; D12 = (DT)C12;
+      I0 = (DT)(AD[0] << 16); I1 = (DT)(AD[1] << 16); I2 = (DT)(AD[2] << 16);
+    }
     S = r.S0; U0 = r.U[0]; U1 = r.U[1]; U2 = r.U[2];
     w = r.w;
     w_fx = __double2ll_rn((double)w * kFxScale);
@@ -427,8 +441,8 @@ __global__ void __launch_bounds__(256, 4) walk_kernel(const __grid_constant__ Wa
     // x < y < z), predicated on the lane still having a voxel to go.
     const bool stp = it + 1 < n;
     const bool g0 = k0 > 0, g1 = k1 > 0, g2 = k2 > 0;
-    const bool yf = g1 & (!g0 | (D01 > 0));
-    const bool zf = g2 & (yf ? (D12 > 0) : (!g0 | (D02 > 0)));
+    const bool yf = g1 & (!g0 | ((ST)D01 > 0));
+    const bool zf = g2 & (yf ? ((ST)D12 > 0) : (!g0 | ((ST)D02 > 0)));
     const bool bz = stp & zf, by = stp & yf & !zf, bx = stp & !yf & !zf;
     if (bx) { v0 += s0; --k0; D01 += I1; D02 += I2; S -= U0; }
     if (by) { v1 += s1; --k1; D01 -= I0; D12 += I2; S -= U1; }
@@ -571,11 +585,14 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
   {
     ProfScope ps_(sm, "ray_walk_update", st);
     const bool cw = sm->cfg.weighting == 0 && total <= kMaxPackedRays;
+    // every ray spans < 2^12 voxels per axis if (max_range + tau) / s + 2 < 4096 (domain check O3 bounds
+    // the rest): then the crossing-order differences fit 32 bits (see walk_kernel)
+    const bool k32 = ((double)sensor.max_range + sm->cfg.truncation) / sm->cfg.voxel_size + 2.0 < 4096.0;
     if (sm->aggregate) {
-      if (cw) walk_kernel<true, true><<<blocks, 256, 0, st>>>(wp);
-      else walk_kernel<true, false><<<blocks, 256, 0, st>>>(wp);
+      if (cw) { if (k32) walk_kernel<true, true, true><<<blocks, 256, 0, st>>>(wp); else walk_kernel<true, true, false><<<blocks, 256, 0, st>>>(wp); }
+      else { if (k32) walk_kernel<true, false, true><<<blocks, 256, 0, st>>>(wp); else walk_kernel<true, false, false><<<blocks, 256, 0, st>>>(wp); }
     } else {
-      walk_kernel<false, false><<<blocks, 256, 0, st>>>(wp);
+      walk_kernel<false, false, false><<<blocks, 256, 0, st>>>(wp);
     }
   }
   if (sm->aggregate && sm->cfg.weighting == 0 && total <= kMaxPackedRays) {

@@ -232,3 +232,18 @@ def test_reset_and_pack_roundtrip(tiny):
     b2, D2, W2, E2 = gpu_export_sorted(sm)
     assert np.array_equal(b2, b) and np.array_equal(D2.view(np.uint32), D.view(np.uint32))
     assert np.array_equal(E2.view(np.uint32), E.view(np.uint32))
+
+
+def test_wide_and_narrow_dda_paths_agree(tiny, orc):
+    """A sensor max range beyond 4096 voxels selects the 64-bit crossing-order path of the walk; the
+    32-bit path (default) and the 64-bit path must give bit-identical TSDFs and match the oracle."""
+    frames = [0, 4, 8]
+    narrow, _ = gpu_build(tiny, frames, finalize=False)
+    wide_cfg = dict(tiny, sensor=dict(tiny["sensor"], max_range=1.0e6))
+    wide, _ = gpu_build(wide_cfg, frames, finalize=False)
+    a, b = gpu_export_sorted(narrow), gpu_export_sorted(wide)
+    assert np.array_equal(a[0], b[0])
+    assert np.array_equal(a[1].view(np.uint32), b[1].view(np.uint32))
+    assert np.array_equal(a[2].view(np.uint32), b[2].view(np.uint32))
+    o, _ = oracle_build(wide_cfg, frames)
+    assert_tsdf_parity(b, o.export())
