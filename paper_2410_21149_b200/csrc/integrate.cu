@@ -272,14 +272,17 @@ __device__ __forceinline__ void reduce_peers(unsigned m, unsigned peers, int lan
 // difference-form DDA as the voxel walk.  The loop is warp-uniform; in each step only the first lane
 // of every run of equal keys among adjacent lanes (adjacent rays) probes the hash table and the slot
 // is shuffled to the rest of the run.
+template <bool k32>   // 32-bit crossing-order differences, as in walk_kernel (unit 2^19 instead of 2^16)
 __global__ void __launch_bounds__(256) block_walk_kernel(const __grid_constant__ WalkParams p) {
+  using DT = typename std::conditional<k32, unsigned, unsigned long long>::type;
+  using ST = typename std::conditional<k32, int, long long>::type;
   const int n_rays = *(volatile int*)&p.ctr->n_rays;
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   if ((idx & ~31) >= n_rays) return;
   const bool have = idx < n_rays;
   int b0 = 0, b1 = 0, b2 = 0, s0 = 1, s1 = 1, s2 = 1, k0 = 0, k1 = 0, k2 = 0, nb = 0;
-  long long D01 = 0, D02 = 0, D12 = 0, I0 = 0, I1 = 0, I2 = 0;
+  DT D01 = 0, D02 = 0, D12 = 0, I0 = 0, I1 = 0, I2 = 0;
   int* list = nullptr;
   if (have) {
     const RayRec r = p.rays[idx];
@@ -297,10 +300,16 @@ __global__ void __launch_bounds__(256) block_walk_kernel(const __grid_constant__
     }
     b0 = bb[0]; b1 = bb[1]; b2 = bb[2]; s0 = st[0]; s1 = st[1]; s2 = st[2]; k0 = kk[0]; k1 = kk[1]; k2 = kk[2];
     nb = 1 + k0 + k1 + k2;
-    D01 = R[0] * AD[1] - R[1] * AD[0];
-    D02 = R[0] * AD[2] - R[2] * AD[0];
-    D12 = R[1] * AD[2] - R[2] * AD[1];
-    I0 = AD[0] << 19; I1 = AD[1] << 19; I2 = AD[2] << 19;
+    const long long C01 = R[0] * AD[1] - R[1] * AD[0];
+    const long long C02 = R[0] * AD[2] - R[2] * AD[0];
+    const long long C12 = R[1] * AD[2] - R[2] * AD[1];
+    if (k32) {
+      D01 = (DT)(-((-C01) >> 19)); D02 = (DT)(-((-C02) >> 19)); D12 = (DT)(-((-C12) >> 19));
+      I0 = (DT)AD[0]; I1 = (DT)AD[1]; I2 = (DT)AD[2];
+    } else {
+      D01 = (DT)C01; D02 = (DT)C02; D12 = (DT)C12;
+      I0 = (DT)(AD[0] << 19); I1 = (DT)(AD[1] << 19); I2 = (DT)(AD[2] << 19);
+    }
     list = r.list_off >= 0 ? p.slots + r.list_off : nullptr;
   }
   const int maxnb = (int)__reduce_max_sync(0xffffffffu, (unsigned)nb);
@@ -319,8 +328,8 @@ __global__ void __launch_bounds__(256) block_walk_kernel(const __grid_constant__
     // O4 at block granularity: earliest crossing among axes with crossings left, ties x < y < z
     const bool stp = j + 1 < nb;
     const bool g0 = k0 > 0, g1 = k1 > 0, g2 = k2 > 0;
-    const bool yf = g1 & (!g0 | (D01 > 0));
-    const bool zf = g2 & (yf ? (D12 > 0) : (!g0 | (D02 > 0)));
+    const bool yf = g1 & (!g0 | ((ST)D01 > 0));
+    const bool zf = g2 & (yf ? ((ST)D12 > 0) : (!g0 | ((ST)D02 > 0)));
     const bool bz = stp & zf, by = stp & yf & !zf, bx = stp & !yf & !zf;
     if (bx) { b0 += s0; --k0; D01 += I1; D02 += I2; }
     if (by) { b1 += s1; --k1; D01 -= I0; D12 += I2; }
@@ -578,16 +587,17 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
   wp.s = (float)sm->cfg.voxel_size; wp.tau = (float)sm->cfg.truncation;
   wp.tq = (int)std::llround(std::ldexp(sm->cfg.truncation, q));
   wp.q = q;
+  // every ray spans < 2^12 voxels per axis if (max_range + tau) / s + 2 < 4096 (domain check O3 bounds
+  // the rest): then the crossing-order differences fit 32 bits (see walk_kernel)
+  const bool k32 = ((double)sensor.max_range + sm->cfg.truncation) / sm->cfg.voxel_size + 2.0 < 4096.0;
   {
     ProfScope ps_(sm, "block_walk_allocate", st);
-    block_walk_kernel<<<blocks, 256, 0, st>>>(wp);
+    if (k32) block_walk_kernel<true><<<blocks, 256, 0, st>>>(wp);
+    else block_walk_kernel<false><<<blocks, 256, 0, st>>>(wp);
   }
   {
     ProfScope ps_(sm, "ray_walk_update", st);
     const bool cw = sm->cfg.weighting == 0 && total <= kMaxPackedRays;
-    // every ray spans < 2^12 voxels per axis if (max_range + tau) / s + 2 < 4096 (domain check O3 bounds
-    // the rest): then the crossing-order differences fit 32 bits (see walk_kernel)
-    const bool k32 = ((double)sensor.max_range + sm->cfg.truncation) / sm->cfg.voxel_size + 2.0 < 4096.0;
     if (sm->aggregate) {
       if (cw) { if (k32) walk_kernel<true, true, true><<<blocks, 256, 0, st>>>(wp); else walk_kernel<true, true, false><<<blocks, 256, 0, st>>>(wp); }
       else { if (k32) walk_kernel<true, false, true><<<blocks, 256, 0, st>>>(wp); else walk_kernel<true, false, false><<<blocks, 256, 0, st>>>(wp); }
