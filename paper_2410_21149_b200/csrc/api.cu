@@ -105,9 +105,18 @@ void free_all(cvx_submap* sm) {
   if (sm->pool.coords) cudaFree(sm->pool.coords);
   if (sm->ctr) cudaFree(sm->ctr);
   if (sm->ctr_host) cudaFreeHost(sm->ctr_host);
-  if (sm->frame_T) cudaFree(sm->frame_T);
-  if (sm->rays) cudaFree(sm->rays);
-  if (sm->slot_lists) cudaFree(sm->slot_lists);
+  for (auto& B : sm->buf) {
+    if (B.frame_T) cudaFree(B.frame_T);
+    if (B.rays) cudaFree(B.rays);
+    if (B.slot_lists) cudaFree(B.slot_lists);
+    if (B.lcnt) cudaFree(B.lcnt);
+  }
+  if (sm->side) cudaStreamDestroy(sm->side);
+  if (sm->ev_entry) cudaEventDestroy(sm->ev_entry);
+  for (int b = 0; b < 2; ++b) {
+    if (sm->ev_prepared[b]) cudaEventDestroy(sm->ev_prepared[b]);
+    if (sm->ev_free[b]) cudaEventDestroy(sm->ev_free[b]);
+  }
   if (sm->edt) cudaFree(sm->edt);
   if (sm->block_grid) cudaFree(sm->block_grid);
   delete sm->prof;
@@ -163,7 +172,15 @@ cvx_status cvx_create_submap(const cvx_grid_config* cfg, const double* T_world_s
       (e = cudaMalloc(&sm->pool.coords, nb * 16)) != cudaSuccess ||
       (e = cudaMalloc(&sm->ctr, sizeof(cvx::Counters))) != cudaSuccess ||
       (e = cudaMallocHost(&sm->ctr_host, sizeof(cvx::Counters))) != cudaSuccess ||
-      (e = cudaMalloc(&sm->frame_T, sizeof(double) * 16 * cvx::kMaxBatch)) != cudaSuccess) {
+      (e = cudaMalloc(&sm->buf[0].frame_T, sizeof(double) * 16 * cvx::kMaxBatch)) != cudaSuccess ||
+      (e = cudaMalloc(&sm->buf[1].frame_T, sizeof(double) * 16 * cvx::kMaxBatch)) != cudaSuccess ||
+      (e = cudaMalloc(&sm->buf[0].lcnt, 16)) != cudaSuccess || (e = cudaMalloc(&sm->buf[1].lcnt, 16)) != cudaSuccess ||
+      (e = cudaStreamCreateWithFlags(&sm->side, cudaStreamNonBlocking)) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&sm->ev_entry, cudaEventDisableTiming)) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&sm->ev_prepared[0], cudaEventDisableTiming)) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&sm->ev_prepared[1], cudaEventDisableTiming)) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&sm->ev_free[0], cudaEventDisableTiming)) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&sm->ev_free[1], cudaEventDisableTiming)) != cudaSuccess) {
     free_all(sm);
     delete sm;
     return cuda_fail(e, "allocating submap");
@@ -174,6 +191,8 @@ cvx_status cvx_create_submap(const cvx_grid_config* cfg, const double* T_world_s
   cudaMemset(sm->pool.acc, 0, nb * cvx::kBlockVox * 8);
   cudaMemset(sm->pool.esdf, 0, nb * cvx::kBlockVox * 4);
   e = cvx::launch_reset(sm, 0);
+  if (e == cudaSuccess) e = cudaEventRecord(sm->ev_free[0], 0);
+  if (e == cudaSuccess) e = cudaEventRecord(sm->ev_free[1], 0);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     free_all(sm);
@@ -223,13 +242,8 @@ cvx_status cvx_integrate_batch(cvx_submap* sm, const float* data, int64_t n_per_
   DeviceGuard g(sm->device);
   if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
   cudaStream_t st = (cudaStream_t)stream;
-  int64_t ray_limit = (1ll << 31) - 1;
-  if (sm->cfg.weighting == 0 && n_per_frame <= cvx::kMaxPackedRays) ray_limit = cvx::kMaxPackedRays;  // packed accumulators
-  const int64_t per_launch = std::max<int64_t>(1, std::min<int64_t>(cvx::kMaxBatch, ray_limit / std::max<int64_t>(1, n_per_frame)));
-  for (int64_t f0 = 0; f0 < n_frames && n_per_frame > 0; f0 += per_launch) {
-    const int nf = (int)std::min<int64_t>(per_launch, n_frames - f0);
-    const int64_t elems = sensor->kind == 1 ? n_per_frame : 3 * n_per_frame;
-    cudaError_t e = cvx::launch_integrate(sm, data + f0 * elems, n_per_frame, nf, T_world_sensor + 16 * f0, *sensor, st);
+  if (n_per_frame > 0 && n_frames > 0) {
+    cudaError_t e = cvx::launch_integrate(sm, data, n_per_frame, n_frames, T_world_sensor, *sensor, st);
     if (e != cudaSuccess) return cuda_fail(e, "integrate");
   }
   if (stats) {

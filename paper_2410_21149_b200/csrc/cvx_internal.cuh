@@ -30,10 +30,6 @@ struct Counters {
   unsigned err;            // sticky ErrBits
   int aabb_lo[3];          // block coordinates
   int aabb_hi[3];
-  int n_rays;              // compacted rays of the current integrate call
-  int n_slots;             // block-slot list entries claimed by the current integrate call
-  int next_ray;            // ray queue head of the persistent update walk
-  int pad;
   unsigned long long rays_in, rays_used, skipped_invalid, skipped_range, skipped_domain, voxel_updates,
       new_blocks;
 };

@@ -103,6 +103,7 @@ struct PrepParams {
   const double* frame_T;
   RayRec* rays;
   Counters* ctr;
+  int* lcnt;        // {n_rays, n_slots} of this launch (8-byte aligned)
   int list_cap;
 };
 
@@ -222,7 +223,7 @@ __global__ void __launch_bounds__(256) prepare_kernel(const __grid_constant__ Pr
         c[t] += x;
       }
     unsigned long long base = 0;
-    if (c[0] | c[1]) base = atomicAdd(reinterpret_cast<unsigned long long*>(&p.ctr->n_rays), (c[1] << 32) | c[0]);
+    if (c[0] | c[1]) base = atomicAdd(reinterpret_cast<unsigned long long*>(p.lcnt), (c[1] << 32) | c[0]);
     s_base = base;
     if (c[2]) atomicAdd(&p.ctr->rays_in, c[2]);
     if (c[0]) atomicAdd(&p.ctr->rays_used, c[0]);
@@ -246,6 +247,7 @@ struct WalkParams {
   HashView hash;
   PoolView pool;
   int* slots;       // block-slot lists
+  const int* lcnt;  // {n_rays, n_slots} of this launch
   float s, tau;
   int tq;           // round(tau 2^q): the clamp bound (and packed offset) of the quantised sdf
   int q;            // sdf quantum 2^-q m
@@ -276,7 +278,7 @@ template <bool k32>   // 32-bit crossing-order differences, as in walk_kernel (u
 __global__ void __launch_bounds__(256) block_walk_kernel(const __grid_constant__ WalkParams p) {
   using DT = typename std::conditional<k32, unsigned, unsigned long long>::type;
   using ST = typename std::conditional<k32, int, long long>::type;
-  const int n_rays = *(volatile int*)&p.ctr->n_rays;
+  const int n_rays = p.lcnt[0];
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   if ((idx & ~31) >= n_rays) return;
@@ -346,7 +348,7 @@ template <bool kAggregate, bool kConstW, bool k32>
 __global__ void __launch_bounds__(256, 4) walk_kernel(const __grid_constant__ WalkParams p) {
   using DT = typename std::conditional<k32, unsigned, unsigned long long>::type;
   using ST = typename std::conditional<k32, int, long long>::type;
-  const int n_rays = *(volatile int*)&p.ctr->n_rays;
+  const int n_rays = p.lcnt[0];
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   if ((idx & ~31) >= n_rays) return;                       // whole warp beyond the rays
@@ -530,84 +532,105 @@ cudaError_t launch_reset(cvx_submap* sm, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+static cudaError_t grow(void** ptr, int64_t* cap, int64_t need, size_t elem) {
+  if (*cap >= need) return cudaSuccess;
+  if (*ptr) cudaFree(*ptr);
+  *ptr = nullptr;
+  *cap = 0;
+  cudaError_t e = cudaMalloc(ptr, elem * (size_t)need);
+  if (e == cudaSuccess) *cap = need;
+  return e;
+}
+
 cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_frame, int n_frames,
                              const double* T_world_sensor, const cvx_sensor_model& sensor, cudaStream_t st) {
-  const long long total = (long long)n_per_frame * n_frames;
-  if (total <= 0) return cudaSuccess;
-  if (sm->ray_cap < total) {
-    if (sm->rays) cudaFree(sm->rays);
-    sm->rays = nullptr;
-    sm->ray_cap = 0;
-    cudaError_t e = cudaMalloc(&sm->rays, sizeof(RayRec) * (size_t)total);
+  if (n_per_frame <= 0 || n_frames <= 0) return cudaSuccess;
+  // launches of equal size; at most kMaxBatch frames, and (constant weights) <= kMaxPackedRays rays so
+  // the packed accumulators cannot overflow (R6/R7)
+  const bool cw_ok = sm->aggregate && sm->cfg.weighting == 0 && n_per_frame <= kMaxPackedRays;
+  const long long ray_limit = cw_ok ? kMaxPackedRays : (1ll << 31) - 1;
+  const int lim = (int)std::max<long long>(1, std::min<long long>(kMaxBatch, ray_limit / n_per_frame));
+  const int chunks = (n_frames + lim - 1) / lim;
+  const int per = (n_frames + chunks - 1) / chunks;
+  const long long cap_rays = (long long)per * n_per_frame;
+  for (int b = 0; b < 2; ++b) {
+    cudaError_t e = grow(&sm->buf[b].rays, &sm->buf[b].ray_cap, cap_rays, sizeof(RayRec));
+    if (e == cudaSuccess) e = grow(reinterpret_cast<void**>(&sm->buf[b].slot_lists), &sm->buf[b].slot_cap,
+                                   cap_rays * kSlotsPerRay + 1024, sizeof(int));
     if (e != cudaSuccess) return e;
-    sm->ray_cap = total;
   }
-  const long long list_need = total * kSlotsPerRay + 1024;
-  if (sm->slot_cap < list_need) {
-    if (sm->slot_lists) cudaFree(sm->slot_lists);
-    sm->slot_lists = nullptr;
-    sm->slot_cap = 0;
-    cudaError_t e = cudaMalloc(&sm->slot_lists, sizeof(int) * (size_t)list_need);
-    if (e != cudaSuccess) return e;
-    sm->slot_cap = list_need;
-  }
-  ComposeParams cp;
-  for (int i = 0; i < 16; ++i) cp.Tws[i] = sm->T_ws[i];
-  for (int f = 0; f < n_frames; ++f)
-    for (int i = 0; i < 16; ++i) cp.Twc[f][i] = T_world_sensor[16 * f + i];
-  cp.n = n_frames;
-  cp.s = sm->cfg.voxel_size;
-  {
-    ProfScope ps_(sm, "compose_poses", st);
-    compose_kernel<<<1, kMaxBatch, 0, st>>>(cp, sm->frame_T);
-  }
-  cudaMemsetAsync(&sm->ctr->n_rays, 0, 4 * sizeof(int), st);   // n_rays, n_slots, next_ray, pad
-
-  PrepParams pp;
-  pp.data = data; pp.n_per_frame = n_per_frame; pp.total = total;
-  pp.kind = sensor.kind; pp.width = sensor.width;
-  pp.fx = sensor.fx; pp.fy = sensor.fy; pp.cx = sensor.cx; pp.cy = sensor.cy;
-  pp.rmin = (double)sensor.min_range; pp.rmax = (double)sensor.max_range;
-  pp.s = sm->cfg.voxel_size; pp.tau = sm->cfg.truncation; pp.rfloor = sm->cfg.weight_range_floor;
-  pp.weighting = sm->cfg.weighting; pp.carve = sm->cfg.carve;
   const int q = packed_q(sm->cfg.truncation);
-  pp.sdf_scale = std::ldexp(1.0, q + kSdfF);
-  pp.height = sensor.height;
-  pp.frame_T = sm->frame_T; pp.rays = (RayRec*)sm->rays; pp.ctr = sm->ctr;
-  pp.list_cap = (int)std::min<long long>(sm->slot_cap, 0x7fffffffll);
-  const unsigned blocks = (unsigned)((total + 255) / 256);
-  {
-    ProfScope ps_(sm, "ray_prepare", st);
-    prepare_kernel<<<blocks, 256, 0, st>>>(pp);
-  }
-
-  WalkParams wp;
-  wp.rays = (const RayRec*)sm->rays; wp.ctr = sm->ctr; wp.hash = sm->hash; wp.pool = sm->pool;
-  wp.slots = sm->slot_lists;
-  wp.s = (float)sm->cfg.voxel_size; wp.tau = (float)sm->cfg.truncation;
-  wp.tq = (int)std::llround(std::ldexp(sm->cfg.truncation, q));
-  wp.q = q;
+  const int tq = (int)std::llround(std::ldexp(sm->cfg.truncation, q));
   // every ray spans < 2^12 voxels per axis if (max_range + tau) / s + 2 < 4096 (domain check O3 bounds
   // the rest): then the crossing-order differences fit 32 bits (see walk_kernel)
   const bool k32 = ((double)sensor.max_range + sm->cfg.truncation) / sm->cfg.voxel_size + 2.0 < 4096.0;
-  {
-    ProfScope ps_(sm, "block_walk_allocate", st);
-    if (k32) block_walk_kernel<true><<<blocks, 256, 0, st>>>(wp);
-    else block_walk_kernel<false><<<blocks, 256, 0, st>>>(wp);
-  }
-  {
-    ProfScope ps_(sm, "ray_walk_update", st);
-    const bool cw = sm->cfg.weighting == 0 && total <= kMaxPackedRays;
-    if (sm->aggregate) {
-      if (cw) { if (k32) walk_kernel<true, true, true><<<blocks, 256, 0, st>>>(wp); else walk_kernel<true, true, false><<<blocks, 256, 0, st>>>(wp); }
-      else { if (k32) walk_kernel<true, false, true><<<blocks, 256, 0, st>>>(wp); else walk_kernel<true, false, false><<<blocks, 256, 0, st>>>(wp); }
-    } else {
-      walk_kernel<false, false, false><<<blocks, 256, 0, st>>>(wp);
+  cudaEventRecord(sm->ev_entry, st);                 // the side stream starts after the caller's prior work
+  cudaStreamWaitEvent(sm->side, sm->ev_entry, 0);
+  for (int f0 = 0; f0 < n_frames; f0 += per) {
+    const int nf = std::min(per, n_frames - f0);
+    const long long total = (long long)nf * n_per_frame;
+    const int b = sm->next_buf;
+    sm->next_buf ^= 1;
+    cvx_submap::Buf& B = sm->buf[b];
+    const unsigned blocks = (unsigned)((total + 255) / 256);
+    // ---- side stream: a1-a3 (compose, prepare/COUNT, ALLOCATE) into buffer b
+    cudaStreamWaitEvent(sm->side, sm->ev_free[b], 0);   // the walk that last read buffer b is done
+    ComposeParams cp;
+    for (int i = 0; i < 16; ++i) cp.Tws[i] = sm->T_ws[i];
+    for (int f = 0; f < nf; ++f)
+      for (int i = 0; i < 16; ++i) cp.Twc[f][i] = T_world_sensor[16 * (f0 + f) + i];
+    cp.n = nf;
+    cp.s = sm->cfg.voxel_size;
+    {
+      ProfScope ps_(sm, "compose_poses", sm->side);
+      compose_kernel<<<1, kMaxBatch, 0, sm->side>>>(cp, B.frame_T);
     }
-  }
-  if (sm->aggregate && sm->cfg.weighting == 0 && total <= kMaxPackedRays) {
-    ProfScope ps_(sm, "fold", st);
-    fold_kernel<<<148 * 8, 256, 0, st>>>(sm->ctr, sm->pool.acc, sm->pool.sums, sm->pool.max_blocks, wp.tq, 30 - q);
+    cudaMemsetAsync(B.lcnt, 0, 4 * sizeof(int), sm->side);
+    PrepParams pp;
+    pp.data = data + (long long)f0 * n_per_frame * (sensor.kind == 1 ? 1 : 3);
+    pp.n_per_frame = n_per_frame; pp.total = total;
+    pp.kind = sensor.kind; pp.width = sensor.width;
+    pp.fx = sensor.fx; pp.fy = sensor.fy; pp.cx = sensor.cx; pp.cy = sensor.cy;
+    pp.rmin = (double)sensor.min_range; pp.rmax = (double)sensor.max_range;
+    pp.s = sm->cfg.voxel_size; pp.tau = sm->cfg.truncation; pp.rfloor = sm->cfg.weight_range_floor;
+    pp.weighting = sm->cfg.weighting; pp.carve = sm->cfg.carve;
+    pp.sdf_scale = std::ldexp(1.0, q + kSdfF);
+    pp.height = sensor.height;
+    pp.frame_T = B.frame_T; pp.rays = (RayRec*)B.rays; pp.ctr = sm->ctr; pp.lcnt = B.lcnt;
+    pp.list_cap = (int)std::min<long long>(B.slot_cap, 0x7fffffffll);
+    {
+      ProfScope ps_(sm, "ray_prepare", sm->side);
+      prepare_kernel<<<blocks, 256, 0, sm->side>>>(pp);
+    }
+    WalkParams wp;
+    wp.rays = (const RayRec*)B.rays; wp.ctr = sm->ctr; wp.hash = sm->hash; wp.pool = sm->pool;
+    wp.slots = B.slot_lists; wp.lcnt = B.lcnt;
+    wp.s = (float)sm->cfg.voxel_size; wp.tau = (float)sm->cfg.truncation;
+    wp.tq = tq;
+    wp.q = q;
+    {
+      ProfScope ps_(sm, "block_walk_allocate", sm->side);
+      if (k32) block_walk_kernel<true><<<blocks, 256, 0, sm->side>>>(wp);
+      else block_walk_kernel<false><<<blocks, 256, 0, sm->side>>>(wp);
+    }
+    cudaEventRecord(sm->ev_prepared[b], sm->side);
+    // ---- caller's stream: a4 UPDATE + a5 FOLD of launch k
+    cudaStreamWaitEvent(st, sm->ev_prepared[b], 0);
+    const bool cw = cw_ok && total <= kMaxPackedRays;
+    {
+      ProfScope ps_(sm, "ray_walk_update", st);
+      if (sm->aggregate) {
+        if (cw) { if (k32) walk_kernel<true, true, true><<<blocks, 256, 0, st>>>(wp); else walk_kernel<true, true, false><<<blocks, 256, 0, st>>>(wp); }
+        else { if (k32) walk_kernel<true, false, true><<<blocks, 256, 0, st>>>(wp); else walk_kernel<true, false, false><<<blocks, 256, 0, st>>>(wp); }
+      } else {
+        walk_kernel<false, false, false><<<blocks, 256, 0, st>>>(wp);
+      }
+    }
+    if (cw) {
+      ProfScope ps_(sm, "fold", st);
+      fold_kernel<<<148 * 8, 256, 0, st>>>(sm->ctr, sm->pool.acc, sm->pool.sums, sm->pool.max_blocks, tq, 30 - q);
+    }
+    cudaEventRecord(sm->ev_free[b], st);
   }
   return cudaGetLastError();
 }

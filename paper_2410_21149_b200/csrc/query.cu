@@ -149,16 +149,18 @@ cudaError_t launch_export(const cvx_submap* sm, int n_blocks, int32_t* bxyz, flo
 cudaError_t launch_import(cvx_submap* sm, const int32_t* bxyz, const float* D, const float* W, int64_t n,
                           cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  // slots scratch: reuse the ray buffer if big enough, else grow it
-  const size_t need = sizeof(int) * (size_t)n;
-  if ((size_t)sm->ray_cap * 96 < need) {
-    if (sm->rays) cudaFree(sm->rays);
-    sm->rays = nullptr; sm->ray_cap = 0;
-    cudaError_t e = cudaMalloc(&sm->rays, need);
+  // slots scratch: the slot-list buffer of integrate buffer 0 (grown if needed); import runs on the
+  // caller's stream after any integrate work on it, so the buffer is free
+  cvx_submap::Buf& B = sm->buf[0];
+  cudaStreamWaitEvent(st, sm->ev_free[0], 0);
+  if (B.slot_cap < n) {
+    if (B.slot_lists) cudaFree(B.slot_lists);
+    B.slot_lists = nullptr; B.slot_cap = 0;
+    cudaError_t e = cudaMalloc(&B.slot_lists, sizeof(int) * (size_t)n);
     if (e != cudaSuccess) return e;
-    sm->ray_cap = (int64_t)((need + 95) / 96);
+    B.slot_cap = n;
   }
-  int* slots = reinterpret_cast<int*>(sm->rays);
+  int* slots = B.slot_lists;
   {
     ProfScope ps_(sm, "import_slots", st);
     import_slots_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(sm->hash, sm->pool, sm->ctr, bxyz, n, slots);

@@ -46,12 +46,19 @@ struct cvx_submap {
   cvx::Counters* ctr = nullptr;       // device
   cvx::Counters* ctr_host = nullptr;  // pinned mirror for synchronising reads
 
-  // integrate scratch (grow-only)
-  double* frame_T = nullptr;  // device [kMaxBatch][16]: R_SC, t_SC, q(t_SC), flag per frame
-  void* rays = nullptr;       // device RayRec [ray_cap]
-  int64_t ray_cap = 0;
-  int* slot_lists = nullptr;  // device block-slot lists of the rays of one launch
-  int64_t slot_cap = 0;
+  // integrate scratch, double-buffered (grow-only): the ingest + ALLOCATE phases of launch k+1 run on
+  // `side` while the update walk of launch k runs on the caller's stream
+  struct Buf {
+    double* frame_T = nullptr;  // device [kMaxBatch][16]: R_SC, t_SC, q(t_SC), flag per frame
+    void* rays = nullptr;       // device RayRec [ray_cap]
+    int64_t ray_cap = 0;
+    int* slot_lists = nullptr;  // device block-slot lists of the rays of one launch
+    int64_t slot_cap = 0;
+    int* lcnt = nullptr;        // device {n_rays, n_slots, -, -} of the launch using this buffer
+  } buf[2];
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_entry = nullptr, ev_prepared[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
+  int next_buf = 0;
   bool aggregate = true;      // warp-aggregate equal-voxel updates before the L2 atomics
 
   // ESDF scratch (grow-only)
