@@ -128,8 +128,9 @@ cvx_status cvx_get_aabb(const cvx_submap* submap, int32_t* lo, int32_t* hi);
 /* Exact ESDF over the allocated blocks (O10-O12): sites S = {v : W(v) > 0 and
  * |D(v)| <= site_threshold}; E(v) = sign(D(v)) * s * sqrt(min_{u in S} |v - u|^2) for observed v,
  * NaN for unobserved v, +inf for every observed v if S is empty.  Marks the submap finalized (no more
- * integration).  Synchronising (reads the block count / AABB to size the dense EDT domain).
- * Errors: CVX_E_STATE (already finalized), CVX_E_CAPACITY / CVX_E_RANGE (sticky), CVX_E_OOM. */
+ * integration); calling it again recomputes the same ESDF (the TSDF is immutable).
+ * Synchronising (reads the block count / AABB to size the dense EDT domain).
+ * Errors: CVX_E_CAPACITY / CVX_E_RANGE (sticky), CVX_E_OOM. */
 cvx_status cvx_finalize_esdf(cvx_submap* submap, void* stream);
 
 /* Distance queries (O13).  points_world (device fp32 [m][3], world frame) ->

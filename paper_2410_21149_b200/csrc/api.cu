@@ -296,7 +296,6 @@ cvx_status cvx_get_aabb(const cvx_submap* sm, int32_t* lo, int32_t* hi) {
 cvx_status cvx_finalize_esdf(cvx_submap* sm, void* stream) {
   g_last_error.clear();
   if (!sm) return fail(CVX_E_INVALID, "submap is NULL");
-  if (sm->finalized) return fail(CVX_E_STATE, "submap already finalized");
   DeviceGuard g(sm->device);
   if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
   cudaStream_t st = (cudaStream_t)stream;

@@ -340,3 +340,54 @@ def make_config(name: str, frames=None, device="cpu", seed=None, lidar_cols: int
         out_frames[int(k)] = dict(data=gen(k, poses[k], rng), T_world_sensor=poses[k])
     return dict(name=name, grid=grid, sensor=sensor, submaps=submaps, frames=out_frames,
                 poses=poses, n_frames=n_frames, seed=seed)
+
+
+# ----------------------------------------------------------------------------- ESDF stress (configs[4])
+def esdf_stress_scene(seed: int = 4, extent=(40.0, 40.0, 10.0), n_boxes: int = 60, n_spheres: int = 40):
+    """~100 analytic boxes / spheres on a ground plane inside a 40 x 40 x 10 m volume."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    ex, ey, ez = extent
+    bc = np.column_stack([rng.uniform(1, ex - 1, n_boxes), rng.uniform(1, ey - 1, n_boxes), np.zeros(n_boxes)])
+    bh = np.column_stack([rng.uniform(0.2, 2.5, n_boxes), rng.uniform(0.2, 2.5, n_boxes), rng.uniform(0.3, 4.0, n_boxes)])
+    bc[:, 2] = bh[:, 2]
+    sc = np.column_stack([rng.uniform(1, ex - 1, n_spheres), rng.uniform(1, ey - 1, n_spheres),
+                          rng.uniform(0.3, max(0.6, ez - 0.5), n_spheres)])
+    sr = rng.uniform(0.2, 1.5, n_spheres)
+    return dict(box_c=bc, box_h=bh, sph_c=sc, sph_r=sr, extent=extent)
+
+
+def analytic_sdf(scene: dict, pts: torch.Tensor) -> torch.Tensor:
+    """Signed distance (m, negative inside) of the union of ground (z = 0), boxes and spheres at pts [N,3]."""
+    dev = pts.device
+    sdf = pts[:, 2].clone()                                               # ground plane z = 0
+    for c, h in zip(scene["box_c"], scene["box_h"]):
+        q = (pts - torch.tensor(c, dtype=pts.dtype, device=dev)).abs() - torch.tensor(h, dtype=pts.dtype, device=dev)
+        d = q.clamp(min=0).norm(dim=1) + q.max(dim=1).values.clamp(max=0)
+        sdf = torch.minimum(sdf, d)
+    for c, r in zip(scene["sph_c"], scene["sph_r"]):
+        d = (pts - torch.tensor(c, dtype=pts.dtype, device=dev)).norm(dim=1) - float(r)
+        sdf = torch.minimum(sdf, d)
+    return sdf
+
+
+def esdf_stress_blocks(voxel_size: float = 0.02, truncation: float = 0.06, extent=(40.0, 40.0, 10.0),
+                       z0: float = -0.5, device="cuda", chunk_blocks: int = 1 << 15, seed: int = 4,
+                       n_boxes: int = 60, n_spheres: int = 40):
+    """Yield (bxyz int32 [n,3], D fp32 [n,512], W fp32 [n,512]) chunks of a fully observed TSDF
+    D = clamp(analytic sdf, +-tau), W = 1 over the volume (BASELINE.json configs[4]).  Block (bx,by,bz)
+    covers voxels 8*b .. 8*b+7; voxel centres at (v + 1/2) s in the submap frame, z offset z0."""
+    scene = esdf_stress_scene(seed, extent, n_boxes, n_spheres)
+    nbx, nby, nbz = (int(round(e / voxel_size)) // 8 for e in extent)
+    bz0 = int(np.floor(z0 / voxel_size / 8))
+    l = torch.arange(512, device=device)
+    loc = torch.stack([l % 8, (l // 8) % 8, l // 64], 1).to(torch.float32)
+    total = nbx * nby * nbz
+    for s0 in range(0, total, chunk_blocks):
+        ids = torch.arange(s0, min(total, s0 + chunk_blocks), device=device)
+        b = torch.stack([ids % nbx, (ids // nbx) % nby, ids // (nbx * nby) + bz0], 1).to(torch.int32)
+        v = b.to(torch.float32)[:, None, :] * 8 + loc[None]
+        pts = ((v + 0.5) * voxel_size).reshape(-1, 3)
+        sdf = analytic_sdf(scene, pts).reshape(-1, 512)
+        D = sdf.clamp(-truncation, truncation).contiguous()
+        W = torch.ones_like(D)
+        yield b.contiguous(), D, W
