@@ -133,10 +133,23 @@ cvx_status cvx_get_aabb(const cvx_submap* submap, int32_t* lo, int32_t* hi);
  * Errors: CVX_E_CAPACITY / CVX_E_RANGE (sticky), CVX_E_OOM. */
 cvx_status cvx_finalize_esdf(cvx_submap* submap, void* stream);
 
+/* Incremental ESDF: update the ESDF of a submap that is still being
+ * integrated, touching only what changed since the previous call.  Per voxel the library keeps a
+ * pointer to its nearest site; new sites, removed sites ("raise": voxels whose parent stopped being a
+ * site lose it) and new blocks queue their block (one region queue per 8^3 block); each queued block
+ * is relaxed by one CTA in shared memory along all axis directions until stable, and blocks whose
+ * shared face changed are queued in turn, until no block is queued.  E follows the same sign / NaN /
+ * +inf conventions as cvx_finalize_esdf; the distances are those of 6-neighbour parent propagation
+ * (the paper's scheme), which can exceed the exact EDT of cvx_finalize_esdf by a bounded amount.
+ * Enables cvx_query_distance.  Synchronising (one host check per propagation wave);
+ * *iterations (nullable, host) = number of waves.  Errors: CVX_E_CAPACITY / CVX_E_RANGE (sticky),
+ * CVX_E_OOM. */
+cvx_status cvx_update_esdf(cvx_submap* submap, void* stream, int32_t* iterations);
+
 /* Distance queries (O13).  points_world (device fp32 [m][3], world frame) ->
  * out_distance (device fp32 [m]) and out_status (device uint8 [m]: 0 OK trilinear over the 8 voxel
  * centres around x, 1 NEAREST = value of the voxel containing x, 2 UNKNOWN = NaN).
- * Errors: CVX_E_STATE before finalize, CVX_E_INVALID. */
+ * Errors: CVX_E_STATE before finalize / update_esdf, CVX_E_INVALID. */
 cvx_status cvx_query_distance(const cvx_submap* submap, const float* points_world, int64_t m,
                               float* out_distance, uint8_t* out_status, void* stream);
 

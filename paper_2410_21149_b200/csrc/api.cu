@@ -119,6 +119,12 @@ void free_all(cvx_submap* sm) {
   }
   if (sm->edt) cudaFree(sm->edt);
   if (sm->block_grid) cudaFree(sm->block_grid);
+  if (sm->inc.par) cudaFree(sm->inc.par);
+  if (sm->inc.sitebits) cudaFree(sm->inc.sitebits);
+  if (sm->inc.active) cudaFree(sm->inc.active);
+  if (sm->inc.list) cudaFree(sm->inc.list);
+  if (sm->inc.cnt) cudaFree(sm->inc.cnt);
+  if (sm->inc.cnt_host) cudaFreeHost(sm->inc.cnt_host);
   delete sm->prof;
   sm->prof = nullptr;
 }
@@ -220,6 +226,9 @@ cvx_status cvx_reset_submap(cvx_submap* sm, void* stream) {
   cudaError_t e = cvx::launch_reset(sm, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "reset");
   sm->finalized = false;
+  sm->esdf_valid = false;
+  sm->inc.nb_prev = 0;
+  if (sm->inc.active) cudaMemsetAsync(sm->inc.active, 0, sizeof(int) * (size_t)sm->pool.max_blocks, (cudaStream_t)stream);
   return CVX_OK;
 }
 
@@ -315,11 +324,34 @@ cvx_status cvx_finalize_esdf(cvx_submap* sm, void* stream) {
   return CVX_OK;
 }
 
+cvx_status cvx_update_esdf(cvx_submap* sm, void* stream, int32_t* iterations) {
+  g_last_error.clear();
+  if (!sm) return fail(CVX_E_INVALID, "submap is NULL");
+  DeviceGuard g(sm->device);
+  if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+  cudaStream_t st = (cudaStream_t)stream;
+  cvx::Counters c;
+  cvx_status rc = read_counters(sm, st, &c);
+  if (rc != CVX_OK) return rc;
+  if ((rc = sticky(c)) != CVX_OK) return rc;
+  const int nb = c.n_blocks < sm->pool.max_blocks ? c.n_blocks : sm->pool.max_blocks;
+  if (nb > 0)
+    for (int a = 0; a < 3; ++a)
+      if ((int64_t)8 * ((int64_t)c.aabb_hi[a] - c.aabb_lo[a] + 1) > 65528)
+        return fail(CVX_E_RANGE, "submap AABB exceeds 65528 voxels along an axis");
+  int its = 0;
+  cudaError_t e = cvx::launch_update_esdf(sm, nb, c.aabb_lo, c.aabb_hi, st, &its);
+  if (e != cudaSuccess) return cuda_fail(e, "update_esdf");
+  if (iterations) *iterations = its;
+  sm->esdf_valid = true;
+  return CVX_OK;
+}
+
 cvx_status cvx_query_distance(const cvx_submap* sm, const float* pts, int64_t m, float* out, uint8_t* status,
                               void* stream) {
   g_last_error.clear();
   if (!sm) return fail(CVX_E_INVALID, "submap is NULL");
-  if (!sm->finalized) return fail(CVX_E_STATE, "query before finalize_esdf");
+  if (!sm->finalized && !sm->esdf_valid) return fail(CVX_E_STATE, "query before finalize_esdf / update_esdf");
   if (m < 0) return fail(CVX_E_INVALID, "m < 0");
   if (m > 0 && (!pts || !out || !status)) return fail(CVX_E_INVALID, "NULL buffer");
   DeviceGuard g(sm->device);

@@ -313,3 +313,289 @@ cudaError_t launch_finalize(cvx_submap* sm, int n_blocks, const int lo[3], const
 }
 
 }  // namespace cvx
+
+// ================================================================================================
+// Incremental ESDF: keep, per voxel, a pointer to its nearest site
+// (packed offset) and, after new integration, update only what changed:
+//   inc_classify   new / removed sites (site = observed and |D| <= tau_site, R4) per voxel; new blocks
+//                  start without a parent; blocks with changes are queued (one region queue = one block)
+//   inc_invalidate "raise": every voxel whose parent is no longer a site loses it (one direct check per
+//                  voxel instead of a wavefront)
+//   inc_propagate  "lower": per queued block, one CTA relaxes the 8^3 voxels plus the neighbour faces in
+//                  shared memory (sweeps along all axis directions until the block is stable, P:L149
+//                  "process every axis direction within each queued block"), writes back, and queues the
+//                  neighbour blocks whose shared face changed; repeated until no block is queued
+//   inc_write      E = sign(D) s |v - parent| (NaN unobserved, +inf without a site)
+// The fixpoint is the 6-neighbour parent-propagation distance of the paper's scheme, not always the
+// exact EDT; tests/test_gpu_esdf_incremental.py bounds the difference to finalize_esdf.
+namespace cvx {
+namespace {
+
+constexpr unsigned long long kNoPar = 1ull << 63;
+constexpr unsigned long long kFld = (1ull << 21) - 1;
+
+__device__ __forceinline__ unsigned long long pack3(int x, int y, int z) {
+  return ((unsigned long long)(x & (int)kFld) << 42) | ((unsigned long long)(y & (int)kFld) << 21) |
+         (unsigned long long)(z & (int)kFld);
+}
+__device__ __forceinline__ int fld(unsigned long long p, int sh) {
+  return (int)((long long)(p << (43 - sh)) >> 43);   // sign-extend the 21-bit field at bit sh
+}
+
+struct IncParams {
+  const long long* sums;
+  float* esdf;
+  const int4* coords;
+  unsigned long long* par;   // per voxel: packed offset (parent - v), kNoPar = none
+  unsigned* sitebits;        // per block: 16 x 32 bits
+  int* active;               // per block: queued flag
+  int* list;                 // compacted queue
+  int* cnt;                  // queue length
+  const int* grid;           // dense slot grid over the AABB
+  int lo0, lo1, lo2, nbx, nby, nbz;
+  int nb, nb_prev;
+  double site_thr;
+  float s;
+};
+
+__device__ __forceinline__ int grid_slot(const IncParams& p, int bx, int by, int bz) {
+  bx -= p.lo0; by -= p.lo1; bz -= p.lo2;
+  if (bx < 0 || by < 0 || bz < 0 || bx >= p.nbx || by >= p.nby || bz >= p.nbz) return -1;
+  return p.grid[((long long)bz * p.nby + by) * p.nbx + bx];
+}
+
+__device__ __forceinline__ bool is_site(const IncParams& p, long long vi, bool& observed, bool& neg) {
+  const longlong2 sw = reinterpret_cast<const longlong2*>(p.sums)[vi];
+  observed = sw.y > 0;
+  if (!observed) { neg = false; return false; }
+  const float D = (float)((double)sw.x / (double)sw.y);
+  neg = D < 0.0f;
+  return fabs((double)D) <= p.site_thr;
+}
+
+__global__ void inc_classify(const __grid_constant__ IncParams p) {
+  const long long n = (long long)p.nb * kBlockVox;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int slot = (int)(i >> 9), l = (int)(i & 511);
+    bool obs, neg;
+    const bool site = is_site(p, i, obs, neg);
+    const bool fresh = slot >= p.nb_prev;
+    const bool old = !fresh && ((p.sitebits[(long long)slot * 16 + (l >> 5)] >> (l & 31)) & 1u);
+    if (fresh) p.par[i] = site ? 0ull : kNoPar;
+    else if (site && !old) p.par[i] = 0ull;
+    else if (!site && old) p.par[i] = kNoPar;
+    const unsigned bits = __ballot_sync(0xffffffffu, site);   // 32 consecutive voxels of one block
+    if ((l & 31) == 0) p.sitebits[(long long)slot * 16 + (l >> 5)] = bits;
+    if (fresh || site != old) p.active[slot] = 1;
+  }
+}
+
+__global__ void inc_invalidate(const __grid_constant__ IncParams p) {
+  const long long n = (long long)p.nb_prev * kBlockVox;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long q = p.par[i];
+    if (q == kNoPar || q == 0ull) continue;
+    const int slot = (int)(i >> 9), l = (int)(i & 511);
+    const int4 c = p.coords[slot];
+    const int px = 8 * c.x + (l & 7) + fld(q, 42), py = 8 * c.y + ((l >> 3) & 7) + fld(q, 21),
+              pz = 8 * c.z + (l >> 6) + fld(q, 0);
+    const int ps = grid_slot(p, px >> 3, py >> 3, pz >> 3);
+    const int pl = (px & 7) | ((py & 7) << 3) | ((pz & 7) << 6);
+    const bool alive = ps >= 0 && ((p.sitebits[(long long)ps * 16 + (pl >> 5)] >> (pl & 31)) & 1u);
+    if (!alive) { p.par[i] = kNoPar; p.active[slot] = 1; }
+  }
+}
+
+__global__ void inc_compact(const __grid_constant__ IncParams p) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < p.nb; b += gridDim.x * blockDim.x)
+    if (p.active[b]) { p.active[b] = 0; p.list[atomicAdd(p.cnt, 1)] = b; }
+}
+
+// squared distance from local voxel (x,y,z) to a parent given relative to the block origin
+__device__ __forceinline__ long long pd2(unsigned long long a, int x, int y, int z) {
+  const long long dx = fld(a, 42) - x, dy = fld(a, 21) - y, dz = fld(a, 0) - z;
+  return dx * dx + dy * dy + dz * dz;
+}
+
+// one CTA per queued block; shared memory holds the block + its 6 face neighbours (10^3 halo cube) as
+// parents relative to the block origin
+__global__ void __launch_bounds__(128) inc_propagate(const __grid_constant__ IncParams p) {
+  __shared__ unsigned long long cur[1000], nxt[1000];
+  __shared__ int nb_slot[6];
+  __shared__ int face_changed[6];
+  const int slot = p.list[blockIdx.x];
+  const int4 c = p.coords[slot];
+  const int t = threadIdx.x;
+  if (t < 6) {
+    const int d = (t >> 1), sg = (t & 1) ? 1 : -1;
+    nb_slot[t] = grid_slot(p, c.x + (d == 0) * sg, c.y + (d == 1) * sg, c.z + (d == 2) * sg);
+    face_changed[t] = 0;
+  }
+  for (int k = t; k < 1000; k += 128) cur[k] = kNoPar;
+  __syncthreads();
+  // own voxels
+  for (int l = t; l < 512; l += 128) {
+    const int x = l & 7, y = (l >> 3) & 7, z = l >> 6;
+    const unsigned long long q = p.par[(long long)slot * kBlockVox + l];
+    cur[(x + 1) + 10 * (y + 1) + 100 * (z + 1)] = q == kNoPar ? kNoPar : pack3(x + fld(q, 42), y + fld(q, 21), z + fld(q, 0));
+  }
+  // face halo: 6 faces x 64 voxels
+  for (int k = t; k < 384; k += 128) {
+    const int f = k >> 6, a = k & 7, b = (k >> 3) & 7, d = f >> 1, hi = f & 1;
+    const int ns = nb_slot[f];
+    int x, y, z, nl;   // local coords (in this block's frame) of the halo voxel, and its index in the neighbour
+    if (d == 0) { x = hi ? 8 : -1; y = a; z = b; nl = (hi ? 0 : 7) | (a << 3) | (b << 6); }
+    else if (d == 1) { x = a; y = hi ? 8 : -1; z = b; nl = a | ((hi ? 0 : 7) << 3) | (b << 6); }
+    else { x = a; y = b; z = hi ? 8 : -1; nl = a | (b << 3) | ((hi ? 0 : 7) << 6); }
+    unsigned long long v = kNoPar;
+    if (ns >= 0) {
+      const unsigned long long q = *(volatile const unsigned long long*)&p.par[(long long)ns * kBlockVox + nl];
+      if (q != kNoPar) v = pack3(x + fld(q, 42), y + fld(q, 21), z + fld(q, 0));
+    }
+    cur[(x + 1) + 10 * (y + 1) + 100 * (z + 1)] = v;
+  }
+  __syncthreads();
+  // relax to a local fixpoint: every voxel takes the nearest parent among itself and its 6 neighbours
+  // (ties: smaller packed parent, so the result does not depend on the evaluation order)
+  for (int round = 0; round < 32; ++round) {
+    int changed = 0;
+    for (int l = t; l < 512; l += 128) {
+      const int x = l & 7, y = (l >> 3) & 7, z = l >> 6;
+      const int ci = (x + 1) + 10 * (y + 1) + 100 * (z + 1);
+      unsigned long long best = cur[ci];
+      long long bd = best == kNoPar ? 0x7fffffffffffffffll : pd2(best, x, y, z);
+      const int nbr[6] = {ci - 1, ci + 1, ci - 10, ci + 10, ci - 100, ci + 100};
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        const unsigned long long cnd = cur[nbr[k]];
+        if (cnd == kNoPar) continue;
+        const long long d = pd2(cnd, x, y, z);
+        if (d < bd || (d == bd && cnd < best)) { bd = d; best = cnd; }
+      }
+      nxt[ci] = best;
+      changed |= best != cur[ci];
+    }
+    __syncthreads();
+    for (int l = t; l < 512; l += 128) {
+      const int ci = ((l & 7) + 1) + 10 * (((l >> 3) & 7) + 1) + 100 * ((l >> 6) + 1);
+      cur[ci] = nxt[ci];
+    }
+    if (!__syncthreads_or(changed)) break;
+  }
+  // write back; a changed face voxel queues the neighbour block across that face
+  for (int l = t; l < 512; l += 128) {
+    const int x = l & 7, y = (l >> 3) & 7, z = l >> 6;
+    const unsigned long long b = cur[(x + 1) + 10 * (y + 1) + 100 * (z + 1)];
+    const unsigned long long nq = b == kNoPar ? kNoPar : pack3(fld(b, 42) - x, fld(b, 21) - y, fld(b, 0) - z);
+    unsigned long long* dst = &p.par[(long long)slot * kBlockVox + l];
+    if (*dst != nq) {
+      *dst = nq;
+      if (x == 0) face_changed[0] = 1;
+      if (x == 7) face_changed[1] = 1;
+      if (y == 0) face_changed[2] = 1;
+      if (y == 7) face_changed[3] = 1;
+      if (z == 0) face_changed[4] = 1;
+      if (z == 7) face_changed[5] = 1;
+    }
+  }
+  __syncthreads();
+  if (t < 6 && face_changed[t] && nb_slot[t] >= 0) p.active[nb_slot[t]] = 1;
+}
+
+__global__ void inc_write(const __grid_constant__ IncParams p) {
+  const long long n = (long long)p.nb * kBlockVox;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    bool obs, neg;
+    (void)is_site(p, i, obs, neg);
+    float e;
+    const unsigned long long q = p.par[i];
+    if (!obs) e = __int_as_float(0x7fc00000);
+    else if (q == kNoPar) e = __int_as_float(0x7f800000);
+    else {
+      const long long dx = fld(q, 42), dy = fld(q, 21), dz = fld(q, 0);
+      const float m = (float)((double)p.s * sqrt((double)(dx * dx + dy * dy + dz * dz)));
+      e = neg ? -m : m;
+    }
+    p.esdf[i] = e;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_update_esdf(cvx_submap* sm, int n_blocks, const int lo[3], const int hi[3], cudaStream_t st,
+                               int* iterations) {
+  *iterations = 0;
+  if (n_blocks <= 0) return cudaSuccess;
+  cudaError_t e;
+  const size_t mb = (size_t)sm->pool.max_blocks;
+  if (!sm->inc.par) {
+    if ((e = cudaMalloc(&sm->inc.par, mb * kBlockVox * 8)) != cudaSuccess ||
+        (e = cudaMalloc(&sm->inc.sitebits, mb * 64)) != cudaSuccess ||
+        (e = cudaMalloc(&sm->inc.active, mb * 4)) != cudaSuccess ||
+        (e = cudaMalloc(&sm->inc.list, mb * 4)) != cudaSuccess ||
+        (e = cudaMallocHost(&sm->inc.cnt_host, 4)) != cudaSuccess ||
+        (e = cudaMalloc(&sm->inc.cnt, 4)) != cudaSuccess)
+      return e;
+    cudaMemsetAsync(sm->inc.active, 0, mb * 4, st);
+    sm->inc.nb_prev = 0;
+  }
+  const int nbx = hi[0] - lo[0] + 1, nby = hi[1] - lo[1] + 1, nbz = hi[2] - lo[2] + 1;
+  const long long nblk = (long long)nbx * nby * nbz;
+  if (sm->block_grid_cap < nblk) {
+    if (sm->block_grid) cudaFree(sm->block_grid);
+    sm->block_grid = nullptr; sm->block_grid_cap = 0;
+    if ((e = cudaMalloc(&sm->block_grid, sizeof(int) * (size_t)nblk)) != cudaSuccess) return e;
+    sm->block_grid_cap = nblk;
+  }
+  // dense slot grid (the colmask / rowmask side outputs go to a scratch tail of the EDT buffer)
+  const long long mask_bytes = (long long)nbx * nby + (long long)nby * nbz + 256;
+  if (sm->edt_bytes < mask_bytes) {
+    if (sm->edt) cudaFree(sm->edt);
+    sm->edt = nullptr; sm->edt_bytes = 0;
+    if ((e = cudaMalloc(&sm->edt, (size_t)mask_bytes)) != cudaSuccess) return e;
+    sm->edt_bytes = mask_bytes;
+  }
+  unsigned char* colmask = reinterpret_cast<unsigned char*>(sm->edt);
+  cudaMemsetAsync(sm->block_grid, 0xff, sizeof(int) * (size_t)nblk, st);
+  {
+    ProfScope ps_(sm, "inc_block_grid", st);
+    block_grid_kernel<<<148 * 4, 256, 0, st>>>(sm->ctr, sm->pool.coords, sm->pool.max_blocks, sm->block_grid,
+                                               colmask, colmask + (size_t)nbx * nby, lo[0], lo[1], lo[2], nbx, nby);
+  }
+  IncParams ip;
+  ip.sums = sm->pool.sums; ip.esdf = sm->pool.esdf; ip.coords = sm->pool.coords; ip.par = sm->inc.par;
+  ip.sitebits = sm->inc.sitebits; ip.active = sm->inc.active; ip.list = sm->inc.list; ip.cnt = sm->inc.cnt;
+  ip.grid = sm->block_grid; ip.lo0 = lo[0]; ip.lo1 = lo[1]; ip.lo2 = lo[2]; ip.nbx = nbx; ip.nby = nby; ip.nbz = nbz;
+  ip.nb = n_blocks; ip.nb_prev = std::min(sm->inc.nb_prev, n_blocks);
+  ip.site_thr = sm->cfg.site_threshold; ip.s = (float)sm->cfg.voxel_size;
+  {
+    ProfScope ps_(sm, "inc_classify", st);
+    inc_classify<<<148 * 8, 256, 0, st>>>(ip);
+  }
+  if (ip.nb_prev > 0) {
+    ProfScope ps_(sm, "inc_invalidate", st);
+    inc_invalidate<<<148 * 8, 256, 0, st>>>(ip);
+  }
+  for (int it = 0; it < 100000; ++it) {
+    cudaMemsetAsync(sm->inc.cnt, 0, 4, st);
+    {
+      ProfScope ps_(sm, "inc_compact", st);
+      inc_compact<<<(n_blocks + 255) / 256, 256, 0, st>>>(ip);
+    }
+    cudaMemcpyAsync(sm->inc.cnt_host, sm->inc.cnt, 4, cudaMemcpyDeviceToHost, st);
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+    const int q = *sm->inc.cnt_host;
+    if (q == 0) break;
+    ++*iterations;
+    ProfScope ps_(sm, "inc_propagate", st);
+    inc_propagate<<<q, 128, 0, st>>>(ip);
+  }
+  {
+    ProfScope ps_(sm, "inc_write", st);
+    inc_write<<<148 * 8, 256, 0, st>>>(ip);
+  }
+  sm->inc.nb_prev = n_blocks;
+  return cudaGetLastError();
+}
+
+}  // namespace cvx

@@ -39,6 +39,7 @@ struct cvx_submap {
   double T_ws[16] = {};    // world <- submap
   int device = 0;
   bool finalized = false;
+  bool esdf_valid = false;    // an (incremental) ESDF was computed since the last reset
 
   // hash table + pool (HBM, see cvx_internal.cuh)
   cvx::HashView hash{};
@@ -67,6 +68,17 @@ struct cvx_submap {
   int* block_grid = nullptr;  // device int32 [nbz][nby][nbx]
   int64_t block_grid_cap = 0;
 
+  // incremental ESDF state (allocated on the first cvx_update_esdf)
+  struct Inc {
+    unsigned long long* par = nullptr;  // per voxel: packed offset to the nearest site
+    unsigned* sitebits = nullptr;       // per block: site bitmask at the last update
+    int* active = nullptr;              // per block: queued
+    int* list = nullptr;                // compacted queue
+    int* cnt = nullptr;
+    int* cnt_host = nullptr;            // pinned
+    int nb_prev = 0;                    // blocks covered by the last update
+  } inc;
+
   cvx::Prof* prof = nullptr;  // owned
 };
 
@@ -90,6 +102,8 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
                              const double* T_world_sensor, const cvx_sensor_model& sensor, cudaStream_t st);
 // esdf.cu
 cudaError_t launch_finalize(cvx_submap* sm, int n_blocks, const int lo[3], const int hi[3], cudaStream_t st);
+cudaError_t launch_update_esdf(cvx_submap* sm, int n_blocks, const int lo[3], const int hi[3], cudaStream_t st,
+                               int* iterations);
 // query.cu
 cudaError_t launch_query(const cvx_submap* sm, const float* pts, int64_t m, float* out, uint8_t* status,
                          cudaStream_t st);

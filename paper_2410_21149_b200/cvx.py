@@ -63,6 +63,7 @@ SIGNATURES = {
     "cvx_get_block_count": (C.c_int32, [_P, C.POINTER(C.c_int64)]),
     "cvx_get_aabb": (C.c_int32, [_P, _P, _P]),
     "cvx_finalize_esdf": (C.c_int32, [_P, _P]),
+    "cvx_update_esdf": (C.c_int32, [_P, _P, C.POINTER(C.c_int32)]),
     "cvx_query_distance": (C.c_int32, [_P, _P, C.c_int64, _P, _P, _P]),
     "cvx_export_blocks": (C.c_int32, [_P, _P, _P, _P, _P, C.c_int64, C.POINTER(C.c_int64), _P]),
     "cvx_import_tsdf_blocks": (C.c_int32, [_P, _P, _P, _P, C.c_int64, _P]),
@@ -180,6 +181,12 @@ class Submap:
 
     def finalize_esdf(self):
         _check(lib().cvx_finalize_esdf(self._h, self._stream()))
+
+    def update_esdf(self) -> int:
+        """Incremental ESDF update (cvx_update_esdf); returns the number of propagation waves."""
+        it = C.c_int32()
+        _check(lib().cvx_update_esdf(self._h, self._stream(), C.byref(it)))
+        return int(it.value)
 
     def query(self, points_world: torch.Tensor, out: torch.Tensor | None = None,
               status: torch.Tensor | None = None):
