@@ -196,6 +196,60 @@ def ncu_traffic(kernel):
     return None
 
 
+def run_incremental(args, world, rank, local, every=10):
+    """configs[1] integrated in batches of `every` scans with an incremental ESDF update
+    after each batch (the paper's per-frame ESDF maintenance), against one exact
+    finalize_esdf of the same submap per batch."""
+    import paper_2410_21149_b200 as cvx
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    cfg, data, poses = make_workload(rank, dev)
+    sm = cvx.Submap(cfg["grid"], cfg["submaps"][0]["T_world_submap"], local)
+    stream = torch.cuda.current_stream(dev)
+
+    def run(mode):
+        sm.reset()
+        t_upd, waves = 0.0, 0
+        for c in range(0, N_SCANS, every):
+            sm.integrate_batch(data[c:c + every], poses[c:c + every], cfg["sensor"])
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            if mode == "inc":
+                waves += sm.update_esdf()
+            else:
+                sm.finalize_esdf()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            t_upd += e0.elapsed_time(e1)
+            if mode == "full":
+                sm.reset()                      # finalize freezes the submap: rebuild up to this batch
+                sm.integrate_batch(data[:c + every].contiguous(), poses[:c + every], cfg["sensor"])
+        return t_upd, waves
+
+    for _ in range(max(1, args.warmup)):
+        run("inc")
+    sm.profile(True)
+    t_inc, waves = run("inc")
+    prof = {k: v for k, v in sm.profile_report().items() if k.startswith("inc_")}
+    sm.profile(False)
+    sm.reset()                                  # warm the grow-only EDT scratch at the final AABB size
+    sm.integrate_batch(data, poses, cfg["sensor"])
+    sm.finalize_esdf()
+    t_full, _ = run("full")
+    n_upd = N_SCANS // every
+    line = {"metric": "incremental ESDF update ms (configs[1], update every %d scans)" % every,
+            "value": t_inc / n_upd, "unit": "ms/update", "higher_is_better": False, "n_gpus": world,
+            "steps": n_upd, "warmup": args.warmup, "data": "synthetic", "dtype": "i64",
+            "config": {"workload": "lidar_submap_os1_64x1024_200scans_0.2m (BJ configs[1])", "every_scans": every},
+            "propagation_waves_per_update": waves / n_upd,
+            "exact_finalize_ms_per_update": t_full / n_upd,
+            "inc_kernel_ms_per_update": {k: v["ms"] / n_upd for k, v in prof.items()},
+            "inc_launches_per_update": {k: v["n"] / n_upd for k, v in prof.items()},
+            "speedup_vs_exact_recompute": t_full / t_inc}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 def run_esdf_stress(args, world, rank, local):
     """BASELINE.json configs[4]: 2 cm voxels over 40 x 40 x 10 m (2e9 voxels, ~3.9 M blocks), TSDF imported
     from an analytic SDF (D = clamp(sdf, +-0.06), W = 1), one full exact ESDF recompute per step."""
@@ -260,7 +314,7 @@ def main():
     ap.add_argument("--queries", type=int, default=1 << 20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--workload", default="lidar", choices=["lidar", "esdf_stress"],
+    ap.add_argument("--workload", default="lidar", choices=["lidar", "esdf_stress", "incremental"],
                     help="lidar: configs[1] (default bench line); esdf_stress: configs[4] full ESDF recompute")
     args = ap.parse_args()
     world, rank, local = dist_setup()
@@ -269,6 +323,9 @@ def main():
         return
     if args.workload == "esdf_stress":
         run_esdf_stress(args, world, rank, local)
+        return
+    if args.workload == "incremental":
+        run_incremental(args, world, rank, local)
         return
 
     import paper_2410_21149_b200 as cvx

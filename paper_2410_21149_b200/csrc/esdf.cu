@@ -417,89 +417,95 @@ __device__ __forceinline__ long long pd2(unsigned long long a, int x, int y, int
   return dx * dx + dy * dy + dz * dz;
 }
 
-// one CTA per queued block; shared memory holds the block + its 6 face neighbours (10^3 halo cube) as
-// parents relative to the block origin
-__global__ void __launch_bounds__(128) inc_propagate(const __grid_constant__ IncParams p) {
-  __shared__ unsigned long long cur[1000], nxt[1000];
+// one 64-thread CTA per queued block (grid-stride over the queue); shared memory holds the block + its 6
+// face neighbours (10^3 halo cube) as parents relative to the block origin.  The block is relaxed by
+// directional sweeps ("process every axis direction within each queued block"): thread t owns
+// line t along the swept axis and carries the best parent forward (then backward) over the 8 voxels;
+// rounds of the six sweeps repeat until no voxel changes, which is the 6-neighbour local fixpoint.
+__global__ void __launch_bounds__(64) inc_propagate(const __grid_constant__ IncParams p) {
+  __shared__ unsigned long long cur[1000];
   __shared__ int nb_slot[6];
   __shared__ int face_changed[6];
-  const int slot = p.list[blockIdx.x];
-  const int4 c = p.coords[slot];
+  const int qlen = *(volatile const int*)p.cnt;
   const int t = threadIdx.x;
-  if (t < 6) {
-    const int d = (t >> 1), sg = (t & 1) ? 1 : -1;
-    nb_slot[t] = grid_slot(p, c.x + (d == 0) * sg, c.y + (d == 1) * sg, c.z + (d == 2) * sg);
-    face_changed[t] = 0;
-  }
-  for (int k = t; k < 1000; k += 128) cur[k] = kNoPar;
-  __syncthreads();
-  // own voxels
-  for (int l = t; l < 512; l += 128) {
-    const int x = l & 7, y = (l >> 3) & 7, z = l >> 6;
-    const unsigned long long q = p.par[(long long)slot * kBlockVox + l];
-    cur[(x + 1) + 10 * (y + 1) + 100 * (z + 1)] = q == kNoPar ? kNoPar : pack3(x + fld(q, 42), y + fld(q, 21), z + fld(q, 0));
-  }
-  // face halo: 6 faces x 64 voxels
-  for (int k = t; k < 384; k += 128) {
-    const int f = k >> 6, a = k & 7, b = (k >> 3) & 7, d = f >> 1, hi = f & 1;
-    const int ns = nb_slot[f];
-    int x, y, z, nl;   // local coords (in this block's frame) of the halo voxel, and its index in the neighbour
-    if (d == 0) { x = hi ? 8 : -1; y = a; z = b; nl = (hi ? 0 : 7) | (a << 3) | (b << 6); }
-    else if (d == 1) { x = a; y = hi ? 8 : -1; z = b; nl = a | ((hi ? 0 : 7) << 3) | (b << 6); }
-    else { x = a; y = b; z = hi ? 8 : -1; nl = a | (b << 3) | ((hi ? 0 : 7) << 6); }
-    unsigned long long v = kNoPar;
-    if (ns >= 0) {
-      const unsigned long long q = *(volatile const unsigned long long*)&p.par[(long long)ns * kBlockVox + nl];
-      if (q != kNoPar) v = pack3(x + fld(q, 42), y + fld(q, 21), z + fld(q, 0));
-    }
-    cur[(x + 1) + 10 * (y + 1) + 100 * (z + 1)] = v;
-  }
-  __syncthreads();
-  // relax to a local fixpoint: every voxel takes the nearest parent among itself and its 6 neighbours
-  // (ties: smaller packed parent, so the result does not depend on the evaluation order)
-  for (int round = 0; round < 32; ++round) {
-    int changed = 0;
-    for (int l = t; l < 512; l += 128) {
-      const int x = l & 7, y = (l >> 3) & 7, z = l >> 6;
-      const int ci = (x + 1) + 10 * (y + 1) + 100 * (z + 1);
-      unsigned long long best = cur[ci];
-      long long bd = best == kNoPar ? 0x7fffffffffffffffll : pd2(best, x, y, z);
-      const int nbr[6] = {ci - 1, ci + 1, ci - 10, ci + 10, ci - 100, ci + 100};
-#pragma unroll
-      for (int k = 0; k < 6; ++k) {
-        const unsigned long long cnd = cur[nbr[k]];
-        if (cnd == kNoPar) continue;
-        const long long d = pd2(cnd, x, y, z);
-        if (d < bd || (d == bd && cnd < best)) { bd = d; best = cnd; }
-      }
-      nxt[ci] = best;
-      changed |= best != cur[ci];
+  for (int qi = blockIdx.x; qi < qlen; qi += gridDim.x) {
+    __syncthreads();
+    const int slot = p.list[qi];
+    const int4 c = p.coords[slot];
+    if (t < 6) {
+      const int d = (t >> 1), sg = (t & 1) ? 1 : -1;
+      nb_slot[t] = grid_slot(p, c.x + (d == 0) * sg, c.y + (d == 1) * sg, c.z + (d == 2) * sg);
+      face_changed[t] = 0;
     }
     __syncthreads();
-    for (int l = t; l < 512; l += 128) {
-      const int ci = ((l & 7) + 1) + 10 * (((l >> 3) & 7) + 1) + 100 * ((l >> 6) + 1);
-      cur[ci] = nxt[ci];
+    for (int l = t; l < 512; l += 64) {
+      const int x = l & 7, y = (l >> 3) & 7, z = l >> 6;
+      const unsigned long long q = p.par[(long long)slot * kBlockVox + l];
+      cur[(x + 1) + 10 * (y + 1) + 100 * (z + 1)] = q == kNoPar ? kNoPar : pack3(x + fld(q, 42), y + fld(q, 21), z + fld(q, 0));
     }
-    if (!__syncthreads_or(changed)) break;
-  }
-  // write back; a changed face voxel queues the neighbour block across that face
-  for (int l = t; l < 512; l += 128) {
-    const int x = l & 7, y = (l >> 3) & 7, z = l >> 6;
-    const unsigned long long b = cur[(x + 1) + 10 * (y + 1) + 100 * (z + 1)];
-    const unsigned long long nq = b == kNoPar ? kNoPar : pack3(fld(b, 42) - x, fld(b, 21) - y, fld(b, 0) - z);
-    unsigned long long* dst = &p.par[(long long)slot * kBlockVox + l];
-    if (*dst != nq) {
-      *dst = nq;
-      if (x == 0) face_changed[0] = 1;
-      if (x == 7) face_changed[1] = 1;
-      if (y == 0) face_changed[2] = 1;
-      if (y == 7) face_changed[3] = 1;
-      if (z == 0) face_changed[4] = 1;
-      if (z == 7) face_changed[5] = 1;
+    for (int k = t; k < 384; k += 64) {   // face halo: 6 faces x 64 voxels
+      const int f = k >> 6, a = k & 7, b = (k >> 3) & 7, d = f >> 1, hi = f & 1;
+      const int ns = nb_slot[f];
+      int x, y, z, nl;
+      if (d == 0) { x = hi ? 8 : -1; y = a; z = b; nl = (hi ? 0 : 7) | (a << 3) | (b << 6); }
+      else if (d == 1) { x = a; y = hi ? 8 : -1; z = b; nl = a | ((hi ? 0 : 7) << 3) | (b << 6); }
+      else { x = a; y = b; z = hi ? 8 : -1; nl = a | (b << 3) | ((hi ? 0 : 7) << 6); }
+      unsigned long long v = kNoPar;
+      if (ns >= 0) {
+        const unsigned long long q = *(volatile const unsigned long long*)&p.par[(long long)ns * kBlockVox + nl];
+        if (q != kNoPar) v = pack3(x + fld(q, 42), y + fld(q, 21), z + fld(q, 0));
+      }
+      cur[(x + 1) + 10 * (y + 1) + 100 * (z + 1)] = v;
     }
+    __syncthreads();
+    const int la = t & 7, lb = t >> 3;   // this thread's line: the two coordinates other than the swept one
+    for (int round = 0; round < 16; ++round) {
+      int changed = 0;
+#pragma unroll 1
+      for (int sw = 0; sw < 6; ++sw) {
+        const int ax = sw >> 1, dir = (sw & 1) ? -1 : 1;
+        const int stride = ax == 0 ? 1 : (ax == 1 ? 10 : 100);
+        int x0, y0, z0;   // first voxel of the line in sweep order (local coords)
+        if (ax == 0) { x0 = dir > 0 ? 0 : 7; y0 = la; z0 = lb; }
+        else if (ax == 1) { x0 = la; y0 = dir > 0 ? 0 : 7; z0 = lb; }
+        else { x0 = la; y0 = lb; z0 = dir > 0 ? 0 : 7; }
+        int ci = (x0 + 1) + 10 * (y0 + 1) + 100 * (z0 + 1);
+        unsigned long long carry = cur[ci - dir * stride];   // halo / previous voxel
+        int x = x0, y = y0, z = z0;
+        for (int st = 0; st < 8; ++st) {
+          unsigned long long best = cur[ci];
+          long long bd = best == kNoPar ? 0x7fffffffffffffffll : pd2(best, x, y, z);
+          if (carry != kNoPar) {
+            const long long d = pd2(carry, x, y, z);
+            if (d < bd || (d == bd && carry < best)) { bd = d; best = carry; cur[ci] = best; changed = 1; }
+          }
+          carry = best;
+          ci += dir * stride;
+          if (ax == 0) x += dir; else if (ax == 1) y += dir; else z += dir;
+        }
+        __syncthreads();
+      }
+      if (!__syncthreads_or(changed)) break;
+    }
+    // write back; a changed face voxel queues the neighbour block across that face
+    for (int l = t; l < 512; l += 64) {
+      const int x = l & 7, y = (l >> 3) & 7, z = l >> 6;
+      const unsigned long long b = cur[(x + 1) + 10 * (y + 1) + 100 * (z + 1)];
+      const unsigned long long nq = b == kNoPar ? kNoPar : pack3(fld(b, 42) - x, fld(b, 21) - y, fld(b, 0) - z);
+      unsigned long long* dst = &p.par[(long long)slot * kBlockVox + l];
+      if (*dst != nq) {
+        *dst = nq;
+        if (x == 0) face_changed[0] = 1;
+        if (x == 7) face_changed[1] = 1;
+        if (y == 0) face_changed[2] = 1;
+        if (y == 7) face_changed[3] = 1;
+        if (z == 0) face_changed[4] = 1;
+        if (z == 7) face_changed[5] = 1;
+      }
+    }
+    __syncthreads();
+    if (t < 6 && face_changed[t] && nb_slot[t] >= 0) p.active[nb_slot[t]] = 1;
   }
-  __syncthreads();
-  if (t < 6 && face_changed[t] && nb_slot[t] >= 0) p.active[nb_slot[t]] = 1;
 }
 
 __global__ void inc_write(const __grid_constant__ IncParams p) {
@@ -576,19 +582,30 @@ cudaError_t launch_update_esdf(cvx_submap* sm, int n_blocks, const int lo[3], co
     ProfScope ps_(sm, "inc_invalidate", st);
     inc_invalidate<<<148 * 8, 256, 0, st>>>(ip);
   }
-  for (int it = 0; it < 100000; ++it) {
+  // waves are launched in groups of kWaves between host checks of the queue: a wave whose queue is empty
+  // costs two tiny launches (the propagate grid exits at once), a host round trip costs far more.
+  // Each wave: propagate the queued blocks, then compact the blocks they queued into the next list.
+  constexpr int kWaves = 8;
+  const unsigned pgrid = (unsigned)std::min<long long>(n_blocks, 148ll * 32);
+  auto compact = [&]() {
     cudaMemsetAsync(sm->inc.cnt, 0, 4, st);
-    {
-      ProfScope ps_(sm, "inc_compact", st);
-      inc_compact<<<(n_blocks + 255) / 256, 256, 0, st>>>(ip);
+    ProfScope ps_(sm, "inc_compact", st);
+    inc_compact<<<(n_blocks + 255) / 256, 256, 0, st>>>(ip);
+  };
+  compact();
+  cudaMemcpyAsync(sm->inc.cnt_host, sm->inc.cnt, 4, cudaMemcpyDeviceToHost, st);
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+  for (int group = 0; *sm->inc.cnt_host != 0 && group < 100000; ++group) {
+    for (int w = 0; w < kWaves; ++w) {
+      {
+        ProfScope ps_(sm, "inc_propagate", st);
+        inc_propagate<<<pgrid, 64, 0, st>>>(ip);
+      }
+      compact();
     }
+    *iterations += kWaves;
     cudaMemcpyAsync(sm->inc.cnt_host, sm->inc.cnt, 4, cudaMemcpyDeviceToHost, st);
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
-    const int q = *sm->inc.cnt_host;
-    if (q == 0) break;
-    ++*iterations;
-    ProfScope ps_(sm, "inc_propagate", st);
-    inc_propagate<<<q, 128, 0, st>>>(ip);
   }
   {
     ProfScope ps_(sm, "inc_write", st);
