@@ -416,18 +416,18 @@ def main():
     e2e = None
     if not args.no_e2e:
         host_frames = data.cpu().pin_memory()
-        dev_frames = torch.empty_like(data)
         host_out = torch.empty(args.queries, dtype=torch.float32).pin_memory()
         host_st = torch.empty(args.queries, dtype=torch.uint8).pin_memory()
         host_q = queries.cpu().pin_memory()
         dev_q = torch.empty_like(queries)
 
         def e2e_step():
-            dev_frames.copy_(host_frames, non_blocking=True)
+            # the library copies each launch's scans from pinned host memory on its side stream, so the
+            # transfer of launch k+1 overlaps the walk of launch k (cvx_integrate_batch_host)
             dev_q.copy_(host_q, non_blocking=True)
             sm.reset()
             for c in range(0, N_SCANS, args.batch):
-                sm.integrate_batch(dev_frames[c:c + args.batch], poses[c:c + args.batch], sensor)
+                sm.integrate_batch_host(host_frames[c:c + args.batch], poses[c:c + args.batch], sensor)
             sm.finalize_esdf()
             sm.query(dev_q, qout, qst)
             gather()

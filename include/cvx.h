@@ -115,6 +115,14 @@ cvx_status cvx_integrate_batch(cvx_submap* submap, const float* data, int64_t n_
                                int32_t n_frames, const double* T_world_sensor,
                                const cvx_sensor_model* sensor, void* stream, cvx_integrate_stats* stats);
 
+/* cvx_integrate_batch with the frames in HOST memory (page-locked recommended; pageable memory works
+ * but its copies are synchronous): the library copies each launch's frames to the device on its side
+ * stream, so the transfer of launch k+1 overlaps the update walk of launch k.  `host_data` must stay
+ * valid and unmodified until `stream` has passed this call's work.  Same results and errors. */
+cvx_status cvx_integrate_batch_host(cvx_submap* submap, const float* host_data, int64_t n_per_frame,
+                                    int32_t n_frames, const double* T_world_sensor,
+                                    const cvx_sensor_model* sensor, void* stream, cvx_integrate_stats* stats);
+
 /* Cumulative counters (synchronising). Returns the sticky device errors. */
 cvx_status cvx_get_stats(const cvx_submap* submap, cvx_integrate_stats* out);
 

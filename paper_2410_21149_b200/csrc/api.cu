@@ -110,6 +110,7 @@ void free_all(cvx_submap* sm) {
     if (B.rays) cudaFree(B.rays);
     if (B.slot_lists) cudaFree(B.slot_lists);
     if (B.lcnt) cudaFree(B.lcnt);
+    if (B.staging) cudaFree(B.staging);
   }
   if (sm->side) cudaStreamDestroy(sm->side);
   if (sm->ev_entry) cudaEventDestroy(sm->ev_entry);
@@ -232,9 +233,9 @@ cvx_status cvx_reset_submap(cvx_submap* sm, void* stream) {
   return CVX_OK;
 }
 
-cvx_status cvx_integrate_batch(cvx_submap* sm, const float* data, int64_t n_per_frame, int32_t n_frames,
-                               const double* T_world_sensor, const cvx_sensor_model* sensor, void* stream,
-                               cvx_integrate_stats* stats) {
+static cvx_status integrate_impl(cvx_submap* sm, const float* data, int64_t n_per_frame, int32_t n_frames,
+                                 const double* T_world_sensor, const cvx_sensor_model* sensor, void* stream,
+                                 cvx_integrate_stats* stats, bool host_data) {
   g_last_error.clear();
   if (!sm) return fail(CVX_E_INVALID, "submap is NULL");
   if (sm->finalized) return fail(CVX_E_STATE, "submap is finalized (S:L443): integrate rejected");
@@ -252,7 +253,7 @@ cvx_status cvx_integrate_batch(cvx_submap* sm, const float* data, int64_t n_per_
   if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
   cudaStream_t st = (cudaStream_t)stream;
   if (n_per_frame > 0 && n_frames > 0) {
-    cudaError_t e = cvx::launch_integrate(sm, data, n_per_frame, n_frames, T_world_sensor, *sensor, st);
+    cudaError_t e = cvx::launch_integrate(sm, data, n_per_frame, n_frames, T_world_sensor, *sensor, st, host_data);
     if (e != cudaSuccess) return cuda_fail(e, "integrate");
   }
   if (stats) {
@@ -262,6 +263,18 @@ cvx_status cvx_integrate_batch(cvx_submap* sm, const float* data, int64_t n_per_
     return sticky(c);
   }
   return CVX_OK;
+}
+
+cvx_status cvx_integrate_batch(cvx_submap* sm, const float* data, int64_t n_per_frame, int32_t n_frames,
+                               const double* T_world_sensor, const cvx_sensor_model* sensor, void* stream,
+                               cvx_integrate_stats* stats) {
+  return integrate_impl(sm, data, n_per_frame, n_frames, T_world_sensor, sensor, stream, stats, false);
+}
+
+cvx_status cvx_integrate_batch_host(cvx_submap* sm, const float* host_data, int64_t n_per_frame, int32_t n_frames,
+                                    const double* T_world_sensor, const cvx_sensor_model* sensor, void* stream,
+                                    cvx_integrate_stats* stats) {
+  return integrate_impl(sm, host_data, n_per_frame, n_frames, T_world_sensor, sensor, stream, stats, true);
 }
 
 cvx_status cvx_integrate_pointcloud(cvx_submap* sm, const float* data, int64_t n, const double* T_world_sensor,

@@ -543,8 +543,10 @@ static cudaError_t grow(void** ptr, int64_t* cap, int64_t need, size_t elem) {
 }
 
 cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_frame, int n_frames,
-                             const double* T_world_sensor, const cvx_sensor_model& sensor, cudaStream_t st) {
+                             const double* T_world_sensor, const cvx_sensor_model& sensor, cudaStream_t st,
+                             bool host_data) {
   if (n_per_frame <= 0 || n_frames <= 0) return cudaSuccess;
+  const long long elems_per_frame = n_per_frame * (sensor.kind == 1 ? 1 : 3);
   // launches of equal size; at most kMaxBatch frames, and (constant weights) <= kMaxPackedRays rays so
   // the packed accumulators cannot overflow (R6/R7)
   const bool cw_ok = sm->aggregate && sm->cfg.weighting == 0 && n_per_frame <= kMaxPackedRays;
@@ -557,6 +559,9 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     cudaError_t e = grow(&sm->buf[b].rays, &sm->buf[b].ray_cap, cap_rays, sizeof(RayRec));
     if (e == cudaSuccess) e = grow(reinterpret_cast<void**>(&sm->buf[b].slot_lists), &sm->buf[b].slot_cap,
                                    cap_rays * kSlotsPerRay + 1024, sizeof(int));
+    if (e == cudaSuccess && host_data)
+      e = grow(reinterpret_cast<void**>(&sm->buf[b].staging), &sm->buf[b].staging_cap, (long long)per * elems_per_frame,
+               sizeof(float));
     if (e != cudaSuccess) return e;
   }
   const int q = packed_q(sm->cfg.truncation);
@@ -586,8 +591,14 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
       compose_kernel<<<1, kMaxBatch, 0, sm->side>>>(cp, B.frame_T);
     }
     cudaMemsetAsync(B.lcnt, 0, 4 * sizeof(int), sm->side);
+    const float* chunk = data + (long long)f0 * elems_per_frame;
+    if (host_data) {   // host frames: the H2D copy of launch k+1 overlaps the walk of launch k
+      cudaMemcpyAsync(B.staging, chunk, sizeof(float) * (size_t)(nf * elems_per_frame), cudaMemcpyHostToDevice,
+                      sm->side);
+      chunk = B.staging;
+    }
     PrepParams pp;
-    pp.data = data + (long long)f0 * n_per_frame * (sensor.kind == 1 ? 1 : 3);
+    pp.data = chunk;
     pp.n_per_frame = n_per_frame; pp.total = total;
     pp.kind = sensor.kind; pp.width = sensor.width;
     pp.fx = sensor.fx; pp.fy = sensor.fy; pp.cx = sensor.cx; pp.cy = sensor.cy;

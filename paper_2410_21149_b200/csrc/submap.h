@@ -56,6 +56,8 @@ struct cvx_submap {
     int* slot_lists = nullptr;  // device block-slot lists of the rays of one launch
     int64_t slot_cap = 0;
     int* lcnt = nullptr;        // device {n_rays, n_slots, -, -} of the launch using this buffer
+    float* staging = nullptr;   // device copy of host frames (cvx_integrate_batch_host)
+    int64_t staging_cap = 0;
   } buf[2];
   cudaStream_t side = nullptr;
   cudaEvent_t ev_entry = nullptr, ev_prepared[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
@@ -99,7 +101,8 @@ constexpr int kSlotsPerRay = 40; // average block-slot list capacity per ray (ov
 // integrate.cu
 cudaError_t launch_reset(cvx_submap* sm, cudaStream_t st);
 cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_frame, int n_frames,
-                             const double* T_world_sensor, const cvx_sensor_model& sensor, cudaStream_t st);
+                             const double* T_world_sensor, const cvx_sensor_model& sensor, cudaStream_t st,
+                             bool host_data);
 // esdf.cu
 cudaError_t launch_finalize(cvx_submap* sm, int n_blocks, const int lo[3], const int hi[3], cudaStream_t st);
 cudaError_t launch_update_esdf(cvx_submap* sm, int n_blocks, const int lo[3], const int hi[3], cudaStream_t st,

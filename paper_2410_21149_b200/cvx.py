@@ -59,6 +59,8 @@ SIGNATURES = {
     "cvx_integrate_pointcloud": (C.c_int32, [_P, _P, C.c_int64, _P, C.POINTER(SensorModel), _P, C.POINTER(Stats)]),
     "cvx_integrate_batch": (C.c_int32, [_P, _P, C.c_int64, C.c_int32, _P, C.POINTER(SensorModel), _P,
                                         C.POINTER(Stats)]),
+    "cvx_integrate_batch_host": (C.c_int32, [_P, _P, C.c_int64, C.c_int32, _P, C.POINTER(SensorModel), _P,
+                                             C.POINTER(Stats)]),
     "cvx_get_stats": (C.c_int32, [_P, C.POINTER(Stats)]),
     "cvx_get_block_count": (C.c_int32, [_P, C.POINTER(C.c_int64)]),
     "cvx_get_aabb": (C.c_int32, [_P, _P, _P]),
@@ -177,6 +179,19 @@ class Submap:
         st = Stats() if stats else None
         _check(lib().cvx_integrate_batch(self._h, self._dev(data, torch.float32, "data"), n, F, _ptr(poses),
                                          C.byref(sm), self._stream(), C.byref(st) if st is not None else None))
+        return st.asdict() if st is not None else None
+
+    def integrate_batch_host(self, data: torch.Tensor, T_world_sensor, sensor: dict, stats: bool = False):
+        """Like integrate_batch with `data` a CPU tensor (pin_memory() for asynchronous copies)."""
+        if data.is_cuda or data.dtype != torch.float32 or not data.is_contiguous():
+            raise ValueError("data must be a contiguous float32 CPU tensor")
+        sm = sensor_model(sensor)
+        F = data.shape[0]
+        n = data[0].numel() if sensor["kind"] == 1 else data[0].numel() // 3
+        poses = _pose(T_world_sensor)
+        st = Stats() if stats else None
+        _check(lib().cvx_integrate_batch_host(self._h, C.c_void_p(data.data_ptr()), n, F, _ptr(poses), C.byref(sm),
+                                              self._stream(), C.byref(st) if st is not None else None))
         return st.asdict() if st is not None else None
 
     def finalize_esdf(self):

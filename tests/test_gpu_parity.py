@@ -247,3 +247,18 @@ def test_wide_and_narrow_dda_paths_agree(tiny, orc):
     assert np.array_equal(a[2].view(np.uint32), b[2].view(np.uint32))
     o, _ = oracle_build(wide_cfg, frames)
     assert_tsdf_parity(b, o.export())
+
+
+def test_host_frames_equal_device_frames(tiny):
+    """cvx_integrate_batch_host (library-side overlapped H2D copies) == cvx_integrate_batch, bit for bit."""
+    from paper_2410_21149_b200 import Submap
+    frames = list(range(10))
+    a, _ = gpu_build(tiny, frames, batch=True, finalize=False)
+    b = Submap(tiny["grid"], tiny["submaps"][0]["T_world_submap"], 0)
+    host = torch.stack([tiny["frames"][k]["data"] for k in frames]).contiguous().pin_memory()
+    poses = np.stack([tiny["frames"][k]["T_world_sensor"] for k in frames])
+    b.integrate_batch_host(host, poses, tiny["sensor"])
+    ea, eb = gpu_export_sorted(a), gpu_export_sorted(b)
+    assert np.array_equal(ea[0], eb[0])
+    assert np.array_equal(ea[1].view(np.uint32), eb[1].view(np.uint32))
+    assert np.array_equal(ea[2].view(np.uint32), eb[2].view(np.uint32))
