@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(256) block_walk_kernel(const __grid_constant__
 // 2^16 a_j / -2^16 a_i, and |H_ij| <= 3 max(a) while both axes have crossings left.  Exact whenever
 // every |D_a| < 2^28 (spans < 2^12 voxels), which the launch checks from the sensor's max range.
 template <bool kAggregate, bool kConstW, bool k32>
-__global__ void __launch_bounds__(256, 4) walk_kernel(const __grid_constant__ WalkParams p) {
+__global__ void __launch_bounds__(128, 8) walk_kernel(const __grid_constant__ WalkParams p) {
   using DT = typename std::conditional<k32, unsigned, unsigned long long>::type;
   using ST = typename std::conditional<k32, int, long long>::type;
   const int n_rays = p.lcnt[0];
@@ -630,11 +630,12 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     const bool cw = cw_ok && total <= kMaxPackedRays;
     {
       ProfScope ps_(sm, "ray_walk_update", st);
+      const unsigned wblocks = (unsigned)((total + 127) / 128);   // 128-thread CTAs (measured best)
       if (sm->aggregate) {
-        if (cw) { if (k32) walk_kernel<true, true, true><<<blocks, 256, 0, st>>>(wp); else walk_kernel<true, true, false><<<blocks, 256, 0, st>>>(wp); }
-        else { if (k32) walk_kernel<true, false, true><<<blocks, 256, 0, st>>>(wp); else walk_kernel<true, false, false><<<blocks, 256, 0, st>>>(wp); }
+        if (cw) { if (k32) walk_kernel<true, true, true><<<wblocks, 128, 0, st>>>(wp); else walk_kernel<true, true, false><<<wblocks, 128, 0, st>>>(wp); }
+        else { if (k32) walk_kernel<true, false, true><<<wblocks, 128, 0, st>>>(wp); else walk_kernel<true, false, false><<<wblocks, 128, 0, st>>>(wp); }
       } else {
-        walk_kernel<false, false, false><<<blocks, 256, 0, st>>>(wp);
+        walk_kernel<false, false, false><<<wblocks, 128, 0, st>>>(wp);
       }
     }
     if (cw) {
