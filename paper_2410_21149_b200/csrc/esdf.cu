@@ -150,13 +150,22 @@ __device__ __forceinline__ long long floordiv(long long a, long long b) {  // b 
 }
 
 // Lower envelope along one line of length m; element q lives at base + q*stride.
-template <bool kZ>
+// kSplit = 2 (pass y, whose line count nx*nz is small): the two halves of a line go to lanes l and l+16
+// of one warp; each builds the envelope of the sites in its half and evaluates it over the whole line,
+// and the two results are combined with one shuffle per position (2x the evaluation work, 2x the
+// threads in flight for a latency-bound pass).
+template <bool kZ, int kSplit>
 __global__ void __launch_bounds__(256) pass_line_kernel(const __grid_constant__ LineParams p) {
   const long long nlines = kZ ? (long long)p.nx * p.ny : (long long)p.nx * p.nz;
-  const long long line = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (line >= nlines) return;
-  const int x = (int)(line % p.nx);
-  const int o2 = (int)(line / p.nx);                  // pass y: z ; pass z: y
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int half = kSplit == 2 ? (lane >> 4) : 0;
+  const long long line = kSplit == 2 ? (tid >> 5) * 16 + (lane & 15) : tid;
+  const bool valid = line < nlines;
+  if (kSplit == 1 && !valid) return;
+  if (kSplit == 2 && ((tid >> 5) * 16) >= nlines) return;   // whole warp beyond the lines
+  const int x = valid ? (int)(line % p.nx) : 0;
+  const int o2 = valid ? (int)(line / p.nx) : 0;      // pass y: z ; pass z: y
   const int m = kZ ? p.nz : p.ny;
   const long long stride = kZ ? (long long)p.nx * p.ny : (long long)p.nx;
   const long long base = kZ ? (long long)o2 * p.nx + x : (long long)o2 * p.nx * p.ny + x;
@@ -170,14 +179,15 @@ __global__ void __launch_bounds__(256) pass_line_kernel(const __grid_constant__ 
       return v == kNone16 ? kInfF : (long long)v * v;
     }
   };
-  // forward: build the envelope (Meijster phase 2 with a linked stack).  The line is read in chunks
-  // of 8 independent loads so each thread keeps 8 requests in flight (the pass is latency-bound).
+  // forward: build the envelope (Meijster phase 2 with a linked stack) of the sites in [qa, qb).  The
+  // line is read in chunks of 8 independent loads so each thread keeps 8 requests in flight.
+  const int qa = kSplit == 2 ? half * (m >> 1) : 0, qb = kSplit == 2 ? qa + (m >> 1) : m;
   int top = -1, t_top = 0;
   long long f_top = 0;
-  for (int q0 = 0; q0 < m; q0 += 8) {
+  for (int q0 = qa; q0 < qb; q0 += 8) {
     long long fv[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) fv[u] = q0 + u < m ? f_at(q0 + u) : kInfF;
+    for (int u = 0; u < 8; ++u) fv[u] = (valid && q0 + u < qb) ? f_at(q0 + u) : kInfF;
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int q = q0 + u;
@@ -230,8 +240,9 @@ __global__ void __launch_bounds__(256) pass_line_kernel(const __grid_constant__ 
         const long long dq = (long long)(q - top);
         d2 = dq * dq + f_top;
       }
+      if (kSplit == 2) d2 = min(d2, __shfl_xor_sync(0xffffffffu, d2, 16));
       if (!kZ) {
-        p.gout[base + (long long)q * stride] = d2 >= kInfF ? kInf32 : (unsigned)d2;
+        if (valid && half == 0) p.gout[base + (long long)q * stride] = d2 >= kInfF ? kInf32 : (unsigned)d2;
       } else if (!isnan(ph[u])) {
         float e;
         if (d2 >= kInfF) e = __int_as_float(0x7f800000);             // S empty -> +inf (O11)
@@ -301,13 +312,14 @@ cudaError_t launch_finalize(cvx_submap* sm, int n_blocks, const int lo[3], const
   long long nl = (long long)nx * nz;
   {
     ProfScope ps_(sm, "esdf_pass_y", st);
-    pass_line_kernel<false><<<(unsigned)((nl + 255) / 256), 256, 0, st>>>(lp);
+    // (the 2-way split of pass_line_kernel measured no faster on configs[1] and 1.6x slower on configs[4])
+    pass_line_kernel<false, 1><<<(unsigned)((nl + 255) / 256), 256, 0, st>>>(lp);
   }
   lp.fin = g2;
   nl = (long long)nx * ny;
   {
     ProfScope ps_(sm, "esdf_pass_z", st);
-    pass_line_kernel<true><<<(unsigned)((nl + 255) / 256), 256, 0, st>>>(lp);
+    pass_line_kernel<true, 1><<<(unsigned)((nl + 255) / 256), 256, 0, st>>>(lp);
   }
   return cudaGetLastError();
 }
