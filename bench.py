@@ -196,6 +196,78 @@ def ncu_traffic(kernel):
     return None
 
 
+def run_mav(args, world, rank, local):
+    """BASELINE.json configs[3]: a ~400 m MAV flight (2000 OS1-64 scans) cut into 40 submaps of 50
+    contiguous scans, sharded over the ranks by longest-processing-time on the rays per submap (strong
+    scaling: the whole flight is the fixed job).  Each rank builds its submaps (integrate -> exact ESDF
+    -> pack); the packed ESDFs of all ranks are then all-gathered (NCCL when N > 1)."""
+    import paper_2410_21149_b200 as cvx
+    import synth
+    from paper_2410_21149_b200.parallel import gather_packed, shard_submaps
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+    cfg = synth.make_config("mav", frames=[], device=dev)
+    subs = cfg["submaps"]
+    # work estimate per submap from the trajectory alone (same on every rank): scans x 1 (uniform)
+    mine = shard_submaps([len(sm["frames"]) for sm in subs], world)[rank]
+    frames = sorted(k for i in mine for k in subs[i]["frames"])
+    cfgf = synth.make_config("mav", frames=frames, device=dev)
+    data = {i: torch.stack([cfgf["frames"][k]["data"] for k in subs[i]["frames"]]).contiguous() for i in mine}
+    poses = {i: np.stack([cfgf["frames"][k]["T_world_sensor"] for k in subs[i]["frames"]]) for i in mine}
+    grid = cfg["grid"]
+    builders = [cvx.Submap(grid, subs[i]["T_world_submap"], local) for i in mine[:1]]
+    sm = builders[0] if builders else None
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        payloads = []
+        for i in mine:
+            sm.reset(subs[i]["T_world_submap"])
+            sm.integrate_batch(data[i], poses[i], cfg["sensor"])
+            sm.finalize_esdf()
+            payloads.append(sm.pack().clone())
+        if pg is not None:
+            blob = torch.cat(payloads) if payloads else torch.zeros(0, dtype=torch.uint8, device=dev)
+            gather_packed(blob)
+        return payloads
+
+    for _ in range(args.warmup):
+        step()
+    if pg is not None:
+        pg.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    if pg is not None:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        ms = float(t.item())
+    n_scans = sum(len(sm_["frames"]) for sm_ in subs)
+    line = {"metric": METRIC, "value": n_scans / (ms / 1e3), "unit": "scans/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32+i64", "data": "synthetic",
+            "config": {"workload": "mav_400m_flight_2000scans_40submaps_0.2m (BJ configs[3])",
+                       "submaps": len(subs), "submaps_per_rank_max": max(len(x) for x in shard_submaps([1] * len(subs), world)),
+                       "parallelism": f"submap-sharded x{world} (LPT)"},
+            "clocks": clk.summary()}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if pg is not None:
+        pg.barrier()
+        pg.destroy_process_group()
+
+
 def run_incremental(args, world, rank, local, every=10):
     """configs[1] integrated in batches of `every` scans with an incremental ESDF update
     after each batch (the paper's per-frame ESDF maintenance), against one exact
@@ -314,7 +386,7 @@ def main():
     ap.add_argument("--queries", type=int, default=1 << 20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--workload", default="lidar", choices=["lidar", "esdf_stress", "incremental"],
+    ap.add_argument("--workload", default="lidar", choices=["lidar", "esdf_stress", "incremental", "mav"],
                     help="lidar: configs[1] (default bench line); esdf_stress: configs[4] full ESDF recompute")
     args = ap.parse_args()
     world, rank, local = dist_setup()
@@ -326,6 +398,9 @@ def main():
         return
     if args.workload == "incremental":
         run_incremental(args, world, rank, local)
+        return
+    if args.workload == "mav":
+        run_mav(args, world, rank, local)
         return
 
     import paper_2410_21149_b200 as cvx

@@ -95,6 +95,12 @@ cvx_status cvx_destroy_submap(cvx_submap* submap);
  * the hash table, AABB, counters and the finalized flag.  Stream-ordered. */
 cvx_status cvx_reset_submap(cvx_submap* submap, void* stream);
 
+/* Replace the submap pose T_world_submap (host fp64 4x4, same checks as create).  Intended right after
+ * cvx_reset_submap, to reuse one submap's device state for the next submap of a trajectory:
+ * work already enqueued keeps the pose it was launched with; later integrate / query calls use the new
+ * one.  Not synchronising. */
+cvx_status cvx_set_submap_pose(cvx_submap* submap, const double* T_world_submap);
+
 /* Integrate one frame.  `data` (device, fp32): kind 0/2 points [n][3] in the
  * sensor frame, kind 1 depth [height][width] metres (n = width*height).  T_world_sensor: host fp64 4x4
  * row-major.  Every used ray updates every voxel it traverses from the sensor origin to tau behind the

@@ -265,6 +265,14 @@ static cvx_status integrate_impl(cvx_submap* sm, const float* data, int64_t n_pe
   return CVX_OK;
 }
 
+cvx_status cvx_set_submap_pose(cvx_submap* sm, const double* T_world_submap) {
+  g_last_error.clear();
+  if (!sm) return fail(CVX_E_INVALID, "submap is NULL");
+  if (!valid_pose(T_world_submap)) return fail(CVX_E_INVALID, "T_world_submap must be a finite rigid 4x4");
+  std::memcpy(sm->T_ws, T_world_submap, sizeof(sm->T_ws));
+  return CVX_OK;
+}
+
 cvx_status cvx_integrate_batch(cvx_submap* sm, const float* data, int64_t n_per_frame, int32_t n_frames,
                                const double* T_world_sensor, const cvx_sensor_model* sensor, void* stream,
                                cvx_integrate_stats* stats) {

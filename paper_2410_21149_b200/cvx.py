@@ -56,6 +56,7 @@ SIGNATURES = {
     "cvx_create_submap": (C.c_int32, [C.POINTER(GridConfig), _P, C.c_int, C.POINTER(_P)]),
     "cvx_destroy_submap": (C.c_int32, [_P]),
     "cvx_reset_submap": (C.c_int32, [_P, _P]),
+    "cvx_set_submap_pose": (C.c_int32, [_P, _P]),
     "cvx_integrate_pointcloud": (C.c_int32, [_P, _P, C.c_int64, _P, C.POINTER(SensorModel), _P, C.POINTER(Stats)]),
     "cvx_integrate_batch": (C.c_int32, [_P, _P, C.c_int64, C.c_int32, _P, C.POINTER(SensorModel), _P,
                                         C.POINTER(Stats)]),
@@ -216,8 +217,13 @@ class Submap:
         return out, status
 
     # -- state / inspection --------------------------------------------------------------------
-    def reset(self):
+    def reset(self, T_world_submap=None):
+        """Empty the submap (cvx_reset_submap); optionally give it a new pose (cvx_set_submap_pose)."""
         _check(lib().cvx_reset_submap(self._h, self._stream()))
+        if T_world_submap is not None:
+            T = _pose(T_world_submap)
+            _check(lib().cvx_set_submap_pose(self._h, _ptr(T)))
+            self.T_ws = T[0].reshape(4, 4).copy()
 
     def stats(self) -> dict:
         torch.cuda.current_stream(self.device).synchronize()

@@ -262,3 +262,17 @@ def test_host_frames_equal_device_frames(tiny):
     assert np.array_equal(ea[0], eb[0])
     assert np.array_equal(ea[1].view(np.uint32), eb[1].view(np.uint32))
     assert np.array_equal(ea[2].view(np.uint32), eb[2].view(np.uint32))
+
+
+def test_reset_with_new_pose_matches_fresh_submap(tiny):
+    """cvx_reset_submap + cvx_set_submap_pose == a freshly created submap with that pose (bitwise)."""
+    from paper_2410_21149_b200 import Submap
+    T2 = synth.pose(synth.rot_zyx(-0.4), [0.2, 0.1, -0.3])
+    a, _ = gpu_build(tiny, [0, 1], finalize=False)
+    a.reset(T2)
+    dev = torch.device("cuda", 0)
+    for k in (2, 3):
+        a.integrate(tiny["frames"][k]["data"].to(dev), tiny["frames"][k]["T_world_sensor"], tiny["sensor"])
+    b, _ = gpu_build(tiny, [2, 3], T_ws=T2, finalize=False)
+    ea, eb = gpu_export_sorted(a), gpu_export_sorted(b)
+    assert np.array_equal(ea[0], eb[0]) and np.array_equal(ea[1].view(np.uint32), eb[1].view(np.uint32))
