@@ -167,6 +167,23 @@ cvx_status cvx_update_esdf(cvx_submap* submap, void* stream, int32_t* iterations
 cvx_status cvx_query_distance(const cvx_submap* submap, const float* points_world, int64_t m,
                               float* out_distance, uint8_t* out_status, void* stream);
 
+/* Registration look-ups: cvx_query_distance plus the world-frame gradient of
+ * the trilinear interpolant, grad (device fp32 [m][3]) = R_WS dE/dx_s; NaN unless status is OK.
+ * Same errors as cvx_query_distance. */
+cvx_status cvx_query_distance_gradient(const cvx_submap* submap, const float* points_world, int64_t m,
+                                       float* out_distance, float* out_gradient, uint8_t* out_status,
+                                       void* stream);
+
+/* Weight-proportional surface-point sampling for registration (R12):
+ * candidates = sites (observed, |D| <= site_threshold) in lexicographic (bx,by,bz) block order then
+ * local index order, with integer weights W in units of 2^-20; each uniform u (device uint32 [m]) picks
+ * the first candidate whose prefix sum exceeds floor(T u / 2^32) (T = total weight).  out_xyz (device
+ * fp32 [m][3]) = the voxel centre in the world frame (NaN if there is no site), out_weight (device fp32
+ * [m], nullable) = its W; *total_weight (host, nullable) = T.  Synchronising.  Works before and after
+ * finalize.  Errors: CVX_E_INVALID, CVX_E_OOM, CVX_E_CUDA. */
+cvx_status cvx_sample_surface(cvx_submap* submap, const uint32_t* uniforms, int64_t m, float* out_xyz,
+                              float* out_weight, int64_t* total_weight, void* stream);
+
 /* Export every allocated block in slot order (synchronising): bxyz (device int32 [nb][3] block coords),
  * D, W (device fp32 [nb][512], local index lx + 8 ly + 64 lz; D = sum(w d)/sum(w), 0 if W = 0), E
  * (device fp32 [nb][512] or NULL; valid after finalize).  capacity_blocks bounds nb; *n_out = nb.

@@ -73,7 +73,9 @@ def lib():
             L.orc_esdf_sample.restype = C.c_int32
             L.orc_esdf_sample.argtypes = [P, P, P, C.c_int64, C.c_double, P, C.c_int64, P]
             L.orc_query.restype = C.c_int32
-            L.orc_query.argtypes = [P, P, C.c_int64, C.c_double, P, P, C.c_int64, P, P]
+            L.orc_query.argtypes = [P, P, C.c_int64, C.c_double, P, P, C.c_int64, P, P, P]
+            L.orc_sample_surface.restype = C.c_int32
+            L.orc_sample_surface.argtypes = [P, P, P, C.c_int64, C.c_double, C.c_double, P, P, C.c_int64, P, P, P]
             _lib = L
     return _lib
 
@@ -177,8 +179,8 @@ def esdf_sample(bxyz, D, W, site_threshold: float, voxels):
     return out
 
 
-def query(bxyz, E, voxel_size: float, T_world_submap, pts):
-    """(value fp64 [m], status uint8 [m]) per O13."""
+def query(bxyz, E, voxel_size: float, T_world_submap, pts, gradient: bool = False):
+    """(value fp64 [m], status uint8 [m]) per O13; with gradient=True also the world-frame gradient [m,3]."""
     b = np.ascontiguousarray(bxyz, dtype=np.int32)
     Ed = np.ascontiguousarray(E, dtype=np.float64)
     T = np.ascontiguousarray(T_world_submap, dtype=np.float64)
@@ -186,9 +188,28 @@ def query(bxyz, E, voxel_size: float, T_world_submap, pts):
     m = x.shape[0]
     out = np.zeros(m, np.float64)
     st = np.zeros(m, np.uint8)
-    rc = lib().orc_query(_p(b), _p(Ed), b.shape[0], voxel_size, _p(T), _p(x), m, _p(out), _p(st))
+    g = np.zeros((m, 3), np.float64) if gradient else None
+    rc = lib().orc_query(_p(b), _p(Ed), b.shape[0], voxel_size, _p(T), _p(x), m, _p(out), _p(st),
+                         _p(g) if gradient else None)
     assert rc == 0
-    return out, st
+    return (out, st, g) if gradient else (out, st)
+
+
+def sample_surface(bxyz, D, W, site_threshold: float, voxel_size: float, T_world_submap, uniforms):
+    """(xyz fp32 [m,3], weight fp64 [m], total) per DESIGN.md R12 (f4)."""
+    b = np.ascontiguousarray(bxyz, dtype=np.int32)
+    Dd = np.ascontiguousarray(D, dtype=np.float64)
+    Wd = np.ascontiguousarray(W, dtype=np.float64)
+    T = np.ascontiguousarray(T_world_submap, dtype=np.float64)
+    u = np.ascontiguousarray(uniforms, dtype=np.uint32)
+    m = u.shape[0]
+    xyz = np.zeros((m, 3), np.float32)
+    w = np.zeros(m, np.float64)
+    tot = np.zeros(1, np.uint64)
+    rc = lib().orc_sample_surface(_p(b), _p(Dd), _p(Wd), b.shape[0], site_threshold, voxel_size, _p(T), _p(u), m,
+                                  _p(xyz), _p(w), _p(tot))
+    assert rc == 0
+    return xyz, w, int(tot[0])
 
 
 def build_submap(cfg: dict, submap: int = 0, frames=None) -> tuple[OracleSubmap, list]:

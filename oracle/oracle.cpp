@@ -423,8 +423,11 @@ int32_t orc_esdf_sample(const int32_t* bxyz, const double* D, const double* W, i
 //   x_s = T_WS^-1 x ; g = x_s/s - 1/2 ; i0 = floor(g) ; f = g - i0.
 //   all 8 corners observed -> sum over corners with non-zero weight of weight*E (status 0 OK);
 //   else voxel floor(x_s/s) observed -> its E (status 1 NEAREST); else NaN (status 2 UNKNOWN).
+// grad (nullable) [m][3]: world-frame gradient of the trilinear interpolant for status OK (f4),
+// NaN otherwise: dE/dx_world = R_WS (dE/df) / s with dE/df_x = sum_c (dx ? 1 : -1) w_y w_z E_c (all 8 corners).
 int32_t orc_query(const int32_t* bxyz, const double* E, int64_t nb, double voxel_size,
-                  const double* T_world_submap, const float* pts, int64_t m, double* out, uint8_t* status) {
+                  const double* T_world_submap, const float* pts, int64_t m, double* out, uint8_t* status,
+                  double* grad) {
   std::unordered_map<int64_t, int64_t> idx;
   auto pack = [](int64_t x, int64_t y, int64_t z) {
     return ((x + (1 << 20)) << 42) | ((y + (1 << 20)) << 21) | (z + (1 << 20));
@@ -451,22 +454,77 @@ int32_t orc_query(const int32_t* bxyz, const double* E, int64_t nb, double voxel
       i0[a] = (int64_t)fl;
       f[a] = gg[a] - fl;
     }
-    double acc = 0.0;
+    double acc = 0.0, gs[3] = {0.0, 0.0, 0.0};
     bool all = true;
     for (int c = 0; c < 8 && all; ++c) {
       int dx = c & 1, dy = (c >> 1) & 1, dz = (c >> 2) & 1;
       double e;
       if (!lookup(i0[0] + dx, i0[1] + dy, i0[2] + dz, &e)) { all = false; break; }
-      double wgt = (dx ? f[0] : 1.0 - f[0]) * (dy ? f[1] : 1.0 - f[1]) * (dz ? f[2] : 1.0 - f[2]);
+      double wx = dx ? f[0] : 1.0 - f[0], wy = dy ? f[1] : 1.0 - f[1], wz = dz ? f[2] : 1.0 - f[2];
+      double wgt = (wx * wy) * wz;
       if (wgt > 0) acc += wgt * e;
+      gs[0] += (dx ? 1.0 : -1.0) * wy * wz * e;
+      gs[1] += (dy ? 1.0 : -1.0) * wx * wz * e;
+      gs[2] += (dz ? 1.0 : -1.0) * wx * wy * e;
     }
+    if (grad)
+      for (int a = 0; a < 3; ++a)
+        grad[3 * i + a] = all ? (T[4 * a] * gs[0] + T[4 * a + 1] * gs[1] + T[4 * a + 2] * gs[2]) / voxel_size
+                              : std::numeric_limits<double>::quiet_NaN();
     if (all) { out[i] = acc; status[i] = 0; continue; }
     double e;
     int64_t v[3] = {(int64_t)std::floor(xs[0] / voxel_size), (int64_t)std::floor(xs[1] / voxel_size),
                     (int64_t)std::floor(xs[2] / voxel_size)};
+    if (grad) for (int a = 0; a < 3; ++a) grad[3 * i + a] = std::numeric_limits<double>::quiet_NaN();
     if (lookup(v[0], v[1], v[2], &e)) { out[i] = e; status[i] = 1; continue; }
     out[i] = std::numeric_limits<double>::quiet_NaN();
     status[i] = 2;
+  }
+  return 0;
+}
+
+// Weight-proportional surface sampling (f4; R12), written out: sites in
+// lexicographic block order then local order, integer weights floor(round(W 2^30) / 2^10), prefix sums,
+// target = floor(T u / 2^32), first candidate with prefix sum > target, world voxel centre.
+int32_t orc_sample_surface(const int32_t* bxyz, const double* D, const double* W, int64_t nb, double site_threshold,
+                           double voxel_size, const double* T, const uint32_t* u, int64_t m, float* xyz, double* wout,
+                           uint64_t* total) {
+  std::vector<int64_t> order(nb);
+  for (int64_t b = 0; b < nb; ++b) order[b] = b;
+  std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+    Key ka = {bxyz[3 * a], bxyz[3 * a + 1], bxyz[3 * a + 2]}, kb = {bxyz[3 * b], bxyz[3 * b + 1], bxyz[3 * b + 2]};
+    return ka < kb;
+  });
+  std::vector<uint64_t> cum;
+  std::vector<int64_t> idx;   // flat voxel index b * 512 + l of each candidate
+  uint64_t acc = 0;
+  for (int64_t ob : order)
+    for (int l = 0; l < kBV; ++l) {
+      const double w = W[ob * kBV + l], d = D[ob * kBV + l];
+      if (!(w > 0 && std::fabs(d) <= site_threshold)) continue;
+      const uint64_t wi = (uint64_t)std::llround(w * 1073741824.0) >> 10;
+      acc += wi;
+      cum.push_back(acc);
+      idx.push_back(ob * kBV + l);
+    }
+  if (total) *total = acc;
+  for (int64_t i = 0; i < m; ++i) {
+    if (acc == 0) {
+      for (int a = 0; a < 3; ++a) xyz[3 * i + a] = std::numeric_limits<float>::quiet_NaN();
+      if (wout) wout[i] = 0.0;
+      continue;
+    }
+    const uint64_t target = (uint64_t)(((unsigned __int128)acc * u[i]) >> 32);
+    const int64_t k = std::upper_bound(cum.begin(), cum.end(), target) - cum.begin();
+    const int64_t b = idx[k] / kBV;
+    const int l = (int)(idx[k] % kBV);
+    const double v[3] = {(double)(8 * (int64_t)bxyz[3 * b] + l % 8), (double)(8 * (int64_t)bxyz[3 * b + 1] + (l / 8) % 8),
+                         (double)(8 * (int64_t)bxyz[3 * b + 2] + l / 64)};
+    double c[3];
+    for (int a = 0; a < 3; ++a) c[a] = (v[a] + 0.5) * voxel_size;
+    for (int a = 0; a < 3; ++a)
+      xyz[3 * i + a] = (float)(((T[4 * a] * c[0] + T[4 * a + 1] * c[1]) + T[4 * a + 2] * c[2]) + T[4 * a + 3]);
+    if (wout) wout[i] = W[idx[k]];
   }
   return 0;
 }

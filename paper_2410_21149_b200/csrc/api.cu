@@ -381,6 +381,38 @@ cvx_status cvx_query_distance(const cvx_submap* sm, const float* pts, int64_t m,
   return CVX_OK;
 }
 
+cvx_status cvx_query_distance_gradient(const cvx_submap* sm, const float* pts, int64_t m, float* out, float* grad,
+                                       uint8_t* status, void* stream) {
+  g_last_error.clear();
+  if (!sm) return fail(CVX_E_INVALID, "submap is NULL");
+  if (!sm->finalized && !sm->esdf_valid) return fail(CVX_E_STATE, "query before finalize_esdf / update_esdf");
+  if (m < 0) return fail(CVX_E_INVALID, "m < 0");
+  if (m > 0 && (!pts || !out || !grad || !status)) return fail(CVX_E_INVALID, "NULL buffer");
+  DeviceGuard g(sm->device);
+  cudaError_t e = cvx::launch_query(sm, pts, m, out, status, (cudaStream_t)stream, grad);
+  if (e != cudaSuccess) return cuda_fail(e, "query_distance_gradient");
+  return CVX_OK;
+}
+
+cvx_status cvx_sample_surface(cvx_submap* sm, const uint32_t* uniforms, int64_t m, float* out_xyz, float* out_weight,
+                              int64_t* total_weight, void* stream) {
+  g_last_error.clear();
+  if (!sm) return fail(CVX_E_INVALID, "submap is NULL");
+  if (m < 0) return fail(CVX_E_INVALID, "m < 0");
+  if (m > 0 && (!uniforms || !out_xyz)) return fail(CVX_E_INVALID, "NULL buffer");
+  DeviceGuard g(sm->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  cvx::Counters c;
+  cvx_status rc = read_counters(sm, st, &c);
+  if (rc != CVX_OK) return rc;
+  const int nb = c.n_blocks < sm->pool.max_blocks ? c.n_blocks : sm->pool.max_blocks;
+  long long tot = 0;
+  cudaError_t e = cvx::launch_sample_surface(sm, nb, uniforms, m, out_xyz, out_weight, st, &tot);
+  if (e != cudaSuccess) return cuda_fail(e, "sample_surface");
+  if (total_weight) *total_weight = tot;
+  return CVX_OK;
+}
+
 cvx_status cvx_export_blocks(const cvx_submap* sm, int32_t* bxyz, float* D, float* W, float* E,
                              int64_t capacity_blocks, int64_t* n_out, void* stream) {
   g_last_error.clear();

@@ -13,6 +13,7 @@ struct QueryParams {
   const float* pts;
   long long m;
   float* out;
+  float* grad;          // nullable: [m][3] world-frame gradient of the trilinear interpolant (status OK)
   unsigned char* status;
   HashView hash;
   const float* esdf;
@@ -50,23 +51,39 @@ __global__ void __launch_bounds__(256) query_kernel(const __grid_constant__ Quer
   }
   unsigned long long ckey = ~0ull;
   int cslot = -1;
+  const float qnan = __int_as_float(0x7fc00000);
   if (ok) {
-    double acc = 0.0;
+    double acc = 0.0, gs[3] = {0.0, 0.0, 0.0};
     bool all = true;
     for (int c = 0; c < 8; ++c) {
       const int dx = c & 1, dy = (c >> 1) & 1, dz = (c >> 2) & 1;
       float e;
       if (!voxel_e(p, i0[0] + dx, i0[1] + dy, i0[2] + dz, ckey, cslot, &e)) { all = false; break; }
-      const double wgt = dm(dm(dx ? f[0] : ds(1.0, f[0]), dy ? f[1] : ds(1.0, f[1])), dz ? f[2] : ds(1.0, f[2]));
+      const double wx = dx ? f[0] : ds(1.0, f[0]), wy = dy ? f[1] : ds(1.0, f[1]), wz = dz ? f[2] : ds(1.0, f[2]);
+      const double wgt = dm(dm(wx, wy), wz);
       if (wgt > 0) acc = da(acc, dm(wgt, (double)e));
+      if (p.grad) {   // d/df of the trilinear weights (f4: value + gradient look-ups for registration)
+        gs[0] += (dx ? 1.0 : -1.0) * wy * wz * (double)e;
+        gs[1] += (dy ? 1.0 : -1.0) * wx * wz * (double)e;
+        gs[2] += (dz ? 1.0 : -1.0) * wx * wy * (double)e;
+      }
     }
-    if (all) { p.out[i] = (float)acc; p.status[i] = 0; return; }
+    if (all) {
+      p.out[i] = (float)acc;
+      p.status[i] = 0;
+      if (p.grad)   // dE/dx_world = R_WS dE/dx_s, dE/dx_s = (dE/df) / s
+        for (int a = 0; a < 3; ++a)
+          p.grad[3 * i + a] = (float)((p.T[4 * a] * gs[0] + p.T[4 * a + 1] * gs[1] + p.T[4 * a + 2] * gs[2]) / p.s);
+      return;
+    }
+    if (p.grad) { p.grad[3 * i] = qnan; p.grad[3 * i + 1] = qnan; p.grad[3 * i + 2] = qnan; }
     int v[3];
     for (int a = 0; a < 3; ++a) v[a] = (int)floor(__ddiv_rn(xs[a], p.s));
     float e;
     if (voxel_e(p, v[0], v[1], v[2], ckey, cslot, &e)) { p.out[i] = e; p.status[i] = 1; return; }
   }
-  p.out[i] = __int_as_float(0x7fc00000);
+  if (p.grad && !ok) { p.grad[3 * i] = qnan; p.grad[3 * i + 1] = qnan; p.grad[3 * i + 2] = qnan; }
+  p.out[i] = qnan;
   p.status[i] = 2;
 }
 
@@ -123,10 +140,10 @@ __global__ void pack_kernel(const float* esdf, const int4* coords, int nb, unsig
 }  // namespace
 
 cudaError_t launch_query(const cvx_submap* sm, const float* pts, int64_t m, float* out, uint8_t* status,
-                         cudaStream_t st) {
+                         cudaStream_t st, float* grad) {
   if (m <= 0) return cudaSuccess;
   QueryParams q;
-  q.pts = pts; q.m = m; q.out = out; q.status = status; q.hash = sm->hash; q.esdf = sm->pool.esdf;
+  q.pts = pts; q.m = m; q.out = out; q.status = status; q.grad = grad; q.hash = sm->hash; q.esdf = sm->pool.esdf;
   for (int i = 0; i < 16; ++i) q.T[i] = sm->T_ws[i];
   q.s = sm->cfg.voxel_size;
   {

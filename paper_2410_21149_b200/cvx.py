@@ -68,6 +68,8 @@ SIGNATURES = {
     "cvx_finalize_esdf": (C.c_int32, [_P, _P]),
     "cvx_update_esdf": (C.c_int32, [_P, _P, C.POINTER(C.c_int32)]),
     "cvx_query_distance": (C.c_int32, [_P, _P, C.c_int64, _P, _P, _P]),
+    "cvx_query_distance_gradient": (C.c_int32, [_P, _P, C.c_int64, _P, _P, _P, _P]),
+    "cvx_sample_surface": (C.c_int32, [_P, _P, C.c_int64, _P, _P, C.POINTER(C.c_int64), _P]),
     "cvx_export_blocks": (C.c_int32, [_P, _P, _P, _P, _P, C.c_int64, C.POINTER(C.c_int64), _P]),
     "cvx_import_tsdf_blocks": (C.c_int32, [_P, _P, _P, _P, C.c_int64, _P]),
     "cvx_pack_esdf": (C.c_int32, [_P, _P, C.c_int64, C.POINTER(C.c_int64), _P]),
@@ -215,6 +217,31 @@ class Submap:
                                         self._dev(out, torch.float32, "out"),
                                         self._dev(status, torch.uint8, "status"), self._stream()))
         return out, status
+
+    def query_gradient(self, points_world: torch.Tensor):
+        """(distance [m], gradient [m,3] world frame, status [m]) — cvx_query_distance_gradient."""
+        m = points_world.shape[0]
+        dev = points_world.device
+        out = torch.empty(m, dtype=torch.float32, device=dev)
+        grad = torch.empty((m, 3), dtype=torch.float32, device=dev)
+        status = torch.empty(m, dtype=torch.uint8, device=dev)
+        _check(lib().cvx_query_distance_gradient(self._h, self._dev(points_world, torch.float32, "points"), m,
+                                                 self._dev(out, torch.float32, "out"),
+                                                 self._dev(grad, torch.float32, "grad"),
+                                                 self._dev(status, torch.uint8, "status"), self._stream()))
+        return out, grad, status
+
+    def sample_surface(self, uniforms: torch.Tensor):
+        """(xyz [m,3] world, weight [m], total weight) for uint32 uniforms [m] (int32 tensor bit patterns)."""
+        m = uniforms.shape[0]
+        dev = uniforms.device
+        xyz = torch.empty((m, 3), dtype=torch.float32, device=dev)
+        w = torch.empty(m, dtype=torch.float32, device=dev)
+        tot = C.c_int64()
+        _check(lib().cvx_sample_surface(self._h, self._dev(uniforms, torch.int32, "uniforms"), m,
+                                        self._dev(xyz, torch.float32, "xyz"), self._dev(w, torch.float32, "w"),
+                                        C.byref(tot), self._stream()))
+        return xyz, w, int(tot.value)
 
     # -- state / inspection --------------------------------------------------------------------
     def reset(self, T_world_submap=None):

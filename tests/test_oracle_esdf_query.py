@@ -142,3 +142,63 @@ def test_esdf_sample_equals_full_transform(orc):
     pick = rng.choice(vox.shape[0], 300, replace=False)
     s = orc.esdf_sample(b, D, W, 0.02, vox[pick])
     assert np.array_equal(s, d2.reshape(-1)[pick])
+
+
+def test_query_gradient_affine_and_finite_differences(orc):
+    """f4 pin: on an affine field the trilinear gradient is the field's gradient (rotated to world);
+    elsewhere it matches central finite differences of the interpolated value inside a cell."""
+    s = 0.25
+    a = np.array([0.3, -1.1, 0.7, 0.05])
+    b, E = _affine_blocks(a, s)
+    import synth
+    T = synth.pose(synth.rot_zyx(0.4, 0.1, -0.2), [0.5, -0.25, 0.1])
+    rng = np.random.default_rng(3)
+    xs = rng.uniform(-6 * s, 6 * s, (300, 3))
+    xw = (xs @ T[:3, :3].T + T[:3, 3]).astype(np.float32)
+    val, st, g = orc.query(b, E, s, T, xw, gradient=True)
+    assert (st == 0).all()
+    assert np.allclose(g, np.tile(T[:3, :3] @ a[:3], (300, 1)), atol=1e-9)
+    # non-affine field: finite differences of the interpolant along random world directions
+    rng2 = np.random.default_rng(4)
+    E2 = rng2.normal(size=E.shape)
+    x0 = rng.uniform(-5 * s, 5 * s, (50, 3))
+    h = 1e-4
+    for d in np.eye(3):
+        xp = ((x0 + h * d) @ T[:3, :3].T + T[:3, 3])
+        xm = ((x0 - h * d) @ T[:3, :3].T + T[:3, 3])
+        x_ = (x0 @ T[:3, :3].T + T[:3, 3])
+        vp, _ = orc.query(b, E2, s, T, xp)
+        vm, _ = orc.query(b, E2, s, T, xm)
+        _, _, g2 = orc.query(b, E2, s, T, x_, gradient=True)
+        fd = (vp - vm) / (2 * h)                                     # derivative along submap axis d
+        assert np.allclose(g2 @ T[:3, :3] @ d, fd, atol=2e-2)
+
+
+def test_sample_surface_proportional_and_brute_force(orc):
+    """f4 pin: picks follow the weight distribution (exact counts for evenly spaced uniforms) and equal a
+    brute-force linear search over the candidate list."""
+    rng = np.random.default_rng(8)
+    b, D, W = _random_tsdf(rng)
+    W = np.round(W * 3)                                 # integer weights (constant-weight fusion)
+    thr = 0.05
+    site = (W > 0) & (np.abs(D) <= thr)
+    m = 4096
+    u = (np.arange(m, dtype=np.uint64) * (1 << 32) // m).astype(np.uint32)
+    xyz, w, tot = orc.sample_surface(b, D, W, thr, 0.1, np.eye(4), u)
+    assert tot == int((W[site] * (1 << 20)).sum())
+    # brute force: candidates in lexicographic block order, then local order
+    order = np.lexsort((b[:, 2], b[:, 1], b[:, 0]))
+    cand, wts = [], []
+    l = np.arange(512)
+    for ob in order:
+        for li in l[site[ob]]:
+            cand.append(((8 * b[ob, 0] + li % 8 + 0.5) * 0.1, (8 * b[ob, 1] + (li // 8) % 8 + 0.5) * 0.1,
+                         (8 * b[ob, 2] + li // 64 + 0.5) * 0.1))
+            wts.append(int(W[ob, li]) << 20)
+    cum = np.cumsum(wts)
+    tgt = (tot * u.astype(object)) // (1 << 32)
+    ks = [int(np.searchsorted(cum, int(t), side="right")) for t in tgt]
+    assert np.allclose(xyz, np.array(cand, np.float32)[ks], atol=1e-6)
+    # proportionality: evenly spaced uniforms hit each candidate about w_k / T * m times
+    counts = np.bincount(ks, minlength=len(cand))
+    assert np.abs(counts - np.array(wts) / tot * m).max() <= 1.0 + 1e-9
