@@ -129,6 +129,18 @@ cvx_status cvx_integrate_batch_host(cvx_submap* submap, const float* host_data, 
                                     int32_t n_frames, const double* T_world_sensor,
                                     const cvx_sensor_model* sensor, void* stream, cvx_integrate_stats* stats);
 
+/* Block-count submap trigger ("the area covered by sensor trajectory is approximated by
+ * considering the number of blocks used by the current submap"): integrate the frames in
+ * order, one launch per frame, and stop after the first frame at which the submap holds
+ * >= block_threshold blocks; *frames_integrated (host) = the frames taken (the caller starts the next
+ * submap with the rest).  The check runs on the device after each frame's ALLOCATE phase, so the frames
+ * are still pipelined; one synchronisation at the end.  Same results as calling
+ * cvx_integrate_pointcloud frame by frame and testing the block count after each.  Errors as
+ * cvx_integrate_batch; CVX_E_INVALID if block_threshold is not in [1, max_blocks]. */
+cvx_status cvx_integrate_until(cvx_submap* submap, const float* data, int64_t n_per_frame, int32_t n_frames,
+                               const double* T_world_sensor, const cvx_sensor_model* sensor,
+                               int64_t block_threshold, void* stream, int32_t* frames_integrated);
+
 /* Cumulative counters (synchronising). Returns the sticky device errors. */
 cvx_status cvx_get_stats(const cvx_submap* submap, cvx_integrate_stats* out);
 

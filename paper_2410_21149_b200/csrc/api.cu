@@ -126,6 +126,8 @@ void free_all(cvx_submap* sm) {
   if (sm->inc.list) cudaFree(sm->inc.list);
   if (sm->inc.cnt) cudaFree(sm->inc.cnt);
   if (sm->inc.cnt_host) cudaFreeHost(sm->inc.cnt_host);
+  if (sm->trig) cudaFree(sm->trig);
+  if (sm->trig_host) cudaFreeHost(sm->trig_host);
   delete sm->prof;
   sm->prof = nullptr;
 }
@@ -288,6 +290,38 @@ cvx_status cvx_integrate_batch_host(cvx_submap* sm, const float* host_data, int6
 cvx_status cvx_integrate_pointcloud(cvx_submap* sm, const float* data, int64_t n, const double* T_world_sensor,
                                     const cvx_sensor_model* sensor, void* stream, cvx_integrate_stats* stats) {
   return cvx_integrate_batch(sm, data, n, 1, T_world_sensor, sensor, stream, stats);
+}
+
+cvx_status cvx_integrate_until(cvx_submap* sm, const float* data, int64_t n_per_frame, int32_t n_frames,
+                               const double* T_world_sensor, const cvx_sensor_model* sensor, int64_t block_threshold,
+                               void* stream, int32_t* frames_integrated) {
+  g_last_error.clear();
+  if (!sm || !frames_integrated) return fail(CVX_E_INVALID, "NULL argument");
+  if (block_threshold < 1 || block_threshold > sm->pool.max_blocks)
+    return fail(CVX_E_INVALID, "block_threshold must be in [1, max_blocks]");
+  *frames_integrated = 0;
+  if (sm->finalized) return fail(CVX_E_STATE, "submap is finalized (S:L443): integrate rejected");
+  if (n_per_frame < 0 || n_frames < 0) return fail(CVX_E_INVALID, "negative sizes");
+  cvx_status rc = check_sensor(sensor, n_per_frame);
+  if (rc != CVX_OK) return rc;
+  if (n_frames == 0 || n_per_frame == 0) return CVX_OK;
+  if (!data || !T_world_sensor) return fail(CVX_E_INVALID, "NULL buffer");
+  for (int f = 0; f < n_frames; ++f)
+    if (!valid_pose(T_world_sensor + 16 * f)) return fail(CVX_E_INVALID, "T_world_sensor must be a finite rigid 4x4");
+  DeviceGuard g(sm->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaSuccess;
+  if (!sm->trig && ((e = cudaMalloc(&sm->trig, 16)) != cudaSuccess || (e = cudaMallocHost(&sm->trig_host, 16)) != cudaSuccess))
+    return cuda_fail(e, "allocating trigger state");
+  sm->trig_host[0] = (int)block_threshold; sm->trig_host[1] = 0; sm->trig_host[2] = 0; sm->trig_host[3] = 0;
+  if ((e = cudaMemcpyAsync(sm->trig, sm->trig_host, 16, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+    return cuda_fail(e, "integrate_until");
+  e = cvx::launch_integrate(sm, data, n_per_frame, n_frames, T_world_sensor, *sensor, st, false, sm->trig);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(sm->trig_host, sm->trig, 16, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "integrate_until");
+  *frames_integrated = sm->trig_host[1] ? sm->trig_host[2] : n_frames;
+  return CVX_OK;
 }
 
 cvx_status cvx_get_stats(const cvx_submap* sm, cvx_integrate_stats* out) {

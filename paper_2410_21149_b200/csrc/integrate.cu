@@ -105,9 +105,11 @@ struct PrepParams {
   Counters* ctr;
   int* lcnt;        // {n_rays, n_slots} of this launch (8-byte aligned)
   int list_cap;
+  const int* trig;  // nullable: {threshold, hit, consumed}; a hit submap takes no further frames
 };
 
 __global__ void __launch_bounds__(256) prepare_kernel(const __grid_constant__ PrepParams p) {
+  if (p.trig && *(volatile const int*)&p.trig[1]) return;   // block-count trigger fired: frame not taken
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   int status = -1;  // -1 no thread, 0 used, 1 invalid, 2 range, 3 domain
@@ -471,6 +473,12 @@ __global__ void __launch_bounds__(128, 8) walk_kernel(const __grid_constant__ Wa
   }
 }
 
+// Block-count submap trigger: after the ALLOCATE phase of frame k, fire once the
+// submap holds >= threshold blocks; frame k is the last one it takes.
+__global__ void trigger_check_kernel(const Counters* ctr, int* trig, int frame) {
+  if (!trig[1] && ctr->n_blocks >= trig[0]) { trig[1] = 1; trig[2] = frame + 1; }
+}
+
 // a5 FOLD of the packed per-launch accumulators into the exact sums: sum(w d) += (sum d' - n tq) 2^(30-q),
 // sum(w) += n 2^30 (w = 1).  Every update contributes exactly round(d 2^q) 2^(30-q), so the result does
 // not depend on how frames are grouped into launches.
@@ -544,14 +552,14 @@ static cudaError_t grow(void** ptr, int64_t* cap, int64_t need, size_t elem) {
 
 cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_frame, int n_frames,
                              const double* T_world_sensor, const cvx_sensor_model& sensor, cudaStream_t st,
-                             bool host_data) {
+                             bool host_data, int* trig) {
   if (n_per_frame <= 0 || n_frames <= 0) return cudaSuccess;
   const long long elems_per_frame = n_per_frame * (sensor.kind == 1 ? 1 : 3);
   // launches of equal size; at most kMaxBatch frames, and (constant weights) <= kMaxPackedRays rays so
   // the packed accumulators cannot overflow (R6/R7)
   const bool cw_ok = sm->aggregate && sm->cfg.weighting == 0 && n_per_frame <= kMaxPackedRays;
   const long long ray_limit = cw_ok ? kMaxPackedRays : (1ll << 31) - 1;
-  const int lim = (int)std::max<long long>(1, std::min<long long>(kMaxBatch, ray_limit / n_per_frame));
+  const int lim = trig ? 1 : (int)std::max<long long>(1, std::min<long long>(kMaxBatch, ray_limit / n_per_frame));
   const int chunks = (n_frames + lim - 1) / lim;
   const int per = (n_frames + chunks - 1) / chunks;
   const long long cap_rays = (long long)per * n_per_frame;
@@ -609,6 +617,7 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     pp.height = sensor.height;
     pp.frame_T = B.frame_T; pp.rays = (RayRec*)B.rays; pp.ctr = sm->ctr; pp.lcnt = B.lcnt;
     pp.list_cap = (int)std::min<long long>(B.slot_cap, 0x7fffffffll);
+    pp.trig = trig;
     {
       ProfScope ps_(sm, "ray_prepare", sm->side);
       prepare_kernel<<<blocks, 256, 0, sm->side>>>(pp);
@@ -624,6 +633,7 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
       if (k32) block_walk_kernel<true><<<blocks, 256, 0, sm->side>>>(wp);
       else block_walk_kernel<false><<<blocks, 256, 0, sm->side>>>(wp);
     }
+    if (trig) trigger_check_kernel<<<1, 1, 0, sm->side>>>(sm->ctr, trig, f0);
     cudaEventRecord(sm->ev_prepared[b], sm->side);
     // ---- caller's stream: a4 UPDATE + a5 FOLD of launch k
     cudaStreamWaitEvent(st, sm->ev_prepared[b], 0);

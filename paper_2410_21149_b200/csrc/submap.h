@@ -81,6 +81,9 @@ struct cvx_submap {
     int nb_prev = 0;                    // blocks covered by the last update
   } inc;
 
+  int* trig = nullptr;        // device {threshold, hit, consumed, -} of cvx_integrate_until
+  int* trig_host = nullptr;   // pinned mirror
+
   cvx::Prof* prof = nullptr;  // owned
 };
 
@@ -102,7 +105,7 @@ constexpr int kSlotsPerRay = 40; // average block-slot list capacity per ray (ov
 cudaError_t launch_reset(cvx_submap* sm, cudaStream_t st);
 cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_frame, int n_frames,
                              const double* T_world_sensor, const cvx_sensor_model& sensor, cudaStream_t st,
-                             bool host_data);
+                             bool host_data, int* trig = nullptr);
 // esdf.cu
 cudaError_t launch_finalize(cvx_submap* sm, int n_blocks, const int lo[3], const int hi[3], cudaStream_t st);
 cudaError_t launch_update_esdf(cvx_submap* sm, int n_blocks, const int lo[3], const int hi[3], cudaStream_t st,

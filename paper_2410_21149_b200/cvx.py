@@ -62,6 +62,8 @@ SIGNATURES = {
                                         C.POINTER(Stats)]),
     "cvx_integrate_batch_host": (C.c_int32, [_P, _P, C.c_int64, C.c_int32, _P, C.POINTER(SensorModel), _P,
                                              C.POINTER(Stats)]),
+    "cvx_integrate_until": (C.c_int32, [_P, _P, C.c_int64, C.c_int32, _P, C.POINTER(SensorModel), C.c_int64, _P,
+                                        C.POINTER(C.c_int32)]),
     "cvx_get_stats": (C.c_int32, [_P, C.POINTER(Stats)]),
     "cvx_get_block_count": (C.c_int32, [_P, C.POINTER(C.c_int64)]),
     "cvx_get_aabb": (C.c_int32, [_P, _P, _P]),
@@ -183,6 +185,17 @@ class Submap:
         _check(lib().cvx_integrate_batch(self._h, self._dev(data, torch.float32, "data"), n, F, _ptr(poses),
                                          C.byref(sm), self._stream(), C.byref(st) if st is not None else None))
         return st.asdict() if st is not None else None
+
+    def integrate_until(self, data: torch.Tensor, T_world_sensor, sensor: dict, block_threshold: int) -> int:
+        """Integrate frames until the submap holds >= block_threshold blocks; returns the frames taken."""
+        sm = sensor_model(sensor)
+        F = data.shape[0]
+        n = data[0].numel() if sensor["kind"] == 1 else data[0].numel() // 3
+        poses = _pose(T_world_sensor)
+        k = C.c_int32()
+        _check(lib().cvx_integrate_until(self._h, self._dev(data, torch.float32, "data"), n, F, _ptr(poses), C.byref(sm),
+                                         int(block_threshold), self._stream(), C.byref(k)))
+        return int(k.value)
 
     def integrate_batch_host(self, data: torch.Tensor, T_world_sensor, sensor: dict, stats: bool = False):
         """Like integrate_batch with `data` a CPU tensor (pin_memory() for asynchronous copies)."""

@@ -276,3 +276,32 @@ def test_reset_with_new_pose_matches_fresh_submap(tiny):
     b, _ = gpu_build(tiny, [2, 3], T_ws=T2, finalize=False)
     ea, eb = gpu_export_sorted(a), gpu_export_sorted(b)
     assert np.array_equal(ea[0], eb[0]) and np.array_equal(ea[1].view(np.uint32), eb[1].view(np.uint32))
+
+
+def test_block_count_trigger_matches_frame_by_frame(tiny):
+    """cvx_integrate_until (P:L115 block-count submap trigger, checked on the device) takes exactly the
+    frames a host loop would (integrate one frame, read the block count, stop at the threshold), with a
+    bit-identical TSDF."""
+    from paper_2410_21149_b200 import Submap
+    dev = torch.device("cuda", 0)
+    frames = list(range(10))
+    data = torch.stack([tiny["frames"][k]["data"] for k in frames]).to(dev).contiguous()
+    poses = np.stack([tiny["frames"][k]["T_world_sensor"] for k in frames])
+    ref = Submap(tiny["grid"], tiny["submaps"][0]["T_world_submap"], 0)
+    counts = []
+    for k in frames:
+        ref.integrate(data[k].contiguous(), poses[k], tiny["sensor"])
+        counts.append(ref.block_count())
+    thr = counts[4] if counts[4] > counts[3] else counts[4] + 1
+    expect = next((i + 1 for i, c in enumerate(counts) if c >= thr), len(frames))
+    a = Submap(tiny["grid"], tiny["submaps"][0]["T_world_submap"], 0)
+    took = a.integrate_until(data, poses, tiny["sensor"], thr)
+    assert took == expect
+    b = Submap(tiny["grid"], tiny["submaps"][0]["T_world_submap"], 0)
+    b.integrate_batch(data[:took].contiguous(), poses[:took], tiny["sensor"])
+    ea, eb = gpu_export_sorted(a), gpu_export_sorted(b)
+    assert np.array_equal(ea[0], eb[0]) and np.array_equal(ea[1].view(np.uint32), eb[1].view(np.uint32))
+    assert a.stats()["rays_in"] == took * data[0].numel()
+    # threshold never reached: every frame is taken
+    c = Submap(tiny["grid"], tiny["submaps"][0]["T_world_submap"], 0)
+    assert c.integrate_until(data, poses, tiny["sensor"], tiny["grid"]["max_blocks"]) == len(frames)
