@@ -268,6 +268,72 @@ def run_mav(args, world, rank, local):
         pg.destroy_process_group()
 
 
+def run_color(args, world, rank, local):
+    """TSDF + Color: the configs[1] submap build with per-point colour fused in the
+    band, timed beside the same build without colour (weak scaling: every rank builds its own submap)."""
+    import paper_2410_21149_b200 as cvx
+    import synth
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+    cfg = synth.make_config("lidar", device=dev, seed=1 + 1000 * rank, color=True)
+    data = torch.stack([cfg["frames"][k]["data"] for k in range(N_SCANS)]).contiguous()
+    rgb = torch.stack([cfg["frames"][k]["rgb"] for k in range(N_SCANS)]).contiguous()
+    poses = np.stack([cfg["frames"][k]["T_world_sensor"] for k in range(N_SCANS)])
+    T_sub = cfg["submaps"][0]["T_world_submap"]
+    stream = torch.cuda.current_stream(dev)
+    res = {}
+    for mode in ("plain", "color"):
+        sm = cvx.Submap(dict(cfg["grid"], color=1 if mode == "color" else 0), T_sub, local)
+
+        def step():
+            sm.reset()
+            for c in range(0, N_SCANS, args.batch):
+                if mode == "color":
+                    sm.integrate_color(data[c:c + args.batch], rgb[c:c + args.batch], poses[c:c + args.batch], cfg["sensor"])
+                else:
+                    sm.integrate_batch(data[c:c + args.batch], poses[c:c + args.batch], cfg["sensor"])
+            sm.finalize_esdf()
+
+        for _ in range(args.warmup):
+            step()
+        if pg is not None:
+            pg.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local) as clk:
+            e0.record(stream)
+            for _ in range(args.steps):
+                step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.steps
+        if pg is not None:
+            t = torch.tensor([ms], device=dev, dtype=torch.float64)
+            pg.all_reduce(t, op=pg.ReduceOp.MAX)
+            ms = float(t.item())
+        res[mode] = (ms, clk.summary())
+        del sm
+    ms, clk = res["color"]
+    line = {"metric": METRIC, "value": world * N_SCANS / (ms / 1e3), "unit": "scans/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32+i64", "data": "synthetic",
+            "config": {"workload": "lidar_submap_os1_64x1024_200scans_0.2m_color (BJ configs[1] + TSDF+Color)",
+                       "scans_per_rank": N_SCANS, "batch_scans": args.batch,
+                       "parallelism": f"submap-sharded x{world}"},
+            "plain_ms_per_step": res["plain"][0], "color_overhead": ms / res["plain"][0] - 1.0,
+            "clocks": clk}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if pg is not None:
+        pg.barrier()
+        pg.destroy_process_group()
+
+
 def run_incremental(args, world, rank, local, every=10):
     """configs[1] integrated in batches of `every` scans with an incremental ESDF update
     after each batch (the paper's per-frame ESDF maintenance), against one exact
@@ -386,7 +452,7 @@ def main():
     ap.add_argument("--queries", type=int, default=1 << 20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--workload", default="lidar", choices=["lidar", "esdf_stress", "incremental", "mav"],
+    ap.add_argument("--workload", default="lidar", choices=["lidar", "esdf_stress", "incremental", "mav", "color"],
                     help="lidar: configs[1] (default bench line); esdf_stress: configs[4] full ESDF recompute")
     args = ap.parse_args()
     world, rank, local = dist_setup()
@@ -399,6 +465,8 @@ def main():
     if args.workload == "incremental":
         run_incremental(args, world, rank, local)
         return
+    if args.workload == "color":
+        return run_color(args, world, rank, local)
     if args.workload == "mav":
         run_mav(args, world, rank, local)
         return

@@ -56,6 +56,7 @@ typedef struct {
   int32_t carve;             /* 1: update o -> p + tau*u (default); 0: band p +- tau*u (Q2) */
   double site_threshold;     /* ESDF site: observed and |D| <= site_threshold (O10, Q14; default s) */
   int64_t max_blocks;        /* block pool capacity; the hash table holds >= 2*max_blocks entries   */
+  int32_t color;             /* 1: also fuse per-point colour (cvx_integrate_color; TSDF + Color) */
 } cvx_grid_config;
 
 /* Sensor model of the incoming frames. */
@@ -140,6 +141,21 @@ cvx_status cvx_integrate_batch_host(cvx_submap* submap, const float* host_data, 
 cvx_status cvx_integrate_until(cvx_submap* submap, const float* data, int64_t n_per_frame, int32_t n_frames,
                                const double* T_world_sensor, const cvx_sensor_model* sensor,
                                int64_t block_threshold, void* stream, int32_t* frames_integrated);
+
+/* TSDF + Color (Fig. 4 "TSDF + Color"; R13): cvx_integrate_batch
+ * plus per-point colour `rgb` (device uint8 [n_frames][n_per_frame][3], same order as `data`).  Every
+ * update inside the truncation band (|sdf| < tau, before clamping) also adds w*(r,g,b) and w to the
+ * voxel's colour sums, so colour = sum(w c) / sum(w) over the band updates.  Requires config.color = 1.
+ * Errors as cvx_integrate_batch; CVX_E_INVALID without colour storage or with rgb NULL. */
+cvx_status cvx_integrate_color(cvx_submap* submap, const float* data, const uint8_t* rgb, int64_t n_per_frame,
+                               int32_t n_frames, const double* T_world_sensor, const cvx_sensor_model* sensor,
+                               void* stream, cvx_integrate_stats* stats);
+
+/* Export the fused colour in slot order (synchronising): rgb (device fp32 [nb][512][3], 0..255; 0 where no
+ * band update) and color_weight (device fp32 [nb][512], nullable).  Errors: CVX_E_INVALID without colour
+ * storage, CVX_E_CAPACITY if nb > capacity_blocks. */
+cvx_status cvx_export_color(const cvx_submap* submap, float* rgb, float* color_weight, int64_t capacity_blocks,
+                            int64_t* n_out, void* stream);
 
 /* Cumulative counters (synchronising). Returns the sticky device errors. */
 cvx_status cvx_get_stats(const cvx_submap* submap, cvx_integrate_stats* out);

@@ -63,6 +63,9 @@ def lib():
             L.orc_free.argtypes = [P]
             L.orc_integrate.restype = C.c_int32
             L.orc_integrate.argtypes = [P, P, C.c_int64, P, C.POINTER(Sensor), C.POINTER(Stats)]
+            L.orc_integrate_color.restype = C.c_int32
+            L.orc_integrate_color.argtypes = [P, P, P, C.c_int64, P, C.POINTER(Sensor), C.POINTER(Stats)]
+            L.orc_export_color.argtypes = [P, P, P]
             L.orc_num_blocks.restype = C.c_int64
             L.orc_num_blocks.argtypes = [P]
             L.orc_export.argtypes = [P, P, P, P]
@@ -128,6 +131,27 @@ class OracleSubmap:
 
     def num_blocks(self) -> int:
         return int(lib().orc_num_blocks(self._h))
+
+    def integrate_color(self, data, rgb, T_world_sensor, sensor: dict) -> dict:
+        """TSDF + Color (R13): as integrate, plus uint8 rgb [n, 3] per point."""
+        d = np.ascontiguousarray(np.asarray(data, dtype=np.float32))
+        n = d.size if sensor["kind"] == 1 else d.size // 3
+        c = np.ascontiguousarray(np.asarray(rgb, dtype=np.uint8))
+        assert c.size == 3 * n
+        T = np.ascontiguousarray(T_world_sensor, dtype=np.float64)
+        sm = sensor_struct(sensor)
+        st = Stats()
+        rc = lib().orc_integrate_color(self._h, _p(d), _p(c), n, _p(T), C.byref(sm), C.byref(st))
+        assert rc == 0
+        return st.asdict()
+
+    def export_color(self):
+        """(rgb fp64 [nb,512,3], colour weight fp64 [nb,512]) in the order of export()."""
+        nb = self.num_blocks()
+        rgb = np.zeros((nb, 512, 3))
+        cw = np.zeros((nb, 512))
+        lib().orc_export_color(self._h, _p(rgb), _p(cw))
+        return rgb, cw
 
     def export(self):
         """(bxyz int32 [nb,3], D fp64 [nb,512], W fp64 [nb,512]) in lexicographic (bx,by,bz) order."""

@@ -69,7 +69,8 @@ struct Key {
 inline int64_t fdiv8(int64_t v) { return (v >= 0) ? v / 8 : -((-v + 7) / 8); }
 inline int64_t fmod8(int64_t v) { return v - 8 * fdiv8(v); }
 
-struct Block { double swd[kBV]; double sw[kBV]; };
+// swd, sw: O8 TSDF sums; cw, cc: TSDF + Color sums (R13) sum(w) and sum(w c) over band updates
+struct Block { double swd[kBV]; double sw[kBV]; double cw[kBV]; double cc[kBV][3]; };
 
 struct Oracle {
   orc_grid g;
@@ -211,8 +212,11 @@ int64_t orc_ray_voxels(const double* o, const double* p, double voxel_size, doub
 // integrate one frame: every used ray updates every traversed voxel with
 // (w*d, w), d = clamp((p - c_v).u, -tau, tau) (O5, Q4); fusion = plain sums (O8: no weight cap, so
 // D = sum(w d)/sum(w) equals the sequential fold of S:L281 in real arithmetic).
-int32_t orc_integrate(void* h, const float* data, int64_t n, const double* T_world_sensor,
-                      const orc_sensor* sm, orc_stats* st) {
+// TSDF + Color ("TSDF + Color"; R13): with rgb (uint8 [n][3]) every update
+// whose unclamped sdf lies inside the truncation band, |sdf| < tau, also adds w and w * (r, g, b) to the
+// voxel's colour sums; colour = sum(w c) / sum(w).
+static int32_t integrate_frame(void* h, const float* data, const uint8_t* rgb, int64_t n,
+                               const double* T_world_sensor, const orc_sensor* sm, orc_stats* st) {
   Oracle* O = static_cast<Oracle*>(h);
   const orc_grid& g = O->g;
   double R[3][3], t[3];
@@ -260,6 +264,10 @@ int32_t orc_integrate(void* h, const float* data, int64_t n, const double* T_wor
       int local = (int)(fmod8(v.x) + 8 * fmod8(v.y) + 64 * fmod8(v.z));  // O9
       b->swd[local] += ray.w * d;
       b->sw[local] += ray.w;
+      if (rgb && std::fabs(sdf) < tau) {
+        b->cw[local] += ray.w;
+        for (int c3 = 0; c3 < 3; ++c3) b->cc[local][c3] += ray.w * (double)rgb[3 * i + c3];
+      }
       s.voxel_updates++;
     }
   }
@@ -267,6 +275,30 @@ int32_t orc_integrate(void* h, const float* data, int64_t n, const double* T_wor
   s.total_blocks = (int64_t)O->blocks.size();
   if (st) *st = s;
   return 0;
+}
+
+int32_t orc_integrate(void* h, const float* data, int64_t n, const double* T_world_sensor,
+                      const orc_sensor* sm, orc_stats* st) {
+  return integrate_frame(h, data, nullptr, n, T_world_sensor, sm, st);
+}
+
+int32_t orc_integrate_color(void* h, const float* data, const uint8_t* rgb, int64_t n, const double* T_world_sensor,
+                            const orc_sensor* sm, orc_stats* st) {
+  return integrate_frame(h, data, rgb, n, T_world_sensor, sm, st);
+}
+
+// Colour export in the order of orc_export: rgb = sum(w c) / sum(w) (0 where no band update), cw = sum(w).
+void orc_export_color(void* h, double* rgb, double* cw) {
+  Oracle* O = static_cast<Oracle*>(h);
+  int64_t i = 0;
+  for (auto& kv : O->blocks) {
+    for (int l = 0; l < kBV; ++l) {
+      double w = kv.second->cw[l];
+      cw[i * kBV + l] = w;
+      for (int c3 = 0; c3 < 3; ++c3) rgb[(i * kBV + l) * 3 + c3] = w > 0 ? kv.second->cc[l][c3] / w : 0.0;
+    }
+    ++i;
+  }
 }
 
 int64_t orc_num_blocks(void* h) { return (int64_t)static_cast<Oracle*>(h)->blocks.size(); }

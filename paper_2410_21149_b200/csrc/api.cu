@@ -101,6 +101,8 @@ void free_all(cvx_submap* sm) {
   if (sm->hash.e) cudaFree(sm->hash.e);
   if (sm->pool.sums) cudaFree(sm->pool.sums);
   if (sm->pool.acc) cudaFree(sm->pool.acc);
+  if (sm->pool.csum) cudaFree(sm->pool.csum);
+  if (sm->pool.cacc) cudaFree(sm->pool.cacc);
   if (sm->pool.esdf) cudaFree(sm->pool.esdf);
   if (sm->pool.coords) cudaFree(sm->pool.coords);
   if (sm->ctr) cudaFree(sm->ctr);
@@ -153,6 +155,7 @@ cvx_status cvx_create_submap(const cvx_grid_config* cfg, const double* T_world_s
   if (cfg->carve != 0 && cfg->carve != 1) return fail(CVX_E_INVALID, "carve must be 0 or 1");
   if (!(cfg->site_threshold >= 0) || !std::isfinite(cfg->site_threshold)) return fail(CVX_E_INVALID, "site_threshold must be >= 0");
   if (cfg->max_blocks < 1 || cfg->max_blocks >= (1ll << 23)) return fail(CVX_E_INVALID, "max_blocks must be in [1, 2^23)");
+  if (cfg->color != 0 && cfg->color != 1) return fail(CVX_E_INVALID, "color must be 0 or 1");
   if (!valid_pose(T_world_submap)) return fail(CVX_E_INVALID, "T_world_submap must be a finite rigid 4x4 (orthonormal within 1e-6)");
   int ndev = 0;
   cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -189,7 +192,9 @@ cvx_status cvx_create_submap(const cvx_grid_config* cfg, const double* T_world_s
       (e = cudaEventCreateWithFlags(&sm->ev_prepared[0], cudaEventDisableTiming)) != cudaSuccess ||
       (e = cudaEventCreateWithFlags(&sm->ev_prepared[1], cudaEventDisableTiming)) != cudaSuccess ||
       (e = cudaEventCreateWithFlags(&sm->ev_free[0], cudaEventDisableTiming)) != cudaSuccess ||
-      (e = cudaEventCreateWithFlags(&sm->ev_free[1], cudaEventDisableTiming)) != cudaSuccess) {
+      (e = cudaEventCreateWithFlags(&sm->ev_free[1], cudaEventDisableTiming)) != cudaSuccess ||
+      (cfg->color && ((e = cudaMalloc(&sm->pool.csum, nb * cvx::kBlockVox * 32)) != cudaSuccess ||
+                      (e = cudaMalloc(&sm->pool.cacc, nb * cvx::kBlockVox * 16)) != cudaSuccess))) {
     free_all(sm);
     delete sm;
     return cuda_fail(e, "allocating submap");
@@ -199,6 +204,10 @@ cvx_status cvx_create_submap(const cvx_grid_config* cfg, const double* T_world_s
   cudaMemset(sm->pool.sums, 0, nb * cvx::kBlockVox * 16);
   cudaMemset(sm->pool.acc, 0, nb * cvx::kBlockVox * 8);
   cudaMemset(sm->pool.esdf, 0, nb * cvx::kBlockVox * 4);
+  if (cfg->color) {
+    cudaMemset(sm->pool.csum, 0, nb * cvx::kBlockVox * 32);
+    cudaMemset(sm->pool.cacc, 0, nb * cvx::kBlockVox * 16);
+  }
   e = cvx::launch_reset(sm, 0);
   if (e == cudaSuccess) e = cudaEventRecord(sm->ev_free[0], 0);
   if (e == cudaSuccess) e = cudaEventRecord(sm->ev_free[1], 0);
@@ -237,7 +246,7 @@ cvx_status cvx_reset_submap(cvx_submap* sm, void* stream) {
 
 static cvx_status integrate_impl(cvx_submap* sm, const float* data, int64_t n_per_frame, int32_t n_frames,
                                  const double* T_world_sensor, const cvx_sensor_model* sensor, void* stream,
-                                 cvx_integrate_stats* stats, bool host_data) {
+                                 cvx_integrate_stats* stats, bool host_data, const uint8_t* rgb = nullptr) {
   g_last_error.clear();
   if (!sm) return fail(CVX_E_INVALID, "submap is NULL");
   if (sm->finalized) return fail(CVX_E_STATE, "submap is finalized (S:L443): integrate rejected");
@@ -255,7 +264,8 @@ static cvx_status integrate_impl(cvx_submap* sm, const float* data, int64_t n_pe
   if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
   cudaStream_t st = (cudaStream_t)stream;
   if (n_per_frame > 0 && n_frames > 0) {
-    cudaError_t e = cvx::launch_integrate(sm, data, n_per_frame, n_frames, T_world_sensor, *sensor, st, host_data);
+    cudaError_t e = cvx::launch_integrate(sm, data, n_per_frame, n_frames, T_world_sensor, *sensor, st, host_data,
+                                          nullptr, rgb);
     if (e != cudaSuccess) return cuda_fail(e, "integrate");
   }
   if (stats) {
@@ -285,6 +295,35 @@ cvx_status cvx_integrate_batch_host(cvx_submap* sm, const float* host_data, int6
                                     const double* T_world_sensor, const cvx_sensor_model* sensor, void* stream,
                                     cvx_integrate_stats* stats) {
   return integrate_impl(sm, host_data, n_per_frame, n_frames, T_world_sensor, sensor, stream, stats, true);
+}
+
+cvx_status cvx_integrate_color(cvx_submap* sm, const float* data, const uint8_t* rgb, int64_t n_per_frame,
+                               int32_t n_frames, const double* T_world_sensor, const cvx_sensor_model* sensor,
+                               void* stream, cvx_integrate_stats* stats) {
+  g_last_error.clear();
+  if (!sm) return fail(CVX_E_INVALID, "submap is NULL");
+  if (!sm->pool.csum) return fail(CVX_E_INVALID, "submap has no colour storage (config.color = 0)");
+  if (!rgb && n_per_frame > 0 && n_frames > 0) return fail(CVX_E_INVALID, "rgb is NULL");
+  return integrate_impl(sm, data, n_per_frame, n_frames, T_world_sensor, sensor, stream, stats, false, rgb);
+}
+
+cvx_status cvx_export_color(const cvx_submap* sm, float* rgb, float* color_weight, int64_t capacity_blocks,
+                            int64_t* n_out, void* stream) {
+  g_last_error.clear();
+  if (!sm || !n_out || !rgb) return fail(CVX_E_INVALID, "NULL argument");
+  if (!sm->pool.csum) return fail(CVX_E_INVALID, "submap has no colour storage (config.color = 0)");
+  DeviceGuard g(sm->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  cvx::Counters c;
+  cvx_status rc = read_counters(sm, st, &c);
+  if (rc != CVX_OK) return rc;
+  const int nb = c.n_blocks < sm->pool.max_blocks ? c.n_blocks : sm->pool.max_blocks;
+  *n_out = nb;
+  if (nb > capacity_blocks) return fail(CVX_E_CAPACITY, "export buffer smaller than the block count");
+  cudaError_t e = cvx::launch_export_color(sm, nb, rgb, color_weight, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "export_color");
+  return sticky(c);
 }
 
 cvx_status cvx_integrate_pointcloud(cvx_submap* sm, const float* data, int64_t n, const double* T_world_sensor,

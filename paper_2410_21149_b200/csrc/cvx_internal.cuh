@@ -50,6 +50,8 @@ struct HashView {
 struct PoolView {
   long long* sums;         // [max_blocks*512][2]
   unsigned long long* acc; // [max_blocks*512] packed per-launch accumulators (constant weights)
+  long long* csum;         // colour: [max_blocks*512][4] exact sums {sum w, sum w r, sum w g, sum w b} (2^-30)
+  unsigned long long* cacc;// colour: [max_blocks*512][2] packed per-launch {n<<42 | sum r, sum g<<32 | sum b}
   float* esdf;             // [max_blocks*512]
   int4* coords;            // [max_blocks]
   int max_blocks;

@@ -42,7 +42,7 @@ struct __align__(16) RayRec {
   float w;          // weight (O6)
   int n_vox;        // closed-form voxel count (COUNT)
   int list_off;     // offset of the ray's block-slot list, -1 if the list buffer was full
-  int pad;
+  unsigned rgb;     // colour of the point r | g << 8 | b << 16 (TSDF + Color)
 };
 static_assert(sizeof(RayRec) == 96, "RayRec layout");
 
@@ -106,6 +106,7 @@ struct PrepParams {
   int* lcnt;        // {n_rays, n_slots} of this launch (8-byte aligned)
   int list_cap;
   const int* trig;  // nullable: {threshold, hit, consumed}; a hit submap takes no further frames
+  const unsigned char* rgb;   // nullable: per-point colour [total][3]
 };
 
 __global__ void __launch_bounds__(256) prepare_kernel(const __grid_constant__ PrepParams p) {
@@ -183,7 +184,11 @@ __global__ void __launch_bounds__(256) prepare_kernel(const __grid_constant__ Pr
           rec.n_vox += (int)(dv < 0 ? -dv : dv);             // a2: n_r = 1 + sum |dv| (O4)
         }
         rec.list_off = -1;
-        rec.pad = 0;
+        rec.rgb = 0;
+        if (p.rgb) {
+          const unsigned char* c = p.rgb + 3 * src;
+          rec.rgb = (unsigned)c[0] | ((unsigned)c[1] << 8) | ((unsigned)c[2] << 16);
+        }
       }
     }
   }
@@ -253,6 +258,7 @@ struct WalkParams {
   float s, tau;
   int tq;           // round(tau 2^q): the clamp bound (and packed offset) of the quantised sdf
   int q;            // sdf quantum 2^-q m
+  long long band;   // colour band |S| < band, S in the fixed-point sdf units 2^-(q+kSdfF) m (= tau)
 };
 
 // Segmented sum over lanes with equal `peers` groups (log-depth shuffle tree); result valid at the
@@ -346,7 +352,7 @@ __global__ void __launch_bounds__(256) block_walk_kernel(const __grid_constant__
 // E_ij > 0  <=>  H_ij = F_ij - floor(-C_ij / 2^16) > 0; H_ij moves by a_j / -a_i per step like E_ij by
 // 2^16 a_j / -2^16 a_i, and |H_ij| <= 3 max(a) while both axes have crossings left.  Exact whenever
 // every |D_a| < 2^28 (spans < 2^12 voxels), which the launch checks from the sensor's max range.
-template <bool kAggregate, bool kConstW, bool k32>
+template <bool kAggregate, bool kConstW, bool k32, bool kColor = false>
 __global__ void __launch_bounds__(128, 8) walk_kernel(const __grid_constant__ WalkParams p) {
   using DT = typename std::conditional<k32, unsigned, unsigned long long>::type;
   using ST = typename std::conditional<k32, int, long long>::type;
@@ -362,6 +368,7 @@ __global__ void __launch_bounds__(128, 8) walk_kernel(const __grid_constant__ Wa
   DT D01 = 0, D02 = 0, D12 = 0, I0 = 0, I1 = 0, I2 = 0;   // wrap-around arithmetic, compared signed
   long long S = 0, U0 = 0, U1 = 0, U2 = 0;   // fixed-point sdf of the current voxel and its decrements
   int n = 0, nblk = 0, off = -1;
+  unsigned rgb = 0;
   long long w_fx = 0;
   float w = 0.0f;
   if (have) {
@@ -398,6 +405,7 @@ __global__ void __launch_bounds__(128, 8) walk_kernel(const __grid_constant__ Wa
     w_fx = __double2ll_rn((double)w * kFxScale);
     n = r.n_vox;
     off = r.list_off;
+    rgb = r.rgb;
   }
   const int maxn = (int)__reduce_max_sync(0xffffffffu, (unsigned)n);
   const int* list = off >= 0 ? p.slots + off : nullptr;
@@ -450,6 +458,21 @@ __global__ void __launch_bounds__(128, 8) walk_kernel(const __grid_constant__ Wa
         atomicAdd(sums + 2ull * addr + 1, (unsigned long long)w_fx);
       }
     }
+    if (kColor && upd && S > -p.band && S < p.band) {
+      // TSDF + Color (R13): band updates also fuse w (r, g, b); no run merging (neighbouring rays
+      // differ in colour near the surface)
+      const unsigned long long cr = rgb & 0xffu, cg = (rgb >> 8) & 0xffu, cb = (rgb >> 16) & 0xffu;
+      if (kConstW) {
+        atomicAdd(p.pool.cacc + 2ull * addr, (1ull << 42) | cr);
+        atomicAdd(p.pool.cacc + 2ull * addr + 1, (cg << 32) | cb);
+      } else {
+        unsigned long long* cs = reinterpret_cast<unsigned long long*>(p.pool.csum) + 4ull * addr;
+        atomicAdd(cs, (unsigned long long)w_fx);
+        atomicAdd(cs + 1, (unsigned long long)(w_fx * (long long)cr));
+        atomicAdd(cs + 2, (unsigned long long)(w_fx * (long long)cg));
+        atomicAdd(cs + 3, (unsigned long long)(w_fx * (long long)cb));
+      }
+    }
     // O4: step the axis with the earliest next crossing among those with crossings left (ties
     // x < y < z), predicated on the lane still having a voxel to go.
     const bool stp = it + 1 < n;
@@ -477,6 +500,25 @@ __global__ void __launch_bounds__(128, 8) walk_kernel(const __grid_constant__ Wa
 // submap holds >= threshold blocks; frame k is the last one it takes.
 __global__ void trigger_check_kernel(const Counters* ctr, int* trig, int frame) {
   if (!trig[1] && ctr->n_blocks >= trig[0]) { trig[1] = 1; trig[2] = frame + 1; }
+}
+
+// TSDF + Color (R13): fold the packed colour accumulators {n << 42 | sum r, sum g << 32 | sum b} (w = 1)
+// into the exact colour sums {sum w, sum w r, sum w g, sum w b} at 2^-30.
+__global__ void fold_color_kernel(const Counters* ctr, unsigned long long* cacc, long long* csum, int max_blocks) {
+  const int nb = min(ctr->n_blocks, max_blocks);
+  const long long nv = (long long)nb * kBlockVox;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (long long)gridDim.x * blockDim.x) {
+    const ulonglong2 v = reinterpret_cast<ulonglong2*>(cacc)[i];
+    if ((v.x | v.y) == 0ull) continue;
+    longlong2* cs = reinterpret_cast<longlong2*>(csum) + 2 * i;
+    longlong2 a = cs[0], b = cs[1];
+    a.x += (long long)(v.x >> 42) << 30;                  // sum w (w = 1 -> 2^30)
+    a.y += (long long)(v.x & ((1ull << 42) - 1)) << 30;   // sum w r
+    b.x += (long long)(v.y >> 32) << 30;                  // sum w g
+    b.y += (long long)(v.y & 0xffffffffull) << 30;        // sum w b
+    cs[0] = a; cs[1] = b;
+    reinterpret_cast<ulonglong2*>(cacc)[i] = make_ulonglong2(0ull, 0ull);
+  }
 }
 
 // a5 FOLD of the packed per-launch accumulators into the exact sums: sum(w d) += (sum d' - n tq) 2^(30-q),
@@ -518,6 +560,16 @@ __global__ void zero_blocks_kernel(Counters* ctr, long long* sums, unsigned long
   }
 }
 
+__global__ void zero_color_kernel(Counters* ctr, long long* csum, unsigned long long* cacc, int max_blocks) {
+  const int nb = min(*(volatile int*)&ctr->n_blocks, max_blocks);
+  const long long nv = (long long)nb * kBlockVox;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (long long)gridDim.x * blockDim.x) {
+    reinterpret_cast<longlong2*>(csum)[2 * i] = make_longlong2(0, 0);
+    reinterpret_cast<longlong2*>(csum)[2 * i + 1] = make_longlong2(0, 0);
+    reinterpret_cast<ulonglong2*>(cacc)[i] = make_ulonglong2(0ull, 0ull);
+  }
+}
+
 __global__ void reset_counters_kernel(Counters* ctr) {
   Counters c = {};
   c.aabb_lo[0] = c.aabb_lo[1] = c.aabb_lo[2] = 0x7fffffff;
@@ -531,6 +583,10 @@ cudaError_t launch_reset(cvx_submap* sm, cudaStream_t st) {
   {
     ProfScope ps_(sm, "reset_zero_blocks", st);
     zero_blocks_kernel<<<148 * 8, 256, 0, st>>>(sm->ctr, sm->pool.sums, sm->pool.acc, sm->pool.max_blocks);
+  }
+  if (sm->pool.csum) {
+    ProfScope ps_(sm, "reset_zero_color", st);
+    zero_color_kernel<<<148 * 8, 256, 0, st>>>(sm->ctr, sm->pool.csum, sm->pool.cacc, sm->pool.max_blocks);
   }
   {
     ProfScope ps_(sm, "reset_counters", st);
@@ -552,7 +608,7 @@ static cudaError_t grow(void** ptr, int64_t* cap, int64_t need, size_t elem) {
 
 cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_frame, int n_frames,
                              const double* T_world_sensor, const cvx_sensor_model& sensor, cudaStream_t st,
-                             bool host_data, int* trig) {
+                             bool host_data, int* trig, const unsigned char* rgb) {
   if (n_per_frame <= 0 || n_frames <= 0) return cudaSuccess;
   const long long elems_per_frame = n_per_frame * (sensor.kind == 1 ? 1 : 3);
   // launches of equal size; at most kMaxBatch frames, and (constant weights) <= kMaxPackedRays rays so
@@ -618,6 +674,7 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     pp.frame_T = B.frame_T; pp.rays = (RayRec*)B.rays; pp.ctr = sm->ctr; pp.lcnt = B.lcnt;
     pp.list_cap = (int)std::min<long long>(B.slot_cap, 0x7fffffffll);
     pp.trig = trig;
+    pp.rgb = rgb ? rgb + (long long)f0 * n_per_frame * 3 : nullptr;
     {
       ProfScope ps_(sm, "ray_prepare", sm->side);
       prepare_kernel<<<blocks, 256, 0, sm->side>>>(pp);
@@ -628,6 +685,7 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     wp.s = (float)sm->cfg.voxel_size; wp.tau = (float)sm->cfg.truncation;
     wp.tq = tq;
     wp.q = q;
+    wp.band = std::llround(std::ldexp(sm->cfg.truncation, q + kSdfF));
     {
       ProfScope ps_(sm, "block_walk_allocate", sm->side);
       if (k32) block_walk_kernel<true><<<blocks, 256, 0, sm->side>>>(wp);
@@ -641,7 +699,10 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     {
       ProfScope ps_(sm, "ray_walk_update", st);
       const unsigned wblocks = (unsigned)((total + 127) / 128);   // 128-thread CTAs (measured best)
-      if (sm->aggregate) {
+      if (rgb) {
+        if (cw) { if (k32) walk_kernel<true, true, true, true><<<wblocks, 128, 0, st>>>(wp); else walk_kernel<true, true, false, true><<<wblocks, 128, 0, st>>>(wp); }
+        else { if (k32) walk_kernel<true, false, true, true><<<wblocks, 128, 0, st>>>(wp); else walk_kernel<true, false, false, true><<<wblocks, 128, 0, st>>>(wp); }
+      } else if (sm->aggregate) {
         if (cw) { if (k32) walk_kernel<true, true, true><<<wblocks, 128, 0, st>>>(wp); else walk_kernel<true, true, false><<<wblocks, 128, 0, st>>>(wp); }
         else { if (k32) walk_kernel<true, false, true><<<wblocks, 128, 0, st>>>(wp); else walk_kernel<true, false, false><<<wblocks, 128, 0, st>>>(wp); }
       } else {
@@ -651,6 +712,10 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     if (cw) {
       ProfScope ps_(sm, "fold", st);
       fold_kernel<<<148 * 8, 256, 0, st>>>(sm->ctr, sm->pool.acc, sm->pool.sums, sm->pool.max_blocks, tq, 30 - q);
+    }
+    if (cw && rgb) {
+      ProfScope ps_(sm, "fold_color", st);
+      fold_color_kernel<<<148 * 8, 256, 0, st>>>(sm->ctr, sm->pool.cacc, sm->pool.csum, sm->pool.max_blocks);
     }
     cudaEventRecord(sm->ev_free[b], st);
   }

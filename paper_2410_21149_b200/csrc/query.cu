@@ -199,3 +199,25 @@ cudaError_t launch_pack(const cvx_submap* sm, int n_blocks, void* dst_records, c
 }
 
 }  // namespace cvx
+
+namespace cvx {
+// TSDF + Color (R13): colour = sum(w c) / sum(w) per voxel, slot order.
+__global__ void export_color_kernel(const long long* csum, int n_blocks, float* rgb, float* cw) {
+  const long long nv = (long long)n_blocks * kBlockVox;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (long long)gridDim.x * blockDim.x) {
+    const longlong2 a = reinterpret_cast<const longlong2*>(csum)[2 * i];
+    const longlong2 b = reinterpret_cast<const longlong2*>(csum)[2 * i + 1];
+    const double w = (double)a.x;
+    rgb[3 * i + 0] = a.x > 0 ? (float)((double)a.y / w) : 0.0f;
+    rgb[3 * i + 1] = a.x > 0 ? (float)((double)b.x / w) : 0.0f;
+    rgb[3 * i + 2] = a.x > 0 ? (float)((double)b.y / w) : 0.0f;
+    if (cw) cw[i] = (float)((double)a.x * (1.0 / kFxScale));
+  }
+}
+
+cudaError_t launch_export_color(const cvx_submap* sm, int n_blocks, float* rgb, float* cw, cudaStream_t st) {
+  if (n_blocks <= 0) return cudaSuccess;
+  export_color_kernel<<<148 * 8, 256, 0, st>>>(sm->pool.csum, n_blocks, rgb, cw);
+  return cudaGetLastError();
+}
+}  // namespace cvx

@@ -105,7 +105,8 @@ constexpr int kSlotsPerRay = 40; // average block-slot list capacity per ray (ov
 cudaError_t launch_reset(cvx_submap* sm, cudaStream_t st);
 cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_frame, int n_frames,
                              const double* T_world_sensor, const cvx_sensor_model& sensor, cudaStream_t st,
-                             bool host_data, int* trig = nullptr);
+                             bool host_data, int* trig = nullptr, const unsigned char* rgb = nullptr);
+cudaError_t launch_export_color(const cvx_submap* sm, int n_blocks, float* rgb, float* cw, cudaStream_t st);
 // esdf.cu
 cudaError_t launch_finalize(cvx_submap* sm, int n_blocks, const int lo[3], const int hi[3], cudaStream_t st);
 cudaError_t launch_update_esdf(cvx_submap* sm, int n_blocks, const int lo[3], const int hi[3], cudaStream_t st,

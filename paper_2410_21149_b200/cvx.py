@@ -33,7 +33,7 @@ class CvxError(RuntimeError):
 class GridConfig(C.Structure):
     _fields_ = [("voxel_size", C.c_double), ("block_side", C.c_int32), ("truncation", C.c_double),
                 ("weighting", C.c_int32), ("weight_range_floor", C.c_double), ("carve", C.c_int32),
-                ("site_threshold", C.c_double), ("max_blocks", C.c_int64)]
+                ("site_threshold", C.c_double), ("max_blocks", C.c_int64), ("color", C.c_int32)]
 
 
 class SensorModel(C.Structure):
@@ -64,6 +64,9 @@ SIGNATURES = {
                                              C.POINTER(Stats)]),
     "cvx_integrate_until": (C.c_int32, [_P, _P, C.c_int64, C.c_int32, _P, C.POINTER(SensorModel), C.c_int64, _P,
                                         C.POINTER(C.c_int32)]),
+    "cvx_integrate_color": (C.c_int32, [_P, _P, _P, C.c_int64, C.c_int32, _P, C.POINTER(SensorModel), _P,
+                                        C.POINTER(Stats)]),
+    "cvx_export_color": (C.c_int32, [_P, _P, _P, C.c_int64, C.POINTER(C.c_int64), _P]),
     "cvx_get_stats": (C.c_int32, [_P, C.POINTER(Stats)]),
     "cvx_get_block_count": (C.c_int32, [_P, C.POINTER(C.c_int64)]),
     "cvx_get_aabb": (C.c_int32, [_P, _P, _P]),
@@ -117,7 +120,7 @@ def grid_config(grid: dict) -> GridConfig:
     return GridConfig(float(grid["voxel_size"]), int(grid.get("block_side", 8)), float(grid["truncation"]),
                       int(grid.get("weighting", 0)), float(grid.get("weight_range_floor", 0.1)),
                       int(grid.get("carve", 1)), float(grid.get("site_threshold", grid["voxel_size"])),
-                      int(grid.get("max_blocks", 1 << 16)))
+                      int(grid.get("max_blocks", 1 << 16)), int(grid.get("color", 0)))
 
 
 def sensor_model(sensor: dict) -> SensorModel:
@@ -185,6 +188,34 @@ class Submap:
         _check(lib().cvx_integrate_batch(self._h, self._dev(data, torch.float32, "data"), n, F, _ptr(poses),
                                          C.byref(sm), self._stream(), C.byref(st) if st is not None else None))
         return st.asdict() if st is not None else None
+
+    def integrate_color(self, data: torch.Tensor, rgb: torch.Tensor, T_world_sensor, sensor: dict,
+                        stats: bool = False):
+        """TSDF + Color: data as integrate_batch, rgb uint8 [F, n, 3] (same point order)."""
+        sm = sensor_model(sensor)
+        F = data.shape[0]
+        n = data[0].numel() if sensor["kind"] == 1 else data[0].numel() // 3
+        if rgb.numel() != F * n * 3:
+            raise ValueError("rgb must hold 3 bytes per point")
+        poses = _pose(T_world_sensor)
+        if poses.shape[0] != F:
+            raise ValueError("one pose per frame")
+        st = Stats() if stats else None
+        _check(lib().cvx_integrate_color(self._h, self._dev(data, torch.float32, "data"),
+                                         self._dev(rgb, torch.uint8, "rgb"), n, F, _ptr(poses), C.byref(sm),
+                                         self._stream(), C.byref(st) if st is not None else None))
+        return st.asdict() if st is not None else None
+
+    def export_color(self):
+        """(rgb fp32 [nb,512,3] in 0..255, colour weight fp32 [nb,512]), slot order (as export())."""
+        nb = self.block_count()
+        dev = torch.device("cuda", self.device)
+        rgb = torch.empty((nb, 512, 3), dtype=torch.float32, device=dev)
+        cw = torch.empty((nb, 512), dtype=torch.float32, device=dev)
+        n = C.c_int64()
+        _check(lib().cvx_export_color(self._h, C.c_void_p(rgb.data_ptr()), C.c_void_p(cw.data_ptr()), nb,
+                                      C.byref(n), self._stream()))
+        return rgb, cw
 
     def integrate_until(self, data: torch.Tensor, T_world_sensor, sensor: dict, block_threshold: int) -> int:
         """Integrate frames until the submap holds >= block_threshold blocks; returns the frames taken."""

@@ -7,5 +7,5 @@ LiDAR MAV flights and Replica/Redwood RGB-D rooms).  Recipes: DESIGN.md "Input r
 """
 from .scenes import (  # noqa: F401
     Scene, raycast, make_config, CONFIGS, lidar_directions, pinhole_depth, lidar_scan, camera_pose,
-    pose, rot_zyx,
+    pose, rot_zyx, surface_color,
 )

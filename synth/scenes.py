@@ -148,12 +148,27 @@ def lidar_directions(rings: int = 64, cols: int = 1024, fov_deg: float = 33.2) -
     return np.stack([np.cos(E) * np.cos(A), np.cos(E) * np.sin(A), np.sin(E)], -1).reshape(-1, 3)
 
 
+def surface_color(hits_w: torch.Tensor) -> torch.Tensor:
+    """Procedural surface texture: uint8 RGB [N,3] of world hit points (fp64 [N,3]; non-finite -> 0).
+    Smooth in space, so neighbouring returns on a surface carry similar (not equal) colours."""
+    x, y, z = hits_w[:, 0], hits_w[:, 1], hits_w[:, 2]
+    c = torch.stack([128 + 127 * torch.sin(1.3 * x) * torch.cos(0.7 * y),
+                     128 + 127 * torch.sin(0.9 * z + 0.5 * x),
+                     128 + 127 * torch.cos(0.4 * (x + y + z))], -1)
+    c = torch.where(torch.isfinite(c), c, torch.zeros_like(c))
+    return torch.clamp(torch.floor(c), 0, 255).to(torch.uint8)
+
+
 def lidar_scan(scene: Scene, T_ws: np.ndarray, dirs_s: np.ndarray, r_max: float, sigma: float,
-               rng: np.random.Generator, device="cpu") -> torch.Tensor:
-    """Organised LiDAR scan in the sensor frame, fp32 [N,3]; NaN where there is no return."""
+               rng: np.random.Generator, device="cpu", color: bool = False):
+    """Organised LiDAR scan in the sensor frame, fp32 [N,3]; NaN where there is no return.
+    color=True also returns the uint8 [N,3] surface colour of each return (0 where none)."""
     d_s = _t(dirs_s, device)
     R = _t(T_ws[:3, :3], device)
     t = raycast(scene, T_ws[:3, 3], d_s @ R.T)
+    if color:
+        rgb = surface_color(_t(T_ws[:3, 3], device) + (d_s @ R.T) * t.reshape(-1, 1))
+        return lidar_scan(scene, T_ws, dirs_s, r_max, sigma, rng, device), rgb
     noise = _t(rng.normal(0.0, sigma, size=len(dirs_s)), device) if sigma > 0 else 0.0
     ok = t <= r_max
     r = t + noise
@@ -169,11 +184,15 @@ def pinhole_rays(width: int, height: int, fx: float, fy: float, cx: float, cy: f
 
 
 def pinhole_depth(scene: Scene, T_wc: np.ndarray, cam: dict, r_max: float, noise_k: float,
-                  rng: np.random.Generator, device="cpu") -> torch.Tensor:
-    """Depth image fp32 [H,W] (z along the optical axis); 0 where there is no return."""
+                  rng: np.random.Generator, device="cpu", color: bool = False):
+    """Depth image fp32 [H,W] (z along the optical axis); 0 where there is no return.
+    color=True also returns the uint8 [H*W,3] surface colour per pixel (0 where no return)."""
     d_c = _t(pinhole_rays(cam["width"], cam["height"], cam["fx"], cam["fy"], cam["cx"], cam["cy"]), device)
     R = _t(T_wc[:3, :3], device)
     z = raycast(scene, T_wc[:3, 3], d_c @ R.T)       # unit-z rays: parameter == depth
+    if color:
+        rgb = surface_color(_t(T_wc[:3, 3], device) + (d_c @ R.T) * z.reshape(-1, 1))
+        return pinhole_depth(scene, T_wc, cam, r_max, noise_k, rng, device), rgb
     ok = (z * torch.linalg.norm(d_c, dim=1)) <= r_max
     if noise_k > 0:
         z = z + _t(rng.normal(0.0, 1.0, size=z.shape[0]), device) * noise_k * z * z
@@ -261,12 +280,13 @@ def _mav_scene(seed: int) -> Scene:
 CONFIGS = ("tiny", "lidar", "rgbd", "mav")
 
 
-def make_config(name: str, frames=None, device="cpu", seed=None, lidar_cols: int = 1024):
+def make_config(name: str, frames=None, device="cpu", seed=None, lidar_cols: int = 1024, color: bool = False):
     """Build one BASELINE.json config as posed frames.
 
     Returns dict(name, grid, sensor, submaps=[dict(T_world_submap, frames=[idx...])],
     frames=[dict(data=fp32 tensor, T_world_sensor=4x4)]).  `frames` selects a subset of
-    frame indices (the rest are not generated).
+    frame indices (the rest are not generated).  color=True adds per-point surface colour
+    (uint8 [n,3], frame["rgb"]) for TSDF + Color.
     """
     if name == "tiny":                                   # BJ.configs[0]
         seed = 0 if seed is None else seed
@@ -275,7 +295,7 @@ def make_config(name: str, frames=None, device="cpu", seed=None, lidar_cols: int
         n_frames = 10
         poses = [camera_pose([0.0, -0.45 + 0.1 * k, 1.0], 0.0, math.radians(15.0)) for k in range(n_frames)]
         grid = _grid(0.1, 0.3, 1 << 13)
-        gen = lambda k, T, rng: pinhole_depth(scene, T, cam, cam["max_range"], 0.0, rng, device)  # noqa: E731
+        gen = lambda k, T, rng: pinhole_depth(scene, T, cam, cam["max_range"], 0.0, rng, device, color)  # noqa: E731
         submaps = [dict(T_world_submap=np.eye(4), frames=list(range(n_frames)))]
         sensor = cam
     elif name in ("lidar", "mav"):                       # BJ.configs[1], [3]
@@ -313,7 +333,7 @@ def make_config(name: str, frames=None, device="cpu", seed=None, lidar_cols: int
                 submaps.append(dict(T_world_submap=pose(np.eye(3), poses[k0][:3, 3] * np.array([1, 1, 0])),
                                     frames=list(range(k0, k0 + 50))))
             grid = _grid(0.2, 0.6, 1 << 19)
-        gen = lambda k, T, rng: lidar_scan(scene, T, dirs, sensor["max_range"], 0.02, rng, device)  # noqa: E731
+        gen = lambda k, T, rng: lidar_scan(scene, T, dirs, sensor["max_range"], 0.02, rng, device, color)  # noqa: E731
     elif name == "rgbd":                                 # BJ.configs[2]
         seed = 2 if seed is None else seed
         scene = _room_scene(seed)
@@ -329,7 +349,7 @@ def make_config(name: str, frames=None, device="cpu", seed=None, lidar_cols: int
         submaps = [dict(T_world_submap=pose(np.eye(3), [0.0, 0.0, 0.0]), frames=list(range(100 * m, 100 * m + 100)))
                    for m in range(10)]
         grid = _grid(0.05, 0.15, 1 << 16)
-        gen = lambda k, T, rng: pinhole_depth(scene, T, sensor, sensor["max_range"], 0.0012, rng, device)  # noqa: E731
+        gen = lambda k, T, rng: pinhole_depth(scene, T, sensor, sensor["max_range"], 0.0012, rng, device, color)  # noqa: E731
     else:
         raise ValueError(f"unknown config {name!r}")
 
@@ -337,7 +357,11 @@ def make_config(name: str, frames=None, device="cpu", seed=None, lidar_cols: int
     out_frames = {}
     for k in idx:
         rng = np.random.Generator(np.random.PCG64([seed, int(k)]))
-        out_frames[int(k)] = dict(data=gen(k, poses[k], rng), T_world_sensor=poses[k])
+        g = gen(k, poses[k], rng)
+        if color:
+            out_frames[int(k)] = dict(data=g[0], rgb=g[1], T_world_sensor=poses[k])
+        else:
+            out_frames[int(k)] = dict(data=g, T_world_sensor=poses[k])
     return dict(name=name, grid=grid, sensor=sensor, submaps=submaps, frames=out_frames,
                 poses=poses, n_frames=n_frames, seed=seed)
 
