@@ -167,6 +167,10 @@ cvx_status cvx_create_submap(const cvx_grid_config* cfg, const double* T_world_s
   cvx_submap* sm = new cvx_submap();
   sm->prof = new cvx::Prof();
   if (const char* ag = std::getenv("CVX_AGGREGATE")) sm->aggregate = ag[0] != '0';  // tuning knob
+  // CVX_SERIAL=1 (diagnostics): the pipeline's side stream is the legacy default stream, so with a caller
+  // on the default stream every kernel runs alone and per-kernel event times are solo times
+  const bool serial = std::getenv("CVX_SERIAL") && std::getenv("CVX_SERIAL")[0] == '1';
+  if (const char* wc = std::getenv("CVX_WALK_CW")) sm->walk_cw = wc[0] != '0';     // tuning knob
   sm->cfg = *cfg;
   std::memcpy(sm->T_ws, T_world_submap, sizeof(sm->T_ws));
   sm->device = device;
@@ -187,7 +191,7 @@ cvx_status cvx_create_submap(const cvx_grid_config* cfg, const double* T_world_s
       (e = cudaMalloc(&sm->buf[0].frame_T, sizeof(double) * 16 * cvx::kMaxBatch)) != cudaSuccess ||
       (e = cudaMalloc(&sm->buf[1].frame_T, sizeof(double) * 16 * cvx::kMaxBatch)) != cudaSuccess ||
       (e = cudaMalloc(&sm->buf[0].lcnt, 16)) != cudaSuccess || (e = cudaMalloc(&sm->buf[1].lcnt, 16)) != cudaSuccess ||
-      (e = cudaStreamCreateWithFlags(&sm->side, cudaStreamNonBlocking)) != cudaSuccess ||
+      (!serial && (e = cudaStreamCreateWithFlags(&sm->side, cudaStreamNonBlocking)) != cudaSuccess) ||
       (e = cudaEventCreateWithFlags(&sm->ev_entry, cudaEventDisableTiming)) != cudaSuccess ||
       (e = cudaEventCreateWithFlags(&sm->ev_prepared[0], cudaEventDisableTiming)) != cudaSuccess ||
       (e = cudaEventCreateWithFlags(&sm->ev_prepared[1], cudaEventDisableTiming)) != cudaSuccess ||

@@ -135,11 +135,14 @@ __device__ inline int hash_activate(const HashView& h, const PoolView& pool, Cou
   return hash_activate_pf(h, pool, ctr, key, bx, by, bz, ld_entry(h.e + hash_slot(key, h)));
 }
 
-// Packed accumulator: at most kMaxPackedRays updates of one voxel per launch (22-bit count), and the
-// 42-bit field holds their sum of d' <= 2 round(tau 2^q) with q = floor(log2(2^19 / tau)).
-constexpr long long kMaxPackedRays = (1ll << 22) - 1;
+// Packed accumulator u64 = count << kCntShift | sum(d'): between two folds at most kMaxPackedRays
+// updates of one voxel (24-bit count), and the 40-bit field holds their sum of d' <= 2 round(tau 2^q)
+// <= 2^16 with q = floor(log2(2^15 / tau)) (quantum tau 2^-15: rounding <= 1e-5 m at tau = 0.6 m).
+constexpr int kCntShift = 40;
+constexpr long long kMaxPackedRays = (1ll << 24) - 1;
+constexpr long long kLaunchRays = (1ll << 22) - 1;   // rays per walk launch (pipelining granularity)
 inline int packed_q(double tau) {
-  int q = (int)std::floor(std::log2(524288.0 / tau));
+  int q = (int)std::floor(std::log2(32768.0 / tau));
   return q < 0 ? 0 : (q > 30 ? 30 : q);
 }
 

@@ -22,6 +22,7 @@
 //                        fusion is order-independent and deterministic (R6).
 //   reset kernels   zero the used blocks, counters and AABB.
 #include <algorithm>
+#include <vector>
 #include <cmath>
 #include <cstdio>
 #include <type_traits>
@@ -352,8 +353,11 @@ __global__ void __launch_bounds__(256) block_walk_kernel(const __grid_constant__
 // E_ij > 0  <=>  H_ij = F_ij - floor(-C_ij / 2^16) > 0; H_ij moves by a_j / -a_i per step like E_ij by
 // 2^16 a_j / -2^16 a_i, and |H_ij| <= 3 max(a) while both axes have crossings left.  Exact whenever
 // every |D_a| < 2^28 (spans < 2^12 voxels), which the launch checks from the sensor's max range.
+#ifndef CVX_V_MINB
+#define CVX_V_MINB 8
+#endif
 template <bool kAggregate, bool kConstW, bool k32, bool kColor = false>
-__global__ void __launch_bounds__(128, 8) walk_kernel(const __grid_constant__ WalkParams p) {
+__global__ void __launch_bounds__(128, CVX_V_MINB) walk_kernel(const __grid_constant__ WalkParams p) {
   using DT = typename std::conditional<k32, unsigned, unsigned long long>::type;
   using ST = typename std::conditional<k32, int, long long>::type;
   const int n_rays = p.lcnt[0];
@@ -400,7 +404,9 @@ __global__ void __launch_bounds__(128, 8) walk_kernel(const __grid_constant__ Wa
       D01 = (DT)C01; D02 = (DT)C02; D12 = (DT)C12;
       I0 = (DT)(AD[0] << 16); I1 = (DT)(AD[1] << 16); I2 = (DT)(AD[2] << 16);
     }
-    S = r.S0; U0 = r.U[0]; U1 = r.U[1]; U2 = r.U[2];
+    // S carries the rounding half and the clamp offset tq: dq + tq = clamp(S >> kSdfF, 0, 2 tq)
+    S = r.S0 + (1ll << (kSdfF - 1)) + ((long long)p.tq << kSdfF);
+    U0 = r.U[0]; U1 = r.U[1]; U2 = r.U[2];
     w = r.w;
     w_fx = __double2ll_rn((double)w * kFxScale);
     n = r.n_vox;
@@ -415,32 +421,35 @@ __global__ void __launch_bounds__(128, 8) walk_kernel(const __grid_constant__ Wa
     if (list && nblk > 1) nslot = __ldg(list + 1);
   }
   const int tq = p.tq;
+  const long long s_off = (1ll << (kSdfF - 1)) + ((long long)tq << kSdfF);
+  const long long band_lo = s_off - p.band, band_hi = s_off + p.band;   // |sdf| < tau (colour, R13)
   unsigned long long* const sums = reinterpret_cast<unsigned long long*>(p.pool.sums);
   unsigned long long* const acc = p.pool.acc;
   for (int it = 0; it < maxn; ++it) {
     const bool upd = it < n && slot >= 0;
     // O5 + Q4: clamped projective sdf, quantised to 2^-q m: dq = clamp(round(sdf 2^q), -tq, tq)
-    const int sq = (int)((S + (1ll << (kSdfF - 1))) >> kSdfF);
-    const int dq = min(max(sq, -tq), tq);
+    const int dpi = min(max((int)(S >> kSdfF), 0), 2 * tq);   // round(sdf 2^q) + tq, clamped
+    const int dq = dpi - tq;
     const unsigned addr = (unsigned)slot * 512u + (unsigned)((v0 & 7) | ((v1 & 7) << 3) | ((v2 & 7) << 6));
     if (kAggregate && kConstW) {
       // constant weights: one packed 64-bit reduction per run of consecutive lanes with the same
-      // (voxel, contribution) into the per-launch accumulator acc = count << 42 | sum(d'), d' = dq + tq
+      // (voxel, contribution) into the per-launch accumulator acc = count << 40 | sum(d'), d' = dq + tq
       // in [0, 2 tq] (fold_kernel moves it into the exact sums).  Lanes of a run add the same d', so
-      // the run total is len * (1 << 42 | d').  Lanes hold spatially adjacent rays in a serpentine
+      // the run total is len * (1 << 40 | d').  Lanes hold spatially adjacent rays in a serpentine
       // order, so runs capture the rays that share a voxel; no match.any (its cost grows with the
       // number of distinct keys) and no shuffle tree.
-      const unsigned dp = (unsigned)(dq + tq);
+      const unsigned dp = (unsigned)dpi;
       const unsigned long long key = ((unsigned long long)addr << 32) | dp;
       const unsigned long long prev = __shfl_up_sync(0xffffffffu, key, 1);
       const unsigned act = __ballot_sync(0xffffffffu, upd);
-      const bool head = upd && (lane == 0 || prev != key || !((act >> (lane - 1)) & 1u));
+      // branch-free: lane 0 has no predecessor ((act << 1) >> 0 has bit 0 clear)
+      const bool head = upd & (!(((act << 1) >> lane) & 1u) | (prev != key));
       const unsigned stops = __ballot_sync(0xffffffffu, head) | ~act;
-      if (head) {
-        const unsigned above = stops & (0xfffffffeu << lane);
-        const unsigned len = (above ? (unsigned)(__ffs(above) - 1) : 32u) - (unsigned)lane;
-        atomicAdd(acc + addr, (unsigned long long)len * ((1ull << 42) | (unsigned long long)dp));
-      }
+      const unsigned above = stops & (0xfffffffeu << lane);
+      const unsigned len = (unsigned)__clz(__brev(above)) - (unsigned)lane;
+      const unsigned long long val = (unsigned long long)len * ((1ull << kCntShift) | (unsigned long long)dp);
+      asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.relaxed.gpu.global.add.u64 [%0], %1;\n\t}"
+                   :: "l"(acc + addr), "l"(val), "r"((unsigned)head) : "memory");
     } else {
       long long a = __float2ll_rn(w * (float)dq * __int_as_float((127 + 30 - p.q) << 23));  // w d 2^30
       if (kAggregate) {
@@ -458,12 +467,12 @@ __global__ void __launch_bounds__(128, 8) walk_kernel(const __grid_constant__ Wa
         atomicAdd(sums + 2ull * addr + 1, (unsigned long long)w_fx);
       }
     }
-    if (kColor && upd && S > -p.band && S < p.band) {
+    if (kColor && upd && S > band_lo && S < band_hi) {
       // TSDF + Color (R13): band updates also fuse w (r, g, b); no run merging (neighbouring rays
       // differ in colour near the surface)
       const unsigned long long cr = rgb & 0xffu, cg = (rgb >> 8) & 0xffu, cb = (rgb >> 16) & 0xffu;
       if (kConstW) {
-        atomicAdd(p.pool.cacc + 2ull * addr, (1ull << 42) | cr);
+        atomicAdd(p.pool.cacc + 2ull * addr, (1ull << kCntShift) | cr);
         atomicAdd(p.pool.cacc + 2ull * addr + 1, (cg << 32) | cb);
       } else {
         unsigned long long* cs = reinterpret_cast<unsigned long long*>(p.pool.csum) + 4ull * addr;
@@ -496,13 +505,128 @@ __global__ void __launch_bounds__(128, 8) walk_kernel(const __grid_constant__ Wa
   }
 }
 
+// Constant-weight walk with the voxel address carried incrementally (same decisions as walk_kernel
+// <true, true, k32, kColor>; see there for O4/O5).  Per step only the stepped axis' crossing count,
+// DDA differences, sdf and address move; the voxel coordinates are implied by the remaining crossing
+// counts (v = v_B - s k) and rebuilt only on block entry (one step in 8 or fewer per axis).  Block
+// entry: the stepped axis' local field of the address reached its entry value.  Only clamped
+// free-space updates (d' = 2 tq) are run-merged: in-band sdfs differ between rays at the 2^-q quantum,
+// so merging them buys nothing; they go out as single-lane reductions.
+template <bool k32, bool kColor>
+__global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_constant__ WalkParams p) {
+  using DT = typename std::conditional<k32, unsigned, unsigned long long>::type;
+  using ST = typename std::conditional<k32, int, long long>::type;
+  const int n_rays = p.lcnt[0];
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  if ((idx & ~31) >= n_rays) return;
+  const bool have = idx < n_rays;
+  int vb0 = 0, vb1 = 0, vb2 = 0, s0 = 1, s1 = 1, s2 = 1, k0 = 0, k1 = 0, k2 = 0;
+  DT D01 = 0, D02 = 0, D12 = 0, I0 = 0, I1 = 0, I2 = 0;
+  long long S = 0, U0 = 0, U1 = 0, U2 = 0;
+  int n = 0, nblk = 0, off = -1;
+  unsigned rgb = 0, cexp = 0, addr = 0;
+  int v0 = 0, v1 = 0, v2 = 0;
+  if (have) {
+    const RayRec r = p.rays[idx];
+    long long R[3], AD[3];
+    int va[3], vb[3], st[3], kk[3];
+    nblk = 1;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      va[a] = (int)(r.A[a] >> 16);
+      vb[a] = (int)(r.B[a] >> 16);
+      const long long D = r.B[a] - r.A[a];
+      kk[a] = vb[a] > va[a] ? vb[a] - va[a] : va[a] - vb[a];
+      if (D > 0) { st[a] = 1; R[a] = (((long long)va[a] + 1) << 16) - r.A[a]; }
+      else { st[a] = -1; R[a] = r.A[a] - ((long long)va[a] << 16); }
+      AD[a] = D < 0 ? -D : D;
+      const long long db = (r.B[a] >> 19) - (r.A[a] >> 19);
+      nblk += (int)(db < 0 ? -db : db);
+    }
+    v0 = va[0]; v1 = va[1]; v2 = va[2];
+    vb0 = vb[0]; vb1 = vb[1]; vb2 = vb[2];
+    s0 = st[0]; s1 = st[1]; s2 = st[2]; k0 = kk[0]; k1 = kk[1]; k2 = kk[2];
+    cexp = (s0 > 0 ? 0u : 7u) | ((s1 > 0 ? 0u : 7u) << 3) | ((s2 > 0 ? 0u : 7u) << 6);
+    const long long C01 = R[0] * AD[1] - R[1] * AD[0];
+    const long long C02 = R[0] * AD[2] - R[2] * AD[0];
+    const long long C12 = R[1] * AD[2] - R[2] * AD[1];
+    if (k32) {
+      D01 = (DT)(-((-C01) >> 16)); D02 = (DT)(-((-C02) >> 16)); D12 = (DT)(-((-C12) >> 16));
+      I0 = (DT)AD[0]; I1 = (DT)AD[1]; I2 = (DT)AD[2];
+    } else {
+      D01 = (DT)C01; D02 = (DT)C02; D12 = (DT)C12;
+      I0 = (DT)(AD[0] << 16); I1 = (DT)(AD[1] << 16); I2 = (DT)(AD[2] << 16);
+    }
+    S = r.S0 + (1ll << (kSdfF - 1)) + ((long long)p.tq << kSdfF);
+    U0 = r.U[0]; U1 = r.U[1]; U2 = r.U[2];
+    n = r.n_vox;
+    off = r.list_off;
+    rgb = r.rgb;
+  }
+  const int maxn = (int)__reduce_max_sync(0xffffffffu, (unsigned)n);
+  const int* list = off >= 0 ? p.slots + off : nullptr;
+  int slot = kFailed, nslot = kFailed, j = 0;
+  if (have) {
+    slot = list ? __ldg(list) : hash_find(p.hash, pack_key(v0 >> 3, v1 >> 3, v2 >> 3));
+    if (list && nblk > 1) nslot = __ldg(list + 1);
+    addr = (unsigned)slot * 512u + (unsigned)((v0 & 7) | ((v1 & 7) << 3) | ((v2 & 7) << 6));
+  }
+  const int da0 = s0, da1 = 8 * s1, da2 = 64 * s2;
+  const int tq2 = 2 * p.tq;
+  const long long s_off = (1ll << (kSdfF - 1)) + ((long long)p.tq << kSdfF);
+  const long long band_lo = s_off - p.band, band_hi = s_off + p.band;
+  unsigned long long* const acc = p.pool.acc;
+  for (int it = 0; it < maxn; ++it) {
+    const bool upd = it < n && slot >= 0;
+    const int dpi = min(max((int)(S >> kSdfF), 0), tq2);   // round(sdf 2^q) + tq, clamped (O5, Q4)
+    {
+      // key 0xffffffff (never an address: < 2^23 slots): no merging (in-band or idle lane)
+      const unsigned key = (upd & (dpi == tq2)) ? addr : 0xffffffffu;
+      const unsigned prev = __shfl_up_sync(0xffffffffu, key, 1);
+      const bool head = upd & ((lane == 0) | (prev != key) | (key == 0xffffffffu));
+      const unsigned stops = __ballot_sync(0xffffffffu, head | !upd);
+      const unsigned above = stops & (0xfffffffeu << lane);
+      const unsigned len = (unsigned)__clz(__brev(above)) - (unsigned)lane;
+      const unsigned long long val = (unsigned long long)len * ((1ull << kCntShift) | (unsigned long long)dpi);
+      asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.relaxed.gpu.global.add.u64 [%0], %1;\n\t}"
+                   :: "l"(acc + addr), "l"(val), "r"((unsigned)head) : "memory");
+    }
+    if (kColor && upd && S > band_lo && S < band_hi) {
+      const unsigned long long cr = rgb & 0xffu, cg = (rgb >> 8) & 0xffu, cb = (rgb >> 16) & 0xffu;
+      atomicAdd(p.pool.cacc + 2ull * addr, (1ull << kCntShift) | cr);
+      atomicAdd(p.pool.cacc + 2ull * addr + 1, (cg << 32) | cb);
+    }
+    const bool stp = it + 1 < n;
+    const bool g0 = k0 > 0, g1 = k1 > 0, g2 = k2 > 0;
+    const bool yf = g1 & (!g0 | ((ST)D01 > 0));
+    const bool zf = g2 & (yf ? ((ST)D12 > 0) : (!g0 | ((ST)D02 > 0)));
+    const bool bz = stp & zf, by = stp & yf & !zf, bx = stp & !yf & !zf;
+    if (bx) { addr += da0; --k0; D01 += I1; D02 += I2; S -= U0; }
+    if (by) { addr += da1; --k1; D01 -= I0; D12 += I2; S -= U1; }
+    if (bz) { addr += da2; --k2; D02 -= I0; D12 -= I1; S -= U2; }
+    const unsigned m = zf ? 0x1c0u : (yf ? 0x38u : 7u);
+    if (stp & (((addr ^ cexp) & m) == 0u)) {      // entered the next block of the ray
+      ++j;
+      if (list) {
+        slot = nslot;
+        if (j + 1 < nblk) nslot = __ldg(list + j + 1);
+      } else {
+        slot = hash_find(p.hash, pack_key((vb0 - s0 * k0) >> 3, (vb1 - s1 * k1) >> 3, (vb2 - s2 * k2) >> 3));
+      }
+      const int da = zf ? da2 : (yf ? da1 : da0);
+      addr = (unsigned)slot * 512u + ((((addr - (unsigned)da) & 511u) & ~m) | (cexp & m));
+    }
+  }
+}
+
 // Block-count submap trigger: after the ALLOCATE phase of frame k, fire once the
 // submap holds >= threshold blocks; frame k is the last one it takes.
 __global__ void trigger_check_kernel(const Counters* ctr, int* trig, int frame) {
   if (!trig[1] && ctr->n_blocks >= trig[0]) { trig[1] = 1; trig[2] = frame + 1; }
 }
 
-// TSDF + Color (R13): fold the packed colour accumulators {n << 42 | sum r, sum g << 32 | sum b} (w = 1)
+// TSDF + Color (R13): fold the packed colour accumulators {n << 40 | sum r, sum g << 32 | sum b} (w = 1)
 // into the exact colour sums {sum w, sum w r, sum w g, sum w b} at 2^-30.
 __global__ void fold_color_kernel(const Counters* ctr, unsigned long long* cacc, long long* csum, int max_blocks) {
   const int nb = min(ctr->n_blocks, max_blocks);
@@ -512,8 +636,8 @@ __global__ void fold_color_kernel(const Counters* ctr, unsigned long long* cacc,
     if ((v.x | v.y) == 0ull) continue;
     longlong2* cs = reinterpret_cast<longlong2*>(csum) + 2 * i;
     longlong2 a = cs[0], b = cs[1];
-    a.x += (long long)(v.x >> 42) << 30;                  // sum w (w = 1 -> 2^30)
-    a.y += (long long)(v.x & ((1ull << 42) - 1)) << 30;   // sum w r
+    a.x += (long long)(v.x >> kCntShift) << 30;                  // sum w (w = 1 -> 2^30)
+    a.y += (long long)(v.x & ((1ull << kCntShift) - 1)) << 30;   // sum w r
     b.x += (long long)(v.y >> 32) << 30;                  // sum w g
     b.y += (long long)(v.y & 0xffffffffull) << 30;        // sum w b
     cs[0] = a; cs[1] = b;
@@ -532,19 +656,15 @@ __global__ void fold_kernel(const Counters* ctr, unsigned long long* acc, long l
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nv2; i += (long long)gridDim.x * blockDim.x) {
     const ulonglong2 v = a2[i];
     if ((v.x | v.y) == 0ull) continue;
-    if (v.x) {
-      const long long n = (long long)(v.x >> 42), sd = (long long)(v.x & ((1ull << 42) - 1));
-      longlong2 t = s2[2 * i];
-      t.x += (sd - n * tq) << shift;
-      t.y += n << 30;
-      s2[2 * i] = t;
-    }
-    if (v.y) {
-      const long long n = (long long)(v.y >> 42), sd = (long long)(v.y & ((1ull << 42) - 1));
-      longlong2 t = s2[2 * i + 1];
-      t.x += (sd - n * tq) << shift;
-      t.y += n << 30;
-      s2[2 * i + 1] = t;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const unsigned long long a = h ? v.y : v.x;
+      if (!a) continue;
+      const long long n = (long long)(a >> kCntShift), sd = (long long)(a & ((1ull << kCntShift) - 1));
+      longlong2 x = s2[2 * i + h];
+      x.x += (sd - n * tq) << shift;
+      x.y += n << 30;
+      s2[2 * i + h] = x;
     }
     a2[i] = make_ulonglong2(0ull, 0ull);
   }
@@ -611,13 +731,19 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
                              bool host_data, int* trig, const unsigned char* rgb) {
   if (n_per_frame <= 0 || n_frames <= 0) return cudaSuccess;
   const long long elems_per_frame = n_per_frame * (sensor.kind == 1 ? 1 : 3);
-  // launches of equal size; at most kMaxBatch frames, and (constant weights) <= kMaxPackedRays rays so
-  // the packed accumulators cannot overflow (R6/R7)
-  const bool cw_ok = sm->aggregate && sm->cfg.weighting == 0 && n_per_frame <= kMaxPackedRays;
-  const long long ray_limit = cw_ok ? kMaxPackedRays : (1ll << 31) - 1;
+  // launches of equal size; at most kMaxBatch frames and kLaunchRays rays (pipelining granularity).
+  // Constant weights: the packed accumulators are folded whenever the next launch would take them past
+  // kMaxPackedRays rays since the last fold, and at the end of the call (R6/R7)
+  const bool cw_ok = sm->aggregate && sm->cfg.weighting == 0 && n_per_frame <= kLaunchRays;
+  const long long ray_limit = cw_ok ? kLaunchRays : (1ll << 31) - 1;
   const int lim = trig ? 1 : (int)std::max<long long>(1, std::min<long long>(kMaxBatch, ray_limit / n_per_frame));
-  const int chunks = (n_frames + lim - 1) / lim;
-  const int per = (n_frames + chunks - 1) / chunks;
+  std::vector<int> plan;                             // equal chunks
+  {
+    const int chunks = (n_frames + lim - 1) / lim;
+    const int eq = (n_frames + chunks - 1) / chunks;
+    for (int left = n_frames; left > 0; left -= eq) plan.push_back(std::min(eq, left));
+  }
+  const int per = *std::max_element(plan.begin(), plan.end());
   const long long cap_rays = (long long)per * n_per_frame;
   for (int b = 0; b < 2; ++b) {
     cudaError_t e = grow(&sm->buf[b].rays, &sm->buf[b].ray_cap, cap_rays, sizeof(RayRec));
@@ -633,10 +759,23 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
   // every ray spans < 2^12 voxels per axis if (max_range + tau) / s + 2 < 4096 (domain check O3 bounds
   // the rest): then the crossing-order differences fit 32 bits (see walk_kernel)
   const bool k32 = ((double)sensor.max_range + sm->cfg.truncation) / sm->cfg.voxel_size + 2.0 < 4096.0;
+  long long pending = 0;                             // rays in the packed accumulators since the last fold
+  auto fold = [&]() {
+    if (pending == 0) return;
+    {
+      ProfScope ps_(sm, "fold", st);
+      fold_kernel<<<148 * 8, 256, 0, st>>>(sm->ctr, sm->pool.acc, sm->pool.sums, sm->pool.max_blocks, tq, 30 - q);
+    }
+    if (rgb) {
+      ProfScope ps_(sm, "fold_color", st);
+      fold_color_kernel<<<148 * 8, 256, 0, st>>>(sm->ctr, sm->pool.cacc, sm->pool.csum, sm->pool.max_blocks);
+    }
+    pending = 0;
+  };
   cudaEventRecord(sm->ev_entry, st);                 // the side stream starts after the caller's prior work
   cudaStreamWaitEvent(sm->side, sm->ev_entry, 0);
-  for (int f0 = 0; f0 < n_frames; f0 += per) {
-    const int nf = std::min(per, n_frames - f0);
+  int f0 = 0;
+  for (const int nf : plan) {
     const long long total = (long long)nf * n_per_frame;
     const int b = sm->next_buf;
     sm->next_buf ^= 1;
@@ -694,12 +833,16 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     if (trig) trigger_check_kernel<<<1, 1, 0, sm->side>>>(sm->ctr, trig, f0);
     cudaEventRecord(sm->ev_prepared[b], sm->side);
     // ---- caller's stream: a4 UPDATE + a5 FOLD of launch k
+    const bool cw = cw_ok && total <= kLaunchRays;
+    if (cw && pending + total > kMaxPackedRays) fold();
     cudaStreamWaitEvent(st, sm->ev_prepared[b], 0);
-    const bool cw = cw_ok && total <= kMaxPackedRays;
     {
       ProfScope ps_(sm, "ray_walk_update", st);
       const unsigned wblocks = (unsigned)((total + 127) / 128);   // 128-thread CTAs (measured best)
-      if (rgb) {
+      if (cw && sm->aggregate && sm->walk_cw) {
+        if (rgb) { if (k32) walk_cw_kernel<true, true><<<wblocks, 128, 0, st>>>(wp); else walk_cw_kernel<false, true><<<wblocks, 128, 0, st>>>(wp); }
+        else { if (k32) walk_cw_kernel<true, false><<<wblocks, 128, 0, st>>>(wp); else walk_cw_kernel<false, false><<<wblocks, 128, 0, st>>>(wp); }
+      } else if (rgb) {
         if (cw) { if (k32) walk_kernel<true, true, true, true><<<wblocks, 128, 0, st>>>(wp); else walk_kernel<true, true, false, true><<<wblocks, 128, 0, st>>>(wp); }
         else { if (k32) walk_kernel<true, false, true, true><<<wblocks, 128, 0, st>>>(wp); else walk_kernel<true, false, false, true><<<wblocks, 128, 0, st>>>(wp); }
       } else if (sm->aggregate) {
@@ -709,16 +852,11 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
         walk_kernel<false, false, false><<<wblocks, 128, 0, st>>>(wp);
       }
     }
-    if (cw) {
-      ProfScope ps_(sm, "fold", st);
-      fold_kernel<<<148 * 8, 256, 0, st>>>(sm->ctr, sm->pool.acc, sm->pool.sums, sm->pool.max_blocks, tq, 30 - q);
-    }
-    if (cw && rgb) {
-      ProfScope ps_(sm, "fold_color", st);
-      fold_color_kernel<<<148 * 8, 256, 0, st>>>(sm->ctr, sm->pool.cacc, sm->pool.csum, sm->pool.max_blocks);
-    }
+    if (cw) pending += total;
     cudaEventRecord(sm->ev_free[b], st);
+    f0 += nf;
   }
+  fold();
   return cudaGetLastError();
 }
 
