@@ -170,6 +170,7 @@ cvx_status cvx_create_submap(const cvx_grid_config* cfg, const double* T_world_s
   // CVX_SERIAL=1 (diagnostics): the pipeline's side stream is the legacy default stream, so with a caller
   // on the default stream every kernel runs alone and per-kernel event times are solo times
   const bool serial = std::getenv("CVX_SERIAL") && std::getenv("CVX_SERIAL")[0] == '1';
+  if (const char* b2 = std::getenv("CVX_BW2")) sm->bw2 = b2[0] != '0';              // tuning knob
   if (const char* wc = std::getenv("CVX_WALK_CW")) sm->walk_cw = wc[0] != '0';     // tuning knob
   sm->cfg = *cfg;
   std::memcpy(sm->T_ws, T_world_submap, sizeof(sm->T_ws));

@@ -348,6 +348,92 @@ __global__ void __launch_bounds__(256) block_walk_kernel(const __grid_constant__
   }
 }
 
+// Software-pipelined ALLOCATE: the hash entry of step j+1 is loaded (by the run heads of step j+1)
+// before step j's probe is consumed, so the L2 latency of one probe overlaps the DDA and list write of
+// the previous one.  Same decisions and results as block_walk_kernel.
+__device__ __forceinline__ int key_field(unsigned long long key, int sh) {
+  return ((int)((key >> sh) & 0x1fffffu) << 11) >> 11;          // 21-bit two's complement (pack_key)
+}
+
+template <bool k32>
+__global__ void __launch_bounds__(256) block_walk2_kernel(const __grid_constant__ WalkParams p) {
+  using DT = typename std::conditional<k32, unsigned, unsigned long long>::type;
+  using ST = typename std::conditional<k32, int, long long>::type;
+  const int n_rays = p.lcnt[0];
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  if ((idx & ~31) >= n_rays) return;
+  const bool have = idx < n_rays;
+  int b0 = 0, b1 = 0, b2 = 0, s0 = 1, s1 = 1, s2 = 1, k0 = 0, k1 = 0, k2 = 0, nb = 0;
+  DT D01 = 0, D02 = 0, D12 = 0, I0 = 0, I1 = 0, I2 = 0;
+  int* list = nullptr;
+  if (have) {
+    const RayRec r = p.rays[idx];
+    long long R[3], AD[3];
+    int bb[3], st[3], kk[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      bb[a] = (int)(r.A[a] >> 19);
+      const int be = (int)(r.B[a] >> 19);
+      const long long D = r.B[a] - r.A[a];
+      kk[a] = be > bb[a] ? be - bb[a] : bb[a] - be;
+      if (D > 0) { st[a] = 1; R[a] = (((long long)bb[a] + 1) << 19) - r.A[a]; }
+      else { st[a] = -1; R[a] = r.A[a] - ((long long)bb[a] << 19); }
+      AD[a] = D < 0 ? -D : D;
+    }
+    b0 = bb[0]; b1 = bb[1]; b2 = bb[2]; s0 = st[0]; s1 = st[1]; s2 = st[2]; k0 = kk[0]; k1 = kk[1]; k2 = kk[2];
+    nb = 1 + k0 + k1 + k2;
+    const long long C01 = R[0] * AD[1] - R[1] * AD[0];
+    const long long C02 = R[0] * AD[2] - R[2] * AD[0];
+    const long long C12 = R[1] * AD[2] - R[2] * AD[1];
+    if (k32) {
+      D01 = (DT)(-((-C01) >> 19)); D02 = (DT)(-((-C02) >> 19)); D12 = (DT)(-((-C12) >> 19));
+      I0 = (DT)AD[0]; I1 = (DT)AD[1]; I2 = (DT)AD[2];
+    } else {
+      D01 = (DT)C01; D02 = (DT)C02; D12 = (DT)C12;
+      I0 = (DT)(AD[0] << 19); I1 = (DT)(AD[1] << 19); I2 = (DT)(AD[2] << 19);
+    }
+    list = r.list_off >= 0 ? p.slots + r.list_off : nullptr;
+  }
+  const int maxnb = (int)__reduce_max_sync(0xffffffffu, (unsigned)nb);
+  // run heads of step j: first lane of every run of equal keys among adjacent active lanes
+  auto heads_of = [&](bool act, unsigned long long key) -> unsigned {
+    const unsigned long long prev = __shfl_up_sync(0xffffffffu, key, 1);
+    const unsigned actm = __ballot_sync(0xffffffffu, act);
+    const unsigned same = __ballot_sync(0xffffffffu, act && prev == key) & (actm << 1);
+    return actm & ~same;
+  };
+  bool act = 0 < nb;
+  unsigned long long key = act ? pack_key(b0, b1, b2) : ((1ull << 63) | (unsigned)lane);
+  unsigned heads = heads_of(act, key);
+  longlong2 ent = make_longlong2(0, 0);
+  if ((heads >> lane) & 1u) ent = ld_entry(p.hash.e + hash_slot(key, p.hash));
+  for (int j = 0; j < maxnb; ++j) {
+    // advance the DDA to step j+1 (independent of the probe of step j)
+    const bool stp = j + 1 < nb;
+    const bool g0 = k0 > 0, g1 = k1 > 0, g2 = k2 > 0;
+    const bool yf = g1 & (!g0 | ((ST)D01 > 0));
+    const bool zf = g2 & (yf ? ((ST)D12 > 0) : (!g0 | ((ST)D02 > 0)));
+    const bool bz = stp & zf, by = stp & yf & !zf, bx = stp & !yf & !zf;
+    if (bx) { b0 += s0; --k0; D01 += I1; D02 += I2; }
+    if (by) { b1 += s1; --k1; D01 -= I0; D12 += I2; }
+    if (bz) { b2 += s2; --k2; D02 -= I0; D12 -= I1; }
+    const bool actn = stp;
+    const unsigned long long keyn = actn ? pack_key(b0, b1, b2) : ((1ull << 63) | (unsigned)lane);
+    const unsigned headsn = (j + 1 < maxnb) ? heads_of(actn, keyn) : 0u;
+    longlong2 entn = make_longlong2(0, 0);
+    if ((headsn >> lane) & 1u) entn = ld_entry(p.hash.e + hash_slot(keyn, p.hash));   // prefetch j+1
+    // consume step j
+    int slot = kFailed;
+    if ((heads >> lane) & 1u)
+      slot = hash_activate_pf(p.hash, p.pool, p.ctr, key, key_field(key, 42), key_field(key, 21), key_field(key, 0), ent);
+    const unsigned hb = heads & (0xffffffffu >> (31 - lane));
+    slot = __shfl_sync(0xffffffffu, slot, hb ? 31 - __clz(hb) : lane);
+    if (act && list) list[j] = slot;
+    act = actn; key = keyn; heads = headsn; ent = entn;
+  }
+}
+
 // k32: the crossing-order differences fit 32 bits.  With r_i = rho_i + m_i 2^16 (m_i crossings done),
 // E_ij = X_ij - X_ji = C_ij + 2^16 F_ij with C_ij = rho_i a_j - rho_j a_i and F_ij = m_i a_j - m_j a_i, so
 // E_ij > 0  <=>  H_ij = F_ij - floor(-C_ij / 2^16) > 0; H_ij moves by a_j / -a_i per step like E_ij by
@@ -577,12 +663,27 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
   const long long s_off = (1ll << (kSdfF - 1)) + ((long long)p.tq << kSdfF);
   const long long band_lo = s_off - p.band, band_hi = s_off + p.band;
   unsigned long long* const acc = p.pool.acc;
-  for (int it = 0; it < maxn; ++it) {
-    const bool upd = it < n && slot >= 0;
-    const int dpi = min(max((int)(S >> kSdfF), 0), tq2);   // round(sdf 2^q) + tq, clamped (O5, Q4)
+  // Two phases.  While every lane of the warp is surely in clamped free space (S >= 2 tq 2^kSdfF, so
+  // d' = 2 tq), the sdf is not tracked: S_i >= S_0 - i max_a U_a bounds it from the voxel index alone,
+  // which gives each ray a free prefix of m voxels (< n).  After the prefix S is rebuilt exactly from
+  // the steps taken per axis (S_0 - sum_a U_a (K_a - k_a)) and the full update continues.
+  int mfree = 0x7fffffff;
+  const int K0 = k0, K1 = k1, K2 = k2;
+  if (have) {
+    long long thr = (long long)tq2 << kSdfF;
+    if (kColor) thr = max(thr, band_hi);
+    const long long umax = max(U0, max(U1, U2));
+    mfree = 0;
+    if (S > thr && umax > 0) mfree = (int)min((double)(n - 1), floor((double)(S - thr) / (double)umax));
+  }
+  const int mw = (int)__reduce_min_sync(0xffffffffu, (unsigned)mfree);
+  auto body = [&](const int it, auto free_tag) {
+    constexpr bool kFree = decltype(free_tag)::value;
+    const bool upd = kFree ? slot >= 0 : (it < n && slot >= 0);
+    const int dpi = kFree ? tq2 : min(max((int)(S >> kSdfF), 0), tq2);   // round(sdf 2^q) + tq, clamped (O5, Q4)
     {
       // key 0xffffffff (never an address: < 2^23 slots): no merging (in-band or idle lane)
-      const unsigned key = (upd & (dpi == tq2)) ? addr : 0xffffffffu;
+      const unsigned key = (kFree ? upd : (upd & (dpi == tq2))) ? addr : 0xffffffffu;
       const unsigned prev = __shfl_up_sync(0xffffffffu, key, 1);
       const bool head = upd & ((lane == 0) | (prev != key) | (key == 0xffffffffu));
       const unsigned stops = __ballot_sync(0xffffffffu, head | !upd);
@@ -592,7 +693,7 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
       asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.relaxed.gpu.global.add.u64 [%0], %1;\n\t}"
                    :: "l"(acc + addr), "l"(val), "r"((unsigned)head) : "memory");
     }
-    if (kColor && upd && S > band_lo && S < band_hi) {
+    if (!kFree && kColor && upd && S > band_lo && S < band_hi) {
       const unsigned long long cr = rgb & 0xffu, cg = (rgb >> 8) & 0xffu, cb = (rgb >> 16) & 0xffu;
       atomicAdd(p.pool.cacc + 2ull * addr, (1ull << kCntShift) | cr);
       atomicAdd(p.pool.cacc + 2ull * addr + 1, (cg << 32) | cb);
@@ -602,22 +703,26 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
     const bool yf = g1 & (!g0 | ((ST)D01 > 0));
     const bool zf = g2 & (yf ? ((ST)D12 > 0) : (!g0 | ((ST)D02 > 0)));
     const bool bz = stp & zf, by = stp & yf & !zf, bx = stp & !yf & !zf;
-    if (bx) { addr += da0; --k0; D01 += I1; D02 += I2; S -= U0; }
-    if (by) { addr += da1; --k1; D01 -= I0; D12 += I2; S -= U1; }
-    if (bz) { addr += da2; --k2; D02 -= I0; D12 -= I1; S -= U2; }
+    if (bx) { addr += da0; --k0; D01 += I1; D02 += I2; if (!kFree) S -= U0; }
+    if (by) { addr += da1; --k1; D01 -= I0; D12 += I2; if (!kFree) S -= U1; }
+    if (bz) { addr += da2; --k2; D02 -= I0; D12 -= I1; if (!kFree) S -= U2; }
     const unsigned m = zf ? 0x1c0u : (yf ? 0x38u : 7u);
     if (stp & (((addr ^ cexp) & m) == 0u)) {      // entered the next block of the ray
       ++j;
       if (list) {
         slot = nslot;
-        if (j + 1 < nblk) nslot = __ldg(list + j + 1);
+        if (j + 1 < nblk) nslot = __ldg(list + j + 1);   // prefetch one block ahead
       } else {
         slot = hash_find(p.hash, pack_key((vb0 - s0 * k0) >> 3, (vb1 - s1 * k1) >> 3, (vb2 - s2 * k2) >> 3));
       }
       const int da = zf ? da2 : (yf ? da1 : da0);
       addr = (unsigned)slot * 512u + ((((addr - (unsigned)da) & 511u) & ~m) | (cexp & m));
     }
-  }
+  };
+  int it = 0;
+  for (; it < mw; ++it) body(it, std::true_type{});
+  S -= U0 * (K0 - k0) + U1 * (K1 - k1) + U2 * (K2 - k2);
+  for (; it < maxn; ++it) body(it, std::false_type{});
 }
 
 // Block-count submap trigger: after the ALLOCATE phase of frame k, fire once the
@@ -827,8 +932,13 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     wp.band = std::llround(std::ldexp(sm->cfg.truncation, q + kSdfF));
     {
       ProfScope ps_(sm, "block_walk_allocate", sm->side);
-      if (k32) block_walk_kernel<true><<<blocks, 256, 0, sm->side>>>(wp);
-      else block_walk_kernel<false><<<blocks, 256, 0, sm->side>>>(wp);
+      if (sm->bw2) {
+        if (k32) block_walk2_kernel<true><<<blocks, 256, 0, sm->side>>>(wp);
+        else block_walk2_kernel<false><<<blocks, 256, 0, sm->side>>>(wp);
+      } else {
+        if (k32) block_walk_kernel<true><<<blocks, 256, 0, sm->side>>>(wp);
+        else block_walk_kernel<false><<<blocks, 256, 0, sm->side>>>(wp);
+      }
     }
     if (trig) trigger_check_kernel<<<1, 1, 0, sm->side>>>(sm->ctr, trig, f0);
     cudaEventRecord(sm->ev_prepared[b], sm->side);

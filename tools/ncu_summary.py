@@ -34,6 +34,16 @@ if raw:
         for i, c in enumerate(rh):
             if c == key:
                 print(f"{key:<55} {units[i]:<10} {vals[i]}")
+    import re
+    for i, c in enumerate(rh):   # pipe utilisation and reduction traffic
+        if re.search(r"pipe_[a-z_]+(_cycles_active|inst_executed).*pct_of_peak_sustained_active$", c) or \
+                re.search(r"^sm__inst_executed_pipe_[a-z_]+\.avg\.pct_of_peak_sustained_active$", c) or \
+                re.search(r"op_red", c):
+            try:
+                if float(vals[i].replace(",", "")) > 1.0:
+                    print(f"{c:<55} {units[i]:<10} {vals[i]}")
+            except ValueError:
+                pass
 src = list(csv.reader(io.StringIO(run(["--page", "source", "--csv", "--print-source", "sass"]))))
 if len(src) > 2:
     sh = src[1]
