@@ -153,7 +153,7 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline_sample(cfg, data, poses, n=12):
+def cpu_baseline_sample(cfg, data, poses, n=20):
     """The oracle as it stands, single-threaded, on the first n scans of the same workload."""
     import oracle
     g = cfg["grid"]
@@ -597,6 +597,21 @@ def main():
                "h2d_bytes_per_step": int(data.numel() * 4 + queries.numel() * 4),
                "d2h_bytes_per_step": int(args.queries * 5), "ms_per_step": ems / args.steps}
 
+    # ---------------------------------------------------------------- serialised pass (solo kernel times)
+    # the pipelined timed region overlaps a1-a3 of launch k+1 with the walk of launch k, so side-stream
+    # event times include waiting; two more steps with the side work on the caller's stream give every
+    # kernel's solo time (untimed for `value`; used for the kernel shares and per-stage throughputs)
+    sm.profile(True, serialize=True)
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record(stream)
+    for _ in range(2):
+        step()
+    s1.record(stream)
+    torch.cuda.synchronize()
+    serial_ms = s0.elapsed_time(s1) / 2
+    per_step_serial = {k: v["ms"] / 2 for k, v in sm.profile_report().items()}
+    sm.profile(False)
+
     # ---------------------------------------------------------------- roofline of the dominant kernel
     hbm, hbm_src, mp = peaks()
     K = args.steps
@@ -613,8 +628,9 @@ def main():
     n_rays_launch = st["rays_in"] / max(1, prof.get("ray_prepare", {"n": 1})["n"] / K)
     alg_bytes["ray_prepare"] = int(n_rays_launch * (12 + 96))
     dom = max(per_step, key=per_step.get)
-    esdf_ms = sum(v for k, v in per_step.items() if k.startswith("esdf_"))
-    integ_ms = sum(v for k, v in per_step.items() if k in ("compose_poses", "ray_prepare", "ray_walk_update"))
+    esdf_ms = sum(v for k, v in per_step_serial.items() if k.startswith("esdf_"))
+    integ_ms = sum(v for k, v in per_step_serial.items()
+                   if k in ("compose_poses", "ray_prepare", "block_walk_allocate", "ray_walk_update", "fold"))
     walk = prof.get("ray_walk_update", {"ms": 0.0, "n": 1})
     updates_per_step = st["voxel_updates"]
     roofline = {}
@@ -651,6 +667,7 @@ def main():
         "tsdf_scans_per_s_kernels": N_SCANS / (integ_ms / 1e3) if integ_ms else None,
         "voxel_updates_per_step": updates_per_step, "blocks": nb, "aabb_voxels": dims.tolist(),
         "kernel_ms_per_step": per_step,
+        "kernel_ms_per_step_serial": per_step_serial, "serial_ms_per_step": serial_ms,
         "roofline": roofline,
         "gpu_launches": launches,
         "clocks": clk.summary(),

@@ -236,8 +236,10 @@ cvx_status cvx_pack_esdf(const cvx_submap* submap, void* dst, int64_t dst_bytes,
 cvx_status cvx_packed_size(const cvx_submap* submap, int64_t* bytes);
 
 /* Per-kernel timing of this submap's launches with CUDA events recorded on the launching stream
- * (off by default; enabling synchronises the device and clears earlier records).  Used by bench.py
- * for the roofline of the dominant kernel. */
+ * (off by default; enabling synchronises the device and clears earlier records).  enable: bit 0 =
+ * record, bit 1 = serialise (the integration pipeline's side-stream work runs on the caller's stream,
+ * so every kernel runs alone and its event time is its solo time).  Used by bench.py for the roofline
+ * of the dominant kernel and the per-kernel shares. */
 cvx_status cvx_profile_enable(cvx_submap* submap, int32_t enable);
 
 /* Synchronising: writes a JSON object {"kernel": {"ms": total_ms, "n": launches}, ...} of the records

@@ -167,9 +167,6 @@ cvx_status cvx_create_submap(const cvx_grid_config* cfg, const double* T_world_s
   cvx_submap* sm = new cvx_submap();
   sm->prof = new cvx::Prof();
   if (const char* ag = std::getenv("CVX_AGGREGATE")) sm->aggregate = ag[0] != '0';  // tuning knob
-  // CVX_SERIAL=1 (diagnostics): the pipeline's side stream is the legacy default stream, so with a caller
-  // on the default stream every kernel runs alone and per-kernel event times are solo times
-  const bool serial = std::getenv("CVX_SERIAL") && std::getenv("CVX_SERIAL")[0] == '1';
   if (const char* b2 = std::getenv("CVX_BW2")) sm->bw2 = b2[0] != '0';              // tuning knob
   if (const char* wc = std::getenv("CVX_WALK_CW")) sm->walk_cw = wc[0] != '0';     // tuning knob
   sm->cfg = *cfg;
@@ -192,7 +189,7 @@ cvx_status cvx_create_submap(const cvx_grid_config* cfg, const double* T_world_s
       (e = cudaMalloc(&sm->buf[0].frame_T, sizeof(double) * 16 * cvx::kMaxBatch)) != cudaSuccess ||
       (e = cudaMalloc(&sm->buf[1].frame_T, sizeof(double) * 16 * cvx::kMaxBatch)) != cudaSuccess ||
       (e = cudaMalloc(&sm->buf[0].lcnt, 16)) != cudaSuccess || (e = cudaMalloc(&sm->buf[1].lcnt, 16)) != cudaSuccess ||
-      (!serial && (e = cudaStreamCreateWithFlags(&sm->side, cudaStreamNonBlocking)) != cudaSuccess) ||
+      (e = cudaStreamCreateWithFlags(&sm->side, cudaStreamNonBlocking)) != cudaSuccess ||
       (e = cudaEventCreateWithFlags(&sm->ev_entry, cudaEventDisableTiming)) != cudaSuccess ||
       (e = cudaEventCreateWithFlags(&sm->ev_prepared[0], cudaEventDisableTiming)) != cudaSuccess ||
       (e = cudaEventCreateWithFlags(&sm->ev_prepared[1], cudaEventDisableTiming)) != cudaSuccess ||
@@ -567,7 +564,8 @@ cvx_status cvx_profile_enable(cvx_submap* sm, int32_t enable) {
   DeviceGuard g(sm->device);
   cudaDeviceSynchronize();
   sm->prof->recycle();
-  sm->prof->on = enable != 0;
+  sm->prof->on = (enable & 1) != 0;
+  sm->serialize = (enable & 2) != 0;
   return CVX_OK;
 }
 

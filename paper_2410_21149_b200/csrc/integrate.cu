@@ -835,6 +835,9 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
                              const double* T_world_sensor, const cvx_sensor_model& sensor, cudaStream_t st,
                              bool host_data, int* trig, const unsigned char* rgb) {
   if (n_per_frame <= 0 || n_frames <= 0) return cudaSuccess;
+  // pipeline side stream (a1-a3 of launch k+1 under the walk of launch k); the caller's stream itself
+  // when the submap is in serialised profiling mode
+  const cudaStream_t side = sm->serialize ? st : sm->side;
   const long long elems_per_frame = n_per_frame * (sensor.kind == 1 ? 1 : 3);
   // launches of equal size; at most kMaxBatch frames and kLaunchRays rays (pipelining granularity).
   // Constant weights: the packed accumulators are folded whenever the next launch would take them past
@@ -878,7 +881,7 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     pending = 0;
   };
   cudaEventRecord(sm->ev_entry, st);                 // the side stream starts after the caller's prior work
-  cudaStreamWaitEvent(sm->side, sm->ev_entry, 0);
+  cudaStreamWaitEvent(side, sm->ev_entry, 0);
   int f0 = 0;
   for (const int nf : plan) {
     const long long total = (long long)nf * n_per_frame;
@@ -887,7 +890,7 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     cvx_submap::Buf& B = sm->buf[b];
     const unsigned blocks = (unsigned)((total + 255) / 256);
     // ---- side stream: a1-a3 (compose, prepare/COUNT, ALLOCATE) into buffer b
-    cudaStreamWaitEvent(sm->side, sm->ev_free[b], 0);   // the walk that last read buffer b is done
+    cudaStreamWaitEvent(side, sm->ev_free[b], 0);   // the walk that last read buffer b is done
     ComposeParams cp;
     for (int i = 0; i < 16; ++i) cp.Tws[i] = sm->T_ws[i];
     for (int f = 0; f < nf; ++f)
@@ -895,14 +898,14 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     cp.n = nf;
     cp.s = sm->cfg.voxel_size;
     {
-      ProfScope ps_(sm, "compose_poses", sm->side);
-      compose_kernel<<<1, kMaxBatch, 0, sm->side>>>(cp, B.frame_T);
+      ProfScope ps_(sm, "compose_poses", side);
+      compose_kernel<<<1, kMaxBatch, 0, side>>>(cp, B.frame_T);
     }
-    cudaMemsetAsync(B.lcnt, 0, 4 * sizeof(int), sm->side);
+    cudaMemsetAsync(B.lcnt, 0, 4 * sizeof(int), side);
     const float* chunk = data + (long long)f0 * elems_per_frame;
     if (host_data) {   // host frames: the H2D copy of launch k+1 overlaps the walk of launch k
       cudaMemcpyAsync(B.staging, chunk, sizeof(float) * (size_t)(nf * elems_per_frame), cudaMemcpyHostToDevice,
-                      sm->side);
+                      side);
       chunk = B.staging;
     }
     PrepParams pp;
@@ -920,8 +923,8 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     pp.trig = trig;
     pp.rgb = rgb ? rgb + (long long)f0 * n_per_frame * 3 : nullptr;
     {
-      ProfScope ps_(sm, "ray_prepare", sm->side);
-      prepare_kernel<<<blocks, 256, 0, sm->side>>>(pp);
+      ProfScope ps_(sm, "ray_prepare", side);
+      prepare_kernel<<<blocks, 256, 0, side>>>(pp);
     }
     WalkParams wp;
     wp.rays = (const RayRec*)B.rays; wp.ctr = sm->ctr; wp.hash = sm->hash; wp.pool = sm->pool;
@@ -931,17 +934,17 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     wp.q = q;
     wp.band = std::llround(std::ldexp(sm->cfg.truncation, q + kSdfF));
     {
-      ProfScope ps_(sm, "block_walk_allocate", sm->side);
+      ProfScope ps_(sm, "block_walk_allocate", side);
       if (sm->bw2) {
-        if (k32) block_walk2_kernel<true><<<blocks, 256, 0, sm->side>>>(wp);
-        else block_walk2_kernel<false><<<blocks, 256, 0, sm->side>>>(wp);
+        if (k32) block_walk2_kernel<true><<<blocks, 256, 0, side>>>(wp);
+        else block_walk2_kernel<false><<<blocks, 256, 0, side>>>(wp);
       } else {
-        if (k32) block_walk_kernel<true><<<blocks, 256, 0, sm->side>>>(wp);
-        else block_walk_kernel<false><<<blocks, 256, 0, sm->side>>>(wp);
+        if (k32) block_walk_kernel<true><<<blocks, 256, 0, side>>>(wp);
+        else block_walk_kernel<false><<<blocks, 256, 0, side>>>(wp);
       }
     }
-    if (trig) trigger_check_kernel<<<1, 1, 0, sm->side>>>(sm->ctr, trig, f0);
-    cudaEventRecord(sm->ev_prepared[b], sm->side);
+    if (trig) trigger_check_kernel<<<1, 1, 0, side>>>(sm->ctr, trig, f0);
+    cudaEventRecord(sm->ev_prepared[b], side);
     // ---- caller's stream: a4 UPDATE + a5 FOLD of launch k
     const bool cw = cw_ok && total <= kLaunchRays;
     if (cw && pending + total > kMaxPackedRays) fold();

@@ -63,6 +63,7 @@ struct cvx_submap {
   cudaEvent_t ev_entry = nullptr, ev_prepared[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
   int next_buf = 0;
   bool aggregate = true;      // warp-aggregate equal-voxel updates before the L2 atomics
+  bool serialize = false;     // profiling: run the pipeline's side work on the caller's stream
   bool bw2 = true;            // software-pipelined ALLOCATE (block_walk2_kernel)
   bool walk_cw = true;        // constant weights: incremental-address walk (walk_cw_kernel)
 

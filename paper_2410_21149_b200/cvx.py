@@ -335,8 +335,10 @@ class Submap:
                                             self._dev(D, torch.float32, "D"), self._dev(W, torch.float32, "W"),
                                             n, self._stream()))
 
-    def profile(self, enable: bool = True):
-        _check(lib().cvx_profile_enable(self._h, 1 if enable else 0))
+    def profile(self, enable: bool = True, serialize: bool = False):
+        """Per-kernel CUDA-event timing; serialize=True also runs the pipeline's side work on the caller's
+        stream (solo kernel times)."""
+        _check(lib().cvx_profile_enable(self._h, (1 if enable else 0) | (2 if serialize else 0)))
 
     def profile_report(self) -> dict:
         import json

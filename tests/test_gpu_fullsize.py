@@ -53,6 +53,25 @@ def test_fullsize_count_identity_and_batch_independence(lidar, built):
     assert np.array_equal(D7.view(np.uint32), D.view(np.uint32)) and np.array_equal(W7.view(np.uint32), W.view(np.uint32))
 
 
+def test_fold_inside_one_call_is_exact(lidar):
+    """300 scans in one call pass the packed-accumulator limit (2^24 - 1 rays, R6/R7), so the library folds
+    inside the call; the state must equal two separate calls bit for bit."""
+    cfg, data, poses = lidar
+    d300 = torch.cat([data, data[:100]]).contiguous()
+    p300 = np.concatenate([poses, poses[:100]])
+    from paper_2410_21149_b200 import Submap
+    a = Submap(cfg["grid"], cfg["submaps"][0]["T_world_submap"], 0)
+    a.integrate_batch(d300, p300, cfg["sensor"])
+    b = Submap(cfg["grid"], cfg["submaps"][0]["T_world_submap"], 0)
+    b.integrate_batch(d300[:150].contiguous(), p300[:150], cfg["sensor"])
+    b.integrate_batch(d300[150:].contiguous(), p300[150:], cfg["sensor"])
+    ea, eb = gpu_export_sorted(a), gpu_export_sorted(b)
+    assert np.array_equal(ea[0], eb[0])
+    assert np.array_equal(ea[1].view(np.uint32), eb[1].view(np.uint32))
+    assert np.array_equal(ea[2].view(np.uint32), eb[2].view(np.uint32))
+    assert a.stats()["voxel_updates"] == ea[2].astype(np.float64).sum()
+
+
 def test_fullsize_frames_tsdf_parity(lidar, orc):
     cfg, data, poses = lidar
     frames = [0, 100, 199]

@@ -11,6 +11,8 @@ import sys
 from collections import defaultdict
 
 NAMES = [("prepare_kernel", "ray_prepare"), ("block_walk_kernel", "block_walk_allocate"),
+         ("block_walk2_kernel", "block_walk_allocate"), ("walk_cw_kernel", "ray_walk_update"),
+         ("fold_color_kernel", "fold_color"), ("pass_line_kernelILb0", "esdf_pass_y"), ("pass_line_kernelILb1", "esdf_pass_z"), ("pass_line_kernel<0", "esdf_pass_y"), ("pass_line_kernel<1", "esdf_pass_z"),
          ("walk_kernel", "ray_walk_update"), ("fold_kernel", "fold"), ("zero_blocks", "reset_zero_blocks"),
          ("reset_counters", "reset_counters"), ("compose_kernel", "compose_poses"),
          ("block_grid", "esdf_block_grid"), ("pass_x", "esdf_pass_x"), ("pass_line_kernel<0>", "esdf_pass_y"), ("pass_line_kernel<false>", "esdf_pass_y"),
@@ -39,11 +41,13 @@ for r in rows[1:]:
 T = sum(tot.values())
 bench = None
 if len(sys.argv) > 2:
-    bench = json.loads(open(sys.argv[2]).read().strip().splitlines()[-1])["kernel_ms_per_step"]
+    bl = json.loads(open(sys.argv[2]).read().strip().splitlines()[-1])
+    # solo (serialised) event times when present: comparable with ncu's serialised launches
+    bench = bl.get("kernel_ms_per_step_serial") or bl["kernel_ms_per_step"]
     BT = sum(bench.values())
-print(f"{'kernel':<22}{'launches':>9}{'ncu us':>12}{'ncu share':>11}" + (f"{'bench share':>13}" if bench else ""))
+print(f"{'kernel':<26}{'launches':>9}{'ncu us':>12}{'ncu share':>11}" + (f"{'bench share':>13}" if bench else ""))
 for k in sorted(tot, key=lambda k: -tot[k]):
-    line = f"{k:<22}{cnt[k]:>9}{tot[k]:>12.1f}{100 * tot[k] / T:>10.1f}%"
+    line = f"{k:<26}{cnt[k]:>9}{tot[k]:>12.1f}{100 * tot[k] / T:>10.1f}%"
     if bench:
         line += f"{100 * bench.get(k, 0.0) / BT:>12.1f}%"
     print(line)

@@ -57,7 +57,7 @@ the bench numbers come from an unprofiled run with CUDA events.
 * clocks {b['clocks']}
 * cpu_baseline (oracle, {b['cpu_baseline']['cores']} core): {b['cpu_baseline']['value']:.2f} scans/s — {b['cpu_baseline']['sample']}
 
-## Kernel shares: ncu launch list vs bench CUDA events
+## Kernel shares: ncu launch list vs bench CUDA events (serialised pass, solo kernel times)
 
 ```
 {shares}```
