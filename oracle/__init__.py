@@ -66,6 +66,8 @@ def lib():
             L.orc_integrate_color.restype = C.c_int32
             L.orc_integrate_color.argtypes = [P, P, P, C.c_int64, P, C.POINTER(Sensor), C.POINTER(Stats)]
             L.orc_export_color.argtypes = [P, P, P]
+            L.orc_integrate_projective.restype = C.c_int32
+            L.orc_integrate_projective.argtypes = [P, P, C.c_int64, P, C.POINTER(Sensor), C.POINTER(Stats)]
             L.orc_num_blocks.restype = C.c_int64
             L.orc_num_blocks.argtypes = [P]
             L.orc_export.argtypes = [P, P, P, P]
@@ -127,6 +129,17 @@ class OracleSubmap:
         sm = sensor_struct(sensor)
         rc = lib().orc_integrate(self._h, _p(d), n, _p(T), C.byref(sm), C.byref(st))
         assert rc == 0
+        return st.asdict()
+
+    def integrate_projective(self, depth, T_world_sensor, sensor: dict) -> dict:
+        """Projection mapping (R14): ALLOCATE as integrate, then every voxel of
+        the submap is projected into the depth image (nearest pixel) and fused with sdf = depth - z."""
+        d = np.ascontiguousarray(np.asarray(depth, dtype=np.float32))
+        T = np.ascontiguousarray(T_world_sensor, dtype=np.float64)
+        st = Stats()
+        sm = sensor_struct(sensor)
+        rc = lib().orc_integrate_projective(self._h, _p(d), d.size, _p(T), C.byref(sm), C.byref(st))
+        assert rc == 0, "projective integration needs a pinhole depth frame of width*height pixels"
         return st.asdict()
 
     def num_blocks(self) -> int:

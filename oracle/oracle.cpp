@@ -301,6 +301,97 @@ void orc_export_color(void* h, double* rgb, double* cw) {
   }
 }
 
+// Projection-mapping integrator (R14) — the KinectFusion / nvBlox scheme the
+// paper contrasts with raycasting ("projects voxels in the visual field of view into the
+// depth image and computes their distance from the difference between the voxel centre and the depth
+// value in the image", "associating it with the nearest pixel").  Pinhole depth frames only.
+// Per frame, in this order:
+//   1. ALLOCATE exactly as orc_integrate (every block holding a voxel traversed by a used ray, O2-O7),
+//      with no TSDF update from the rays;
+//   2. every voxel v of every block of the submap: c = (v + 1/2) s, x = R_SC^T (c - t_SC) (camera frame);
+//      z = x_2 > 0; nearest pixel (px, py) = (floor(u + 1/2), floor(w + 1/2)) with
+//      u = (fx x_0)(1/z) + cx, w = (fy x_1)(1/z) + cy (pixel centres at integers, Q24) inside the image;
+//      the pixel's depth m valid (> 0, finite) and its O2 point's length L inside [r_min, r_max] (Q10);
+//      sdf = m - z (projective distance along the optical axis); skipped if sdf < -tau (occluded) and,
+//      in band mode (carve = 0), if sdf > tau; d = min(sdf, tau); w = O6 with the pixel's L;
+//      swd += w d, sw += w.
+static void project_frame(Oracle* O, const float* depth, const orc_sensor* sm, const double R[3][3],
+                          const double t[3], int64_t* n_updates) {
+  const orc_grid& g = O->g;
+  const double sv = g.voxel_size, tau = g.truncation;
+  for (auto& kv : O->blocks) {
+    Block* b = kv.second;
+    for (int l = 0; l < kBV; ++l) {
+      const int64_t v[3] = {kv.first.x * kB + l % 8, kv.first.y * kB + (l / 8) % 8, kv.first.z * kB + l / 64};
+      double e[3], x[3];
+      for (int k = 0; k < 3; ++k) e[k] = ((double)v[k] + 0.5) * sv - t[k];
+      for (int i = 0; i < 3; ++i) x[i] = (R[0][i] * e[0] + R[1][i] * e[1]) + R[2][i] * e[2];
+      const double z = x[2];
+      if (!(z > 0.0)) continue;
+      const double inv = 1.0 / z;
+      const double uh = ((double)sm->fx * x[0]) * inv + (double)sm->cx + 0.5;
+      const double wh = ((double)sm->fy * x[1]) * inv + (double)sm->cy + 0.5;
+      if (!(uh >= 0.0 && uh < (double)sm->width && wh >= 0.0 && wh < (double)sm->height)) continue;
+      const int64_t px = (int64_t)std::floor(uh), py = (int64_t)std::floor(wh);
+      const float m = depth[py * sm->width + px];
+      if (!(m > 0.0f) || !std::isfinite(m)) continue;
+      const float pu = (float)px, pv = (float)py;   // O2 point of that pixel, fp32 as written
+      const double pc[3] = {(double)((m * (pu - sm->cx)) / sm->fx), (double)((m * (pv - sm->cy)) / sm->fy), (double)m};
+      const double L = std::sqrt((pc[0] * pc[0] + pc[1] * pc[1]) + pc[2] * pc[2]);
+      if (!(L >= (double)sm->min_range && L <= (double)sm->max_range)) continue;
+      const double sdf = (double)m - z;
+      if (sdf < -tau) continue;
+      if (!g.carve && sdf > tau) continue;
+      const double d = std::min(sdf, tau);
+      double w = 1.0;
+      if (g.weighting != 0) { const double r = std::max(L, g.weight_range_floor); w = 1.0 / (r * r); }
+      b->swd[l] += w * d;
+      b->sw[l] += w;
+      ++*n_updates;
+    }
+  }
+}
+
+int32_t orc_integrate_projective(void* h, const float* depth, int64_t n, const double* T_world_sensor,
+                                 const orc_sensor* sm, orc_stats* st) {
+  Oracle* O = static_cast<Oracle*>(h);
+  if (sm->kind != 1 || n != (int64_t)sm->width * sm->height) return -1;
+  const orc_grid& g = O->g;
+  double R[3][3], t[3];
+  compose_sc(O->Tws, T_world_sensor, R, t);
+  orc_stats s = {};
+  s.rays_in = n;
+  const size_t before = O->blocks.size();
+  std::vector<V3> vs;
+  for (int64_t i = 0; i < n; ++i) {   // 1. ALLOCATE (O2-O7), no update
+    const float z = depth[i];
+    if (!(z > 0.0f) || !std::isfinite(z)) { s.skipped_invalid++; continue; }
+    const float u = (float)(i % sm->width), v = (float)(i / sm->width);
+    const float pc[3] = {(z * (u - sm->cx)) / sm->fx, (z * (v - sm->cy)) / sm->fy, z};
+    Ray ray;
+    const int rc = make_ray(g, *sm, R, t, pc, &ray);
+    if (rc == 1) { s.skipped_invalid++; continue; }
+    if (rc == 2) { s.skipped_range++; continue; }
+    if (rc == 3) { s.skipped_domain++; continue; }
+    s.rays_used++;
+    vs.clear();
+    traverse(ray.A, ray.B, vs);
+    for (const V3& vv : vs) {
+      const Key k = {fdiv8(vv.x), fdiv8(vv.y), fdiv8(vv.z)};
+      if (O->blocks.find(k) == O->blocks.end()) {
+        Block* b = new Block();
+        std::memset(b, 0, sizeof(Block));
+        O->blocks.emplace(k, b);
+      }
+    }
+  }
+  project_frame(O, depth, sm, R, t, &s.voxel_updates);   // 2. projective update of every voxel
+  s.new_blocks = (int64_t)(O->blocks.size() - before);
+  s.total_blocks = (int64_t)O->blocks.size();
+  if (st) *st = s;
+  return 0;
+}
+
 int64_t orc_num_blocks(void* h) { return (int64_t)static_cast<Oracle*>(h)->blocks.size(); }
 
 // Export in (bx, by, bz) lexicographic order: D = sum(w d)/sum(w) (O8), W = sum(w); D = W = 0 where
