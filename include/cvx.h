@@ -151,6 +151,23 @@ cvx_status cvx_integrate_color(cvx_submap* submap, const float* data, const uint
                                int32_t n_frames, const double* T_world_sensor, const cvx_sensor_model* sensor,
                                void* stream, cvx_integrate_stats* stats);
 
+/* Projection-mapping integration (R14) — the KinectFusion / nvBlox voxel-centric
+ * update the paper contrasts with its raycasting ("projects voxels in the visual field of
+ * view into the depth image and computes their distance from the difference between the voxel centre
+ * and the depth value in the image", "associating it with the nearest pixel"), for the in-house
+ * raycast-vs-projection comparison.  `depth` (device fp32 [n_frames][height][width] metres) and the
+ * poses as cvx_integrate_batch; sensor kind must be 1 (pinhole).  Per frame, in order: ALLOCATE exactly
+ * as cvx_integrate_pointcloud (same block set, no update from the rays); then every voxel v of the
+ * submap with camera-frame centre x (z = x_2 > 0) whose nearest pixel (floor(fx x_0 / z + cx + 1/2),
+ * floor(fy x_1 / z + cy + 1/2)) lies in the image, has a valid depth m and a pixel ray length inside
+ * [min_range, max_range] gets sdf = m - z; voxels with sdf < -tau (occluded), and in band mode
+ * (carve = 0) sdf > tau, are skipped; d = min(sdf, tau) is fused with the weight of the pixel (O6).
+ * Batches equal frame-by-frame calls bit for bit.  stats.voxel_updates counts the projective updates.
+ * Errors as cvx_integrate_batch; CVX_E_INVALID for sensor kinds other than 1. */
+cvx_status cvx_integrate_projective(cvx_submap* submap, const float* depth, int64_t n_per_frame, int32_t n_frames,
+                                    const double* T_world_sensor, const cvx_sensor_model* sensor, void* stream,
+                                    cvx_integrate_stats* stats);
+
 /* Export the fused colour in slot order (synchronising): rgb (device fp32 [nb][512][3], 0..255; 0 where no
  * band update) and color_weight (device fp32 [nb][512], nullable).  Errors: CVX_E_INVALID without colour
  * storage, CVX_E_CAPACITY if nb > capacity_blocks. */

@@ -128,6 +128,7 @@ void free_all(cvx_submap* sm) {
   if (sm->inc.list) cudaFree(sm->inc.list);
   if (sm->inc.cnt) cudaFree(sm->inc.cnt);
   if (sm->inc.cnt_host) cudaFreeHost(sm->inc.cnt_host);
+  if (sm->proj_cnt) cudaFree(sm->proj_cnt);
   if (sm->trig) cudaFree(sm->trig);
   if (sm->trig_host) cudaFreeHost(sm->trig_host);
   delete sm->prof;
@@ -248,7 +249,8 @@ cvx_status cvx_reset_submap(cvx_submap* sm, void* stream) {
 
 static cvx_status integrate_impl(cvx_submap* sm, const float* data, int64_t n_per_frame, int32_t n_frames,
                                  const double* T_world_sensor, const cvx_sensor_model* sensor, void* stream,
-                                 cvx_integrate_stats* stats, bool host_data, const uint8_t* rgb = nullptr) {
+                                 cvx_integrate_stats* stats, bool host_data, const uint8_t* rgb = nullptr,
+                                 bool projective = false) {
   g_last_error.clear();
   if (!sm) return fail(CVX_E_INVALID, "submap is NULL");
   if (sm->finalized) return fail(CVX_E_STATE, "submap is finalized (S:L443): integrate rejected");
@@ -266,8 +268,10 @@ static cvx_status integrate_impl(cvx_submap* sm, const float* data, int64_t n_pe
   if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
   cudaStream_t st = (cudaStream_t)stream;
   if (n_per_frame > 0 && n_frames > 0) {
-    cudaError_t e = cvx::launch_integrate(sm, data, n_per_frame, n_frames, T_world_sensor, *sensor, st, host_data,
-                                          nullptr, rgb);
+    cudaError_t e = projective
+                        ? cvx::launch_integrate_projective(sm, data, n_per_frame, n_frames, T_world_sensor, *sensor, st)
+                        : cvx::launch_integrate(sm, data, n_per_frame, n_frames, T_world_sensor, *sensor, st, host_data,
+                                                nullptr, rgb);
     if (e != cudaSuccess) return cuda_fail(e, "integrate");
   }
   if (stats) {
@@ -307,6 +311,15 @@ cvx_status cvx_integrate_color(cvx_submap* sm, const float* data, const uint8_t*
   if (!sm->pool.csum) return fail(CVX_E_INVALID, "submap has no colour storage (config.color = 0)");
   if (!rgb && n_per_frame > 0 && n_frames > 0) return fail(CVX_E_INVALID, "rgb is NULL");
   return integrate_impl(sm, data, n_per_frame, n_frames, T_world_sensor, sensor, stream, stats, false, rgb);
+}
+
+cvx_status cvx_integrate_projective(cvx_submap* sm, const float* depth, int64_t n_per_frame, int32_t n_frames,
+                                    const double* T_world_sensor, const cvx_sensor_model* sensor, void* stream,
+                                    cvx_integrate_stats* stats) {
+  g_last_error.clear();
+  if (!sm || !sensor) return fail(CVX_E_INVALID, "NULL argument");
+  if (sensor->kind != 1) return fail(CVX_E_INVALID, "projection mapping needs a pinhole depth sensor (kind 1)");
+  return integrate_impl(sm, depth, n_per_frame, n_frames, T_world_sensor, sensor, stream, stats, false, nullptr, true);
 }
 
 cvx_status cvx_export_color(const cvx_submap* sm, float* rgb, float* color_weight, int64_t capacity_blocks,

@@ -108,6 +108,7 @@ struct PrepParams {
   int list_cap;
   const int* trig;  // nullable: {threshold, hit, consumed}; a hit submap takes no further frames
   const unsigned char* rgb;   // nullable: per-point colour [total][3]
+  int count_vox;    // add the raycast voxel counts to ctr->voxel_updates (0: projection mapping)
 };
 
 __global__ void __launch_bounds__(256) prepare_kernel(const __grid_constant__ PrepParams p) {
@@ -238,7 +239,7 @@ __global__ void __launch_bounds__(256) prepare_kernel(const __grid_constant__ Pr
     if (c[3]) atomicAdd(&p.ctr->skipped_invalid, c[3]);
     if (c[4]) atomicAdd(&p.ctr->skipped_range, c[4]);
     if (c[5]) { atomicAdd(&p.ctr->skipped_domain, c[5]); atomicOr(&p.ctr->err, (unsigned)kErrRange); }
-    if (c[6]) atomicAdd(&p.ctr->voxel_updates, c[6]);
+    if (c[6] && p.count_vox) atomicAdd(&p.ctr->voxel_updates, c[6]);
   }
   __syncthreads();
   if (status == 0) {
@@ -795,6 +796,108 @@ __global__ void zero_color_kernel(Counters* ctr, long long* csum, unsigned long 
   }
 }
 
+// ---------------------------------------------------------------------------------- projection mapping
+// SURVEY §8 f2 / DESIGN.md R14: the KinectFusion / nvBlox voxel-centric update the paper
+// contrasts with raycasting.  ALLOCATE is the raycast one (prepare + block walk per frame); then every
+// voxel of the submap is projected into the frame's depth image, associated with the nearest pixel and
+// fused with sdf = depth - z.  One CTA owns one 8^3 block at a time (persistent grid-stride over the
+// blocks), each thread 4 voxels, and loops over the frames of the launch with the sums in registers:
+// the TSDF state is read and written once per launch, the depth images are gathered through L1/L2, and
+// no atomics touch the voxels (a voxel has one owner thread).  A block allocated by frame j of the
+// launch has slot >= cnt[j-1] (the pool index is bumped in frame order), so it skips frames before j —
+// the result equals frame-by-frame integration exactly.  Every decision (z > 0, pixel, range, occlusion)
+// is taken in the oracle's fp64 / fp32 operation order without FMA contraction.
+struct ProjParams {
+  const float* depth;      // [nf][height][width]
+  const double* frame_T;   // compose_kernel records of the launch's frames
+  const int* cnt;          // [nf] blocks after frame j's ALLOCATE
+  PoolView pool;
+  Counters* ctr;
+  int nf, width, height;
+  float fx, fy, cx, cy;
+  double rmin, rmax, s, tau, rfloor;
+  int weighting, carve, q;
+};
+
+constexpr int kProjThreads = 128;
+
+__global__ void __launch_bounds__(kProjThreads) project_kernel(const __grid_constant__ ProjParams p) {
+  __shared__ double sT[kMaxBatch][12];   // R_SC (row-major) and t_SC per frame
+  for (int i = threadIdx.x; i < p.nf * 12; i += blockDim.x) sT[i / 12][i % 12] = p.frame_T[kFrameRec * (i / 12) + i % 12];
+  __syncthreads();
+  const int nb = min(p.cnt[p.nf - 1], p.pool.max_blocks);
+  const int t = threadIdx.x;
+  const int lx = t & 7, ly = (t >> 3) & 7, lz0 = t >> 6;   // voxel k of the thread: lz = lz0 + 2k
+  const double dq_scale = (double)(1ll << p.q);
+  const int shift = 30 - p.q;
+  unsigned long long n_upd = 0;
+  for (int blk = blockIdx.x; blk < nb; blk += gridDim.x) {
+    const int4 bc = p.pool.coords[blk];
+    double cx0 = dm(da((double)(bc.x * 8 + lx), 0.5), p.s);
+    double cy0 = dm(da((double)(bc.y * 8 + ly), 0.5), p.s);
+    double cz[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) cz[k] = dm(da((double)(bc.z * 8 + lz0 + 2 * k), 0.5), p.s);
+    long long swd[4] = {0, 0, 0, 0}, sw[4] = {0, 0, 0, 0};
+    for (int j = 0; j < p.nf; ++j) {
+      if (blk >= p.cnt[j]) continue;       // block allocated by a later frame (CTA-uniform)
+      const double* T = sT[j];
+      const float* img = p.depth + (long long)j * p.width * p.height;
+      const double e0 = ds(cx0, T[9]), e1 = ds(cy0, T[10]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const double e2 = ds(cz[k], T[11]);
+        // x = R_SC^T (c - t_SC): x_i = (R[0][i] e0 + R[1][i] e1) + R[2][i] e2
+        const double z = da(da(dm(T[2], e0), dm(T[5], e1)), dm(T[8], e2));
+        if (!(z > 0.0)) continue;
+        const double x0 = da(da(dm(T[0], e0), dm(T[3], e1)), dm(T[6], e2));
+        const double x1 = da(da(dm(T[1], e0), dm(T[4], e1)), dm(T[7], e2));
+        const double inv = __drcp_rn(z);
+        const double uh = da(da(dm(dm((double)p.fx, x0), inv), (double)p.cx), 0.5);
+        const double wh = da(da(dm(dm((double)p.fy, x1), inv), (double)p.cy), 0.5);
+        if (!(uh >= 0.0 && uh < (double)p.width && wh >= 0.0 && wh < (double)p.height)) continue;
+        const int px = (int)uh, py = (int)wh;   // non-negative: truncation == floor
+        const float m = __ldg(img + py * p.width + px);
+        if (!(m > 0.0f) || !isfinite(m)) continue;
+        const float pc0 = __fdiv_rn(__fmul_rn(m, __fsub_rn((float)px, p.cx)), p.fx);
+        const float pc1 = __fdiv_rn(__fmul_rn(m, __fsub_rn((float)py, p.cy)), p.fy);
+        const double L = __dsqrt_rn(da(da(dm((double)pc0, (double)pc0), dm((double)pc1, (double)pc1)),
+                                       dm((double)m, (double)m)));
+        if (!(L >= p.rmin && L <= p.rmax)) continue;
+        const double sdf = ds((double)m, z);
+        if (sdf < -p.tau || (!p.carve && sdf > p.tau)) continue;
+        const long long dq = __double2ll_rn(dm(fmin(sdf, p.tau), dq_scale));   // R2 quantum 2^-q
+        if (p.weighting == 0) {
+          swd[k] += dq << shift;
+          sw[k] += 1ll << 30;
+        } else {
+          const double r = fmax(L, p.rfloor);
+          const double w = __drcp_rn(dm(r, r));
+          swd[k] += __double2ll_rn(dm(dm(w, (double)dq), (double)(1ll << shift)));
+          sw[k] += __double2ll_rn(dm(w, kFxScale));
+        }
+        ++n_upd;
+      }
+    }
+    longlong2* s2 = reinterpret_cast<longlong2*>(p.pool.sums) + (long long)blk * kBlockVox;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (sw[k] == 0) continue;
+      const int l = t + kProjThreads * k;   // = lx + 8 ly + 64 (lz0 + 2k)
+      longlong2 v = s2[l];
+      v.x += swd[k];
+      v.y += sw[k];
+      s2[l] = v;
+    }
+  }
+  n_upd = __reduce_add_sync(0xffffffffu, (unsigned)n_upd);
+  if ((t & 31) == 0 && n_upd) atomicAdd(&p.ctr->voxel_updates, n_upd);
+}
+
+__global__ void record_count_kernel(const Counters* ctr, int* cnt, int j, int max_blocks) {
+  cnt[j] = min(ctr->n_blocks, max_blocks);
+}
+
 __global__ void reset_counters_kernel(Counters* ctr) {
   Counters c = {};
   c.aabb_lo[0] = c.aabb_lo[1] = c.aabb_lo[2] = 0x7fffffff;
@@ -922,6 +1025,7 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     pp.list_cap = (int)std::min<long long>(B.slot_cap, 0x7fffffffll);
     pp.trig = trig;
     pp.rgb = rgb ? rgb + (long long)f0 * n_per_frame * 3 : nullptr;
+    pp.count_vox = 1;
     {
       ProfScope ps_(sm, "ray_prepare", side);
       prepare_kernel<<<blocks, 256, 0, side>>>(pp);
@@ -970,6 +1074,86 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     f0 += nf;
   }
   fold();
+  return cudaGetLastError();
+}
+
+
+// Projection-mapping integration (R14).  Per launch of <= kMaxBatch frames:
+// compose, then per frame prepare + block walk (ALLOCATE) + a birth-count record, then ONE
+// project_kernel over every block for all frames of the launch.  All on the caller's stream.
+cudaError_t launch_integrate_projective(cvx_submap* sm, const float* depth, int64_t n_per_frame, int n_frames,
+                                        const double* T_world_sensor, const cvx_sensor_model& sensor,
+                                        cudaStream_t st) {
+  if (n_per_frame <= 0 || n_frames <= 0) return cudaSuccess;
+  cvx_submap::Buf& B = sm->buf[0];
+  cudaError_t e = grow(&B.rays, &B.ray_cap, n_per_frame, sizeof(RayRec));
+  if (e == cudaSuccess)
+    e = grow(reinterpret_cast<void**>(&B.slot_lists), &B.slot_cap, n_per_frame * kSlotsPerRay + 1024, sizeof(int));
+  if (e == cudaSuccess && !sm->proj_cnt) e = cudaMalloc(&sm->proj_cnt, sizeof(int) * kMaxBatch);
+  if (e != cudaSuccess) return e;
+  const int q = packed_q(sm->cfg.truncation);
+  const bool k32 = ((double)sensor.max_range + sm->cfg.truncation) / sm->cfg.voxel_size + 2.0 < 4096.0;
+  const unsigned blocks = (unsigned)((n_per_frame + 255) / 256);
+  for (int f0 = 0; f0 < n_frames; f0 += kMaxBatch) {
+    const int nf = std::min(kMaxBatch, n_frames - f0);
+    ComposeParams cp;
+    for (int i = 0; i < 16; ++i) cp.Tws[i] = sm->T_ws[i];
+    for (int f = 0; f < nf; ++f)
+      for (int i = 0; i < 16; ++i) cp.Twc[f][i] = T_world_sensor[16 * (f0 + f) + i];
+    cp.n = nf;
+    cp.s = sm->cfg.voxel_size;
+    {
+      ProfScope ps_(sm, "compose_poses", st);
+      compose_kernel<<<1, kMaxBatch, 0, st>>>(cp, B.frame_T);
+    }
+    for (int f = 0; f < nf; ++f) {
+      cudaMemsetAsync(B.lcnt, 0, 4 * sizeof(int), st);
+      PrepParams pp;
+      pp.data = depth + (long long)(f0 + f) * n_per_frame;
+      pp.n_per_frame = n_per_frame; pp.total = n_per_frame;
+      pp.kind = sensor.kind; pp.width = sensor.width;
+      pp.fx = sensor.fx; pp.fy = sensor.fy; pp.cx = sensor.cx; pp.cy = sensor.cy;
+      pp.rmin = (double)sensor.min_range; pp.rmax = (double)sensor.max_range;
+      pp.s = sm->cfg.voxel_size; pp.tau = sm->cfg.truncation; pp.rfloor = sm->cfg.weight_range_floor;
+      pp.weighting = sm->cfg.weighting; pp.carve = sm->cfg.carve;
+      pp.sdf_scale = std::ldexp(1.0, q + kSdfF);
+      pp.height = sensor.height;
+      pp.frame_T = B.frame_T + kFrameRec * f; pp.rays = (RayRec*)B.rays; pp.ctr = sm->ctr; pp.lcnt = B.lcnt;
+      pp.list_cap = (int)std::min<long long>(B.slot_cap, 0x7fffffffll);
+      pp.trig = nullptr;
+      pp.rgb = nullptr;
+      pp.count_vox = 0;   // voxel_updates counts the projective updates instead
+      {
+        ProfScope ps_(sm, "ray_prepare", st);
+        prepare_kernel<<<blocks, 256, 0, st>>>(pp);
+      }
+      WalkParams wp;
+      wp.rays = (const RayRec*)B.rays; wp.ctr = sm->ctr; wp.hash = sm->hash; wp.pool = sm->pool;
+      wp.slots = B.slot_lists; wp.lcnt = B.lcnt;
+      wp.s = (float)sm->cfg.voxel_size; wp.tau = (float)sm->cfg.truncation;
+      wp.tq = (int)std::llround(std::ldexp(sm->cfg.truncation, q));
+      wp.q = q;
+      wp.band = 0;
+      {
+        ProfScope ps_(sm, "block_walk_allocate", st);
+        if (k32) block_walk2_kernel<true><<<blocks, 256, 0, st>>>(wp);
+        else block_walk2_kernel<false><<<blocks, 256, 0, st>>>(wp);
+      }
+      record_count_kernel<<<1, 1, 0, st>>>(sm->ctr, sm->proj_cnt, f, sm->pool.max_blocks);
+    }
+    ProjParams pj;
+    pj.depth = depth + (long long)f0 * n_per_frame;
+    pj.frame_T = B.frame_T; pj.cnt = sm->proj_cnt; pj.pool = sm->pool; pj.ctr = sm->ctr;
+    pj.nf = nf; pj.width = sensor.width; pj.height = sensor.height;
+    pj.fx = sensor.fx; pj.fy = sensor.fy; pj.cx = sensor.cx; pj.cy = sensor.cy;
+    pj.rmin = (double)sensor.min_range; pj.rmax = (double)sensor.max_range;
+    pj.s = sm->cfg.voxel_size; pj.tau = sm->cfg.truncation; pj.rfloor = sm->cfg.weight_range_floor;
+    pj.weighting = sm->cfg.weighting; pj.carve = sm->cfg.carve; pj.q = q;
+    {
+      ProfScope ps_(sm, "project_update", st);
+      project_kernel<<<148 * 8, kProjThreads, 0, st>>>(pj);
+    }
+  }
   return cudaGetLastError();
 }
 

@@ -84,6 +84,7 @@ struct cvx_submap {
     int nb_prev = 0;                    // blocks covered by the last update
   } inc;
 
+  int* proj_cnt = nullptr;    // device [kMaxBatch]: blocks after each frame's ALLOCATE (projection mapping)
   int* trig = nullptr;        // device {threshold, hit, consumed, -} of cvx_integrate_until
   int* trig_host = nullptr;   // pinned mirror
 
@@ -109,6 +110,9 @@ cudaError_t launch_reset(cvx_submap* sm, cudaStream_t st);
 cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_frame, int n_frames,
                              const double* T_world_sensor, const cvx_sensor_model& sensor, cudaStream_t st,
                              bool host_data, int* trig = nullptr, const unsigned char* rgb = nullptr);
+cudaError_t launch_integrate_projective(cvx_submap* sm, const float* depth, int64_t n_per_frame, int n_frames,
+                                        const double* T_world_sensor, const cvx_sensor_model& sensor,
+                                        cudaStream_t st);
 cudaError_t launch_export_color(const cvx_submap* sm, int n_blocks, float* rgb, float* cw, cudaStream_t st);
 // esdf.cu
 cudaError_t launch_finalize(cvx_submap* sm, int n_blocks, const int lo[3], const int hi[3], cudaStream_t st);

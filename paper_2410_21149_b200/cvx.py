@@ -66,6 +66,8 @@ SIGNATURES = {
                                         C.POINTER(C.c_int32)]),
     "cvx_integrate_color": (C.c_int32, [_P, _P, _P, C.c_int64, C.c_int32, _P, C.POINTER(SensorModel), _P,
                                         C.POINTER(Stats)]),
+    "cvx_integrate_projective": (C.c_int32, [_P, _P, C.c_int64, C.c_int32, _P, C.POINTER(SensorModel), _P,
+                                             C.POINTER(Stats)]),
     "cvx_export_color": (C.c_int32, [_P, _P, _P, C.c_int64, C.POINTER(C.c_int64), _P]),
     "cvx_get_stats": (C.c_int32, [_P, C.POINTER(Stats)]),
     "cvx_get_block_count": (C.c_int32, [_P, C.POINTER(C.c_int64)]),
@@ -187,6 +189,22 @@ class Submap:
         st = Stats() if stats else None
         _check(lib().cvx_integrate_batch(self._h, self._dev(data, torch.float32, "data"), n, F, _ptr(poses),
                                          C.byref(sm), self._stream(), C.byref(st) if st is not None else None))
+        return st.asdict() if st is not None else None
+
+    def integrate_projective(self, depth: torch.Tensor, T_world_sensor, sensor: dict, stats: bool = False):
+        """Projection mapping (R14): depth fp32 [F, H, W] (or [H, W]),
+        T_world_sensor [F, 4, 4]; pinhole sensors only."""
+        if depth.dim() == 2:
+            depth = depth.unsqueeze(0)
+        sm = sensor_model(sensor)
+        F = depth.shape[0]
+        poses = _pose(T_world_sensor)
+        if poses.shape[0] != F:
+            raise ValueError("one pose per frame")
+        st = Stats() if stats else None
+        _check(lib().cvx_integrate_projective(self._h, self._dev(depth, torch.float32, "depth"), depth[0].numel(), F,
+                                              _ptr(poses), C.byref(sm), self._stream(),
+                                              C.byref(st) if st is not None else None))
         return st.asdict() if st is not None else None
 
     def integrate_color(self, data: torch.Tensor, rgb: torch.Tensor, T_world_sensor, sensor: dict,
