@@ -128,7 +128,7 @@ void free_all(cvx_submap* sm) {
   if (sm->inc.list) cudaFree(sm->inc.list);
   if (sm->inc.cnt) cudaFree(sm->inc.cnt);
   if (sm->inc.cnt_host) cudaFreeHost(sm->inc.cnt_host);
-  if (sm->proj_cnt) cudaFree(sm->proj_cnt);
+  if (sm->proj_birth) cudaFree(sm->proj_birth);
   if (sm->trig) cudaFree(sm->trig);
   if (sm->trig_host) cudaFreeHost(sm->trig_host);
   delete sm->prof;

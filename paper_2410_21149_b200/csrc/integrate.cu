@@ -109,6 +109,8 @@ struct PrepParams {
   const int* trig;  // nullable: {threshold, hit, consumed}; a hit submap takes no further frames
   const unsigned char* rgb;   // nullable: per-point colour [total][3]
   int count_vox;    // add the raycast voxel counts to ctr->voxel_updates (0: projection mapping)
+  int frame_tag;    // projection mapping: store frame_base + frame index in RayRec::rgb (birth frames)
+  int frame_base;
 };
 
 __global__ void __launch_bounds__(256) prepare_kernel(const __grid_constant__ PrepParams p) {
@@ -186,7 +188,7 @@ __global__ void __launch_bounds__(256) prepare_kernel(const __grid_constant__ Pr
           rec.n_vox += (int)(dv < 0 ? -dv : dv);             // a2: n_r = 1 + sum |dv| (O4)
         }
         rec.list_off = -1;
-        rec.rgb = 0;
+        rec.rgb = p.frame_tag ? (unsigned)(p.frame_base + (int)f) : 0u;
         if (p.rgb) {
           const unsigned char* c = p.rgb + 3 * src;
           rec.rgb = (unsigned)c[0] | ((unsigned)c[1] << 8) | ((unsigned)c[2] << 16);
@@ -261,6 +263,7 @@ struct WalkParams {
   int tq;           // round(tau 2^q): the clamp bound (and packed offset) of the quantised sdf
   int q;            // sdf quantum 2^-q m
   long long band;   // colour band |S| < band, S in the fixed-point sdf units 2^-(q+kSdfF) m (= tau)
+  int* birth;       // projection mapping: per slot, first frame (RayRec::rgb) whose rays touch the block
 };
 
 // Segmented sum over lanes with equal `peers` groups (log-depth shuffle tree); result valid at the
@@ -356,7 +359,7 @@ __device__ __forceinline__ int key_field(unsigned long long key, int sh) {
   return ((int)((key >> sh) & 0x1fffffu) << 11) >> 11;          // 21-bit two's complement (pack_key)
 }
 
-template <bool k32>
+template <bool k32, bool kBirth = false>
 __global__ void __launch_bounds__(256) block_walk2_kernel(const __grid_constant__ WalkParams p) {
   using DT = typename std::conditional<k32, unsigned, unsigned long long>::type;
   using ST = typename std::conditional<k32, int, long long>::type;
@@ -368,8 +371,10 @@ __global__ void __launch_bounds__(256) block_walk2_kernel(const __grid_constant_
   int b0 = 0, b1 = 0, b2 = 0, s0 = 1, s1 = 1, s2 = 1, k0 = 0, k1 = 0, k2 = 0, nb = 0;
   DT D01 = 0, D02 = 0, D12 = 0, I0 = 0, I1 = 0, I2 = 0;
   int* list = nullptr;
+  int frame = 0x7fffffff;
   if (have) {
     const RayRec r = p.rays[idx];
+    if (kBirth) frame = (int)r.rgb;
     long long R[3], AD[3];
     int bb[3], st[3], kk[3];
 #pragma unroll
@@ -431,6 +436,14 @@ __global__ void __launch_bounds__(256) block_walk2_kernel(const __grid_constant_
     const unsigned hb = heads & (0xffffffffu >> (31 - lane));
     slot = __shfl_sync(0xffffffffu, slot, hb ? 31 - __clz(hb) : lane);
     if (act && list) list[j] = slot;
+    if (kBirth) {   // birth frame = min frame over the rays touching the block (one RED per run if uniform)
+      const int fmin = __reduce_min_sync(0xffffffffu, act ? frame : 0x7fffffff);
+      const int fmax = __reduce_max_sync(0xffffffffu, act ? frame : -1);
+      const bool mine = fmin == fmax ? ((heads >> lane) & 1u) != 0u : act;
+      // birth only decreases during a call, so a stale (L1) read is >= the true value: skipping when it is
+      // already <= frame is exact, and it keeps hot blocks (near the sensor) free of same-address REDs
+      if (mine && slot >= 0 && p.birth[slot] > frame) atomicMin(p.birth + slot, frame);
+    }
     act = actn; key = keyn; heads = headsn; ent = entn;
   }
 }
@@ -803,14 +816,17 @@ __global__ void zero_color_kernel(Counters* ctr, long long* csum, unsigned long 
 // fused with sdf = depth - z.  One CTA owns one 8^3 block at a time (persistent grid-stride over the
 // blocks), each thread 4 voxels, and loops over the frames of the launch with the sums in registers:
 // the TSDF state is read and written once per launch, the depth images are gathered through L1/L2, and
-// no atomics touch the voxels (a voxel has one owner thread).  A block allocated by frame j of the
-// launch has slot >= cnt[j-1] (the pool index is bumped in frame order), so it skips frames before j —
-// the result equals frame-by-frame integration exactly.  Every decision (z > 0, pixel, range, occlusion)
+// no atomics touch the voxels (a voxel has one owner thread).  A block created during this call
+// (slot >= the block count at the call's start) carries its birth frame — the first frame whose rays
+// reached it, recorded by the block walk — and skips the frames before it, so the result equals
+// frame-by-frame integration exactly.  Every decision (z > 0, pixel, range, occlusion)
 // is taken in the oracle's fp64 / fp32 operation order without FMA contraction.
 struct ProjParams {
   const float* depth;      // [nf][height][width]
   const double* frame_T;   // compose_kernel records of the launch's frames
-  const int* cnt;          // [nf] blocks after frame j's ALLOCATE
+  const int* start;        // block count at the start of the call (older blocks see every frame)
+  const int* birth;        // per slot: birth frame (call-relative) of blocks created in this call
+  int frame_base;          // call-relative index of the launch's first frame
   PoolView pool;
   Counters* ctr;
   int nf, width, height;
@@ -825,7 +841,8 @@ __global__ void __launch_bounds__(kProjThreads) project_kernel(const __grid_cons
   __shared__ double sT[kMaxBatch][12];   // R_SC (row-major) and t_SC per frame
   for (int i = threadIdx.x; i < p.nf * 12; i += blockDim.x) sT[i / 12][i % 12] = p.frame_T[kFrameRec * (i / 12) + i % 12];
   __syncthreads();
-  const int nb = min(p.cnt[p.nf - 1], p.pool.max_blocks);
+  const int nb = min(p.ctr->n_blocks, p.pool.max_blocks);
+  const int start = *p.start;
   const int t = threadIdx.x;
   const int lx = t & 7, ly = (t >> 3) & 7, lz0 = t >> 6;   // voxel k of the thread: lz = lz0 + 2k
   const double dq_scale = (double)(1ll << p.q);
@@ -839,8 +856,8 @@ __global__ void __launch_bounds__(kProjThreads) project_kernel(const __grid_cons
 #pragma unroll
     for (int k = 0; k < 4; ++k) cz[k] = dm(da((double)(bc.z * 8 + lz0 + 2 * k), 0.5), p.s);
     long long swd[4] = {0, 0, 0, 0}, sw[4] = {0, 0, 0, 0};
-    for (int j = 0; j < p.nf; ++j) {
-      if (blk >= p.cnt[j]) continue;       // block allocated by a later frame (CTA-uniform)
+    const int j0 = blk < start ? 0 : max(0, p.birth[blk] - p.frame_base);   // CTA-uniform
+    for (int j = j0; j < p.nf; ++j) {
       const double* T = sT[j];
       const float* img = p.depth + (long long)j * p.width * p.height;
       const double e0 = ds(cx0, T[9]), e1 = ds(cy0, T[10]);
@@ -1026,6 +1043,8 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     pp.trig = trig;
     pp.rgb = rgb ? rgb + (long long)f0 * n_per_frame * 3 : nullptr;
     pp.count_vox = 1;
+    pp.frame_tag = 0;
+    pp.frame_base = 0;
     {
       ProfScope ps_(sm, "ray_prepare", side);
       prepare_kernel<<<blocks, 256, 0, side>>>(pp);
@@ -1037,6 +1056,7 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     wp.tq = tq;
     wp.q = q;
     wp.band = std::llround(std::ldexp(sm->cfg.truncation, q + kSdfF));
+    wp.birth = nullptr;
     {
       ProfScope ps_(sm, "block_walk_allocate", side);
       if (sm->bw2) {
@@ -1078,39 +1098,51 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
 }
 
 
-// Projection-mapping integration (R14).  Per launch of <= kMaxBatch frames:
-// compose, then per frame prepare + block walk (ALLOCATE) + a birth-count record, then ONE
-// project_kernel over every block for all frames of the launch.  All on the caller's stream.
+// Projection-mapping integration (R14), all on the caller's stream:
+//   record the block count at entry and clear the birth frames;
+//   per group of <= kMaxBatch frames: ALLOCATE in launches of <= kLaunchRays rays (compose, prepare with
+//   frame tags, block walk recording each new block's birth frame with one RED.MIN per run), then ONE
+//   project_kernel over every block for all frames of the group.
 cudaError_t launch_integrate_projective(cvx_submap* sm, const float* depth, int64_t n_per_frame, int n_frames,
                                         const double* T_world_sensor, const cvx_sensor_model& sensor,
                                         cudaStream_t st) {
   if (n_per_frame <= 0 || n_frames <= 0) return cudaSuccess;
+  const int lim = (int)std::max<long long>(1, std::min<long long>(kMaxBatch, kLaunchRays / n_per_frame));
   cvx_submap::Buf& B = sm->buf[0];
-  cudaError_t e = grow(&B.rays, &B.ray_cap, n_per_frame, sizeof(RayRec));
+  cudaError_t e = grow(&B.rays, &B.ray_cap, (long long)lim * n_per_frame, sizeof(RayRec));
   if (e == cudaSuccess)
-    e = grow(reinterpret_cast<void**>(&B.slot_lists), &B.slot_cap, n_per_frame * kSlotsPerRay + 1024, sizeof(int));
-  if (e == cudaSuccess && !sm->proj_cnt) e = cudaMalloc(&sm->proj_cnt, sizeof(int) * kMaxBatch);
+    e = grow(reinterpret_cast<void**>(&B.slot_lists), &B.slot_cap, (long long)lim * n_per_frame * kSlotsPerRay + 1024,
+             sizeof(int));
+  if (e == cudaSuccess && !sm->proj_birth) {
+    e = cudaMalloc(&sm->proj_birth, sizeof(int) * ((size_t)sm->pool.max_blocks + 1));
+    if (e == cudaSuccess) sm->proj_start = sm->proj_birth + sm->pool.max_blocks;
+  }
   if (e != cudaSuccess) return e;
   const int q = packed_q(sm->cfg.truncation);
   const bool k32 = ((double)sensor.max_range + sm->cfg.truncation) / sm->cfg.voxel_size + 2.0 < 4096.0;
-  const unsigned blocks = (unsigned)((n_per_frame + 255) / 256);
-  for (int f0 = 0; f0 < n_frames; f0 += kMaxBatch) {
-    const int nf = std::min(kMaxBatch, n_frames - f0);
+  cudaMemsetAsync(sm->proj_birth, 0x7f, sizeof(int) * (size_t)sm->pool.max_blocks, st);   // "never"
+  record_count_kernel<<<1, 1, 0, st>>>(sm->ctr, sm->proj_start, 0, sm->pool.max_blocks);
+  auto compose = [&](int f0, int nf, double* out) {
     ComposeParams cp;
     for (int i = 0; i < 16; ++i) cp.Tws[i] = sm->T_ws[i];
     for (int f = 0; f < nf; ++f)
       for (int i = 0; i < 16; ++i) cp.Twc[f][i] = T_world_sensor[16 * (f0 + f) + i];
     cp.n = nf;
     cp.s = sm->cfg.voxel_size;
-    {
-      ProfScope ps_(sm, "compose_poses", st);
-      compose_kernel<<<1, kMaxBatch, 0, st>>>(cp, B.frame_T);
-    }
-    for (int f = 0; f < nf; ++f) {
+    ProfScope ps_(sm, "compose_poses", st);
+    compose_kernel<<<1, kMaxBatch, 0, st>>>(cp, out);
+  };
+  for (int g0 = 0; g0 < n_frames; g0 += kMaxBatch) {
+    const int gn = std::min(kMaxBatch, n_frames - g0);
+    for (int f0 = g0; f0 < g0 + gn; f0 += lim) {   // ALLOCATE launches
+      const int nf = std::min(lim, g0 + gn - f0);
+      const long long total = (long long)nf * n_per_frame;
+      const unsigned blocks = (unsigned)((total + 255) / 256);
+      compose(f0, nf, B.frame_T);
       cudaMemsetAsync(B.lcnt, 0, 4 * sizeof(int), st);
       PrepParams pp;
-      pp.data = depth + (long long)(f0 + f) * n_per_frame;
-      pp.n_per_frame = n_per_frame; pp.total = n_per_frame;
+      pp.data = depth + (long long)f0 * n_per_frame;
+      pp.n_per_frame = n_per_frame; pp.total = total;
       pp.kind = sensor.kind; pp.width = sensor.width;
       pp.fx = sensor.fx; pp.fy = sensor.fy; pp.cx = sensor.cx; pp.cy = sensor.cy;
       pp.rmin = (double)sensor.min_range; pp.rmax = (double)sensor.max_range;
@@ -1118,11 +1150,13 @@ cudaError_t launch_integrate_projective(cvx_submap* sm, const float* depth, int6
       pp.weighting = sm->cfg.weighting; pp.carve = sm->cfg.carve;
       pp.sdf_scale = std::ldexp(1.0, q + kSdfF);
       pp.height = sensor.height;
-      pp.frame_T = B.frame_T + kFrameRec * f; pp.rays = (RayRec*)B.rays; pp.ctr = sm->ctr; pp.lcnt = B.lcnt;
+      pp.frame_T = B.frame_T; pp.rays = (RayRec*)B.rays; pp.ctr = sm->ctr; pp.lcnt = B.lcnt;
       pp.list_cap = (int)std::min<long long>(B.slot_cap, 0x7fffffffll);
       pp.trig = nullptr;
       pp.rgb = nullptr;
       pp.count_vox = 0;   // voxel_updates counts the projective updates instead
+      pp.frame_tag = 1;
+      pp.frame_base = f0;
       {
         ProfScope ps_(sm, "ray_prepare", st);
         prepare_kernel<<<blocks, 256, 0, st>>>(pp);
@@ -1134,17 +1168,19 @@ cudaError_t launch_integrate_projective(cvx_submap* sm, const float* depth, int6
       wp.tq = (int)std::llround(std::ldexp(sm->cfg.truncation, q));
       wp.q = q;
       wp.band = 0;
+      wp.birth = sm->proj_birth;
       {
         ProfScope ps_(sm, "block_walk_allocate", st);
-        if (k32) block_walk2_kernel<true><<<blocks, 256, 0, st>>>(wp);
-        else block_walk2_kernel<false><<<blocks, 256, 0, st>>>(wp);
+        if (k32) block_walk2_kernel<true, true><<<blocks, 256, 0, st>>>(wp);
+        else block_walk2_kernel<false, true><<<blocks, 256, 0, st>>>(wp);
       }
-      record_count_kernel<<<1, 1, 0, st>>>(sm->ctr, sm->proj_cnt, f, sm->pool.max_blocks);
     }
+    compose(g0, gn, sm->buf[1].frame_T);
     ProjParams pj;
-    pj.depth = depth + (long long)f0 * n_per_frame;
-    pj.frame_T = B.frame_T; pj.cnt = sm->proj_cnt; pj.pool = sm->pool; pj.ctr = sm->ctr;
-    pj.nf = nf; pj.width = sensor.width; pj.height = sensor.height;
+    pj.depth = depth + (long long)g0 * n_per_frame;
+    pj.frame_T = sm->buf[1].frame_T; pj.start = sm->proj_start; pj.birth = sm->proj_birth; pj.frame_base = g0;
+    pj.pool = sm->pool; pj.ctr = sm->ctr;
+    pj.nf = gn; pj.width = sensor.width; pj.height = sensor.height;
     pj.fx = sensor.fx; pj.fy = sensor.fy; pj.cx = sensor.cx; pj.cy = sensor.cy;
     pj.rmin = (double)sensor.min_range; pj.rmax = (double)sensor.max_range;
     pj.s = sm->cfg.voxel_size; pj.tau = sm->cfg.truncation; pj.rfloor = sm->cfg.weight_range_floor;

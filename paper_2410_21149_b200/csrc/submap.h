@@ -84,7 +84,8 @@ struct cvx_submap {
     int nb_prev = 0;                    // blocks covered by the last update
   } inc;
 
-  int* proj_cnt = nullptr;    // device [kMaxBatch]: blocks after each frame's ALLOCATE (projection mapping)
+  int* proj_birth = nullptr;  // device [max_blocks + 1]: birth frame per slot, then the block count at the
+  int* proj_start = nullptr;  //   start of the call (projection mapping; proj_start points into proj_birth)
   int* trig = nullptr;        // device {threshold, hit, consumed, -} of cvx_integrate_until
   int* trig_host = nullptr;   // pinned mirror
 
