@@ -527,6 +527,60 @@ def run_rgbd(args, world, rank, local):
         pg.destroy_process_group()
 
 
+def run_voxel_sweep(args, world, rank, local):
+    """SURVEY §2.5 E2 (Fig. 4b: "execution time ... increasing the number of voxels from
+    one to four million"): the configs[1] submap (200 scans) integrated at voxel sizes swept so the
+    allocated voxels go from ~1 M to beyond 4 M (tau = 3 s), TSDF integration timed alone and with the
+    exact ESDF.  Reports (voxels, voxel updates, ms) per size; the paper's claim is near-linear scaling."""
+    import paper_2410_21149_b200 as cvx
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    cfg, data, poses = make_workload(rank, dev)
+    rows = []
+    for s in (0.8, 0.64, 0.5, 0.4, 0.32, 0.25, 0.2):
+        g = dict(cfg["grid"], voxel_size=s, truncation=3 * s, site_threshold=s)
+        sm = cvx.Submap(g, cfg["submaps"][0]["T_world_submap"], local)
+        stream = torch.cuda.current_stream(dev)
+
+        def integ():
+            sm.reset()
+            sm.integrate_batch(data, poses, cfg["sensor"])
+
+        for _ in range(args.warmup):
+            integ()
+            sm.finalize_esdf()
+        st = sm.stats()
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        t_int = t_all = 0.0
+        for _ in range(args.steps):
+            torch.cuda.synchronize()
+            e[0].record(stream)
+            integ()
+            e[1].record(stream)
+            sm.finalize_esdf()
+            e[2].record(stream)
+            torch.cuda.synchronize()
+            t_int += e[0].elapsed_time(e[1])
+            t_all += e[0].elapsed_time(e[2])
+        rows.append({"voxel_size": s, "blocks": st["total_blocks"], "voxels": st["total_blocks"] * 512,
+                     "voxel_updates": st["voxel_updates"], "integrate_ms": t_int / args.steps,
+                     "integrate_esdf_ms": t_all / args.steps})
+        del sm
+    base = next(r for r in rows if r["voxels"] >= 0.8e6)
+    for r in rows:
+        r["voxels_rel"] = r["voxels"] / base["voxels"]
+        r["time_rel"] = r["integrate_ms"] / base["integrate_ms"]
+    line = {"metric": METRIC, "value": N_SCANS / (rows[-1]["integrate_esdf_ms"] / 1e3), "unit": "scans/s",
+            "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": rows[-1]["integrate_esdf_ms"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32+i64",
+            "data": "synthetic",
+            "config": {"workload": "voxel_sweep_lidar_submap_200scans (BJ configs[1], E2 / Fig. 4b shape)",
+                       "voxel_sizes": [r["voxel_size"] for r in rows]},
+            "sweep": rows}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 # ------------------------------------------------------------------------------------ product arm
 def main():
     ap = argparse.ArgumentParser()
@@ -538,7 +592,7 @@ def main():
     ap.add_argument("--queries", type=int, default=1 << 20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--workload", default="lidar", choices=["lidar", "esdf_stress", "incremental", "mav", "color", "rgbd"],
+    ap.add_argument("--workload", default="lidar", choices=["lidar", "esdf_stress", "incremental", "mav", "color", "rgbd", "voxel_sweep"],
                     help="lidar: configs[1] (default bench line); esdf_stress: configs[4] full ESDF recompute")
     args = ap.parse_args()
     world, rank, local = dist_setup()
@@ -558,6 +612,9 @@ def main():
         return
     if args.workload == "rgbd":
         run_rgbd(args, world, rank, local)
+        return
+    if args.workload == "voxel_sweep":
+        run_voxel_sweep(args, world, rank, local)
         return
 
     import paper_2410_21149_b200 as cvx
