@@ -48,6 +48,11 @@ struct XParams {
   double site_thr;
 };
 
+#ifndef CVX_XCH
+#define CVX_XCH 4
+#endif
+constexpr int kXCh = CVX_XCH;   // chunks (32 voxels each) whose loads a warp issues together in pass x
+
 __global__ void __launch_bounds__(128) pass_x_kernel(const __grid_constant__ XParams p) {
   extern __shared__ unsigned smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -66,28 +71,40 @@ __global__ void __launch_bounds__(128) pass_x_kernel(const __grid_constant__ XPa
     }
     const int* grow = p.grid + ((long long)(z >> 3) * p.nby + (y >> 3)) * p.nbx;
     const int lyz = 8 * (y & 7) + 64 * (z & 7);
-    // 1) sites of the row -> one 32-bit mask per chunk; E placeholder (sign of D, NaN if unobserved)
-    for (int c = 0; c < nch; ++c) {
-      const int x = (c << 5) + lane;
-      bool site = false;
-      if (x < p.nx) {
-        const int slot = grow[x >> 3];
-        if (slot >= 0) {
-          const long long vi = (long long)slot * kBlockVox + (x & 7) + lyz;
-          const longlong2 sw = reinterpret_cast<const longlong2*>(p.sums)[vi];
+    // 1) sites of the row -> one 32-bit mask per chunk; E placeholder (sign of D, NaN if unobserved).
+    //    kXCh chunks per round: their slot look-ups, then their TSDF loads, are issued back to back so
+    //    every warp keeps kXCh 512-byte requests in flight (the row loop is otherwise latency-bound).
+    for (int c0 = 0; c0 < nch; c0 += kXCh) {
+      int slot[kXCh];
+#pragma unroll
+      for (int u = 0; u < kXCh; ++u) {
+        const int x = ((c0 + u) << 5) + lane;
+        slot[u] = (c0 + u < nch && x < p.nx) ? grow[x >> 3] : -1;
+      }
+      longlong2 sw[kXCh];
+#pragma unroll
+      for (int u = 0; u < kXCh; ++u) {
+        const long long vi = (long long)slot[u] * kBlockVox + (lane & 7) + lyz;   // x & 7 == lane & 7
+        sw[u] = slot[u] >= 0 ? reinterpret_cast<const longlong2*>(p.sums)[vi] : make_longlong2(0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < kXCh; ++u) {
+        bool site = false;
+        if (slot[u] >= 0) {
+          const long long vi = (long long)slot[u] * kBlockVox + (lane & 7) + lyz;
           float ph;
-          if (sw.y > 0) {
-            const float D = (float)((double)sw.x / (double)sw.y);   // exported D (stage-isolated parity)
-            site = fabs((double)D) <= p.site_thr;                    // O10
+          if (sw[u].y > 0) {
+            const float D = (float)((double)sw[u].x / (double)sw[u].y);   // exported D (stage-isolated parity)
+            site = fabs((double)D) <= p.site_thr;                          // O10
             ph = D < 0.0f ? -0.0f : 0.0f;
           } else {
-            ph = __int_as_float(0x7fc00000);                        // unobserved -> NaN (O11)
+            ph = __int_as_float(0x7fc00000);                              // unobserved -> NaN (O11)
           }
           p.esdf[vi] = ph;
         }
+        const unsigned b = __ballot_sync(0xffffffffu, site);
+        if (lane == 0 && c0 + u < nch) msk[c0 + u] = b;
       }
-      const unsigned b = __ballot_sync(0xffffffffu, site);
-      if (lane == 0) msk[c] = b;
     }
     __syncwarp();
     // 2) nearest site strictly before / after each chunk (warp scans over groups of 32 chunks)
@@ -137,7 +154,8 @@ __global__ void __launch_bounds__(128) pass_x_kernel(const __grid_constant__ XPa
 struct LineParams {
   const void* fin;          // pass y: uint16 1-D distances; pass z: uint32 squared distances
   unsigned* gout;           // pass y output (uint32 squared distances)
-  unsigned* meta;           // per-voxel stack links {start t: hi 16, prev: lo 16}
+  void* meta;               // per pushed voxel q — pass z: u64 envelope state below q {f: hi 32, t: 16,
+                            // prev: lo 16}; pass y: u32 {t_q: hi 16, prev: lo 16}
   float* esdf;              // pass z output (ESDF blocks)
   const int* grid;
   const unsigned char* colmask;   // (bx, by) columns with allocated blocks
@@ -154,6 +172,14 @@ __device__ __forceinline__ long long floordiv(long long a, long long b) {  // b 
 // of one warp; each builds the envelope of the sites in its half and evaluates it over the whole line,
 // and the two results are combined with one shuffle per position (2x the evaluation work, 2x the
 // threads in flight for a latency-bound pass).
+#ifndef CVX_META64Y
+#define CVX_META64Y 0
+#endif
+constexpr bool kMeta64Y = CVX_META64Y;
+#ifndef CVX_EDT_LAYOUT
+#define CVX_EDT_LAYOUT 0
+#endif
+
 template <bool kZ, int kSplit>
 __global__ void __launch_bounds__(256) pass_line_kernel(const __grid_constant__ LineParams p) {
   const long long nlines = kZ ? (long long)p.nx * p.ny : (long long)p.nx * p.nz;
@@ -179,11 +205,14 @@ __global__ void __launch_bounds__(256) pass_line_kernel(const __grid_constant__ 
       return v == kNone16 ? kInfF : (long long)v * v;
     }
   };
-  // forward: build the envelope (Meijster phase 2 with a linked stack) of the sites in [qa, qb).  The
-  // line is read in chunks of 8 independent loads so each thread keeps 8 requests in flight.
   const int qa = kSplit == 2 ? half * (m >> 1) : 0, qb = kSplit == 2 ? qa + (m >> 1) : m;
   int top = -1, t_top = 0;
   long long f_top = 0;
+  // Stack links.  Pass z stores with every pushed q the full state of the element below it, so a pop
+  // is ONE load; pass y (u16 input, re-read cheaply) keeps 4-byte links {t_q, prev} and re-reads f —
+  // measured: the 8-byte form costs pass y more in bytes than it saves in latency, pass z the opposite.
+  // forward: build the envelope (Meijster phase 2 with a linked stack) of the sites in [qa, qb).  The
+  // line is read in chunks of 8 independent loads so each thread keeps 8 requests in flight.
   for (int q0 = qa; q0 < qb; q0 += 8) {
     long long fv[8];
 #pragma unroll
@@ -196,12 +225,19 @@ __global__ void __launch_bounds__(256) pass_line_kernel(const __grid_constant__ 
       while (top >= 0) {
         const long long a = (long long)(t_top - top), b = (long long)(t_top - q);
         if (a * a + f_top > b * b + fq) {                 // q beats top already at top's start: pop
-          const unsigned mt = p.meta[base + (long long)top * stride];
-          const int pr = (int)(mt & 0xffffu);
-          if (pr == 0xffff) { top = -1; break; }
-          top = pr;
-          t_top = (int)(p.meta[base + (long long)top * stride] >> 16);
-          f_top = f_at(top);
+          if constexpr (kZ || kMeta64Y) {   // one load restores the whole state below top
+            const unsigned long long mt = static_cast<const unsigned long long*>(p.meta)[base + (long long)top * stride];
+            const int pr = (int)(mt & 0xffffu);
+            if (pr == 0xffff) { top = -1; break; }
+            top = pr; t_top = (int)((mt >> 16) & 0xffffu); f_top = (long long)(mt >> 32);
+          } else {
+            const unsigned mt = static_cast<const unsigned*>(p.meta)[base + (long long)top * stride];
+            const int pr = (int)(mt & 0xffffu);
+            if (pr == 0xffff) { top = -1; break; }
+            top = pr;
+            t_top = (int)(static_cast<const unsigned*>(p.meta)[base + (long long)top * stride] >> 16);
+            f_top = f_at(top);
+          }
         } else {
           break;
         }
@@ -215,7 +251,12 @@ __global__ void __launch_bounds__(256) pass_line_kernel(const __grid_constant__ 
         if (sep + 1 >= m) continue;                             // q never wins inside the line
         tq = (int)(sep + 1);
       }
-      p.meta[base + (long long)q * stride] = ((unsigned)tq << 16) | (unsigned)(top < 0 ? 0xffff : top);
+      if constexpr (kZ || kMeta64Y)
+        static_cast<unsigned long long*>(p.meta)[base + (long long)q * stride] = top < 0 ? 0xffffull
+            : ((unsigned long long)f_top << 32) | ((unsigned long long)t_top << 16) | (unsigned long long)top;
+      else
+        static_cast<unsigned*>(p.meta)[base + (long long)q * stride] =
+            ((unsigned)tq << 16) | (unsigned)(top < 0 ? 0xffff : top);
       top = q; t_top = tq; f_top = fq;
     }
   }
@@ -250,9 +291,17 @@ __global__ void __launch_bounds__(256) pass_line_kernel(const __grid_constant__ 
         p.esdf[(long long)slot * kBlockVox + (x & 7) + 8 * (o2 & 7) + 64 * u] = e;
       }
       if (top >= 0 && q == t_top) {
-        const int pr = (int)(p.meta[base + (long long)top * stride] & 0xffffu);
-        if (pr == 0xffff) { top = -1; }
-        else { top = pr; t_top = (int)(p.meta[base + (long long)top * stride] >> 16); f_top = f_at(top); }
+        if constexpr (kZ || kMeta64Y) {
+          const unsigned long long mt = static_cast<const unsigned long long*>(p.meta)[base + (long long)top * stride];
+          const int pr = (int)(mt & 0xffffu);
+          if (pr == 0xffff) { top = -1; }
+          else { top = pr; t_top = (int)((mt >> 16) & 0xffffu); f_top = (long long)(mt >> 32); }
+        } else {
+          const unsigned* mm = static_cast<const unsigned*>(p.meta);
+          const int pr = (int)(mm[base + (long long)top * stride] & 0xffffu);
+          if (pr == 0xffff) { top = -1; }
+          else { top = pr; t_top = (int)(mm[base + (long long)top * stride] >> 16); f_top = f_at(top); }
+        }
       }
     }
   }
@@ -273,18 +322,24 @@ cudaError_t launch_finalize(cvx_submap* sm, int n_blocks, const int lo[3], const
     if ((e = cudaMalloc(&sm->block_grid, sizeof(int) * (size_t)nblk)) != cudaSuccess) return e;
     sm->block_grid_cap = nblk;
   }
-  const long long need = nvox * (2 + 4 + 4) + (long long)nbx * nby + (long long)nby * nbz + 256;
+  const long long need = nvox * (2 + 4 + 8) + (long long)nbx * nby + (long long)nby * nbz + 256;
   if (sm->edt_bytes < need) {
     if (sm->edt) cudaFree(sm->edt);
     sm->edt = nullptr; sm->edt_bytes = 0;
     if ((e = cudaMalloc(&sm->edt, (size_t)need)) != cudaSuccess) return e;
     sm->edt_bytes = need;
   }
+#if CVX_EDT_LAYOUT == 0
   unsigned* g2 = reinterpret_cast<unsigned*>(sm->edt);
-  unsigned* meta = g2 + nvox;
+  unsigned long long* meta = reinterpret_cast<unsigned long long*>(g2 + nvox);   // nvox % 512 == 0: aligned
   unsigned short* g1 = reinterpret_cast<unsigned short*>(meta + nvox);
-
   unsigned char* colmask = reinterpret_cast<unsigned char*>(g1 + nvox);
+#else
+  unsigned short* g1 = reinterpret_cast<unsigned short*>(sm->edt);
+  unsigned* g2 = reinterpret_cast<unsigned*>(g1 + nvox);
+  unsigned long long* meta = reinterpret_cast<unsigned long long*>(g2 + nvox);
+  unsigned char* colmask = reinterpret_cast<unsigned char*>(meta + nvox);
+#endif
   cudaMemsetAsync(sm->block_grid, 0xff, sizeof(int) * (size_t)nblk, st);
   unsigned char* rowmask = colmask + (size_t)nbx * nby;
   cudaMemsetAsync(colmask, 0, (size_t)nbx * nby + (size_t)nby * nbz, st);

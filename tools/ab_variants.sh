@@ -8,13 +8,16 @@ for r in $(seq $R); do
     cp variants/libcvx_$v.so paper_2410_21149_b200/libcvx.so
     touch paper_2410_21149_b200/libcvx.so
     out=$(CVX_NO_BUILD=1 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e ${BENCH_ARGS} 2>&1 | tail -1)
-    python - "$v" "$out" <<'PY'
+    KEYS="${KEYS}" python - "$v" "$out" <<'PY'
 import json, sys
 v, line = sys.argv[1], sys.argv[2]
 try:
     d = json.loads(line)
     k = d.get("kernel_ms_per_step", {})
-    print(f"{v:10s} step {d['ms_per_step']:.3f} ms  walk {k.get('ray_walk_update', 0):.3f}  bw {k.get('block_walk_allocate', 0):.3f}  prep {k.get('ray_prepare', 0):.3f}", flush=True)
+    import os, re
+    keys = os.environ.get("KEYS", "ray_walk_update|block_walk_allocate|ray_prepare")
+    ks = "  ".join(f"{n} {t:.3f}" for n, t in k.items() if re.search(keys, n))
+    print(f"{v:10s} step {d['ms_per_step']:.3f} ms  {ks}", flush=True)
 except Exception as e:
     print(v, "ERR", line[-300:])
 PY
