@@ -66,6 +66,7 @@ def lib():
             L.orc_integrate_color.restype = C.c_int32
             L.orc_integrate_color.argtypes = [P, P, P, C.c_int64, P, C.POINTER(Sensor), C.POINTER(Stats)]
             L.orc_export_color.argtypes = [P, P, P]
+            L.orc_project_voxels.argtypes = [C.POINTER(Grid), P, P, C.c_int32, P, C.POINTER(Sensor), P, C.c_int64, P, P]
             L.orc_integrate_projective.restype = C.c_int32
             L.orc_integrate_projective.argtypes = [P, P, C.c_int64, P, C.POINTER(Sensor), C.POINTER(Stats)]
             L.orc_num_blocks.restype = C.c_int64
@@ -175,6 +176,22 @@ class OracleSubmap:
         if nb:
             lib().orc_export(self._h, _p(b), _p(D), _p(W))
         return b, D, W
+
+
+def project_voxels(grid: dict, T_world_submap, depth, T_world_sensor, sensor: dict, voxels):
+    """Projective sums (swd, sw) fp64 [m] of listed voxels [m,3] over all frames (R14 step 2 per voxel;
+    for voxels whose block exists from the first frame on)."""
+    g = grid_struct(grid)
+    Tws = np.ascontiguousarray(T_world_submap, dtype=np.float64)
+    d = np.ascontiguousarray(np.asarray(depth, dtype=np.float32))
+    T = np.ascontiguousarray(np.asarray(T_world_sensor, dtype=np.float64).reshape(-1, 16))
+    v = np.ascontiguousarray(voxels, dtype=np.int32)
+    m = v.shape[0]
+    swd = np.zeros(m)
+    sw = np.zeros(m)
+    lib().orc_project_voxels(C.byref(g), _p(Tws), _p(d), T.shape[0], _p(T), C.byref(sensor_struct(sensor)), _p(v), m,
+                             _p(swd), _p(sw))
+    return swd, sw
 
 
 def ray_voxels(o, p, voxel_size: float, truncation: float, carve: int = 1) -> np.ndarray:

@@ -315,39 +315,62 @@ void orc_export_color(void* h, double* rgb, double* cw) {
 //      sdf = m - z (projective distance along the optical axis); skipped if sdf < -tau (occluded) and,
 //      in band mode (carve = 0), if sdf > tau; d = min(sdf, tau); w = O6 with the pixel's L;
 //      swd += w d, sw += w.
+// Step 2 for one voxel v (integer voxel coordinates): adds its projective update, if any, to (swd, sw).
+static bool project_voxel(const orc_grid& g, const float* depth, const orc_sensor* sm, const double R[3][3],
+                          const double t[3], const int64_t v[3], double* swd, double* sw) {
+  const double sv = g.voxel_size, tau = g.truncation;
+  double e[3], x[3];
+  for (int k = 0; k < 3; ++k) e[k] = ((double)v[k] + 0.5) * sv - t[k];
+  for (int i = 0; i < 3; ++i) x[i] = (R[0][i] * e[0] + R[1][i] * e[1]) + R[2][i] * e[2];
+  const double z = x[2];
+  if (!(z > 0.0)) return false;
+  const double inv = 1.0 / z;
+  const double uh = ((double)sm->fx * x[0]) * inv + (double)sm->cx + 0.5;
+  const double wh = ((double)sm->fy * x[1]) * inv + (double)sm->cy + 0.5;
+  if (!(uh >= 0.0 && uh < (double)sm->width && wh >= 0.0 && wh < (double)sm->height)) return false;
+  const int64_t px = (int64_t)std::floor(uh), py = (int64_t)std::floor(wh);
+  const float m = depth[py * sm->width + px];
+  if (!(m > 0.0f) || !std::isfinite(m)) return false;
+  const float pu = (float)px, pv = (float)py;   // O2 point of that pixel, fp32 as written
+  const double pc[3] = {(double)((m * (pu - sm->cx)) / sm->fx), (double)((m * (pv - sm->cy)) / sm->fy), (double)m};
+  const double L = std::sqrt((pc[0] * pc[0] + pc[1] * pc[1]) + pc[2] * pc[2]);
+  if (!(L >= (double)sm->min_range && L <= (double)sm->max_range)) return false;
+  const double sdf = (double)m - z;
+  if (sdf < -tau) return false;
+  if (!g.carve && sdf > tau) return false;
+  const double d = std::min(sdf, tau);
+  double w = 1.0;
+  if (g.weighting != 0) { const double r = std::max(L, g.weight_range_floor); w = 1.0 / (r * r); }
+  *swd += w * d;
+  *sw += w;
+  return true;
+}
+
 static void project_frame(Oracle* O, const float* depth, const orc_sensor* sm, const double R[3][3],
                           const double t[3], int64_t* n_updates) {
-  const orc_grid& g = O->g;
-  const double sv = g.voxel_size, tau = g.truncation;
   for (auto& kv : O->blocks) {
     Block* b = kv.second;
     for (int l = 0; l < kBV; ++l) {
       const int64_t v[3] = {kv.first.x * kB + l % 8, kv.first.y * kB + (l / 8) % 8, kv.first.z * kB + l / 64};
-      double e[3], x[3];
-      for (int k = 0; k < 3; ++k) e[k] = ((double)v[k] + 0.5) * sv - t[k];
-      for (int i = 0; i < 3; ++i) x[i] = (R[0][i] * e[0] + R[1][i] * e[1]) + R[2][i] * e[2];
-      const double z = x[2];
-      if (!(z > 0.0)) continue;
-      const double inv = 1.0 / z;
-      const double uh = ((double)sm->fx * x[0]) * inv + (double)sm->cx + 0.5;
-      const double wh = ((double)sm->fy * x[1]) * inv + (double)sm->cy + 0.5;
-      if (!(uh >= 0.0 && uh < (double)sm->width && wh >= 0.0 && wh < (double)sm->height)) continue;
-      const int64_t px = (int64_t)std::floor(uh), py = (int64_t)std::floor(wh);
-      const float m = depth[py * sm->width + px];
-      if (!(m > 0.0f) || !std::isfinite(m)) continue;
-      const float pu = (float)px, pv = (float)py;   // O2 point of that pixel, fp32 as written
-      const double pc[3] = {(double)((m * (pu - sm->cx)) / sm->fx), (double)((m * (pv - sm->cy)) / sm->fy), (double)m};
-      const double L = std::sqrt((pc[0] * pc[0] + pc[1] * pc[1]) + pc[2] * pc[2]);
-      if (!(L >= (double)sm->min_range && L <= (double)sm->max_range)) continue;
-      const double sdf = (double)m - z;
-      if (sdf < -tau) continue;
-      if (!g.carve && sdf > tau) continue;
-      const double d = std::min(sdf, tau);
-      double w = 1.0;
-      if (g.weighting != 0) { const double r = std::max(L, g.weight_range_floor); w = 1.0 / (r * r); }
-      b->swd[l] += w * d;
-      b->sw[l] += w;
-      ++*n_updates;
+      if (project_voxel(O->g, depth, sm, R, t, v, &b->swd[l], &b->sw[l])) ++*n_updates;
+    }
+  }
+}
+
+// Sampled check hook: the projective sums of m listed voxels (int32 [m][3]) over n_frames depth frames
+// ([n_frames][h][w], poses [n_frames][16]) of a submap with pose T_world_submap, every voxel taking every
+// frame (valid for voxels whose block exists from the first frame on).  swd, sw: fp64 [m].
+void orc_project_voxels(const orc_grid* g, const double* T_world_submap, const float* depth, int32_t n_frames,
+                        const double* T_world_sensor, const orc_sensor* sm, const int32_t* vox, int64_t m,
+                        double* swd, double* sw) {
+  for (int64_t i = 0; i < m; ++i) swd[i] = sw[i] = 0.0;
+  const int64_t npix = (int64_t)sm->width * sm->height;
+  for (int32_t f = 0; f < n_frames; ++f) {
+    double R[3][3], t[3];
+    compose_sc(T_world_submap, T_world_sensor + 16 * f, R, t);
+    for (int64_t i = 0; i < m; ++i) {
+      const int64_t v[3] = {vox[3 * i], vox[3 * i + 1], vox[3 * i + 2]};
+      project_voxel(*g, depth + f * npix, sm, R, t, v, &swd[i], &sw[i]);
     }
   }
 }

@@ -199,3 +199,27 @@ def test_band_mode_and_range_filter(orc):
     far = orc.OracleSubmap(_grid())
     st = far.integrate_projective(depth, T, dict(CAM, max_range=1.5))
     assert st["skipped_range"] == 64 * 48 and far.num_blocks() == 0 and st["voxel_updates"] == 0
+
+
+def test_project_voxels_hook_matches_integration(orc):
+    # the sampled-check hook (per-voxel sums over all frames) equals whole-submap integration for voxels
+    # whose block exists from the first frame on
+    cfg = synth.make_config("tiny", frames=[0, 3, 6])
+    fr = [cfg["frames"][k] for k in (0, 3, 6)]
+    first = orc.OracleSubmap(cfg["grid"])
+    first.integrate_projective(fr[0]["data"].numpy(), fr[0]["T_world_sensor"], cfg["sensor"])
+    b0, _, _ = first.export()
+    full = orc.OracleSubmap(cfg["grid"])
+    for f in fr:
+        full.integrate_projective(f["data"].numpy(), f["T_world_sensor"], cfg["sensor"])
+    b, D, W = full.export()
+    keep = np.array([any((bb == x).all() for x in b0) for bb in b])
+    l = np.arange(512)
+    vox = np.concatenate([np.stack([8 * bb[0] + l % 8, 8 * bb[1] + (l // 8) % 8, 8 * bb[2] + l // 64], 1) for bb in b[keep]])
+    depth = np.stack([f["data"].numpy() for f in fr])
+    poses = np.stack([f["T_world_sensor"] for f in fr])
+    swd, sw = orc.project_voxels(cfg["grid"], np.eye(4), depth, poses, cfg["sensor"], vox)
+    assert np.array_equal(sw, W[keep].reshape(-1))
+    obs = sw > 0
+    assert obs.sum() > 1000
+    assert np.allclose(swd[obs] / sw[obs], D[keep].reshape(-1)[obs], atol=1e-12)
