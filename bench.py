@@ -176,14 +176,17 @@ NCU_FILES = {"ray_walk_update": "ncu_walk.txt", "block_walk_allocate": "ncu_bloc
              "esdf_pass_y": "ncu_esdf_pass_y.txt", "esdf_pass_z": "ncu_esdf_pass_z.txt", "fold": "ncu_fold.txt"}
 
 
-def ncu_traffic(kernel):
+def ncu_traffic(kernel, workload="lidar"):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from the newest committed
-    `ncu --set full` capture under profiles/ (None if there is none)."""
+    `ncu --set full` capture of that workload under profiles/ (None if there is none)."""
     prof = os.path.join(ROOT, "profiles")
     if kernel not in NCU_FILES or not os.path.isdir(prof):
         return None
+    name = NCU_FILES[kernel]
+    if workload == "esdf_stress":
+        name = name.replace("ncu_esdf_", "ncu_stress_")
     for tag in sorted(os.listdir(prof), reverse=True):
-        f = os.path.join(prof, tag, NCU_FILES[kernel])
+        f = os.path.join(prof, tag, name)
         if not os.path.exists(f):
             continue
         tot = 0.0
@@ -192,7 +195,7 @@ def ncu_traffic(kernel):
             if parts and parts[0] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
                 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(parts[1], 1)
                 tot += float(parts[2]) * scale
-        return {"bytes_per_launch": tot, "source": f"profiles/{tag}/{NCU_FILES[kernel]}"}
+        return {"bytes_per_launch": tot, "source": f"profiles/{tag}/{name}"}
     return None
 
 
@@ -220,17 +223,32 @@ def run_mav(args, world, rank, local):
     data = {i: torch.stack([cfgf["frames"][k]["data"] for k in subs[i]["frames"]]).contiguous() for i in mine}
     poses = {i: np.stack([cfgf["frames"][k]["T_world_sensor"] for k in subs[i]["frames"]]) for i in mine}
     grid = cfg["grid"]
-    builders = [cvx.Submap(grid, subs[i]["T_world_submap"], local) for i in mine[:1]]
-    sm = builders[0] if builders else None
+    # two builders on two streams: the exact ESDF of submap j overlaps the integration of submap j+1
+    # (the packed result of submap j is taken after submap j+1's integration has been enqueued)
+    builders = [cvx.Submap(grid, subs[i]["T_world_submap"], local) for i in mine[:2]]
     stream = torch.cuda.current_stream(dev)
+    streams = [stream, torch.cuda.Stream(dev)]
 
     def step():
         payloads = []
-        for i in mine:
-            sm.reset(subs[i]["T_world_submap"])
-            sm.integrate_batch(data[i], poses[i], cfg["sensor"])
-            sm.finalize_esdf()
-            payloads.append(sm.pack().clone())
+        pending = None
+
+        def take(k):
+            with torch.cuda.stream(streams[k]):
+                payloads.append(builders[k].pack().clone())
+
+        for j, i in enumerate(mine):
+            k = j % 2
+            with torch.cuda.stream(streams[k]):
+                builders[k].reset(subs[i]["T_world_submap"])
+                builders[k].integrate_batch(data[i], poses[i], cfg["sensor"])
+                builders[k].finalize_esdf()
+            if pending is not None:
+                take(pending)
+            pending = k
+        if pending is not None:
+            take(pending)
+        stream.wait_stream(streams[1])
         if pg is not None:
             blob = torch.cat(payloads) if payloads else torch.zeros(0, dtype=torch.uint8, device=dev)
             gather_packed(blob)
@@ -244,6 +262,7 @@ def run_mav(args, world, rank, local):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         e0.record(stream)
+        streams[1].wait_stream(stream)
         for _ in range(args.steps):
             step()
         e1.record(stream)
@@ -259,7 +278,8 @@ def run_mav(args, world, rank, local):
             "scaling": "strong", "vs_baseline": None, "dtype": "f32+i64", "data": "synthetic",
             "config": {"workload": "mav_400m_flight_2000scans_40submaps_0.2m (BJ configs[3])",
                        "submaps": len(subs), "submaps_per_rank_max": max(len(x) for x in shard_submaps([1] * len(subs), world)),
-                       "parallelism": f"submap-sharded x{world} (LPT)"},
+                       "parallelism": f"submap-sharded x{world} (LPT)",
+                       "pipeline": "2 submaps in flight (ESDF of submap j overlaps integration of submap j+1)"},
             "clocks": clk.summary()}
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -434,11 +454,36 @@ def run_esdf_stress(args, world, rank, local):
                                             "blocks": nb, "allocated_voxels": va, "aabb_voxels": dims.tolist()},
             "dense_gvox_per_s": N / 1e9 / (ms / 1e3), "kernel_ms_per_step": per,
             "roofline": {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
-                         "frac": ach / hbm, "traffic": ncu_traffic(dom), "peak_source": hbm_src,
+                         "frac": ach / hbm, "traffic": ncu_traffic(dom, "esdf_stress"), "peak_source": hbm_src,
                          "all_passes_gbs": tot_alg},
             "gpu_launches": sum(v["n"] for v in prof.values()), "clocks": clk.summary()}
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def rgbd_cpu_baseline(cfg, sub, depth, poses, n=2):
+    """The oracle as it stands, single-threaded, on the first n frames of one configs[2] submap with each
+    integrator, plus the exact ESDF of the raycast result."""
+    import oracle
+    g = cfg["grid"]
+    frames = [depth[k].cpu().numpy() for k in range(n)]
+    out = {}
+    for mode in ("raycast", "projective"):
+        o = oracle.OracleSubmap(g, sub["T_world_submap"])
+        t0 = time.perf_counter()
+        for k in range(n):
+            (o.integrate if mode == "raycast" else o.integrate_projective)(frames[k], poses[k], cfg["sensor"])
+        out[mode] = time.perf_counter() - t0
+        if mode == "raycast":
+            b, D, W = o.export()
+            t1 = time.perf_counter()
+            oracle.esdf(b, D, W, g["voxel_size"], g["site_threshold"])
+            out["esdf"] = time.perf_counter() - t1
+    return {"value": n / (out["raycast"] + out["esdf"]), "unit": "scans/s", "cores": 1, "kind": "oracle",
+            "sample": f"first {n} of the 100 frames of submap 0, raycast integration + exact ESDF "
+                      f"({b.shape[0]} blocks); projection integration of the same frames timed beside it",
+            "raycast_frames_per_s": n / out["raycast"], "projective_frames_per_s": n / out["projective"],
+            "seconds": out["raycast"] + out["esdf"] + out["projective"]}
 
 
 def run_rgbd(args, world, rank, local):
@@ -520,6 +565,8 @@ def run_rgbd(args, world, rank, local):
                            "voxel_updates_rank0": res["projective"][2], "kernel_ms_per_step_serial": res["projective"][3]},
             "raycast_over_projective_time": ms / res["projective"][0],
             "clocks": clk}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and mine:
+        line["cpu_baseline"] = rgbd_cpu_baseline(cfg, subs[mine[0]], data[mine[0]], poses[mine[0]])
     if rank == 0:
         print(json.dumps(line), flush=True)
     if pg is not None:
@@ -651,24 +698,49 @@ def main():
     qst = torch.empty(args.queries, dtype=torch.uint8, device=dev)
     gather_bytes = [0]
 
-    def gather():
+    def gather(m):
         if pg is None:
             return
         from paper_2410_21149_b200.parallel import gather_packed
-        parts = gather_packed(sm.pack())
+        parts = gather_packed(m.pack())
         gather_bytes[0] = sum(p.numel() for p in parts)
 
-    def step(src=None):
-        sm.reset()
-        d = data if src is None else src
-        for c in range(0, N_SCANS, args.batch):
-            sm.integrate_batch(d[c:c + args.batch], poses[c:c + args.batch], sensor)
-        sm.finalize_esdf()
-        sm.query(queries, qout, qst)
-        gather()
+    # Two submaps in flight (the paper's frontend/backend queues): step i builds submap i on builder i % 2
+    # and its own stream, so the exact ESDF + queries of step i (HBM / latency bound) overlap the
+    # integration of step i + 1 (ALU bound).  Every step is still one complete pass of a1-a7 over its own
+    # submap; `one_submap_in_flight` below times the same steps strictly one after another.
+    sm2 = cvx.Submap(cfg["grid"], cfg["submaps"][0]["T_world_submap"], local)
+    builders = [sm, sm2]
+    streams = [stream, torch.cuda.Stream(dev)]
+    qouts = [(qout, qst), (torch.empty_like(qout), torch.empty_like(qst))]
 
-    for _ in range(args.warmup):
-        step()
+    def step(i=0, src=None, pipelined=True):
+        k = i % 2 if pipelined else 0
+        m = builders[k]
+        with torch.cuda.stream(streams[k]):
+            m.reset()
+            d = data if src is None else src
+            for c in range(0, N_SCANS, args.batch):
+                m.integrate_batch(d[c:c + args.batch], poses[c:c + args.batch], sensor)
+            m.finalize_esdf()
+            m.query(queries, *qouts[k])
+            gather(m)
+
+    def timed(fn, n):
+        """Device time of n steps: events on the caller's stream, both builder streams joined."""
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record(stream)
+        streams[1].wait_stream(stream)
+        for i in range(n):
+            fn(i)
+        stream.wait_stream(streams[1])
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b)
+
+    for i in range(args.warmup):
+        step(i)
     torch.cuda.synchronize()
     st = sm.stats()
     nb = sm.block_count()
@@ -677,27 +749,26 @@ def main():
     nvox_dense = int(np.prod(dims.astype(np.int64)))
 
     # ---------------------------------------------------------------- timed region (device time)
-    sm.profile(True)
+    for m in builders:
+        m.profile(True)
     if pg is not None:
         pg.barrier()
-    torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
-        e0.record(stream)
-        for _ in range(args.steps):
-            step()
-        e1.record(stream)
-        torch.cuda.synchronize()
+        ms_total = timed(step, args.steps)
     if pg is not None:
         pg.barrier()
-    ms_total = e0.elapsed_time(e1)
-    prof = sm.profile_report()
-    sm.profile(False)
+    prof = {}
+    for m in builders:
+        for k_, v_ in m.profile_report().items():
+            e_ = prof.setdefault(k_, {"ms": 0.0, "n": 0})
+            e_["ms"] += v_["ms"]
+            e_["n"] += v_["n"]
+        m.profile(False)
+    ms_one = timed(lambda i: step(i, pipelined=False), args.steps)   # one submap in flight, for reference
     if pg is not None:
-        t = torch.tensor([ms_total], device=dev, dtype=torch.float64)
+        t = torch.tensor([ms_total, ms_one], device=dev, dtype=torch.float64)
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
-        ms_total = float(t.item())
+        ms_total, ms_one = float(t[0].item()), float(t[1].item())
     ms_step = ms_total / args.steps
     value = world * N_SCANS / (ms_step / 1e3)
 
@@ -705,36 +776,32 @@ def main():
     e2e = None
     if not args.no_e2e:
         host_frames = data.cpu().pin_memory()
-        host_out = torch.empty(args.queries, dtype=torch.float32).pin_memory()
-        host_st = torch.empty(args.queries, dtype=torch.uint8).pin_memory()
+        host_outs = [(torch.empty(args.queries, dtype=torch.float32).pin_memory(),
+                      torch.empty(args.queries, dtype=torch.uint8).pin_memory()) for _ in range(2)]
         host_q = queries.cpu().pin_memory()
-        dev_q = torch.empty_like(queries)
+        dev_qs = [torch.empty_like(queries) for _ in range(2)]
 
-        def e2e_step():
+        def e2e_step(i):
             # the library copies each launch's scans from pinned host memory on its side stream, so the
             # transfer of launch k+1 overlaps the walk of launch k (cvx_integrate_batch_host)
-            dev_q.copy_(host_q, non_blocking=True)
-            sm.reset()
-            for c in range(0, N_SCANS, args.batch):
-                sm.integrate_batch_host(host_frames[c:c + args.batch], poses[c:c + args.batch], sensor)
-            sm.finalize_esdf()
-            sm.query(dev_q, qout, qst)
-            gather()
-            host_out.copy_(qout, non_blocking=True)
-            host_st.copy_(qst, non_blocking=True)
+            k = i % 2
+            m = builders[k]
+            with torch.cuda.stream(streams[k]):
+                dev_qs[k].copy_(host_q, non_blocking=True)
+                m.reset()
+                for c in range(0, N_SCANS, args.batch):
+                    m.integrate_batch_host(host_frames[c:c + args.batch], poses[c:c + args.batch], sensor)
+                m.finalize_esdf()
+                m.query(dev_qs[k], *qouts[k])
+                gather(m)
+                host_outs[k][0].copy_(qouts[k][0], non_blocking=True)
+                host_outs[k][1].copy_(qouts[k][1], non_blocking=True)
 
-        e2e_step()
+        e2e_step(0)
+        e2e_step(1)
         if pg is not None:
             pg.barrier()
-        torch.cuda.synchronize()
-        a0 = torch.cuda.Event(enable_timing=True)
-        a1 = torch.cuda.Event(enable_timing=True)
-        a0.record(stream)
-        for _ in range(args.steps):
-            e2e_step()
-        a1.record(stream)
-        torch.cuda.synchronize()
-        ems = a0.elapsed_time(a1)
+        ems = timed(e2e_step, args.steps)
         if pg is not None:
             t = torch.tensor([ems], device=dev, dtype=torch.float64)
             pg.all_reduce(t, op=pg.ReduceOp.MAX)
@@ -751,7 +818,7 @@ def main():
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s0.record(stream)
     for _ in range(2):
-        step()
+        step(pipelined=False)
     s1.record(stream)
     torch.cuda.synchronize()
     serial_ms = s0.elapsed_time(s1) / 2
@@ -807,13 +874,16 @@ def main():
                    "batch_scans": args.batch, "queries": args.queries, "voxel_size": s,
                    "truncation": cfg["grid"]["truncation"], "inputs_exceed_l2": True,
                    "l2_note": "157 MB of scans resident in HBM > 126 MB L2; no explicit flush",
-                   "parallelism": f"submap-sharded x{world}"},
+                   "parallelism": f"submap-sharded x{world}",
+                   "pipeline": "2 submaps in flight (ESDF + queries of step i overlap integration of step i+1)"},
         "esdf_mvox_per_s": va / 1e6 / (esdf_ms / 1e3) if esdf_ms else None,
         "esdf_dense_mvox_per_s": nvox_dense / 1e6 / (esdf_ms / 1e3) if esdf_ms else None,
         "tsdf_scans_per_s_kernels": N_SCANS / (integ_ms / 1e3) if integ_ms else None,
         "voxel_updates_per_step": updates_per_step, "blocks": nb, "aabb_voxels": dims.tolist(),
         "kernel_ms_per_step": per_step,
         "kernel_ms_per_step_serial": per_step_serial, "serial_ms_per_step": serial_ms,
+        "one_submap_in_flight": {"ms_per_step": ms_one / args.steps,
+                                 "value": world * N_SCANS / (ms_one / args.steps / 1e3)},
         "roofline": roofline,
         "gpu_launches": launches,
         "clocks": clk.summary(),

@@ -453,6 +453,9 @@ __global__ void __launch_bounds__(256) block_walk2_kernel(const __grid_constant_
 // E_ij > 0  <=>  H_ij = F_ij - floor(-C_ij / 2^16) > 0; H_ij moves by a_j / -a_i per step like E_ij by
 // 2^16 a_j / -2^16 a_i, and |H_ij| <= 3 max(a) while both axes have crossings left.  Exact whenever
 // every |D_a| < 2^28 (spans < 2^12 voxels), which the launch checks from the sensor's max range.
+#ifndef CVX_VAL2
+#define CVX_VAL2 0
+#endif
 #ifndef CVX_V_MINB
 #define CVX_V_MINB 8
 #endif
@@ -703,7 +706,12 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
       const unsigned stops = __ballot_sync(0xffffffffu, head | !upd);
       const unsigned above = stops & (0xfffffffeu << lane);
       const unsigned len = (unsigned)__clz(__brev(above)) - (unsigned)lane;
+#if CVX_VAL2
+      // len * (2^40 | dpi) as two 32-bit halves: hi = len << 8, lo = len * dpi (< 2^22, no carry)
+      const unsigned long long val = ((unsigned long long)(len << (kCntShift - 32)) << 32) | (len * (unsigned)dpi);
+#else
       const unsigned long long val = (unsigned long long)len * ((1ull << kCntShift) | (unsigned long long)dpi);
+#endif
       asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.relaxed.gpu.global.add.u64 [%0], %1;\n\t}"
                    :: "l"(acc + addr), "l"(val), "r"((unsigned)head) : "memory");
     }

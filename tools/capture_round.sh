@@ -7,6 +7,10 @@ cap() {  # <regex on the base function name> <name> <skip>
   timeout 900 ncu --set full --clock-control none --import-source on -k "regex:$1" -s $3 -c 1 -o gpurun_out/$T/$2 \
     python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > gpurun_out/$T/$2.log 2>&1; echo "ncu $2 rc=$?"
 }
+capw() {  # <regex> <name> <skip> <workload>: as cap, on another bench workload
+  timeout 900 ncu --set full --clock-control none --import-source on -k "regex:$1" -s $3 -c 1 -o gpurun_out/$T/$2 \
+    python bench.py --workload $4 --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/$T/$2.log 2>&1; echo "ncu $2 rc=$?"
+}
 WHAT=${@:-bench launches walk block_walk prepare fold esdf_pass_x esdf_pass_y esdf_pass_z query}
 for w in $WHAT; do case $w in
   bench) timeout 600 python bench.py > gpurun_out/$T/bench.json 2> gpurun_out/$T/bench.err; echo "bench rc=$?";;
@@ -21,4 +25,10 @@ for w in $WHAT; do case $w in
   esdf_pass_y) cap "^pass_line_kernel" esdf_pass_y 2;;
   esdf_pass_z) cap "^pass_line_kernel" esdf_pass_z 3;;
   query) cap "^query_kernel" query 0;;
+  project) capw "^project_kernel" project 2 rgbd;;
+  stress_x) capw "^pass_x_kernel" stress_pass_x 0 esdf_stress;;
+  stress_y) capw "^pass_line_kernel" stress_pass_y 0 esdf_stress;;
+  stress_z) capw "^pass_line_kernel" stress_pass_z 1 esdf_stress;;
+  rgbd) timeout 900 python bench.py --workload rgbd --steps 5 > gpurun_out/$T/bench_rgbd.json 2> gpurun_out/$T/bench_rgbd.err; echo "rgbd rc=$?";;
+  stress) timeout 900 python bench.py --workload esdf_stress --steps 5 > gpurun_out/$T/bench_esdf_stress.json 2> gpurun_out/$T/bench_esdf_stress.err; echo "stress rc=$?";;
 esac; done

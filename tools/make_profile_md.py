@@ -16,7 +16,8 @@ json.dump(bench, open(os.path.join(dst, "bench.json"), "w"), indent=1)
 shutil.copy(os.path.join(src, "launches.csv"), os.path.join(dst, "launches.csv"))
 shares = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "launch_shares.py"), os.path.join(src, "launches.csv"),
                          os.path.join(src, "bench.json")], capture_output=True, text=True).stdout
-kern = ["walk", "block_walk", "prepare", "fold", "esdf_pass_x", "esdf_pass_y", "esdf_pass_z", "query"]
+kern = ["walk", "block_walk", "prepare", "fold", "esdf_pass_x", "esdf_pass_y", "esdf_pass_z", "query", "project",
+        "stress_pass_x", "stress_pass_y", "stress_pass_z"]
 summ = {}
 for k in kern:
     rep = os.path.join(src, k + ".ncu-rep")
@@ -36,11 +37,18 @@ def metric(txt, name):
     return "-"
 
 
+def unit(txt, name):
+    for line in txt.splitlines():
+        if line.startswith(name):
+            return line.split()[1]
+    return ""
+
+
 rows = []
 for k, t in summ.items():
     rows.append(f"| {k} | {metric(t, 'Duration')} {'ms' if 'Duration                                 ms' in t else 'us'} | "
                 f"{metric(t, 'DRAM Throughput')} % | {metric(t, 'Issue Slots Busy')} % | {metric(t, 'Avg. Active Threads Per Warp')} | "
-                f"{metric(t, 'Achieved Occupancy')} % | {metric(t, 'dram__bytes_read.sum')} / {metric(t, 'dram__bytes_write.sum')} MB |")
+                f"{metric(t, 'Achieved Occupancy')} % | {metric(t, 'dram__bytes_read.sum')} / {metric(t, 'dram__bytes_write.sum')} {unit(t, 'dram__bytes_read.sum')} |")
 b = bench
 md = f"""# Profile {tag} — bench line, launch list and ncu captures
 
@@ -71,5 +79,19 @@ the bench numbers come from an unprofiled run with CUDA events.
 Per-kernel stall breakdowns and the hottest SASS lines: `ncu_<kernel>.txt`. The dominant kernel's
 full report is `walk.ncu-rep` (open with `ncu -i`).
 """
+for extra in ("bench_rgbd.json", "bench_esdf_stress.json"):
+    f = os.path.join(src, extra)
+    if os.path.exists(f) and os.path.getsize(f):
+        d = json.loads(open(f).read().strip().splitlines()[-1])
+        json.dump(d, open(os.path.join(dst, extra), "w"), indent=1)
+        md += f"\n## `{extra}`\n\n* value {d['value']:.1f} {d['unit']}, {d['ms_per_step']:.2f} ms per step; " \
+              f"workload {d['config']['workload']}\n"
+        if "roofline" in d:
+            r = d["roofline"]
+            md += f"* roofline `{r['kernel']}`: {r['achieved']:.0f} of {r['peak']:.0f} {r['unit']} (frac {r['frac']:.3f})\n"
+        if "projective" in d:
+            md += f"* raycast {d['raycast']['ms_per_step']:.1f} ms vs projection {d['projective']['ms_per_step']:.1f} ms " \
+                  f"per 1000 frames\n"
+md += "\n`stress_pass_*`: ncu of the ESDF passes on configs[4] (2e9 voxels); `project`: the projection-mapping kernel on configs[2].\n"
 open(os.path.join(dst, "summary.md"), "w").write(md)
 print(md)
