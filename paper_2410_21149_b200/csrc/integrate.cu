@@ -58,6 +58,21 @@ struct ComposeParams {
 // bit patterns), origin-in-domain flag
 constexpr int kFrameRec = 16;
 
+// Organised-sensor patch one warp's rays come from: CVX_PATCH_ROWS rows x 32 / CVX_PATCH_ROWS columns.
+#ifndef CVX_TRASH
+#define CVX_TRASH 1
+#endif
+#ifndef CVX_FREE2
+#define CVX_FREE2 1
+#endif
+#if CVX_FREE2 && !CVX_TRASH
+#error CVX_FREE2 needs CVX_TRASH
+#endif
+#ifndef CVX_PATCH_ROWS
+#define CVX_PATCH_ROWS 4
+#endif
+static_assert(CVX_PATCH_ROWS == 1 || CVX_PATCH_ROWS == 2 || CVX_PATCH_ROWS == 4 || CVX_PATCH_ROWS == 8, "patch rows");
+
 __device__ __forceinline__ double dm(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double da(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double ds(double a, double b) { return __dsub_rn(a, b); }
@@ -122,11 +137,12 @@ __global__ void __launch_bounds__(256) prepare_kernel(const __grid_constant__ Pr
   if (idx < p.total) {
     const long long f = idx / p.n_per_frame;
     long long i = idx - f * p.n_per_frame;
-    if (p.kind != 0 && p.width > 0 && p.height > 0 && (p.width & 7) == 0 && (p.height & 3) == 0) {
-      // organised sensor: warp = 4 rows x 8 columns patch (spatially coherent rays per warp)
-      const long long pt = i >> 5, l = i & 31, pcols = p.width >> 3;
-      const long long r4 = l >> 3, c8 = (r4 & 1) ? 7 - (l & 7) : (l & 7);   // serpentine: lane l+1 neighbours lane l
-      const long long row = (pt / pcols) * 4 + r4, col = (pt % pcols) * 8 + c8;
+    constexpr int PR = CVX_PATCH_ROWS, PC = 32 / CVX_PATCH_ROWS;
+    if (p.kind != 0 && p.width > 0 && p.height > 0 && p.width % PC == 0 && p.height % PR == 0) {
+      // organised sensor: warp = PR rows x PC columns patch (spatially coherent rays per warp)
+      const long long pt = i >> 5, l = i & 31, pcols = p.width / PC;
+      const long long rr = l / PC, cc = (rr & 1) ? PC - 1 - (l % PC) : (l % PC);   // serpentine: lane l+1 neighbours lane l
+      const long long row = (pt / pcols) * PR + rr, col = (pt % pcols) * PC + cc;
       i = row * p.width + col;
     }
     const long long src = f * p.n_per_frame + i;
@@ -670,11 +686,23 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
   const int maxn = (int)__reduce_max_sync(0xffffffffu, (unsigned)n);
   const int* list = off >= 0 ? p.slots + off : nullptr;
   int slot = kFailed, nslot = kFailed, j = 0;
+#if CVX_TRASH
+  // Blocks without a slot (pool overflow: dropped updates, CVX_E_CAPACITY) and idle lanes address the
+  // trash block `max_blocks` of the accumulator (never folded), so no update needs a slot predicate.
+  const int trash = p.pool.max_blocks;
+  addr = (unsigned)trash * 512u;
+#endif
   if (have) {
     slot = list ? __ldg(list) : hash_find(p.hash, pack_key(v0 >> 3, v1 >> 3, v2 >> 3));
     if (list && nblk > 1) nslot = __ldg(list + 1);
+#if CVX_TRASH
+    if (slot < 0) slot = trash;
+#endif
     addr = (unsigned)slot * 512u + (unsigned)((v0 & 7) | ((v1 & 7) << 3) | ((v2 & 7) << 6));
   }
+#if CVX_FREE2
+  if (!have) { k0 = 0x3fffffff; s0 = 0; cexp = 1u; }   // parked idle lane (see the free prefix below)
+#endif
   const int da0 = s0, da1 = 8 * s1, da2 = 64 * s2;
   const int tq2 = 2 * p.tq;
   const long long s_off = (1ll << (kSdfF - 1)) + ((long long)p.tq << kSdfF);
@@ -696,14 +724,28 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
   const int mw = (int)__reduce_min_sync(0xffffffffu, (unsigned)mfree);
   auto body = [&](const int it, auto free_tag) {
     constexpr bool kFree = decltype(free_tag)::value;
+#if CVX_TRASH
+    const bool upd = kFree ? true : it < n;
+#else
     const bool upd = kFree ? slot >= 0 : (it < n && slot >= 0);
+#endif
     const int dpi = kFree ? tq2 : min(max((int)(S >> kSdfF), 0), tq2);   // round(sdf 2^q) + tq, clamped (O5, Q4)
     {
+#if CVX_TRASH
+      // free phase: every lane updates, the key is the address; else key 0xffffffff (never an address:
+      // < 2^23 slots) = no merging (in-band or finished lane)
+      const unsigned key = (kFree || (upd & (dpi == tq2))) ? addr : 0xffffffffu;
+      const unsigned prev = __shfl_up_sync(0xffffffffu, key, 1);
+      const bool head = kFree ? ((lane == 0) | (prev != key))
+                              : (upd & ((lane == 0) | (prev != key) | (key == 0xffffffffu)));
+      const unsigned stops = __ballot_sync(0xffffffffu, kFree ? head : (head | !upd));
+#else
       // key 0xffffffff (never an address: < 2^23 slots): no merging (in-band or idle lane)
       const unsigned key = (kFree ? upd : (upd & (dpi == tq2))) ? addr : 0xffffffffu;
       const unsigned prev = __shfl_up_sync(0xffffffffu, key, 1);
       const bool head = upd & ((lane == 0) | (prev != key) | (key == 0xffffffffu));
       const unsigned stops = __ballot_sync(0xffffffffu, head | !upd);
+#endif
       const unsigned above = stops & (0xfffffffeu << lane);
       const unsigned len = (unsigned)__clz(__brev(above)) - (unsigned)lane;
 #if CVX_VAL2
@@ -720,7 +762,11 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
       atomicAdd(p.pool.cacc + 2ull * addr, (1ull << kCntShift) | cr);
       atomicAdd(p.pool.cacc + 2ull * addr + 1, (cg << 32) | cb);
     }
+#if CVX_TRASH
+    const bool stp = kFree ? have : it + 1 < n;   // the free prefix ends before the last voxel of every ray
+#else
     const bool stp = it + 1 < n;
+#endif
     const bool g0 = k0 > 0, g1 = k1 > 0, g2 = k2 > 0;
     const bool yf = g1 & (!g0 | ((ST)D01 > 0));
     const bool zf = g2 & (yf ? ((ST)D12 > 0) : (!g0 | ((ST)D02 > 0)));
@@ -737,12 +783,55 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
       } else {
         slot = hash_find(p.hash, pack_key((vb0 - s0 * k0) >> 3, (vb1 - s1 * k1) >> 3, (vb2 - s2 * k2) >> 3));
       }
+#if CVX_TRASH
+      if (slot < 0) slot = trash;
+#endif
       const int da = zf ? da2 : (yf ? da1 : da0);
       addr = (unsigned)slot * 512u + ((((addr - (unsigned)da) & 511u) & ~m) | (cexp & m));
     }
   };
   int it = 0;
+#if CVX_FREE2
+  // Free prefix, hand-scheduled: every lane (idle lanes parked on the trash block, stepping x by 0 and
+  // never meeting a block boundary) updates its voxel with the clamped d' = 2 tq; runs of equal
+  // addresses in adjacent lanes issue one reduction of len * (2^40 | 2 tq).
+  {
+    const unsigned above_mask = 0xfffffffeu << lane;
+    const bool lane0 = lane == 0;
+    const unsigned utq2 = (unsigned)tq2;
+    for (; it < mw; ++it) {
+      const unsigned prev = __shfl_up_sync(0xffffffffu, addr, 1);
+      const bool head = lane0 | (prev != addr);
+      const unsigned stops = __ballot_sync(0xffffffffu, head);
+      const unsigned len = (unsigned)__clz(__brev(stops & above_mask)) - (unsigned)lane;
+      const unsigned long long val = ((unsigned long long)(len << (kCntShift - 32)) << 32) | (len * utq2);
+      asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.relaxed.gpu.global.add.u64 [%0], %1;\n\t}"
+                   :: "l"(acc + addr), "l"(val), "r"((unsigned)head) : "memory");
+      const bool g0 = k0 > 0, g1 = k1 > 0, g2 = k2 > 0;
+      const bool yf = g1 & (!g0 | ((ST)D01 > 0));
+      const bool zf = g2 & (yf ? ((ST)D12 > 0) : (!g0 | ((ST)D02 > 0)));
+      const bool by = yf & !zf, bx = !yf & !zf;
+      if (bx) { addr += da0; --k0; D01 += I1; D02 += I2; }
+      if (by) { addr += da1; --k1; D01 -= I0; D12 += I2; }
+      if (zf) { addr += da2; --k2; D02 -= I0; D12 -= I1; }
+      const unsigned m = zf ? 0x1c0u : (yf ? 0x38u : 7u);
+      if (((addr ^ cexp) & m) == 0u) {      // entered the next block of the ray
+        ++j;
+        if (list) {
+          slot = nslot;
+          if (j + 1 < nblk) nslot = __ldg(list + j + 1);   // prefetch one block ahead
+        } else {
+          slot = hash_find(p.hash, pack_key((vb0 - s0 * k0) >> 3, (vb1 - s1 * k1) >> 3, (vb2 - s2 * k2) >> 3));
+        }
+        if (slot < 0) slot = trash;
+        const int da = zf ? da2 : (yf ? da1 : da0);
+        addr = (unsigned)slot * 512u + ((((addr - (unsigned)da) & 511u) & ~m) | (cexp & m));
+      }
+    }
+  }
+#else
   for (; it < mw; ++it) body(it, std::true_type{});
+#endif
   S -= U0 * (K0 - k0) + U1 * (K1 - k1) + U2 * (K2 - k2);
   for (; it < maxn; ++it) body(it, std::false_type{});
 }
