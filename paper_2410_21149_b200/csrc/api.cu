@@ -182,7 +182,7 @@ cvx_status cvx_create_submap(const cvx_grid_config* cfg, const double* T_world_s
   sm->pool.max_blocks = (int)nb;
   if ((e = cudaMalloc(&sm->hash.e, cap * sizeof(cvx::HashEntry))) != cudaSuccess ||
       (e = cudaMalloc(&sm->pool.sums, nb * cvx::kBlockVox * 16)) != cudaSuccess ||
-      (e = cudaMalloc(&sm->pool.acc, (nb + 1) * cvx::kBlockVox * 8)) != cudaSuccess ||
+      (e = cudaMalloc(&sm->pool.acc, (nb + cvx::kTrashBlocks) * cvx::kBlockVox * 8)) != cudaSuccess ||
       (e = cudaMalloc(&sm->pool.esdf, nb * cvx::kBlockVox * 4)) != cudaSuccess ||
       (e = cudaMalloc(&sm->pool.coords, nb * 16)) != cudaSuccess ||
       (e = cudaMalloc(&sm->ctr, sizeof(cvx::Counters))) != cudaSuccess ||
@@ -197,7 +197,7 @@ cvx_status cvx_create_submap(const cvx_grid_config* cfg, const double* T_world_s
       (e = cudaEventCreateWithFlags(&sm->ev_free[0], cudaEventDisableTiming)) != cudaSuccess ||
       (e = cudaEventCreateWithFlags(&sm->ev_free[1], cudaEventDisableTiming)) != cudaSuccess ||
       (cfg->color && ((e = cudaMalloc(&sm->pool.csum, nb * cvx::kBlockVox * 32)) != cudaSuccess ||
-                      (e = cudaMalloc(&sm->pool.cacc, (nb + 1) * cvx::kBlockVox * 16)) != cudaSuccess))) {
+                      (e = cudaMalloc(&sm->pool.cacc, (nb + cvx::kTrashBlocks) * cvx::kBlockVox * 16)) != cudaSuccess))) {
     free_all(sm);
     delete sm;
     return cuda_fail(e, "allocating submap");
@@ -205,11 +205,11 @@ cvx_status cvx_create_submap(const cvx_grid_config* cfg, const double* T_world_s
   // zero-initialised pool (a3 zero-init happens once here; reset re-zeroes only the used blocks)
   cudaMemset(sm->ctr, 0, sizeof(cvx::Counters));
   cudaMemset(sm->pool.sums, 0, nb * cvx::kBlockVox * 16);
-  cudaMemset(sm->pool.acc, 0, (nb + 1) * cvx::kBlockVox * 8);   // + the trash block (slot max_blocks)
+  cudaMemset(sm->pool.acc, 0, (nb + cvx::kTrashBlocks) * cvx::kBlockVox * 8);   // + the trash region (cvx_internal.cuh)
   cudaMemset(sm->pool.esdf, 0, nb * cvx::kBlockVox * 4);
   if (cfg->color) {
     cudaMemset(sm->pool.csum, 0, nb * cvx::kBlockVox * 32);
-    cudaMemset(sm->pool.cacc, 0, (nb + 1) * cvx::kBlockVox * 16);
+    cudaMemset(sm->pool.cacc, 0, (nb + cvx::kTrashBlocks) * cvx::kBlockVox * 16);
   }
   e = cvx::launch_reset(sm, 0);
   if (e == cudaSuccess) e = cudaEventRecord(sm->ev_free[0], 0);

@@ -139,6 +139,9 @@ __device__ inline int hash_activate(const HashView& h, const PoolView& pool, Cou
 // updates of one voxel (24-bit count), and the 40-bit field holds their sum of d' <= 2 round(tau 2^q)
 // <= 2^16 with q = floor(log2(2^15 / tau)) (quantum tau 2^-15: rounding <= 1e-5 m at tau = 0.6 m).
 constexpr int kCntShift = 40;
+// Trash region of the accumulators after the pool (slots max_blocks ..): updates of blocks without a
+// slot and of parked lanes land there; never folded or read.
+constexpr int kTrashBlocks = 64;
 constexpr long long kMaxPackedRays = (1ll << 24) - 1;
 constexpr long long kLaunchRays = (1ll << 22) - 1;   // rays per walk launch (pipelining granularity)
 inline int packed_q(double tau) {

@@ -65,8 +65,14 @@ constexpr int kFrameRec = 16;
 #ifndef CVX_FREE2
 #define CVX_FREE2 1
 #endif
-#if CVX_FREE2 && !CVX_TRASH
-#error CVX_FREE2 needs CVX_TRASH
+#if (CVX_FREE2 || CVX_BAND2) && !CVX_TRASH
+#error CVX_FREE2 / CVX_BAND2 need CVX_TRASH
+#endif
+#ifndef CVX_TIGHT
+#define CVX_TIGHT 0
+#endif
+#ifndef CVX_BAND2
+#define CVX_BAND2 1
 #endif
 #ifndef CVX_PATCH_ROWS
 #define CVX_PATCH_ROWS 4
@@ -624,6 +630,46 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_kernel(const __grid_cons
   }
 }
 
+// Approximate fp32 reciprocal / reciprocal square root (MUFU only; used for guesses that are checked
+// exactly afterwards, so no IEEE slow path is needed).
+__device__ __forceinline__ float rcp_approx(float x) { float y; asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+__device__ __forceinline__ float rsqrt_approx(float x) { float y; asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+
+// Exact free prefix of a ray from a crossing count (checked in the walk's own integer arithmetic).
+// Take a segment fraction f = F / 2^20; the crossings strictly before f are C_a = #boundaries of axis a
+// strictly between A_a and X_a = A_a + f D_a, and the walk takes exactly those first (crossing-time
+// order), so after i_f = sum C_a steps its sdf is S_f = S - sum U_a C_a exactly.  S never grows, so if
+// S_f >= thr every voxel 0..i_f is clamped free space: returns i_f + 1 (<= n - 1), else 0.  f only
+// needs to be a good guess: the sdf falls by ~1 m per metre of segment; back off one voxel diagonal
+// (sum U_a) for the voxel centres.
+__device__ __forceinline__ int tight_free_prefix(const RayRec* rp, long long S, long long thr, int n, float s, int q) {
+  const RayRec& r = *rp;
+  const long long U[3] = {r.U[0], r.U[1], r.U[2]};
+  const long long su = U[0] + U[1] + U[2];
+  const float d0 = (float)(r.B[0] - r.A[0]), d1 = (float)(r.B[1] - r.A[1]), d2 = (float)(r.B[2] - r.A[2]);
+  // segment length in sdf units: |B - A| 2^-16 voxels * s * 2^(q + kSdfF) (a guess: fp32 is plenty)
+  const float l2 = d0 * d0 + d1 * d1 + d2 * d2;
+  const float seg = l2 * rsqrt_approx(l2) * (s * exp2f((float)(q + kSdfF - 16)));
+  const float f = ((float)(S - thr - su - (su >> 4)) - 64.0f) * rcp_approx(seg);
+  if (!(f > 0.0f) || !(seg > 0.0f)) return 0;
+  const long long F = (long long)fminf(floorf(f * 1048576.0f), 1048575.0f);
+  int i_f = 0;
+  long long Sf = S;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const long long D = r.B[a] - r.A[a];
+    const long long va = r.A[a] >> 16;
+    const long long X = (r.A[a] << 20) + F * D;         // 2^-36 voxel units, exact
+    long long c = 0;
+    if (D > 0) c = (-((-X) >> 36)) - 1 - va;
+    else if (D < 0) c = va - (X >> 36);
+    c = c < 0 ? 0 : c;
+    i_f += (int)c;
+    Sf -= U[a] * c;
+  }
+  return (Sf >= thr && i_f + 1 <= n - 1) ? i_f + 1 : 0;
+}
+
 // Constant-weight walk with the voxel address carried incrementally (same decisions as walk_kernel
 // <true, true, k32, kColor>; see there for O4/O5).  Per step only the stepped axis' crossing count,
 // DDA differences, sdf and address move; the voxel coordinates are implied by the remaining crossing
@@ -646,6 +692,7 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
   int n = 0, nblk = 0, off = -1;
   unsigned rgb = 0, cexp = 0, addr = 0;
   int v0 = 0, v1 = 0, v2 = 0;
+  int mtight = 0;
   if (have) {
     const RayRec r = p.rays[idx];
     long long R[3], AD[3];
@@ -682,6 +729,13 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
     n = r.n_vox;
     off = r.list_off;
     rgb = r.rgb;
+#if CVX_TIGHT
+    {
+      long long thr = (long long)(2 * p.tq) << kSdfF;
+      if (kColor) thr = max(thr, (1ll << (kSdfF - 1)) + ((long long)p.tq << kSdfF) + p.band);
+      mtight = tight_free_prefix(p.rays + idx, S, thr, n, p.s, p.q);
+    }
+#endif
   }
   const int maxn = (int)__reduce_max_sync(0xffffffffu, (unsigned)n);
   const int* list = off >= 0 ? p.slots + off : nullptr;
@@ -719,7 +773,15 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
     if (kColor) thr = max(thr, band_hi);
     const long long umax = max(U0, max(U1, U2));
     mfree = 0;
-    if (S > thr && umax > 0) mfree = (int)min((double)(n - 1), floor((double)(S - thr) / (double)umax));
+    if (S > thr && umax > 0) {
+      // floor((S - thr) / umax), capped at n - 1: fp32 guess, then made exact (no fp64 / int64 division)
+      const long long num = S - thr;
+      long long m = (long long)fminf((float)num * rcp_approx((float)umax), (float)(n - 1));
+      while (m > 0 && m * umax > num) --m;
+      while (m < n - 1 && (m + 1) * umax <= num) ++m;
+      mfree = (int)m;
+    }
+    mfree = max(mfree, mtight);
   }
   const int mw = (int)__reduce_min_sync(0xffffffffu, (unsigned)mfree);
   auto body = [&](const int it, auto free_tag) {
@@ -833,6 +895,54 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
   for (; it < mw; ++it) body(it, std::true_type{});
 #endif
   S -= U0 * (K0 - k0) + U1 * (K1 - k1) + U2 * (K2 - k2);
+#if CVX_BAND2
+  if constexpr (!kColor) {
+    // Rest of the rays, hand-scheduled like the free prefix: a lane that has written its last voxel
+    // parks on its warp's trash spot (x step of 0, never a block boundary, d' = 2 tq forever) so no
+    // update or step needs a per-lane predicate; parked lanes' reductions land in the trash region.
+    const unsigned above_mask = 0xfffffffeu << lane;
+    const bool lane0 = lane == 0;
+    const unsigned spot = (unsigned)trash * 512u + ((((unsigned)idx >> 5) & 4095u) << 3);
+    int dx0 = da0;
+    if (it >= n) { addr = spot; k0 = 0x3fffffff; k1 = 0; k2 = 0; dx0 = 0; cexp = 1u; S = (long long)tq2 << (kSdfF + 1); U0 = 0; n = 0x7fffffff; }
+    for (; it < maxn; ++it) {
+      const int dpi = min(max((int)(S >> kSdfF), 0), tq2);   // round(sdf 2^q) + tq, clamped (O5, Q4)
+      const unsigned key = dpi == tq2 ? addr : 0xffffffffu;     // only clamped updates merge
+      const unsigned prev = __shfl_up_sync(0xffffffffu, key, 1);
+      const bool head = lane0 | (prev != key) | (key == 0xffffffffu);
+      const unsigned stops = __ballot_sync(0xffffffffu, head);
+      const unsigned len = (unsigned)__clz(__brev(stops & above_mask)) - (unsigned)lane;
+      const unsigned long long val = ((unsigned long long)(len << (kCntShift - 32)) << 32) | (len * (unsigned)dpi);
+      asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.relaxed.gpu.global.add.u64 [%0], %1;\n\t}"
+                   :: "l"(acc + addr), "l"(val), "r"((unsigned)head) : "memory");
+      if (it + 1 >= n) {   // that was the ray's last voxel: park
+        addr = spot; k0 = 0x3fffffff; k1 = 0; k2 = 0; dx0 = 0; cexp = 1u; S = (long long)tq2 << (kSdfF + 1); U0 = 0;
+        n = 0x7fffffff;
+      }
+      const bool g0 = k0 > 0, g1 = k1 > 0, g2 = k2 > 0;
+      const bool yf = g1 & (!g0 | ((ST)D01 > 0));
+      const bool zf = g2 & (yf ? ((ST)D12 > 0) : (!g0 | ((ST)D02 > 0)));
+      const bool by = yf & !zf, bx = !yf & !zf;
+      if (bx) { addr += dx0; --k0; D01 += I1; D02 += I2; S -= U0; }
+      if (by) { addr += da1; --k1; D01 -= I0; D12 += I2; S -= U1; }
+      if (zf) { addr += da2; --k2; D02 -= I0; D12 -= I1; S -= U2; }
+      const unsigned m = zf ? 0x1c0u : (yf ? 0x38u : 7u);
+      if (((addr ^ cexp) & m) == 0u) {      // entered the next block of the ray
+        ++j;
+        if (list) {
+          slot = nslot;
+          if (j + 1 < nblk) nslot = __ldg(list + j + 1);   // prefetch one block ahead
+        } else {
+          slot = hash_find(p.hash, pack_key((vb0 - s0 * k0) >> 3, (vb1 - s1 * k1) >> 3, (vb2 - s2 * k2) >> 3));
+        }
+        if (slot < 0) slot = trash;
+        const int da = zf ? da2 : (yf ? da1 : dx0);
+        addr = (unsigned)slot * 512u + ((((addr - (unsigned)da) & 511u) & ~m) | (cexp & m));
+      }
+    }
+    return;
+  }
+#endif
   for (; it < maxn; ++it) body(it, std::false_type{});
 }
 
