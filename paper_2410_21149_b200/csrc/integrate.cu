@@ -630,6 +630,33 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_kernel(const __grid_cons
   }
 }
 
+// Predicated read-only load INTO the live register of `dst` (no copy: a plain conditional __ldg makes
+// the compiler load into a temporary and move it, which waits for the load right where it is issued —
+// ncu showed that move as the walk's top stall).  The value is consumed one block later.
+#ifndef CVX_PF_ASM
+#define CVX_PF_ASM 2
+#endif
+__device__ __forceinline__ void prefetch_slot(int& dst, const int* ptr, bool pred) {
+#if CVX_PF_ASM
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p ld.global.nc.u32 %0, [%1];\n\t}"
+               : "+r"(dst) : "l"(ptr), "r"((unsigned)pred));
+#else
+  if (pred) dst = __ldg(ptr);
+#endif
+}
+
+// CVX_PF_ASM == 2: the next block's slot is prefetched with cp.async into a per-thread shared-memory
+// word and read back (after cp.async.wait_all, long complete by then) at the next block entry.
+__device__ __forceinline__ void pf_issue(int* sdst, const int* src, bool pred) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p cp.async.ca.shared.global [%0], [%1], 4;\n\tcp.async.commit_group;\n\t}"
+               :: "r"(sa), "l"(src), "r"((unsigned)pred) : "memory");
+}
+__device__ __forceinline__ int pf_take(const int* sdst) {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  return *(volatile const int*)sdst;
+}
+
 // Approximate fp32 reciprocal / reciprocal square root (MUFU only; used for guesses that are checked
 // exactly afterwards, so no IEEE slow path is needed).
 __device__ __forceinline__ float rcp_approx(float x) { float y; asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
@@ -740,6 +767,9 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
   const int maxn = (int)__reduce_max_sync(0xffffffffu, (unsigned)n);
   const int* list = off >= 0 ? p.slots + off : nullptr;
   int slot = kFailed, nslot = kFailed, j = 0;
+#if CVX_PF_ASM == 2
+  __shared__ int s_pf[128];
+#endif
 #if CVX_TRASH
   // Blocks without a slot (pool overflow: dropped updates, CVX_E_CAPACITY) and idle lanes address the
   // trash block `max_blocks` of the accumulator (never folded), so no update needs a slot predicate.
@@ -748,7 +778,11 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
 #endif
   if (have) {
     slot = list ? __ldg(list) : hash_find(p.hash, pack_key(v0 >> 3, v1 >> 3, v2 >> 3));
+#if CVX_PF_ASM == 2
+    pf_issue(s_pf + threadIdx.x, list + 1, list && nblk > 1);
+#else
     if (list && nblk > 1) nslot = __ldg(list + 1);
+#endif
 #if CVX_TRASH
     if (slot < 0) slot = trash;
 #endif
@@ -841,7 +875,7 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
       ++j;
       if (list) {
         slot = nslot;
-        if (j + 1 < nblk) nslot = __ldg(list + j + 1);   // prefetch one block ahead
+        prefetch_slot(nslot, list + j + 1, j + 1 < nblk);   // prefetch one block ahead
       } else {
         slot = hash_find(p.hash, pack_key((vb0 - s0 * k0) >> 3, (vb1 - s1 * k1) >> 3, (vb2 - s2 * k2) >> 3));
       }
@@ -880,8 +914,13 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
       if (((addr ^ cexp) & m) == 0u) {      // entered the next block of the ray
         ++j;
         if (list) {
+#if CVX_PF_ASM == 2
+          slot = pf_take(s_pf + threadIdx.x);
+          pf_issue(s_pf + threadIdx.x, list + j + 1, j + 1 < nblk);   // prefetch one block ahead
+#else
           slot = nslot;
-          if (j + 1 < nblk) nslot = __ldg(list + j + 1);   // prefetch one block ahead
+          prefetch_slot(nslot, list + j + 1, j + 1 < nblk);   // prefetch one block ahead
+#endif
         } else {
           slot = hash_find(p.hash, pack_key((vb0 - s0 * k0) >> 3, (vb1 - s1 * k1) >> 3, (vb2 - s2 * k2) >> 3));
         }
@@ -930,8 +969,13 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
       if (((addr ^ cexp) & m) == 0u) {      // entered the next block of the ray
         ++j;
         if (list) {
+#if CVX_PF_ASM == 2
+          slot = pf_take(s_pf + threadIdx.x);
+          pf_issue(s_pf + threadIdx.x, list + j + 1, j + 1 < nblk);   // prefetch one block ahead
+#else
           slot = nslot;
-          if (j + 1 < nblk) nslot = __ldg(list + j + 1);   // prefetch one block ahead
+          prefetch_slot(nslot, list + j + 1, j + 1 < nblk);   // prefetch one block ahead
+#endif
         } else {
           slot = hash_find(p.hash, pack_key((vb0 - s0 * k0) >> 3, (vb1 - s1 * k1) >> 3, (vb2 - s2 * k2) >> 3));
         }
@@ -942,6 +986,9 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
     }
     return;
   }
+#endif
+#if CVX_PF_ASM == 2
+  if (list) nslot = pf_take(s_pf + threadIdx.x);   // the general band body keeps the prefetch in a register
 #endif
   for (; it < maxn; ++it) body(it, std::false_type{});
 }
