@@ -704,7 +704,13 @@ __device__ __forceinline__ int tight_free_prefix(const RayRec* rp, long long S, 
 // entry: the stepped axis' local field of the address reached its entry value.  Only clamped
 // free-space updates (d' = 2 tq) are run-merged: in-band sdfs differ between rays at the 2^-q quantum,
 // so merging them buys nothing; they go out as single-lane reductions.
-template <bool k32, bool kColor>
+// kFuse: ALLOCATE (a3) is done here instead of by block_walk2_kernel — the first block of a ray is
+// activated at the start, and on entering each block its hash entry has already been fetched: at every
+// block entry the entries of the three axis neighbours of the new block (the next block is one of them:
+// the traversal crosses one block face at a time) are copied into shared memory with cp.async, and the
+// next entry takes the one on the stepped axis; a hit is the slot, anything else (absent: insert, other
+// key: probe on, pending) goes through hash_activate_pf with that entry as its first probe.
+template <bool k32, bool kColor, bool kFuse = false>
 __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_constant__ WalkParams p) {
   using DT = typename std::conditional<k32, unsigned, unsigned long long>::type;
   using ST = typename std::conditional<k32, int, long long>::type;
@@ -776,13 +782,65 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
   const int trash = p.pool.max_blocks;
   addr = (unsigned)trash * 512u;
 #endif
-  if (have) {
-    slot = list ? __ldg(list) : hash_find(p.hash, pack_key(v0 >> 3, v1 >> 3, v2 >> 3));
+  // kFuse: current block coordinates and the prefetched neighbour entries, per thread
+  __shared__ int4 s_cb[kFuse ? 128 : 1];
+  __shared__ longlong2 s_cand[kFuse ? 3 * 128 : 1];
+  auto issue_candidates = [&](const int4 cb) {
+    const int sa[3] = {s0, s1, s2};
+    const int kk[3] = {k0, k1, k2};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const unsigned long long key = pack_key(cb.x + (a == 0 ? sa[0] : 0), cb.y + (a == 1 ? sa[1] : 0),
+                                              cb.z + (a == 2 ? sa[2] : 0));
+      const HashEntry* src = p.hash.e + hash_slot(key, p.hash);
+      const unsigned dst = (unsigned)__cvta_generic_to_shared(&s_cand[3 * threadIdx.x + a]);
+      asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p cp.async.cg.shared.global [%0], [%1], 16;\n\t}"
+                   :: "r"(dst), "l"(src), "r"((unsigned)(kk[a] > 0)) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  // slot of the block entered by a step along axis ax (kFuse), or from the list / the hash
+  auto next_slot = [&](const int ax) -> int {
+    if constexpr (kFuse) {
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      int4 cb = s_cb[threadIdx.x];
+      if (ax == 0) cb.x += s0; else if (ax == 1) cb.y += s1; else cb.z += s2;
+      const unsigned long long key = pack_key(cb.x, cb.y, cb.z);
+      const longlong2 e = s_cand[3 * threadIdx.x + ax];   // complete: cp.async.wait_all above
+      int sl = (int)(e.y & 0xffffffffll);
+      if ((unsigned long long)e.x != key || sl < 0) sl = hash_activate_pf(p.hash, p.pool, p.ctr, key, cb.x, cb.y, cb.z, e);
+      s_cb[threadIdx.x] = cb;
+      issue_candidates(cb);
+      return sl;
+    } else {
+      if (list) {
 #if CVX_PF_ASM == 2
-    pf_issue(s_pf + threadIdx.x, list + 1, list && nblk > 1);
+        const int sl = pf_take(s_pf + threadIdx.x);
+        pf_issue(s_pf + threadIdx.x, list + j + 1, j + 1 < nblk);   // prefetch one block ahead
+        return sl;
 #else
-    if (list && nblk > 1) nslot = __ldg(list + 1);
+        const int sl = nslot;
+        prefetch_slot(nslot, list + j + 1, j + 1 < nblk);
+        return sl;
 #endif
+      }
+      return hash_find(p.hash, pack_key((vb0 - s0 * k0) >> 3, (vb1 - s1 * k1) >> 3, (vb2 - s2 * k2) >> 3));
+    }
+  };
+  if (have) {
+    if constexpr (kFuse) {
+      const int4 cb = make_int4(v0 >> 3, v1 >> 3, v2 >> 3, 0);
+      slot = hash_activate(p.hash, p.pool, p.ctr, pack_key(cb.x, cb.y, cb.z), cb.x, cb.y, cb.z);
+      s_cb[threadIdx.x] = cb;
+      issue_candidates(cb);
+    } else {
+      slot = list ? __ldg(list) : hash_find(p.hash, pack_key(v0 >> 3, v1 >> 3, v2 >> 3));
+#if CVX_PF_ASM == 2
+      pf_issue(s_pf + threadIdx.x, list + 1, list && nblk > 1);
+#else
+      if (list && nblk > 1) nslot = __ldg(list + 1);
+#endif
+    }
 #if CVX_TRASH
     if (slot < 0) slot = trash;
 #endif
@@ -913,17 +971,7 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
       const unsigned m = zf ? 0x1c0u : (yf ? 0x38u : 7u);
       if (((addr ^ cexp) & m) == 0u) {      // entered the next block of the ray
         ++j;
-        if (list) {
-#if CVX_PF_ASM == 2
-          slot = pf_take(s_pf + threadIdx.x);
-          pf_issue(s_pf + threadIdx.x, list + j + 1, j + 1 < nblk);   // prefetch one block ahead
-#else
-          slot = nslot;
-          prefetch_slot(nslot, list + j + 1, j + 1 < nblk);   // prefetch one block ahead
-#endif
-        } else {
-          slot = hash_find(p.hash, pack_key((vb0 - s0 * k0) >> 3, (vb1 - s1 * k1) >> 3, (vb2 - s2 * k2) >> 3));
-        }
+        slot = next_slot(zf ? 2 : (yf ? 1 : 0));
         if (slot < 0) slot = trash;
         const int da = zf ? da2 : (yf ? da1 : da0);
         addr = (unsigned)slot * 512u + ((((addr - (unsigned)da) & 511u) & ~m) | (cexp & m));
@@ -968,17 +1016,7 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
       const unsigned m = zf ? 0x1c0u : (yf ? 0x38u : 7u);
       if (((addr ^ cexp) & m) == 0u) {      // entered the next block of the ray
         ++j;
-        if (list) {
-#if CVX_PF_ASM == 2
-          slot = pf_take(s_pf + threadIdx.x);
-          pf_issue(s_pf + threadIdx.x, list + j + 1, j + 1 < nblk);   // prefetch one block ahead
-#else
-          slot = nslot;
-          prefetch_slot(nslot, list + j + 1, j + 1 < nblk);   // prefetch one block ahead
-#endif
-        } else {
-          slot = hash_find(p.hash, pack_key((vb0 - s0 * k0) >> 3, (vb1 - s1 * k1) >> 3, (vb2 - s2 * k2) >> 3));
-        }
+        slot = next_slot(zf ? 2 : (yf ? 1 : 0));
         if (slot < 0) slot = trash;
         const int da = zf ? da2 : (yf ? da1 : dx0);
         addr = (unsigned)slot * 512u + ((((addr - (unsigned)da) & 511u) & ~m) | (cexp & m));
@@ -1311,7 +1349,10 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     wp.q = q;
     wp.band = std::llround(std::ldexp(sm->cfg.truncation, q + kSdfF));
     wp.birth = nullptr;
-    {
+    const bool cw = cw_ok && total <= kLaunchRays;
+    // constant weights, no colour, no block-count trigger: ALLOCATE runs inside the update walk
+    const bool fuse = sm->fuse_alloc && cw && sm->aggregate && sm->walk_cw && !rgb && !trig;
+    if (!fuse) {
       ProfScope ps_(sm, "block_walk_allocate", side);
       if (sm->bw2) {
         if (k32) block_walk2_kernel<true><<<blocks, 256, 0, side>>>(wp);
@@ -1324,7 +1365,6 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     if (trig) trigger_check_kernel<<<1, 1, 0, side>>>(sm->ctr, trig, f0);
     cudaEventRecord(sm->ev_prepared[b], side);
     // ---- caller's stream: a4 UPDATE + a5 FOLD of launch k
-    const bool cw = cw_ok && total <= kLaunchRays;
     if (cw && pending + total > kMaxPackedRays) fold();
     cudaStreamWaitEvent(st, sm->ev_prepared[b], 0);
     {
@@ -1332,6 +1372,7 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
       const unsigned wblocks = (unsigned)((total + 127) / 128);   // 128-thread CTAs (measured best)
       if (cw && sm->aggregate && sm->walk_cw) {
         if (rgb) { if (k32) walk_cw_kernel<true, true><<<wblocks, 128, 0, st>>>(wp); else walk_cw_kernel<false, true><<<wblocks, 128, 0, st>>>(wp); }
+        else if (fuse) { if (k32) walk_cw_kernel<true, false, true><<<wblocks, 128, 0, st>>>(wp); else walk_cw_kernel<false, false, true><<<wblocks, 128, 0, st>>>(wp); }
         else { if (k32) walk_cw_kernel<true, false><<<wblocks, 128, 0, st>>>(wp); else walk_cw_kernel<false, false><<<wblocks, 128, 0, st>>>(wp); }
       } else if (rgb) {
         if (cw) { if (k32) walk_kernel<true, true, true, true><<<wblocks, 128, 0, st>>>(wp); else walk_kernel<true, true, false, true><<<wblocks, 128, 0, st>>>(wp); }

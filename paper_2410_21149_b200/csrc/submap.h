@@ -66,6 +66,7 @@ struct cvx_submap {
   bool serialize = false;     // profiling: run the pipeline's side work on the caller's stream
   bool bw2 = true;            // software-pipelined ALLOCATE (block_walk2_kernel)
   bool walk_cw = true;        // constant weights: incremental-address walk (walk_cw_kernel)
+  bool fuse_alloc = false;    // constant weights: ALLOCATE inside walk_cw_kernel (measured 1.4x slower: off)
 
   // ESDF scratch (grow-only)
   void* edt = nullptr;        // device: g2 u32 | meta u32 | g1 u16 over the dense AABB
