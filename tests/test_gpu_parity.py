@@ -305,3 +305,21 @@ def test_block_count_trigger_matches_frame_by_frame(tiny):
     # threshold never reached: every frame is taken
     c = Submap(tiny["grid"], tiny["submaps"][0]["T_world_submap"], 0)
     assert c.integrate_until(data, poses, tiny["sensor"], tiny["grid"]["max_blocks"]) == len(frames)
+
+
+@pytest.mark.parametrize("knob", ["CVX_FUSE_ALLOC=1", "CVX_BW2=0", "CVX_WALK_CW=0"])
+def test_walk_variants_bitexact(tiny, orc, monkeypatch, knob):
+    """The tuning variants of the integrate path (ALLOCATE fused into the walk, the first block walk,
+    the general walk kernel) read at submap creation: each must give the default path's TSDF bit for
+    bit (R1 exact sums) and match the oracle."""
+    frames = [0, 3, 6, 9]
+    ref, _ = gpu_build(tiny, frames, batch=True, finalize=False)
+    k, v = knob.split("=")
+    monkeypatch.setenv(k, v)
+    var, _ = gpu_build(tiny, frames, batch=True, finalize=False)
+    a, b = gpu_export_sorted(ref), gpu_export_sorted(var)
+    assert np.array_equal(a[0], b[0])
+    assert np.array_equal(a[1].view(np.uint32), b[1].view(np.uint32))
+    assert np.array_equal(a[2].view(np.uint32), b[2].view(np.uint32))
+    o, _ = oracle_build(tiny, frames)
+    assert_tsdf_parity(b, o.export())
