@@ -176,6 +176,31 @@ NCU_FILES = {"ray_walk_update": "ncu_walk.txt", "block_walk_allocate": "ncu_bloc
              "esdf_pass_y": "ncu_esdf_pass_y.txt", "esdf_pass_z": "ncu_esdf_pass_z.txt", "fold": "ncu_fold.txt"}
 
 
+def ncu_metric(kernel, name, workload="lidar"):
+    """A '<name>  <unit>  <value>' line (e.g. Issue Slots Busy, %) of the newest committed ncu summary of
+    `kernel` under profiles/, as {"value", "unit", "source"} (None if there is none)."""
+    prof = os.path.join(ROOT, "profiles")
+    if kernel not in NCU_FILES or not os.path.isdir(prof):
+        return None
+    fname = NCU_FILES[kernel]
+    if workload == "esdf_stress":
+        fname = fname.replace("ncu_esdf_", "ncu_stress_")
+    for tag in sorted(os.listdir(prof), reverse=True):
+        f = os.path.join(prof, tag, fname)
+        if not os.path.exists(f):
+            continue
+        for line in open(f):
+            if line.startswith(name):
+                parts = line[len(name):].split()
+                try:
+                    return {"value": float(parts[-1]), "unit": parts[0] if len(parts) > 1 else "",
+                            "source": f"profiles/{tag}/{fname}"}
+                except ValueError:
+                    return None
+        return None
+    return None
+
+
 def ncu_traffic(kernel, workload="lidar"):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from the newest committed
     `ncu --set full` capture of that workload under profiles/ (None if there is none)."""
@@ -866,6 +891,10 @@ def main():
                     "updates_per_s": upd_launch / (avg_ms / 1e3), "ops_per_update": 13,
                     "peak_source": f"148 SM x 128 lanes x {clk_mhz:.0f} MHz (median under load)"}
     roofline["traffic"] = ncu_traffic(dom)
+    if dom == "ray_walk_update":
+        # the walk's real ceiling is the issue rate (one warp instruction per SMSP per clock): ncu's issue
+        # utilisation of the same kernel says how close the instruction stream is to it
+        roofline["ncu_issue_slots_busy"] = ncu_metric(dom, "Issue Slots Busy")
     line = {
         "metric": METRIC, "value": value, "unit": "scans/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
