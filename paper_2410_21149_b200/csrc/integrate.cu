@@ -453,8 +453,11 @@ __global__ void __launch_bounds__(256) block_walk2_kernel(const __grid_constant_
     if ((headsn >> lane) & 1u) entn = ld_entry(p.hash.e + hash_slot(keyn, p.hash));   // prefetch j+1
     // consume step j
     int slot = kFailed;
-    if ((heads >> lane) & 1u)
-      slot = hash_activate_pf(p.hash, p.pool, p.ctr, key, key_field(key, 42), key_field(key, 21), key_field(key, 0), ent);
+    if ((heads >> lane) & 1u) {   // hit on the prefetched entry: done; else the full activate (insert / probe / wait)
+      slot = (int)(ent.y & 0xffffffffll);
+      if ((unsigned long long)ent.x != key || slot < 0)
+        slot = hash_activate_pf(p.hash, p.pool, p.ctr, key, key_field(key, 42), key_field(key, 21), key_field(key, 0), ent);
+    }
     const unsigned hb = heads & (0xffffffffu >> (31 - lane));
     slot = __shfl_sync(0xffffffffu, slot, hb ? 31 - __clz(hb) : lane);
     if (act && list) list[j] = slot;
