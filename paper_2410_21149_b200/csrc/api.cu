@@ -115,6 +115,11 @@ void free_all(cvx_submap* sm) {
     if (B.staging) cudaFree(B.staging);
   }
   if (sm->side) cudaStreamDestroy(sm->side);
+  if (sm->copy) cudaStreamDestroy(sm->copy);
+  for (int b = 0; b < 2; ++b) {
+    if (sm->ev_staged[b]) cudaEventDestroy(sm->ev_staged[b]);
+    if (sm->ev_stage_free[b]) cudaEventDestroy(sm->ev_stage_free[b]);
+  }
   if (sm->ev_entry) cudaEventDestroy(sm->ev_entry);
   for (int b = 0; b < 2; ++b) {
     if (sm->ev_prepared[b]) cudaEventDestroy(sm->ev_prepared[b]);

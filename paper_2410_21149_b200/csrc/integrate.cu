@@ -1297,6 +1297,19 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
   };
   cudaEventRecord(sm->ev_entry, st);                 // the side stream starts after the caller's prior work
   cudaStreamWaitEvent(side, sm->ev_entry, 0);
+  cudaStream_t cstream = side;                       // host frames: H2D copies (own stream unless serialised)
+  if (host_data && !sm->serialize) {
+    if (!sm->copy) {
+      cudaError_t e = cudaStreamCreateWithFlags(&sm->copy, cudaStreamNonBlocking);
+      for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+        e = cudaEventCreateWithFlags(&sm->ev_staged[b], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&sm->ev_stage_free[b], cudaEventDisableTiming);
+      }
+      if (e != cudaSuccess) return e;
+    }
+    cstream = sm->copy;
+    cudaStreamWaitEvent(cstream, sm->ev_entry, 0);
+  }
   int f0 = 0;
   for (const int nf : plan) {
     const long long total = (long long)nf * n_per_frame;
@@ -1304,6 +1317,14 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     sm->next_buf ^= 1;
     cvx_submap::Buf& B = sm->buf[b];
     const unsigned blocks = (unsigned)((total + 255) / 256);
+    const float* chunk = data + (long long)f0 * elems_per_frame;
+    if (host_data) {   // host frames: the H2D copy of launch k+1 overlaps the walk of launch k
+      if (cstream != side) cudaStreamWaitEvent(cstream, sm->ev_stage_free[b], 0);   // prepare done with staging[b]
+      cudaMemcpyAsync(B.staging, chunk, sizeof(float) * (size_t)(nf * elems_per_frame), cudaMemcpyHostToDevice,
+                      cstream);
+      if (cstream != side) cudaEventRecord(sm->ev_staged[b], cstream);
+      chunk = B.staging;
+    }
     // ---- side stream: a1-a3 (compose, prepare/COUNT, ALLOCATE) into buffer b
     cudaStreamWaitEvent(side, sm->ev_free[b], 0);   // the walk that last read buffer b is done
     ComposeParams cp;
@@ -1317,12 +1338,7 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
       compose_kernel<<<1, kMaxBatch, 0, side>>>(cp, B.frame_T);
     }
     cudaMemsetAsync(B.lcnt, 0, 4 * sizeof(int), side);
-    const float* chunk = data + (long long)f0 * elems_per_frame;
-    if (host_data) {   // host frames: the H2D copy of launch k+1 overlaps the walk of launch k
-      cudaMemcpyAsync(B.staging, chunk, sizeof(float) * (size_t)(nf * elems_per_frame), cudaMemcpyHostToDevice,
-                      side);
-      chunk = B.staging;
-    }
+    if (host_data && cstream != side) cudaStreamWaitEvent(side, sm->ev_staged[b], 0);
     PrepParams pp;
     pp.data = chunk;
     pp.n_per_frame = n_per_frame; pp.total = total;
@@ -1344,6 +1360,7 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
       ProfScope ps_(sm, "ray_prepare", side);
       prepare_kernel<<<blocks, 256, 0, side>>>(pp);
     }
+    if (host_data && cstream != side) cudaEventRecord(sm->ev_stage_free[b], side);   // staging[b] consumed
     WalkParams wp;
     wp.rays = (const RayRec*)B.rays; wp.ctr = sm->ctr; wp.hash = sm->hash; wp.pool = sm->pool;
     wp.slots = B.slot_lists; wp.lcnt = B.lcnt;

@@ -61,6 +61,11 @@ struct cvx_submap {
   } buf[2];
   cudaStream_t side = nullptr;
   cudaEvent_t ev_entry = nullptr, ev_prepared[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
+  // host frames (cvx_integrate_batch_host): H2D copies on their own stream, created on first use; the copy
+  // into staging[b] waits only for the prepare that last read staging[b] (ev_stage_free), so it runs up
+  // to one launch ahead of the side stream's ingest
+  cudaStream_t copy = nullptr;
+  cudaEvent_t ev_staged[2] = {nullptr, nullptr}, ev_stage_free[2] = {nullptr, nullptr};
   int next_buf = 0;
   bool aggregate = true;      // warp-aggregate equal-voxel updates before the L2 atomics
   bool serialize = false;     // profiling: run the pipeline's side work on the caller's stream
