@@ -59,15 +59,6 @@ struct ComposeParams {
 constexpr int kFrameRec = 16;
 
 // Organised-sensor patch one warp's rays come from: CVX_PATCH_ROWS rows x 32 / CVX_PATCH_ROWS columns.
-#ifndef CVX_TRASH
-#define CVX_TRASH 1
-#endif
-#ifndef CVX_FREE2
-#define CVX_FREE2 1
-#endif
-#if (CVX_FREE2 || CVX_BAND2) && !CVX_TRASH
-#error CVX_FREE2 / CVX_BAND2 need CVX_TRASH
-#endif
 #ifndef CVX_TIGHT
 #define CVX_TIGHT 0
 #endif
@@ -779,12 +770,10 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
 #if CVX_PF_ASM == 2
   __shared__ int s_pf[128];
 #endif
-#if CVX_TRASH
   // Blocks without a slot (pool overflow: dropped updates, CVX_E_CAPACITY) and idle lanes address the
   // trash block `max_blocks` of the accumulator (never folded), so no update needs a slot predicate.
   const int trash = p.pool.max_blocks;
   addr = (unsigned)trash * 512u;
-#endif
   // kFuse: current block coordinates and the prefetched neighbour entries, per thread
   __shared__ int4 s_cb[kFuse ? 128 : 1];
   __shared__ longlong2 s_cand[kFuse ? 3 * 128 : 1];
@@ -844,14 +833,10 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
       if (list && nblk > 1) nslot = __ldg(list + 1);
 #endif
     }
-#if CVX_TRASH
     if (slot < 0) slot = trash;
-#endif
     addr = (unsigned)slot * 512u + (unsigned)((v0 & 7) | ((v1 & 7) << 3) | ((v2 & 7) << 6));
   }
-#if CVX_FREE2
   if (!have) { k0 = 0x3fffffff; s0 = 0; cexp = 1u; }   // parked idle lane (see the free prefix below)
-#endif
   const int da0 = s0, da1 = 8 * s1, da2 = 64 * s2;
   const int tq2 = 2 * p.tq;
   const long long s_off = (1ll << (kSdfF - 1)) + ((long long)p.tq << kSdfF);
@@ -881,14 +866,9 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
   const int mw = (int)__reduce_min_sync(0xffffffffu, (unsigned)mfree);
   auto body = [&](const int it, auto free_tag) {
     constexpr bool kFree = decltype(free_tag)::value;
-#if CVX_TRASH
     const bool upd = kFree ? true : it < n;
-#else
-    const bool upd = kFree ? slot >= 0 : (it < n && slot >= 0);
-#endif
     const int dpi = kFree ? tq2 : min(max((int)(S >> kSdfF), 0), tq2);   // round(sdf 2^q) + tq, clamped (O5, Q4)
     {
-#if CVX_TRASH
       // free phase: every lane updates, the key is the address; else key 0xffffffff (never an address:
       // < 2^23 slots) = no merging (in-band or finished lane)
       const unsigned key = (kFree || (upd & (dpi == tq2))) ? addr : 0xffffffffu;
@@ -896,13 +876,6 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
       const bool head = kFree ? ((lane == 0) | (prev != key))
                               : (upd & ((lane == 0) | (prev != key) | (key == 0xffffffffu)));
       const unsigned stops = __ballot_sync(0xffffffffu, kFree ? head : (head | !upd));
-#else
-      // key 0xffffffff (never an address: < 2^23 slots): no merging (in-band or idle lane)
-      const unsigned key = (kFree ? upd : (upd & (dpi == tq2))) ? addr : 0xffffffffu;
-      const unsigned prev = __shfl_up_sync(0xffffffffu, key, 1);
-      const bool head = upd & ((lane == 0) | (prev != key) | (key == 0xffffffffu));
-      const unsigned stops = __ballot_sync(0xffffffffu, head | !upd);
-#endif
       const unsigned above = stops & (0xfffffffeu << lane);
       const unsigned len = (unsigned)__clz(__brev(above)) - (unsigned)lane;
 #if CVX_VAL2
@@ -919,11 +892,7 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
       atomicAdd(p.pool.cacc + 2ull * addr, (1ull << kCntShift) | cr);
       atomicAdd(p.pool.cacc + 2ull * addr + 1, (cg << 32) | cb);
     }
-#if CVX_TRASH
     const bool stp = kFree ? have : it + 1 < n;   // the free prefix ends before the last voxel of every ray
-#else
-    const bool stp = it + 1 < n;
-#endif
     const bool g0 = k0 > 0, g1 = k1 > 0, g2 = k2 > 0;
     const bool yf = g1 & (!g0 | ((ST)D01 > 0));
     const bool zf = g2 & (yf ? ((ST)D12 > 0) : (!g0 | ((ST)D02 > 0)));
@@ -940,15 +909,12 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
       } else {
         slot = hash_find(p.hash, pack_key((vb0 - s0 * k0) >> 3, (vb1 - s1 * k1) >> 3, (vb2 - s2 * k2) >> 3));
       }
-#if CVX_TRASH
       if (slot < 0) slot = trash;
-#endif
       const int da = zf ? da2 : (yf ? da1 : da0);
       addr = (unsigned)slot * 512u + ((((addr - (unsigned)da) & 511u) & ~m) | (cexp & m));
     }
   };
   int it = 0;
-#if CVX_FREE2
   // Free prefix, hand-scheduled: every lane (idle lanes parked on the trash block, stepping x by 0 and
   // never meeting a block boundary) updates its voxel with the clamped d' = 2 tq; runs of equal
   // addresses in adjacent lanes issue one reduction of len * (2^40 | 2 tq).
@@ -981,9 +947,6 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
       }
     }
   }
-#else
-  for (; it < mw; ++it) body(it, std::true_type{});
-#endif
   S -= U0 * (K0 - k0) + U1 * (K1 - k1) + U2 * (K2 - k2);
 #if CVX_BAND2
   if constexpr (!kColor) {
