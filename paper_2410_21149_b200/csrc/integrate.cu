@@ -469,9 +469,6 @@ __global__ void __launch_bounds__(256) block_walk2_kernel(const __grid_constant_
 // E_ij > 0  <=>  H_ij = F_ij - floor(-C_ij / 2^16) > 0; H_ij moves by a_j / -a_i per step like E_ij by
 // 2^16 a_j / -2^16 a_i, and |H_ij| <= 3 max(a) while both axes have crossings left.  Exact whenever
 // every |D_a| < 2^28 (spans < 2^12 voxels), which the launch checks from the sensor's max range.
-#ifndef CVX_VAL2
-#define CVX_VAL2 0
-#endif
 #ifndef CVX_V_MINB
 #define CVX_V_MINB 8
 #endif
@@ -649,6 +646,21 @@ __device__ __forceinline__ void pf_issue(int* sdst, const int* src, bool pred) {
 __device__ __forceinline__ int pf_take(const int* sdst) {
   asm volatile("cp.async.wait_all;" ::: "memory");
   return *(volatile const int*)sdst;
+}
+
+// Length of the run headed by `lane`: distance to the next run head above it (`above` = the heads above
+// `lane`), 32 - lane for the last run.  brev + bfind.shiftamt is count-trailing-zeros, 0xffffffff for 0.
+#ifndef CVX_RUNLEN_PTX
+#define CVX_RUNLEN_PTX 1
+#endif
+__device__ __forceinline__ unsigned run_len(unsigned above, int lane) {
+#if CVX_RUNLEN_PTX
+  unsigned r;
+  asm("{\n\t.reg .b32 t;\n\tbrev.b32 t, %1;\n\tbfind.shiftamt.u32 %0, t;\n\t}" : "=r"(r) : "r"(above));
+  return min(r, 32u) - (unsigned)lane;
+#else
+  return (unsigned)__clz(__brev(above)) - (unsigned)lane;
+#endif
 }
 
 // Approximate fp32 reciprocal / reciprocal square root (MUFU only; used for guesses that are checked
@@ -864,42 +876,36 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
     mfree = max(mfree, mtight);
   }
   const int mw = (int)__reduce_min_sync(0xffffffffu, (unsigned)mfree);
-  auto body = [&](const int it, auto free_tag) {
-    constexpr bool kFree = decltype(free_tag)::value;
-    const bool upd = kFree ? true : it < n;
-    const int dpi = kFree ? tq2 : min(max((int)(S >> kSdfF), 0), tq2);   // round(sdf 2^q) + tq, clamped (O5, Q4)
+  // General band step (TSDF + Color: colour sums need the per-lane band test; and CVX_BAND2 = 0): finished
+  // lanes (it >= n) are masked instead of parked.
+  auto band_body = [&](const int it) {
+    const bool upd = it < n;
+    const int dpi = min(max((int)(S >> kSdfF), 0), tq2);   // round(sdf 2^q) + tq, clamped (O5, Q4)
     {
-      // free phase: every lane updates, the key is the address; else key 0xffffffff (never an address:
-      // < 2^23 slots) = no merging (in-band or finished lane)
-      const unsigned key = (kFree || (upd & (dpi == tq2))) ? addr : 0xffffffffu;
+      // key 0xffffffff (never an address: < 2^23 slots) = no merging (in-band or finished lane)
+      const unsigned key = (upd & (dpi == tq2)) ? addr : 0xffffffffu;
       const unsigned prev = __shfl_up_sync(0xffffffffu, key, 1);
-      const bool head = kFree ? ((lane == 0) | (prev != key))
-                              : (upd & ((lane == 0) | (prev != key) | (key == 0xffffffffu)));
-      const unsigned stops = __ballot_sync(0xffffffffu, kFree ? head : (head | !upd));
-      const unsigned above = stops & (0xfffffffeu << lane);
-      const unsigned len = (unsigned)__clz(__brev(above)) - (unsigned)lane;
-#if CVX_VAL2
+      const bool head = upd & ((lane == 0) | (prev != key) | (key == 0xffffffffu));
+      const unsigned stops = __ballot_sync(0xffffffffu, head | !upd);
+      const unsigned len = run_len(stops & (0xfffffffeu << lane), lane);
       // len * (2^40 | dpi) as two 32-bit halves: hi = len << 8, lo = len * dpi (< 2^22, no carry)
       const unsigned long long val = ((unsigned long long)(len << (kCntShift - 32)) << 32) | (len * (unsigned)dpi);
-#else
-      const unsigned long long val = (unsigned long long)len * ((1ull << kCntShift) | (unsigned long long)dpi);
-#endif
       asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.relaxed.gpu.global.add.u64 [%0], %1;\n\t}"
                    :: "l"(acc + addr), "l"(val), "r"((unsigned)head) : "memory");
     }
-    if (!kFree && kColor && upd && S > band_lo && S < band_hi) {
+    if (kColor && upd && S > band_lo && S < band_hi) {
       const unsigned long long cr = rgb & 0xffu, cg = (rgb >> 8) & 0xffu, cb = (rgb >> 16) & 0xffu;
       atomicAdd(p.pool.cacc + 2ull * addr, (1ull << kCntShift) | cr);
       atomicAdd(p.pool.cacc + 2ull * addr + 1, (cg << 32) | cb);
     }
-    const bool stp = kFree ? have : it + 1 < n;   // the free prefix ends before the last voxel of every ray
+    const bool stp = it + 1 < n;
     const bool g0 = k0 > 0, g1 = k1 > 0, g2 = k2 > 0;
     const bool yf = g1 & (!g0 | ((ST)D01 > 0));
     const bool zf = g2 & (yf ? ((ST)D12 > 0) : (!g0 | ((ST)D02 > 0)));
     const bool bz = stp & zf, by = stp & yf & !zf, bx = stp & !yf & !zf;
-    if (bx) { addr += da0; --k0; D01 += I1; D02 += I2; if (!kFree) S -= U0; }
-    if (by) { addr += da1; --k1; D01 -= I0; D12 += I2; if (!kFree) S -= U1; }
-    if (bz) { addr += da2; --k2; D02 -= I0; D12 -= I1; if (!kFree) S -= U2; }
+    if (bx) { addr += da0; --k0; D01 += I1; D02 += I2; S -= U0; }
+    if (by) { addr += da1; --k1; D01 -= I0; D12 += I2; S -= U1; }
+    if (bz) { addr += da2; --k2; D02 -= I0; D12 -= I1; S -= U2; }
     const unsigned m = zf ? 0x1c0u : (yf ? 0x38u : 7u);
     if (stp & (((addr ^ cexp) & m) == 0u)) {      // entered the next block of the ray
       ++j;
@@ -926,7 +932,7 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
       const unsigned prev = __shfl_up_sync(0xffffffffu, addr, 1);
       const bool head = lane0 | (prev != addr);
       const unsigned stops = __ballot_sync(0xffffffffu, head);
-      const unsigned len = (unsigned)__clz(__brev(stops & above_mask)) - (unsigned)lane;
+      const unsigned len = run_len(stops & above_mask, lane);
       const unsigned long long val = ((unsigned long long)(len << (kCntShift - 32)) << 32) | (len * utq2);
       asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.relaxed.gpu.global.add.u64 [%0], %1;\n\t}"
                    :: "l"(acc + addr), "l"(val), "r"((unsigned)head) : "memory");
@@ -964,7 +970,7 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
       const unsigned prev = __shfl_up_sync(0xffffffffu, key, 1);
       const bool head = lane0 | (prev != key) | (key == 0xffffffffu);
       const unsigned stops = __ballot_sync(0xffffffffu, head);
-      const unsigned len = (unsigned)__clz(__brev(stops & above_mask)) - (unsigned)lane;
+      const unsigned len = run_len(stops & above_mask, lane);
       const unsigned long long val = ((unsigned long long)(len << (kCntShift - 32)) << 32) | (len * (unsigned)dpi);
       asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.relaxed.gpu.global.add.u64 [%0], %1;\n\t}"
                    :: "l"(acc + addr), "l"(val), "r"((unsigned)head) : "memory");
@@ -994,7 +1000,7 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
 #if CVX_PF_ASM == 2
   if (list) nslot = pf_take(s_pf + threadIdx.x);   // the general band body keeps the prefetch in a register
 #endif
-  for (; it < maxn; ++it) body(it, std::false_type{});
+  for (; it < maxn; ++it) band_body(it);
 }
 
 // Block-count submap trigger: after the ALLOCATE phase of frame k, fire once the
