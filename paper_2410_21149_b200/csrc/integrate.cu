@@ -668,6 +668,7 @@ __device__ __forceinline__ unsigned run_len(unsigned above, int lane) {
 __device__ __forceinline__ float rcp_approx(float x) { float y; asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
 __device__ __forceinline__ float rsqrt_approx(float x) { float y; asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
 
+#if CVX_TIGHT
 // Exact free prefix of a ray from a crossing count (checked in the walk's own integer arithmetic).
 // Take a segment fraction f = F / 2^20; the crossings strictly before f are C_a = #boundaries of axis a
 // strictly between A_a and X_a = A_a + f D_a, and the walk takes exactly those first (crossing-time
@@ -702,6 +703,7 @@ __device__ __forceinline__ int tight_free_prefix(const RayRec* rp, long long S, 
   }
   return (Sf >= thr && i_f + 1 <= n - 1) ? i_f + 1 : 0;
 }
+#endif
 
 // Constant-weight walk with the voxel address carried incrementally (same decisions as walk_kernel
 // <true, true, k32, kColor>; see there for O4/O5).  Per step only the stepped axis' crossing count,
@@ -955,10 +957,11 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
   }
   S -= U0 * (K0 - k0) + U1 * (K1 - k1) + U2 * (K2 - k2);
 #if CVX_BAND2
-  if constexpr (!kColor) {
+  {
     // Rest of the rays, hand-scheduled like the free prefix: a lane that has written its last voxel
-    // parks on its warp's trash spot (x step of 0, never a block boundary, d' = 2 tq forever) so no
-    // update or step needs a per-lane predicate; parked lanes' reductions land in the trash region.
+    // parks on its warp's trash spot (x step of 0, never a block boundary, d' = 2 tq forever, outside
+    // the colour band) so no update or step needs a per-lane predicate; parked lanes' reductions land
+    // in the trash region.
     const unsigned above_mask = 0xfffffffeu << lane;
     const bool lane0 = lane == 0;
     const unsigned spot = (unsigned)trash * 512u + ((((unsigned)idx >> 5) & 4095u) << 3);
@@ -974,6 +977,11 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
       const unsigned long long val = ((unsigned long long)(len << (kCntShift - 32)) << 32) | (len * (unsigned)dpi);
       asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.relaxed.gpu.global.add.u64 [%0], %1;\n\t}"
                    :: "l"(acc + addr), "l"(val), "r"((unsigned)head) : "memory");
+      if (kColor && S > band_lo && S < band_hi) {   // TSDF + Color: band updates carry the point's colour (R13)
+        const unsigned long long cr = rgb & 0xffu, cg = (rgb >> 8) & 0xffu, cb = (rgb >> 16) & 0xffu;
+        atomicAdd(p.pool.cacc + 2ull * addr, (1ull << kCntShift) | cr);
+        atomicAdd(p.pool.cacc + 2ull * addr + 1, (cg << 32) | cb);
+      }
       if (it + 1 >= n) {   // that was the ray's last voxel: park
         addr = spot; k0 = 0x3fffffff; k1 = 0; k2 = 0; dx0 = 0; cexp = 1u; S = (long long)tq2 << (kSdfF + 1); U0 = 0;
         n = 0x7fffffff;
