@@ -666,9 +666,9 @@ __device__ __forceinline__ unsigned run_len(unsigned above, int lane) {
 // Approximate fp32 reciprocal / reciprocal square root (MUFU only; used for guesses that are checked
 // exactly afterwards, so no IEEE slow path is needed).
 __device__ __forceinline__ float rcp_approx(float x) { float y; asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
-__device__ __forceinline__ float rsqrt_approx(float x) { float y; asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
 
 #if CVX_TIGHT
+__device__ __forceinline__ float rsqrt_approx(float x) { float y; asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
 // Exact free prefix of a ray from a crossing count (checked in the walk's own integer arithmetic).
 // Take a segment fraction f = F / 2^20; the crossings strictly before f are C_a = #boundaries of axis a
 // strictly between A_a and X_a = A_a + f D_a, and the walk takes exactly those first (crossing-time
