@@ -323,3 +323,24 @@ def test_walk_variants_bitexact(tiny, orc, monkeypatch, knob):
     assert np.array_equal(a[2].view(np.uint32), b[2].view(np.uint32))
     o, _ = oracle_build(tiny, frames)
     assert_tsdf_parity(b, o.export())
+
+
+def test_host_frames_many_launches_and_calls(tiny):
+    """Host frames over several walk launches (300 frames > kMaxBatch = 128 per launch) and several calls
+    of uneven size: the copy stream refills the two staging buffers while earlier launches are still
+    being ingested; the TSDF must equal one device-resident call bit for bit."""
+    from paper_2410_21149_b200 import Submap
+    idx = [k % 10 for k in range(300)]
+    dev_frames = torch.stack([tiny["frames"][k]["data"] for k in idx]).contiguous()
+    poses = np.stack([tiny["frames"][k]["T_world_sensor"] for k in idx])
+    a = Submap(tiny["grid"], tiny["submaps"][0]["T_world_submap"], 0)
+    a.integrate_batch(dev_frames.cuda(), poses, tiny["sensor"])
+    b = Submap(tiny["grid"], tiny["submaps"][0]["T_world_submap"], 0)
+    host = dev_frames.pin_memory()
+    for lo, hi in ((0, 100), (100, 250), (250, 300)):
+        b.integrate_batch_host(host[lo:hi], poses[lo:hi], tiny["sensor"])
+    ea, eb = gpu_export_sorted(a), gpu_export_sorted(b)
+    assert np.array_equal(ea[0], eb[0])
+    assert np.array_equal(ea[1].view(np.uint32), eb[1].view(np.uint32))
+    assert np.array_equal(ea[2].view(np.uint32), eb[2].view(np.uint32))
+    assert a.stats()["rays_used"] == b.stats()["rays_used"] > 0
