@@ -123,8 +123,9 @@ cvx_status cvx_integrate_batch(cvx_submap* submap, const float* data, int64_t n_
                                const cvx_sensor_model* sensor, void* stream, cvx_integrate_stats* stats);
 
 /* cvx_integrate_batch with the frames in HOST memory (page-locked recommended; pageable memory works
- * but its copies are synchronous): the library copies each launch's frames to the device on its side
- * stream, so the transfer of launch k+1 overlaps the update walk of launch k.  `host_data` must stay
+ * but its copies are synchronous): the library copies each launch's frames to the device on its own copy
+ * stream into one of two staging buffers, each copy waiting only for the ingest that last read that
+ * buffer, so the transfer of launch k+1 overlaps the ingest and update walk of launch k.  `host_data` must stay
  * valid and unmodified until `stream` has passed this call's work.  Same results and errors. */
 cvx_status cvx_integrate_batch_host(cvx_submap* submap, const float* host_data, int64_t n_per_frame,
                                     int32_t n_frames, const double* T_world_sensor,
