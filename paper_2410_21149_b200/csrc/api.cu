@@ -176,6 +176,7 @@ cvx_status cvx_create_submap(const cvx_grid_config* cfg, const double* T_world_s
   if (const char* b2 = std::getenv("CVX_BW2")) sm->bw2 = b2[0] != '0';              // tuning knob
   if (const char* wc = std::getenv("CVX_WALK_CW")) sm->walk_cw = wc[0] != '0';     // tuning knob
   if (const char* fa = std::getenv("CVX_FUSE_ALLOC")) sm->fuse_alloc = fa[0] != '0'; // tuning knob
+  if (const char* lc = std::getenv("CVX_LIST_CAP")) sm->list_cap_limit = std::atoll(lc);  // test knob
   sm->cfg = *cfg;
   std::memcpy(sm->T_ws, T_world_submap, sizeof(sm->T_ws));
   sm->device = device;

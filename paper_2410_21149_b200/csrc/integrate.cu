@@ -1327,7 +1327,7 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     pp.sdf_scale = std::ldexp(1.0, q + kSdfF);
     pp.height = sensor.height;
     pp.frame_T = B.frame_T; pp.rays = (RayRec*)B.rays; pp.ctr = sm->ctr; pp.lcnt = B.lcnt;
-    pp.list_cap = (int)std::min<long long>(B.slot_cap, 0x7fffffffll);
+    pp.list_cap = (int)std::min<long long>(std::min<long long>(B.slot_cap, sm->list_cap_limit), 0x7fffffffll);
     pp.trig = trig;
     pp.rgb = rgb ? rgb + (long long)f0 * n_per_frame * 3 : nullptr;
     pp.count_vox = 1;
