@@ -95,7 +95,20 @@ def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("CVX_BENCH_ONE_GPU") == "1":
+        local = 0        # test knob: every rank on cuda:0 (exercises the N > 1 code path on a 1-GPU box)
     return world, rank, local
+
+
+def init_pg(dev):
+    """NCCL process group (one rank per GPU); CVX_BENCH_BACKEND=gloo is the 1-GPU test knob (NCCL refuses
+    two ranks on one device)."""
+    import torch.distributed as dist
+    backend = os.environ.get("CVX_BENCH_BACKEND", "nccl")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group(backend)
 
 
 def make_workload(rank: int, device: torch.device):
@@ -237,7 +250,7 @@ def run_mav(args, world, rank, local):
     pg = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        init_pg(dev)
         pg = dist
     cfg = synth.make_config("mav", frames=[], device=dev)
     subs = cfg["submaps"]
@@ -323,7 +336,7 @@ def run_color(args, world, rank, local):
     pg = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        init_pg(dev)
         pg = dist
     cfg = synth.make_config("lidar", device=dev, seed=1 + 1000 * rank, color=True)
     data = torch.stack([cfg["frames"][k]["data"] for k in range(N_SCANS)]).contiguous()
@@ -525,7 +538,7 @@ def run_rgbd(args, world, rank, local):
     pg = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        init_pg(dev)
         pg = dist
     cfg0 = synth.make_config("rgbd", frames=[], device=dev)
     subs = cfg0["submaps"]
@@ -695,7 +708,7 @@ def main():
     pg = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        init_pg(dev)
         pg = dist
     cfg, data, poses = make_workload(rank, dev)
     sensor = cfg["sensor"]
