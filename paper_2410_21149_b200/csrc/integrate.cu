@@ -65,6 +65,11 @@ constexpr int kFrameRec = 16;
 #ifndef CVX_BAND2
 #define CVX_BAND2 1
 #endif
+// Slimmer block entry in walk_cw_kernel: the next slot is prefetched without a bound check (the slot-list
+// buffer keeps one spare entry past list_cap) and mapped to the trash block with one unsigned min.
+#ifndef CVX_ENTRY2
+#define CVX_ENTRY2 1
+#endif
 #ifndef CVX_PATCH_ROWS
 #define CVX_PATCH_ROWS 4
 #endif
@@ -643,6 +648,10 @@ __device__ __forceinline__ void pf_issue(int* sdst, const int* src, bool pred) {
   asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p cp.async.ca.shared.global [%0], [%1], 4;\n\tcp.async.commit_group;\n\t}"
                :: "r"(sa), "l"(src), "r"((unsigned)pred) : "memory");
 }
+__device__ __forceinline__ void pf_issue_u(int* sdst, const int* src) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n\tcp.async.commit_group;" :: "r"(sa), "l"(src) : "memory");
+}
 __device__ __forceinline__ int pf_take(const int* sdst) {
   asm volatile("cp.async.wait_all;" ::: "memory");
   return *(volatile const int*)sdst;
@@ -817,20 +826,26 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
       if ((unsigned long long)e.x != key || sl < 0) sl = hash_activate_pf(p.hash, p.pool, p.ctr, key, cb.x, cb.y, cb.z, e);
       s_cb[threadIdx.x] = cb;
       issue_candidates(cb);
-      return sl;
+      return CVX_ENTRY2 ? (int)min((unsigned)sl, (unsigned)trash) : sl;
     } else {
       if (list) {
 #if CVX_PF_ASM == 2
         const int sl = pf_take(s_pf + threadIdx.x);
+#if CVX_ENTRY2
+        pf_issue_u(s_pf + threadIdx.x, list + j + 1);   // one block ahead; past the last block: the spare entry
+        return (int)min((unsigned)sl, (unsigned)trash);   // kFailed (< 0) -> trash
+#else
         pf_issue(s_pf + threadIdx.x, list + j + 1, j + 1 < nblk);   // prefetch one block ahead
         return sl;
+#endif
 #else
         const int sl = nslot;
         prefetch_slot(nslot, list + j + 1, j + 1 < nblk);
         return sl;
 #endif
       }
-      return hash_find(p.hash, pack_key((vb0 - s0 * k0) >> 3, (vb1 - s1 * k1) >> 3, (vb2 - s2 * k2) >> 3));
+      const int sl = hash_find(p.hash, pack_key((vb0 - s0 * k0) >> 3, (vb1 - s1 * k1) >> 3, (vb2 - s2 * k2) >> 3));
+      return CVX_ENTRY2 ? (int)min((unsigned)sl, (unsigned)trash) : sl;
     }
   };
   if (have) {
@@ -842,7 +857,7 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
     } else {
       slot = list ? __ldg(list) : hash_find(p.hash, pack_key(v0 >> 3, v1 >> 3, v2 >> 3));
 #if CVX_PF_ASM == 2
-      pf_issue(s_pf + threadIdx.x, list + 1, list && nblk > 1);
+      pf_issue(s_pf + threadIdx.x, list + 1, CVX_ENTRY2 ? list != nullptr : (list && nblk > 1));
 #else
       if (list && nblk > 1) nslot = __ldg(list + 1);
 #endif
@@ -949,7 +964,7 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
       if (((addr ^ cexp) & m) == 0u) {      // entered the next block of the ray
         ++j;
         slot = next_slot(zf ? 2 : (yf ? 1 : 0));
-        if (slot < 0) slot = trash;
+        if (!CVX_ENTRY2 && slot < 0) slot = trash;
         const int da = zf ? da2 : (yf ? da1 : da0);
         addr = (unsigned)slot * 512u + ((((addr - (unsigned)da) & 511u) & ~m) | (cexp & m));
       }
@@ -997,7 +1012,7 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
       if (((addr ^ cexp) & m) == 0u) {      // entered the next block of the ray
         ++j;
         slot = next_slot(zf ? 2 : (yf ? 1 : 0));
-        if (slot < 0) slot = trash;
+        if (!CVX_ENTRY2 && slot < 0) slot = trash;
         const int da = zf ? da2 : (yf ? da1 : dx0);
         addr = (unsigned)slot * 512u + ((((addr - (unsigned)da) & 511u) & ~m) | (cexp & m));
       }
@@ -1327,7 +1342,8 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     pp.sdf_scale = std::ldexp(1.0, q + kSdfF);
     pp.height = sensor.height;
     pp.frame_T = B.frame_T; pp.rays = (RayRec*)B.rays; pp.ctr = sm->ctr; pp.lcnt = B.lcnt;
-    pp.list_cap = (int)std::min<long long>(std::min<long long>(B.slot_cap, sm->list_cap_limit), 0x7fffffffll);
+    // one spare entry: walk_cw_kernel prefetches the entry after a ray's last block unconditionally
+    pp.list_cap = (int)std::min<long long>(std::min<long long>(B.slot_cap - 1, sm->list_cap_limit), 0x7fffffffll);
     pp.trig = trig;
     pp.rgb = rgb ? rgb + (long long)f0 * n_per_frame * 3 : nullptr;
     pp.count_vox = 1;
@@ -1443,7 +1459,7 @@ cudaError_t launch_integrate_projective(cvx_submap* sm, const float* depth, int6
       pp.sdf_scale = std::ldexp(1.0, q + kSdfF);
       pp.height = sensor.height;
       pp.frame_T = B.frame_T; pp.rays = (RayRec*)B.rays; pp.ctr = sm->ctr; pp.lcnt = B.lcnt;
-      pp.list_cap = (int)std::min<long long>(B.slot_cap, 0x7fffffffll);
+      pp.list_cap = (int)std::min<long long>(B.slot_cap - 1, 0x7fffffffll);
       pp.trig = nullptr;
       pp.rgb = nullptr;
       pp.count_vox = 0;   // voxel_updates counts the projective updates instead
