@@ -70,6 +70,9 @@ constexpr int kFrameRec = 16;
 #ifndef CVX_ENTRY2
 #define CVX_ENTRY2 1
 #endif
+#ifndef CVX_WG0
+#define CVX_WG0 1
+#endif
 #ifndef CVX_PATCH_ROWS
 #define CVX_PATCH_ROWS 4
 #endif
@@ -653,7 +656,11 @@ __device__ __forceinline__ void pf_issue_u(int* sdst, const int* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n\tcp.async.commit_group;" :: "r"(sa), "l"(src) : "memory");
 }
 __device__ __forceinline__ int pf_take(const int* sdst) {
+#if CVX_WG0
+  asm volatile("cp.async.wait_group 0;" ::: "memory");   // every cp.async here is committed at issue
+#else
   asm volatile("cp.async.wait_all;" ::: "memory");
+#endif
   return *(volatile const int*)sdst;
 }
 
@@ -828,7 +835,7 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
       issue_candidates(cb);
       return CVX_ENTRY2 ? (int)min((unsigned)sl, (unsigned)trash) : sl;
     } else {
-      if (list) {
+      if (off >= 0) {   // == list != nullptr, one 32-bit compare
 #if CVX_PF_ASM == 2
         const int sl = pf_take(s_pf + threadIdx.x);
 #if CVX_ENTRY2
@@ -966,7 +973,13 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
         slot = next_slot(zf ? 2 : (yf ? 1 : 0));
         if (!CVX_ENTRY2 && slot < 0) slot = trash;
         const int da = zf ? da2 : (yf ? da1 : da0);
+#if CVX_ENTRY2
+        // the step wrapped the stepped axis' local field (carry / borrow into the next field): -8 da undoes
+        // the carry and leaves the field at its entry value; keep the local bits, switch the slot
+        addr = ((unsigned)slot << 9) | ((addr - 8u * (unsigned)da) & 511u);
+#else
         addr = (unsigned)slot * 512u + ((((addr - (unsigned)da) & 511u) & ~m) | (cexp & m));
+#endif
       }
     }
   }
@@ -1014,7 +1027,13 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
         slot = next_slot(zf ? 2 : (yf ? 1 : 0));
         if (!CVX_ENTRY2 && slot < 0) slot = trash;
         const int da = zf ? da2 : (yf ? da1 : dx0);
+#if CVX_ENTRY2
+        // the step wrapped the stepped axis' local field (carry / borrow into the next field): -8 da undoes
+        // the carry and leaves the field at its entry value; keep the local bits, switch the slot
+        addr = ((unsigned)slot << 9) | ((addr - 8u * (unsigned)da) & 511u);
+#else
         addr = (unsigned)slot * 512u + ((((addr - (unsigned)da) & 511u) & ~m) | (cexp & m));
+#endif
       }
     }
     return;
