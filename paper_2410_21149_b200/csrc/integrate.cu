@@ -847,8 +847,8 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
 #endif
 #else
         const int sl = nslot;
-        prefetch_slot(nslot, list + j + 1, j + 1 < nblk);
-        return sl;
+        prefetch_slot(nslot, list + j + 1, CVX_ENTRY2 ? true : j + 1 < nblk);
+        return CVX_ENTRY2 ? (int)min((unsigned)sl, (unsigned)trash) : sl;
 #endif
       }
       const int sl = hash_find(p.hash, pack_key((vb0 - s0 * k0) >> 3, (vb1 - s1 * k1) >> 3, (vb2 - s2 * k2) >> 3));
