@@ -743,6 +743,23 @@ def main():
         parts = gather_packed(m.pack())
         gather_bytes[0] = sum(p.numel() for p in parts)
 
+    # N > 1: the gather of step i (pack + all-gather; the sizes exchange reads back to the host) is issued
+    # after the integration of step i + 1, so that host sync does not serialise the two submaps in flight
+    pending = []
+
+    def finish_pending():
+        while pending:
+            m_, st_ = pending.pop()
+            with torch.cuda.stream(st_):
+                gather(m_)
+
+    def defer_gather(m, k, pipelined):
+        if pg is None:
+            return
+        pending.append((m, streams[k]))
+        if not pipelined:
+            finish_pending()
+
     # Two submaps in flight (the paper's frontend/backend queues): step i builds submap i on builder i % 2
     # and its own stream, so the exact ESDF + queries of step i (HBM / latency bound) overlap the
     # integration of step i + 1 (ALU bound).  Every step is still one complete pass of a1-a7 over its own
@@ -760,9 +777,11 @@ def main():
             d = data if src is None else src
             for c in range(0, N_SCANS, args.batch):
                 m.integrate_batch(d[c:c + args.batch], poses[c:c + args.batch], sensor)
+        finish_pending()                 # gather of the previous step (N > 1)
+        with torch.cuda.stream(streams[k]):
             m.finalize_esdf()
             m.query(queries, *qouts[k])
-            gather(m)
+        defer_gather(m, k, pipelined)
 
     def timed(fn, n):
         """Device time of n steps: events on the caller's stream, both builder streams joined."""
@@ -772,6 +791,7 @@ def main():
         streams[1].wait_stream(stream)
         for i in range(n):
             fn(i)
+        finish_pending()
         stream.wait_stream(streams[1])
         b.record(stream)
         torch.cuda.synchronize()
@@ -779,6 +799,7 @@ def main():
 
     for i in range(args.warmup):
         step(i)
+    finish_pending()
     torch.cuda.synchronize()
     st = sm.stats()
     nb = sm.block_count()
@@ -829,14 +850,17 @@ def main():
                 m.reset()
                 for c in range(0, N_SCANS, args.batch):
                     m.integrate_batch_host(host_frames[c:c + args.batch], poses[c:c + args.batch], sensor)
+            finish_pending()
+            with torch.cuda.stream(streams[k]):
                 m.finalize_esdf()
                 m.query(dev_qs[k], *qouts[k])
-                gather(m)
                 host_outs[k][0].copy_(qouts[k][0], non_blocking=True)
                 host_outs[k][1].copy_(qouts[k][1], non_blocking=True)
+            defer_gather(m, k, True)
 
         e2e_step(0)
         e2e_step(1)
+        finish_pending()
         if pg is not None:
             pg.barrier()
         ems = timed(e2e_step, args.steps)
