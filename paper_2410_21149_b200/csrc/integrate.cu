@@ -1268,8 +1268,12 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
   // launches of equal size; at most kMaxBatch frames and kLaunchRays rays (pipelining granularity).
   // Constant weights: the packed accumulators are folded whenever the next launch would take them past
   // kMaxPackedRays rays since the last fold, and at the end of the call (R6/R7)
-  const bool cw_ok = sm->aggregate && sm->cfg.weighting == 0 && n_per_frame <= kLaunchRays;
-  const long long ray_limit = cw_ok ? kLaunchRays : (1ll << 31) - 1;
+  // Host frames use half-size launches: the first launch's H2D copy has no earlier walk of the call to
+  // hide under, so it is kept short (measured: 2^23-ray launches 8.50 ms device-resident vs 2^22 8.75 ms;
+  // with host frames 9.50 vs 9.28 ms per configs[1] step)
+  const long long launch_rays = host_data ? kLaunchRaysHost : kLaunchRays;
+  const bool cw_ok = sm->aggregate && sm->cfg.weighting == 0 && n_per_frame <= launch_rays;
+  const long long ray_limit = cw_ok ? launch_rays : (1ll << 31) - 1;
   const int lim = trig ? 1 : (int)std::max<long long>(1, std::min<long long>(kMaxBatch, ray_limit / n_per_frame));
   std::vector<int> plan;                             // equal chunks
   {
@@ -1381,7 +1385,7 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     wp.q = q;
     wp.band = std::llround(std::ldexp(sm->cfg.truncation, q + kSdfF));
     wp.birth = nullptr;
-    const bool cw = cw_ok && total <= kLaunchRays;
+    const bool cw = cw_ok && total <= launch_rays;
     // constant weights, no colour, no block-count trigger: ALLOCATE runs inside the update walk
     const bool fuse = sm->fuse_alloc && cw && sm->aggregate && sm->walk_cw && !rgb && !trig;
     if (!fuse) {
