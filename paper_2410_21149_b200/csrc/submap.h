@@ -110,7 +110,10 @@ struct ProfScope {
 
 namespace cvx {
 
-constexpr int kMaxBatch = 128;   // frames per integrate launch
+#ifndef CVX_MAX_BATCH
+#define CVX_MAX_BATCH 200
+#endif
+constexpr int kMaxBatch = CVX_MAX_BATCH;   // frames per integrate launch (poses travel as kernel parameters)
 constexpr int kSlotsPerRay = 40; // average block-slot list capacity per ray (overflow -> hashed walk)
 
 // integrate.cu

@@ -327,7 +327,7 @@ def test_walk_variants_bitexact(tiny, orc, monkeypatch, knob):
 
 
 def test_host_frames_many_launches_and_calls(tiny):
-    """Host frames over several walk launches (300 frames > kMaxBatch = 128 per launch) and several calls
+    """Host frames over several walk launches (300 frames > kMaxBatch = 200 per launch) and several calls
     of uneven size: the copy stream refills the two staging buffers while earlier launches are still
     being ingested; the TSDF must equal one device-resident call bit for bit."""
     from paper_2410_21149_b200 import Submap
