@@ -743,27 +743,32 @@ def main():
         parts = gather_packed(m.pack())
         gather_bytes[0] = sum(p.numel() for p in parts)
 
-    # N > 1: the gather of step i (pack + all-gather; the sizes exchange reads back to the host) is issued
-    # after the integration of step i + 1, so that host sync does not serialise the two submaps in flight
-    pending = []
-
-    def finish_pending():
-        while pending:
-            m_, st_ = pending.pop()
-            with torch.cuda.stream(st_):
-                gather(m_)
-
-    def defer_gather(m, k, pipelined):
-        if pg is None:
-            return
-        pending.append((m, streams[k]))
-        if not pipelined:
-            finish_pending()
-
     # Two submaps in flight (the paper's frontend/backend queues): step i builds submap i on builder i % 2
-    # and its own stream, so the exact ESDF + queries of step i (HBM / latency bound) overlap the
-    # integration of step i + 1 (ALU bound).  Every step is still one complete pass of a1-a7 over its own
-    # submap; `one_submap_in_flight` below times the same steps strictly one after another.
+    # and its own stream.  Its front half (reset + integration) is enqueued first, then the back half
+    # (finalize_esdf, queries, N > 1 gather) of step i - 1, so the exact ESDF + queries of step i - 1
+    # (HBM / latency bound) overlap the integration of step i (ALU bound) and the host syncs of the back
+    # half (finalize reads the block count / AABB; the gather exchanges sizes) never stall the next
+    # integration.  Every step is still one complete pass of a1-a7 over its own submap; the last back half
+    # runs inside the timed region (flush); `one_submap_in_flight` below times the same steps strictly one
+    # after another.
+    # The integrations themselves stay in order (step i's waits for step i - 1's on the device, not the
+    # host): two concurrent walks only compete for the same ALU slots, while a walk beside an ESDF pass
+    # fills them.  With host frames the library's copies of step i still start early (copy stream).
+    backlog = []
+    integrated = [torch.cuda.Event(), torch.cuda.Event()]
+    last_integrated = [None]
+
+    def flush():
+        while backlog:
+            backlog.pop()()
+
+    def after_previous_integration(k):
+        if last_integrated[0] is not None:
+            streams[k].wait_event(last_integrated[0])
+
+    def mark_integrated(k):
+        integrated[k].record(streams[k])
+        last_integrated[0] = integrated[k]
     sm2 = cvx.Submap(cfg["grid"], cfg["submaps"][0]["T_world_submap"], local)
     builders = [sm, sm2]
     streams = [stream, torch.cuda.Stream(dev)]
@@ -773,15 +778,22 @@ def main():
         k = i % 2 if pipelined else 0
         m = builders[k]
         with torch.cuda.stream(streams[k]):
+            after_previous_integration(k)
             m.reset()
             d = data if src is None else src
             for c in range(0, N_SCANS, args.batch):
                 m.integrate_batch(d[c:c + args.batch], poses[c:c + args.batch], sensor)
-        finish_pending()                 # gather of the previous step (N > 1)
-        with torch.cuda.stream(streams[k]):
-            m.finalize_esdf()
-            m.query(queries, *qouts[k])
-        defer_gather(m, k, pipelined)
+            mark_integrated(k)
+
+        def back():
+            with torch.cuda.stream(streams[k]):
+                m.finalize_esdf()
+                m.query(queries, *qouts[k])
+                gather(m)
+        flush()                          # back half of the previous step
+        backlog.append(back)
+        if not pipelined:
+            flush()
 
     def timed(fn, n):
         """Device time of n steps: events on the caller's stream, both builder streams joined."""
@@ -791,7 +803,7 @@ def main():
         streams[1].wait_stream(stream)
         for i in range(n):
             fn(i)
-        finish_pending()
+        flush()
         stream.wait_stream(streams[1])
         b.record(stream)
         torch.cuda.synchronize()
@@ -799,7 +811,7 @@ def main():
 
     for i in range(args.warmup):
         step(i)
-    finish_pending()
+    flush()
     torch.cuda.synchronize()
     st = sm.stats()
     nb = sm.block_count()
@@ -847,20 +859,25 @@ def main():
             m = builders[k]
             with torch.cuda.stream(streams[k]):
                 dev_qs[k].copy_(host_q, non_blocking=True)
+                after_previous_integration(k)
                 m.reset()
                 for c in range(0, N_SCANS, args.batch):
                     m.integrate_batch_host(host_frames[c:c + args.batch], poses[c:c + args.batch], sensor)
-            finish_pending()
-            with torch.cuda.stream(streams[k]):
-                m.finalize_esdf()
-                m.query(dev_qs[k], *qouts[k])
-                host_outs[k][0].copy_(qouts[k][0], non_blocking=True)
-                host_outs[k][1].copy_(qouts[k][1], non_blocking=True)
-            defer_gather(m, k, True)
+                mark_integrated(k)
+
+            def back():
+                with torch.cuda.stream(streams[k]):
+                    m.finalize_esdf()
+                    m.query(dev_qs[k], *qouts[k])
+                    host_outs[k][0].copy_(qouts[k][0], non_blocking=True)
+                    host_outs[k][1].copy_(qouts[k][1], non_blocking=True)
+                    gather(m)
+            flush()
+            backlog.append(back)
 
         e2e_step(0)
         e2e_step(1)
-        finish_pending()
+        flush()
         if pg is not None:
             pg.barrier()
         ems = timed(e2e_step, args.steps)
