@@ -492,7 +492,8 @@ def run_esdf_stress(args, world, rank, local):
                                             "blocks": nb, "allocated_voxels": va, "aabb_voxels": dims.tolist()},
             "dense_gvox_per_s": N / 1e9 / (ms / 1e3), "kernel_ms_per_step": per,
             "roofline": {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
-                         "frac": ach / hbm, "traffic": ncu_traffic(dom, "esdf_stress"), "peak_source": hbm_src,
+                         "frac": ach / hbm, "traffic": (ncu_traffic(dom, "esdf_stress") or {}).get("bytes_per_launch"),
+                         "traffic_source": (ncu_traffic(dom, "esdf_stress") or {}).get("source"), "peak_source": hbm_src,
                          "all_passes_gbs": tot_alg},
             "gpu_launches": sum(v["n"] for v in prof.values()), "clocks": clk.summary()}
     if rank == 0:
@@ -944,7 +945,9 @@ def main():
                     "frac": ach / peak_tops, "traffic": None,
                     "updates_per_s": upd_launch / (avg_ms / 1e3), "ops_per_update": 13,
                     "peak_source": f"148 SM x 128 lanes x {clk_mhz:.0f} MHz (median under load)"}
-    roofline["traffic"] = ncu_traffic(dom)
+    tr = ncu_traffic(dom)
+    roofline["traffic"] = tr["bytes_per_launch"] if tr else None   # DRAM bytes per launch (ncu)
+    roofline["traffic_source"] = tr["source"] if tr else None
     if dom == "ray_walk_update":
         # the walk's real ceiling is the issue rate (one warp instruction per SMSP per clock): ncu's issue
         # utilisation of the same kernel says how close the instruction stream is to it
