@@ -148,7 +148,10 @@ constexpr long long kMaxPackedRays = (1ll << 24) - 1;
 #endif
 constexpr long long kLaunchRays = (1ll << CVX_LAUNCH_LOG2) - 1;   // rays per walk launch (pipelining granularity)
 static_assert(CVX_LAUNCH_LOG2 <= 24, "the fold runs once per 2^24 rays; a launch must not exceed it");
-constexpr long long kLaunchRaysHost = (1ll << 22) - 1;   // host frames (copy pipelining)
+#ifndef CVX_HOST_LAUNCH_LOG2
+#define CVX_HOST_LAUNCH_LOG2 22
+#endif
+constexpr long long kLaunchRaysHost = (1ll << CVX_HOST_LAUNCH_LOG2) - 1;   // host frames (copy pipelining)
 inline int packed_q(double tau) {
   int q = (int)std::floor(std::log2(32768.0 / tau));
   return q < 0 ? 0 : (q > 30 ? 30 : q);
