@@ -73,6 +73,9 @@ constexpr int kFrameRec = 16;
 #ifndef CVX_WG0
 #define CVX_WG0 1
 #endif
+#ifndef CVX_COPY_EARLY
+#define CVX_COPY_EARLY 1
+#endif
 #ifndef CVX_PATCH_ROWS
 #define CVX_PATCH_ROWS 4
 #endif
@@ -1268,9 +1271,8 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
   // launches of equal size; at most kMaxBatch frames and kLaunchRays rays (pipelining granularity).
   // Constant weights: the packed accumulators are folded whenever the next launch would take them past
   // kMaxPackedRays rays since the last fold, and at the end of the call (R6/R7)
-  // Host frames use half-size launches: the first launch's H2D copy has no earlier walk of the call to
-  // hide under, so it is kept short (measured: 2^23-ray launches 8.50 ms device-resident vs 2^22 8.75 ms;
-  // with host frames 9.50 vs 9.28 ms per configs[1] step)
+  // Host frames use smaller launches (kLaunchRaysHost) so the H2D copies pipeline with the ingest of the
+  // call's earlier launches (configs[1] e2e step, copies started early: 2^22 8.80 ms, 2^23 8.70, 2^24 8.8-9.0)
   const long long launch_rays = host_data ? kLaunchRaysHost : kLaunchRays;
   const bool cw_ok = sm->aggregate && sm->cfg.weighting == 0 && n_per_frame <= launch_rays;
   const long long ray_limit = cw_ok ? launch_rays : (1ll << 31) - 1;
@@ -1323,7 +1325,12 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
       if (e != cudaSuccess) return e;
     }
     cstream = sm->copy;
+#if !CVX_COPY_EARLY
     cudaStreamWaitEvent(cstream, sm->ev_entry, 0);
+#endif
+    // CVX_COPY_EARLY: the copy into staging[b] waits only for the prepare that last read staging[b]
+    // (ev_stage_free) — nothing else on the device touches the staging buffers — so a call's copies can
+    // run under whatever the caller's stream is still doing (e.g. the previous submap's walk)
   }
   int f0 = 0;
   for (const int nf : plan) {
