@@ -125,8 +125,11 @@ cvx_status cvx_integrate_batch(cvx_submap* submap, const float* data, int64_t n_
 /* cvx_integrate_batch with the frames in HOST memory (page-locked recommended; pageable memory works
  * but its copies are synchronous): the library copies each launch's frames to the device on its own copy
  * stream into one of two staging buffers, each copy waiting only for the ingest that last read that
- * buffer, so the transfer of launch k+1 overlaps the ingest and update walk of launch k.  `host_data` must stay
- * valid and unmodified until `stream` has passed this call's work.  Same results and errors. */
+ * buffer, so the transfer of launch k+1 overlaps the ingest and update walk of launch k.  The copies are
+ * NOT ordered after earlier work on `stream` (they may run under it, e.g. the previous submap's update
+ * walk): `host_data` must hold its final contents when the call is made (not be the target of a pending
+ * device-to-host copy) and stay valid and unmodified until `stream` has passed this call's work.  Same
+ * results and errors. */
 cvx_status cvx_integrate_batch_host(cvx_submap* submap, const float* host_data, int64_t n_per_frame,
                                     int32_t n_frames, const double* T_world_sensor,
                                     const cvx_sensor_model* sensor, void* stream, cvx_integrate_stats* stats);
