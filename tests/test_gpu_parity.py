@@ -326,6 +326,46 @@ def test_walk_variants_bitexact(tiny, orc, monkeypatch, knob):
     assert_tsdf_parity(b, o.export())
 
 
+def test_host_frames_two_submaps_in_flight(tiny):
+    """The bench's schedule with host frames: two submaps on two streams; after checking submap k's round
+    r, its round r + 1 (other frames) is issued while the other submap's round r may still run.  The
+    host-frame copies are not ordered after earlier work on the caller's stream (they wait only for the
+    prepare that last read their staging buffer), so this checks that the early copies never feed a
+    prepare stale or foreign data: every round must equal a device-resident call bit for bit."""
+    from paper_2410_21149_b200 import Submap
+    R = 4
+    sets = []
+    for r in range(R):
+        idx = [(k + 3 * r) % 10 for k in range(240 - 20 * r)]
+        dev = torch.stack([tiny["frames"][k]["data"] for k in idx]).contiguous().cuda()
+        poses = np.stack([tiny["frames"][k]["T_world_sensor"] for k in idx])
+        ref = Submap(tiny["grid"], tiny["submaps"][0]["T_world_submap"], 0)
+        ref.integrate_batch(dev, poses, tiny["sensor"])
+        sets.append((dev.cpu().pin_memory(), poses, gpu_export_sorted(ref)))
+    subs = [Submap(tiny["grid"], tiny["submaps"][0]["T_world_submap"], 0) for _ in range(2)]
+    streams = [torch.cuda.current_stream(), torch.cuda.Stream()]
+
+    def issue(k, r):
+        with torch.cuda.stream(streams[k]):
+            subs[k].reset()
+            subs[k].integrate_batch_host(sets[r][0], sets[r][1], tiny["sensor"])
+
+    issue(0, 0)
+    issue(1, 0)
+    for r in range(R):
+        for k in (0, 1):
+            with torch.cuda.stream(streams[k]):   # stream-local sync: the other submap keeps running
+                b, D, W, E = subs[k].export(with_esdf=True)
+                streams[k].synchronize()
+            e = sort_blocks(b.cpu().numpy(), D.cpu().numpy(), W.cpu().numpy(), E.cpu().numpy())
+            er = sets[r][2]
+            assert np.array_equal(er[0], e[0]), (r, k)
+            assert np.array_equal(er[1].view(np.uint32), e[1].view(np.uint32)), (r, k)
+            assert np.array_equal(er[2].view(np.uint32), e[2].view(np.uint32)), (r, k)
+            if r + 1 < R:
+                issue(k, r + 1)
+
+
 def test_host_frames_many_launches_and_calls(tiny):
     """Host frames over several walk launches (300 frames > kMaxBatch = 200 per launch) and several calls
     of uneven size: the copy stream refills the two staging buffers while earlier launches are still
