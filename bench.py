@@ -214,6 +214,33 @@ def ncu_metric(kernel, name, workload="lidar"):
     return None
 
 
+def l2_red_view(kernel):
+    """The walk's per-voxel reductions against the MEASURED L2 reduction ceiling: RED sectors
+    per second of the newest ncu capture (lts__t_sectors_srcunit_tex_op_red.sum / gpu__time_duration.sum)
+    vs microbench/l2_atomics.cu's scattered and lane-coherent 64-bit RED rates (profiles/*/l2_atomics.json,
+    32 MB footprint, i.e. L2-resident like the accumulators of the hot blocks)."""
+    sec = ncu_metric(kernel, "lts__t_sectors_srcunit_tex_op_red.sum")
+    dur = ncu_metric(kernel, "gpu__time_duration.sum")
+    prof = os.path.join(ROOT, "profiles")
+    ceil = None
+    for tag in sorted(os.listdir(prof), reverse=True) if os.path.isdir(prof) else []:
+        f = os.path.join(prof, tag, "l2_atomics.json")
+        if os.path.exists(f):
+            d = json.load(open(f)).get("32MB", {})
+            ceil = {"scattered_Gops": d.get("red64_Gops"), "coherent_Gops": d.get("red64_coherent_Gops"),
+                    "source": f"profiles/{tag}/l2_atomics.json"}
+            break
+    if not sec or not dur or not dur["value"]:
+        return None
+    scale = {"ms": 1e-3, "us": 1e-6, "ns": 1e-9, "s": 1.0, "msecond": 1e-3, "usecond": 1e-6}.get(dur["unit"], 1e-3)
+    ach = sec["value"] / (dur["value"] * scale) / 1e9
+    out = {"achieved_Gsectors_per_s": ach, "source": sec["source"]}
+    if ceil and ceil["scattered_Gops"]:
+        out.update({"ceiling": ceil, "frac_of_scattered": ach / ceil["scattered_Gops"],
+                    "frac_of_coherent": ach / ceil["coherent_Gops"] if ceil["coherent_Gops"] else None})
+    return out
+
+
 def ncu_traffic(kernel, workload="lidar"):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from the newest committed
     `ncu --set full` capture of that workload under profiles/ (None if there is none)."""
@@ -952,6 +979,7 @@ def main():
         # the walk's real ceiling is the issue rate (one warp instruction per SMSP per clock): ncu's issue
         # utilisation of the same kernel says how close the instruction stream is to it
         roofline["ncu_issue_slots_busy"] = ncu_metric(dom, "Issue Slots Busy")
+        roofline["l2_red"] = l2_red_view(dom)
     line = {
         "metric": METRIC, "value": value, "unit": "scans/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
