@@ -76,6 +76,8 @@ def lib():
             L.orc_ray_voxels.argtypes = [P, P, C.c_double, C.c_double, C.c_int32, P, C.c_int64]
             L.orc_esdf.restype = C.c_int32
             L.orc_esdf.argtypes = [P, P, P, C.c_int64, C.c_double, C.c_double, C.c_int32, P, P]
+            L.orc_esdf_capped.restype = C.c_int32
+            L.orc_esdf_capped.argtypes = [P, P, P, C.c_int64, C.c_double, C.c_double, C.c_double, C.c_int32, P]
             L.orc_esdf_sample.restype = C.c_int32
             L.orc_esdf_sample.argtypes = [P, P, P, C.c_int64, C.c_double, P, C.c_int64, P]
             L.orc_query.restype = C.c_int32
@@ -219,6 +221,20 @@ def esdf(bxyz, D, W, voxel_size: float, site_threshold: float, brute: bool = Fal
         rc = lib().orc_esdf(_p(b), _p(Dd), _p(Wd), nb, voxel_size, site_threshold, int(brute), _p(E), _p(d2))
         assert rc == 0
     return E, d2
+
+
+def esdf_capped(bxyz, D, W, voxel_size: float, site_threshold: float, max_distance: float, brute: bool = False):
+    """E fp64 [nb,512] of the incremental ESDF (f1, R11): O11 clamped at max_distance."""
+    b = np.ascontiguousarray(bxyz, dtype=np.int32)
+    Dd = np.ascontiguousarray(D, dtype=np.float64)
+    Wd = np.ascontiguousarray(W, dtype=np.float64)
+    nb = b.shape[0]
+    E = np.zeros((nb, 512), np.float64)
+    if nb:
+        rc = lib().orc_esdf_capped(_p(b), _p(Dd), _p(Wd), nb, voxel_size, site_threshold, max_distance, int(brute),
+                                   _p(E))
+        assert rc == 0
+    return E
 
 
 def esdf_sample(bxyz, D, W, site_threshold: float, voxels):

@@ -540,6 +540,27 @@ int32_t orc_esdf(const int32_t* bxyz, const double* D, const double* W, int64_t 
   return 0;
 }
 
+// f1 incremental ESDF (R11): the value the incremental update keeps
+// is the exact EDT of O11 clamped at max_distance d_max ("max_esdf_distance default 2.0 m";
+// the paper gives no cap, and without one a single site change can move distances anywhere):
+//   E(v) = NaN if v unobserved; sign(D(v)) * min(s * sqrt(d2(v)), d_max) otherwise (d_max when S is empty).
+// Written out on top of orc_esdf's d2 (same sites, same integers).
+int32_t orc_esdf_capped(const int32_t* bxyz, const double* D, const double* W, int64_t nb, double voxel_size,
+                        double site_threshold, double max_distance, int32_t brute, double* E_out) {
+  if (nb <= 0) return 0;
+  std::vector<double> E(nb * kBV);
+  std::vector<int64_t> d2(nb * kBV);
+  int32_t rc = orc_esdf(bxyz, D, W, nb, voxel_size, site_threshold, brute, E.data(), d2.data());
+  if (rc != 0) return rc;
+  for (int64_t i = 0; i < nb * kBV; ++i) {
+    if (!(W[i] > 0)) { E_out[i] = std::numeric_limits<double>::quiet_NaN(); continue; }
+    const double sg = D[i] < 0 ? -1.0 : 1.0;
+    const double m = d2[i] < 0 ? HUGE_VAL : voxel_size * std::sqrt((double)d2[i]);
+    E_out[i] = sg * std::min(m, max_distance);
+  }
+  return 0;
+}
+
 // Brute force O11 at sample voxels (full-size parity): d2 of each sample voxel (int64 [m][3] voxel
 // coordinates) to the nearest site of the given TSDF, literally min over all sites; -1 if no site.
 int32_t orc_esdf_sample(const int32_t* bxyz, const double* D, const double* W, int64_t nb, double site_threshold,

@@ -70,7 +70,14 @@ cvx_status check_sensor(const cvx_sensor_model* s, int64_t n_per_frame) {
   return CVX_OK;
 }
 
+// Counter read-back.  With a caller stream the read is ordered after that stream's work; the
+// stream-less synchronising calls (get_stats / get_block_count / get_aabb / packed_size) wait for the
+// whole device first, so work on non-blocking streams (e.g. torch's pool streams) is included.
 cvx_status read_counters(const cvx_submap* sm, cudaStream_t st, cvx::Counters* out) {
+  if (st == nullptr) {
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(e, "synchronising before the counter read");
+  }
   cudaError_t e = cudaMemcpyAsync(sm->ctr_host, sm->ctr, sizeof(cvx::Counters), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "reading submap counters");
@@ -431,8 +438,9 @@ cvx_status cvx_finalize_esdf(cvx_submap* sm, void* stream) {
   const int nb = c.n_blocks < sm->pool.max_blocks ? c.n_blocks : sm->pool.max_blocks;
   if (nb > 0) {
     for (int a = 0; a < 3; ++a)
-      if ((int64_t)8 * ((int64_t)c.aabb_hi[a] - c.aabb_lo[a] + 1) > 65528)
-        return fail(CVX_E_RANGE, "submap AABB exceeds 65528 voxels along an axis (dense EDT domain)");
+      if ((int64_t)8 * ((int64_t)c.aabb_hi[a] - c.aabb_lo[a] + 1) > cvx::kMaxEdtAxis)
+        return fail(CVX_E_RANGE, "submap AABB exceeds 46336 voxels along an axis (dense EDT domain: 2-D squared "
+                                 "distances must fit 32 bits)");
     cudaError_t e = cvx::launch_finalize(sm, nb, c.aabb_lo, c.aabb_hi, st);
     if (e != cudaSuccess) return cuda_fail(e, "finalize_esdf");
   }
@@ -453,8 +461,8 @@ cvx_status cvx_update_esdf(cvx_submap* sm, void* stream, int32_t* iterations) {
   const int nb = c.n_blocks < sm->pool.max_blocks ? c.n_blocks : sm->pool.max_blocks;
   if (nb > 0)
     for (int a = 0; a < 3; ++a)
-      if ((int64_t)8 * ((int64_t)c.aabb_hi[a] - c.aabb_lo[a] + 1) > 65528)
-        return fail(CVX_E_RANGE, "submap AABB exceeds 65528 voxels along an axis");
+      if ((int64_t)8 * ((int64_t)c.aabb_hi[a] - c.aabb_lo[a] + 1) > cvx::kMaxEdtAxis)
+        return fail(CVX_E_RANGE, "submap AABB exceeds 46336 voxels along an axis");
   int its = 0;
   cudaError_t e = cvx::launch_update_esdf(sm, nb, c.aabb_lo, c.aabb_hi, st, &its);
   if (e != cudaSuccess) return cuda_fail(e, "update_esdf");

@@ -157,6 +157,10 @@ inline int packed_q(double tau) {
   return q < 0 ? 0 : (q > 30 ? 30 : q);
 }
 
+// Longest dense EDT axis (voxels, multiple of 8): 2 (n - 1)^2 < 2^32 - 1, so the 2-D squared distances
+// of the ESDF's second pass fit uint32 with 0xffffffff left as the "no site" marker.
+constexpr long long kMaxEdtAxis = 46336;
+
 // Floor division / modulo by 8 on int32 voxel coordinates (S:L200-207 floor semantics).
 __host__ __device__ inline int bdiv(int v) { return v >> 3; }
 __host__ __device__ inline int bmod(int v) { return v & 7; }

@@ -21,9 +21,18 @@ struct QueryParams {
   double s;
 };
 
-// E of voxel (x,y,z) through the hash (block cached); false if unallocated or unobserved (NaN).
+// Voxel coordinates of the 21-bit block-key domain (O3: |voxel| < 2^23, blocks in [-2^20, 2^20)); a
+// coordinate outside it cannot be allocated, and pack_key would alias it onto an in-range block.
+__device__ __forceinline__ bool in_key_domain(int x, int y, int z) {
+  constexpr int lo = -(1 << 23), hi = (1 << 23) - 1;
+  return x >= lo && x <= hi && y >= lo && y <= hi && z >= lo && z <= hi;
+}
+
+// E of voxel (x,y,z) through the hash (block cached); false if unallocated, outside the key domain or
+// unobserved (NaN).
 __device__ __forceinline__ bool voxel_e(const QueryParams& p, int x, int y, int z, unsigned long long& ckey,
                                         int& cslot, float* e) {
+  if (!in_key_domain(x, y, z)) return false;
   const unsigned long long key = pack_key(x >> 3, y >> 3, z >> 3);
   if (key != ckey) { ckey = key; cslot = hash_find(p.hash, key); }
   if (cslot < 0) return false;
@@ -78,7 +87,10 @@ __global__ void __launch_bounds__(256) query_kernel(const __grid_constant__ Quer
     }
     if (p.grad) { p.grad[3 * i] = qnan; p.grad[3 * i + 1] = qnan; p.grad[3 * i + 2] = qnan; }
     int v[3];
-    for (int a = 0; a < 3; ++a) v[a] = (int)floor(__ddiv_rn(xs[a], p.s));
+    for (int a = 0; a < 3; ++a) {
+      const double fv = floor(__ddiv_rn(xs[a], p.s));
+      v[a] = fabs(fv) < 1073741824.0 ? (int)fv : (1 << 30);   // |v| >= 2^30: outside the key domain
+    }
     float e;
     if (voxel_e(p, v[0], v[1], v[2], ckey, cslot, &e)) { p.out[i] = e; p.status[i] = 1; return; }
   }

@@ -241,6 +241,8 @@ class Submap:
         F = data.shape[0]
         n = data[0].numel() if sensor["kind"] == 1 else data[0].numel() // 3
         poses = _pose(T_world_sensor)
+        if poses.shape[0] != F:
+            raise ValueError("one pose per frame")
         k = C.c_int32()
         _check(lib().cvx_integrate_until(self._h, self._dev(data, torch.float32, "data"), n, F, _ptr(poses), C.byref(sm),
                                          int(block_threshold), self._stream(), C.byref(k)))
@@ -254,6 +256,8 @@ class Submap:
         F = data.shape[0]
         n = data[0].numel() if sensor["kind"] == 1 else data[0].numel() // 3
         poses = _pose(T_world_sensor)
+        if poses.shape[0] != F:
+            raise ValueError("one pose per frame")
         st = Stats() if stats else None
         _check(lib().cvx_integrate_batch_host(self._h, C.c_void_p(data.data_ptr()), n, F, _ptr(poses), C.byref(sm),
                                               self._stream(), C.byref(st) if st is not None else None))

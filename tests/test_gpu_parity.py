@@ -385,3 +385,35 @@ def test_host_frames_many_launches_and_calls(tiny):
     assert np.array_equal(ea[1].view(np.uint32), eb[1].view(np.uint32))
     assert np.array_equal(ea[2].view(np.uint32), eb[2].view(np.uint32))
     assert a.stats()["rays_used"] == b.stats()["rays_used"] > 0
+
+
+@pytest.mark.parametrize("name,frames", [("tiny", list(range(10))), ("lidar", [0, 20, 40, 60, 80, 100])])
+def test_block_count_trigger_matches_oracle(orc, name, frames):
+    """cvx_integrate_until (the submap ends once it holds block_threshold blocks) against the
+    ORACLE's per-frame block counts (orc_num_blocks after each frame, O7): the frame at which the oracle's
+    block set first reaches the threshold is the last one the GPU takes, and the GPU submap after the call
+    equals the oracle's submap of those frames (block sets bit-exact, TSDF within tolerance)."""
+    from paper_2410_21149_b200 import Submap
+    cfg = synth.make_config(name, frames=frames)
+    o = orc.OracleSubmap(cfg["grid"], cfg["submaps"][0]["T_world_submap"])
+    counts = []
+    for k in frames:
+        o.integrate(cfg["frames"][k]["data"].numpy(), cfg["frames"][k]["T_world_sensor"], cfg["sensor"])
+        counts.append(o.num_blocks())
+    dev = torch.device("cuda", 0)
+    data = torch.stack([cfg["frames"][k]["data"] for k in frames]).to(dev).contiguous()
+    poses = np.stack([cfg["frames"][k]["T_world_sensor"] for k in frames])
+    for j in range(1, len(frames)):
+        if counts[j] == counts[j - 1]:
+            continue
+        for thr in (counts[j], counts[j - 1] + 1):          # reached exactly / just past the previous count
+            expect = next(i + 1 for i, c in enumerate(counts) if c >= thr)
+            sm = Submap(cfg["grid"], cfg["submaps"][0]["T_world_submap"], 0)
+            took = sm.integrate_until(data, poses, cfg["sensor"], thr)
+            assert took == expect, (thr, took, expect, counts)
+            assert sm.block_count() == counts[took - 1]
+        if j == len(frames) // 2:
+            ref, _ = oracle_build(cfg, frames[:took])
+            assert_tsdf_parity(gpu_export_sorted(sm), ref.export())
+    sm = Submap(cfg["grid"], cfg["submaps"][0]["T_world_submap"], 0)
+    assert sm.integrate_until(data, poses, cfg["sensor"], counts[-1] + 1) == len(frames)

@@ -202,3 +202,43 @@ def test_sample_surface_proportional_and_brute_force(orc):
     # proportionality: evenly spaced uniforms hit each candidate about w_k / T * m times
     counts = np.bincount(ks, minlength=len(cand))
     assert np.abs(counts - np.array(wts) / tot * m).max() <= 1.0 + 1e-9
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_capped_esdf_pins(orc, seed):
+    """f1's value (R11): O11 clamped at d_max.  Pinned against scipy's exact EDT on the dense AABB
+    (independent of orc_esdf), single-site closed form, empty site set -> +-d_max, brute == separable, and
+    an infinite cap reproducing the uncapped O11 exactly."""
+    rng = np.random.default_rng(100 + seed)
+    b, D, W = _random_tsdf(rng, nb_side=(4, 3, 2), fill=0.7)
+    s, thr, dmax = 0.1, 0.01, 0.45
+    Ec = orc.esdf_capped(b, D, W, s, thr, dmax)
+    assert np.array_equal(Ec, orc.esdf_capped(b, D, W, s, thr, dmax, brute=True), equal_nan=True)
+    site = (W > 0) & (np.abs(D) <= thr)
+    G, lo = _dense(b, site, False)
+    ref = ndimage.distance_transform_edt(~G) * s
+    l = np.arange(512)
+    obs = W > 0
+    for i in range(b.shape[0]):
+        r = ref[8 * b[i, 0] - lo[0] + l % 8, 8 * b[i, 1] - lo[1] + (l // 8) % 8, 8 * b[i, 2] - lo[2] + l // 64]
+        want = np.where(D[i] < 0, -1.0, 1.0) * np.minimum(r, dmax)
+        o = obs[i]
+        assert np.allclose(Ec[i][o], want[o], rtol=0, atol=1e-12)
+        assert np.isnan(Ec[i][~o]).all()
+    assert np.nanmax(np.abs(Ec)) == dmax                      # the cap binds somewhere in this scene
+    E, _ = orc.esdf(b, D, W, s, thr)
+    assert np.array_equal(orc.esdf_capped(b, D, W, s, thr, np.inf), E, equal_nan=True)
+    # no site at all: every observed voxel holds +-d_max
+    Dn = np.where(W > 0, np.where(D < 0, -0.2, 0.2), 0.0)
+    En = orc.esdf_capped(b, Dn, W, s, thr, dmax)
+    assert np.array_equal(np.abs(En[obs]), np.full(obs.sum(), dmax))
+    assert (np.signbit(En[obs]) == (Dn[obs] < 0)).all()
+    # one site: closed form min(s |v - u|, d_max)
+    D1 = np.full_like(D, 0.2)
+    W1 = np.ones_like(W)
+    D1[0, 3 + 8 * 2 + 64 * 5] = 0.0
+    u = 8 * b[0] + np.array([3, 2, 5])
+    E1 = orc.esdf_capped(b, D1, W1, s, thr, dmax)
+    for i in range(b.shape[0]):
+        v = 8 * b[i][None, :] + np.stack([l % 8, (l // 8) % 8, l // 64], 1)
+        assert np.allclose(E1[i], np.minimum(s * np.linalg.norm(v - u, axis=1), dmax), rtol=0, atol=1e-12)

@@ -230,9 +230,10 @@ def test_depth_backprojection_plane(orc):
         delta = (vz + 0.5) * 0.1
         bound = abs(delta) * (1 / math.cos(th) - 1) + 0.1 * math.sqrt(3) / 2 * math.tan(th)
         assert abs(d - min(max(delta, -0.3), 0.3)) <= bound + 1e-5
-    # the footprint: pixel (u, v) lands at distance 2*|(u - cx, v - cy)|/f from the nadir
+    # (the pixel -> point mapping itself is pinned exactly, pixel by pixel, in
+    # test_depth_backprojection_exact_per_pixel below)
     b, D, Wt = s.export()
-    assert Wt.sum() > 0
+    assert (Wt > 0).sum() == len(t)
 
 
 def test_invalid_and_range_counting(orc):
@@ -243,3 +244,44 @@ def test_invalid_and_range_counting(orc):
     assert st["skipped_invalid"] == 2 and st["skipped_range"] == 2
     st = s.integrate(np.zeros((0, 3), np.float32), np.eye(4), dict(kind=0, min_range=0.1, max_range=10.0))
     assert st["rays_in"] == 0 and st["voxel_updates"] == 0   # S:L283 empty frame is a no-op
+
+
+def test_depth_backprojection_exact_per_pixel(orc):
+    """O2 pinned pixel by pixel (SURVEY §8c O2, Q24): pixel (u, v) = (i % W, i // W) of a W x H depth image
+    with depth z back-projects to p_c = (z (u - cx) / fx, z (v - cy) / fy, z), integer pixel indices, no
+    +1/2.  W != H, cx != (W-1)/2, cy != (H-1)/2 and a distinct dyadic depth per pixel, so every input is
+    exact in fp32 and the expected point is an exact rational; only one pixel is valid per frame, so the
+    observed voxels are exactly that ray's traversal (pinned separately, test_oracle_traversal.py) and
+    D on them is the closed-form clamped sdf (p - c_v).u of the exact point.  A u/v swap, a transposed
+    index (i % H), a +1/2 pixel centre or swapped intrinsics moves the point by >= 1 voxel and fails."""
+    from fractions import Fraction as Fr
+    W_, H_ = 5, 3
+    fx, fy, cx, cy = 4.0, 2.0, 1.25, 0.5            # dyadic: fp32 arithmetic below is exact
+    sensor = dict(kind=1, width=W_, height=H_, fx=fx, fy=fy, cx=cx, cy=cy, min_range=0.0, max_range=100.0)
+    g = dict(GRID, voxel_size=0.05, truncation=0.1)
+    s, tau = g["voxel_size"], g["truncation"]
+    for i in range(W_ * H_):
+        u, v = i % W_, i // W_
+        z = 1.0 + i / 8.0                              # distinct per pixel, dyadic
+        depth = np.zeros((H_, W_), np.float32)
+        depth[v, u] = z
+        p = [Fr(z) * (Fr(u) - Fr(cx)) / Fr(fx), Fr(z) * (Fr(v) - Fr(cy)) / Fr(fy), Fr(z)]
+        pf = np.array([float(c) for c in p])
+        assert all(Fr(float(c)) == c for c in p)       # the expected point is exact in fp64
+        sm = orc.OracleSubmap(g)
+        st = sm.integrate(depth, np.eye(4), sensor)
+        assert st["rays_used"] == 1 and st["skipped_invalid"] == W_ * H_ - 1
+        expect = orc.ray_voxels(np.zeros(3), pf, s, tau, 1)
+        got = _voxel_table(sm)
+        assert set(got) == set(map(tuple, expect.tolist())), (u, v)
+        assert st["voxel_updates"] == expect.shape[0]
+        L = float(np.sqrt(pf @ pf))
+        assert abs(L - math.sqrt(float(sum(c * c for c in p)))) == 0.0
+        uhat = pf / L
+        for vox, (d, w) in got.items():
+            c = (np.array(vox, np.float64) + 0.5) * s
+            assert w == 1.0
+            assert abs(d - min(max(float((pf - c) @ uhat), -tau), tau)) <= 1e-12
+        # the ray ends tau behind the exact point: its last voxel holds e = p + tau u
+        e = pf + tau * uhat
+        assert tuple(expect[-1].tolist()) == tuple(int(np.floor(c / s)) for c in e)
