@@ -57,6 +57,9 @@ typedef struct {
   double site_threshold;     /* ESDF site: observed and |D| <= site_threshold (O10, Q14; default s) */
   int64_t max_blocks;        /* block pool capacity; the hash table holds >= 2*max_blocks entries   */
   int32_t color;             /* 1: also fuse per-point colour (cvx_integrate_color; TSDF + Color) */
+  double esdf_max_distance;  /* d_max > 0 of the incremental ESDF (cvx_update_esdf): distances are clamped
+                                there (SPEC S:L373 default 2 m; R11).  cvx_finalize_esdf is exact
+                                and unclamped (Q16) and ignores it.                                      */
 } cvx_grid_config;
 
 /* Sensor model of the incoming frames. */
@@ -192,22 +195,27 @@ cvx_status cvx_get_aabb(const cvx_submap* submap, int32_t* lo, int32_t* hi);
  * |D(v)| <= site_threshold}; E(v) = sign(D(v)) * s * sqrt(min_{u in S} |v - u|^2) for observed v,
  * NaN for unobserved v, +inf for every observed v if S is empty.  Marks the submap finalized (no more
  * integration); calling it again recomputes the same ESDF (the TSDF is immutable).
- * Synchronising (reads the block count / AABB to size the dense EDT domain).
+ * Synchronising (reads the block count / AABB to size the dense EDT domain).  The dense AABB may span at
+ * most 46336 voxels per axis (2-D squared distances fit 32 bits), else CVX_E_RANGE.  Scratch (6 bytes per
+ * AABB voxel) is allocated stream-ordered (cudaMallocAsync) and kept for the next call.
  * Errors: CVX_E_CAPACITY / CVX_E_RANGE (sticky), CVX_E_OOM. */
 cvx_status cvx_finalize_esdf(cvx_submap* submap, void* stream);
 
-/* Incremental ESDF: update the ESDF of a submap that is still being
- * integrated, touching only what changed since the previous call.  Per voxel the library keeps a
- * pointer to its nearest site; new sites, removed sites ("raise": voxels whose parent stopped being a
- * site lose it) and new blocks queue their block (one region queue per 8^3 block); each queued block
- * is relaxed by one CTA in shared memory along all axis directions until stable, and blocks whose
- * shared face changed are queued in turn, until no block is queued.  E follows the same sign / NaN /
- * +inf conventions as cvx_finalize_esdf; the distances are those of 6-neighbour parent propagation
- * (the paper's scheme), which can exceed the exact EDT of cvx_finalize_esdf by a bounded amount.
- * Enables cvx_query_distance.  Synchronising (one host check per propagation wave);
- * *iterations (nullable, host) = number of waves.  Errors: CVX_E_CAPACITY / CVX_E_RANGE (sticky),
- * CVX_E_OOM. */
-cvx_status cvx_update_esdf(cvx_submap* submap, void* stream, int32_t* iterations);
+/* Incremental ESDF (R11): keep the ESDF of a submap that is still
+ * being integrated current, recomputing only the blocks a change can reach.  The value maintained is the
+ * exact EDT of cvx_finalize_esdf clamped at d_max = config.esdf_max_distance:
+ *   E(v) = sign(D(v)) * min(s * sqrt(min_{u in S} |v - u|^2), d_max) for observed v (d_max if S is empty),
+ *   NaN for unobserved v,
+ * identical for every update schedule (after any sequence of integrate / update calls it equals the
+ * clamped exact EDT of the current TSDF).  A site within d_max of a voxel lies within r = ceil(d_max / s)
+ * voxels per axis, so each call classifies every allocated block (observed / sign / site bit-planes from
+ * the fused sums), queues every block within ceil(r / 8) blocks of a block whose sites changed (raise and
+ * lower alike) plus the blocks whose own planes changed or that are new (one region queue per 8^3 block,
+ * P:L147), and recomputes each queued block exactly from the sites around it.  Windows of more than 7^3
+ * blocks (d_max > 24 s) use the dense exact EDT of finalize with the clamp.  Enables cvx_query_distance.
+ * Synchronising.  *blocks_updated (nullable, host) = the number of blocks recomputed.  Errors:
+ * CVX_E_CAPACITY / CVX_E_RANGE (sticky), CVX_E_OOM. */
+cvx_status cvx_update_esdf(cvx_submap* submap, void* stream, int32_t* blocks_updated);
 
 /* Distance queries (O13).  points_world (device fp32 [m][3], world frame) ->
  * out_distance (device fp32 [m]) and out_status (device uint8 [m]: 0 OK trilinear over the 8 voxel

@@ -132,14 +132,7 @@ void free_all(cvx_submap* sm) {
     if (sm->ev_prepared[b]) cudaEventDestroy(sm->ev_prepared[b]);
     if (sm->ev_free[b]) cudaEventDestroy(sm->ev_free[b]);
   }
-  if (sm->edt) cudaFree(sm->edt);
-  if (sm->block_grid) cudaFree(sm->block_grid);
-  if (sm->inc.par) cudaFree(sm->inc.par);
-  if (sm->inc.sitebits) cudaFree(sm->inc.sitebits);
-  if (sm->inc.active) cudaFree(sm->inc.active);
-  if (sm->inc.list) cudaFree(sm->inc.list);
-  if (sm->inc.cnt) cudaFree(sm->inc.cnt);
-  if (sm->inc.cnt_host) cudaFreeHost(sm->inc.cnt_host);
+  cvx::release_esdf(sm);
   if (sm->proj_birth) cudaFree(sm->proj_birth);
   if (sm->trig) cudaFree(sm->trig);
   if (sm->trig_host) cudaFreeHost(sm->trig_host);
@@ -169,6 +162,8 @@ cvx_status cvx_create_submap(const cvx_grid_config* cfg, const double* T_world_s
   if (!(cfg->site_threshold >= 0) || !std::isfinite(cfg->site_threshold)) return fail(CVX_E_INVALID, "site_threshold must be >= 0");
   if (cfg->max_blocks < 1 || cfg->max_blocks >= (1ll << 23)) return fail(CVX_E_INVALID, "max_blocks must be in [1, 2^23)");
   if (cfg->color != 0 && cfg->color != 1) return fail(CVX_E_INVALID, "color must be 0 or 1");
+  if (!(cfg->esdf_max_distance > 0) || !std::isfinite(cfg->esdf_max_distance))
+    return fail(CVX_E_INVALID, "esdf_max_distance must be > 0 and finite");
   if (!valid_pose(T_world_submap)) return fail(CVX_E_INVALID, "T_world_submap must be a finite rigid 4x4 (orthonormal within 1e-6)");
   int ndev = 0;
   cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -257,7 +252,6 @@ cvx_status cvx_reset_submap(cvx_submap* sm, void* stream) {
   sm->finalized = false;
   sm->esdf_valid = false;
   sm->inc.nb_prev = 0;
-  if (sm->inc.active) cudaMemsetAsync(sm->inc.active, 0, sizeof(int) * (size_t)sm->pool.max_blocks, (cudaStream_t)stream);
   return CVX_OK;
 }
 
@@ -448,7 +442,7 @@ cvx_status cvx_finalize_esdf(cvx_submap* sm, void* stream) {
   return CVX_OK;
 }
 
-cvx_status cvx_update_esdf(cvx_submap* sm, void* stream, int32_t* iterations) {
+cvx_status cvx_update_esdf(cvx_submap* sm, void* stream, int32_t* blocks_updated) {
   g_last_error.clear();
   if (!sm) return fail(CVX_E_INVALID, "submap is NULL");
   DeviceGuard g(sm->device);
@@ -463,10 +457,10 @@ cvx_status cvx_update_esdf(cvx_submap* sm, void* stream, int32_t* iterations) {
     for (int a = 0; a < 3; ++a)
       if ((int64_t)8 * ((int64_t)c.aabb_hi[a] - c.aabb_lo[a] + 1) > cvx::kMaxEdtAxis)
         return fail(CVX_E_RANGE, "submap AABB exceeds 46336 voxels along an axis");
-  int its = 0;
-  cudaError_t e = cvx::launch_update_esdf(sm, nb, c.aabb_lo, c.aabb_hi, st, &its);
+  int nq = 0;
+  cudaError_t e = cvx::launch_update_esdf(sm, nb, c.aabb_lo, c.aabb_hi, st, &nq);
   if (e != cudaSuccess) return cuda_fail(e, "update_esdf");
-  if (iterations) *iterations = its;
+  if (blocks_updated) *blocks_updated = nq;
   sm->esdf_valid = true;
   return CVX_OK;
 }

@@ -1,19 +1,46 @@
-// esdf.cu — exact ESDF finalize for sm_100a.
+// esdf.cu — exact ESDF finalize and the incremental ESDF
+// (row f1) for sm_100a.
 //
-// PBA-class separable exact EDT over the dense AABB of the allocated blocks (O10-O12):
-//   block_grid_kernel  slot index per block of the AABB (direct index, no hashing in the passes)
-//   pass_x_kernel      one warp per x-row: reads the TSDF sums of the row's allocated voxels (coalesced,
-//                      8 voxels x 16 B per block row), decides sites S = {W > 0, |D| <= tau_site} with
-//                      warp ballots, writes the sign/observed placeholder of E, and the exact 1-D
-//                      distance to the nearest site along x (uint16) from per-chunk bit masks kept in
-//                      shared memory (prefix max / suffix min scans across chunks).
-//   pass_yz_kernel     one thread per line (consecutive x in a warp -> coalesced): lower envelope of
-//                      parabolas f(q) + (p - q)^2 (Meijster / Felzenszwalb-Huttenlocher) with the
-//                      stack stored in place as per-voxel {prev, start} links (PBA phase 2 idea: the
-//                      proximate sites live at their own positions), integer arithmetic throughout.
-//                      Pass y writes the 2-D squared distance (uint32); pass z writes E = sign * s *
+// Finalize: PBA-class separable exact EDT over the dense AABB of the allocated blocks (O10-O12):
+//   block_grid_kernel  slot index per block of the AABB (direct index, no hashing in the passes, P:L98)
+//   pass_x_kernel      one warp per x-row: reads the TSDF sums of the row's allocated voxels (coalesced),
+//                      decides observed / sign / site S = {W > 0, |D| <= tau_site} with warp ballots and
+//                      stores them as per-slot bit-planes (3 bits per voxel instead of a 4-byte E
+//                      placeholder), and writes the exact 1-D distance to the nearest site along x (u16)
+//                      from per-chunk bit masks (prefix max / suffix min scans across chunks).
+//   pba_line_kernel    passes y and z: one CTA per tile of `tx` parallel lines (consecutive x, so every
+//                      line position is one contiguous row segment) staged whole into shared memory by
+//                      TMA (cp.async.bulk.tensor, one box per <= 256 positions, mbarrier completion).  Each
+//                      line is cut into `nbands` bands (PBA's banding): every band builds the
+//                      lower envelope of the parabolas f(q) + (p - q)^2 of its own sites over the whole
+//                      line (Meijster / Felzenszwalb-Huttenlocher stack, kept in shared memory as an
+//                      array in the band's own rows), the band envelopes are merged pairwise in log2(B)
+//                      levels (the merge only touches the junction: it pops the left envelope's top and
+//                      drops the right envelope's bottom while they are dominated — exactly the pushes
+//                      the sequential algorithm would do), and every band then writes its own output
+//                      range by walking the merged envelope.  Integer arithmetic throughout.
+//                      Pass y writes the 2-D squared distance (u32, dense); pass z writes E = sign * s *
 //                      sqrt(d^2) straight into the 8^3 ESDF blocks (NaN unobserved, +inf no sites).
+//
+// Incremental (f1, R11): the ESDF kept current while the submap is integrated is the exact EDT
+// clamped at d_max = esdf_max_distance.  A site within d_max of a voxel is within r = ceil(d_max / s)
+// voxels along every axis, so a site change can only move the (clamped) distance of blocks within
+// Rb = ceil(r / 8) blocks of it.  Per update:
+//   inc_classify   new bit-planes of every allocated block from the sums; a block whose site plane
+//                  changed is a raise / lower source, a block whose planes changed at all (or is new)
+//                  must be rewritten
+//   inc_dilate     every block within Rb blocks of a source is queued ("Each region uses its own queue",
+//                  one region = one block)
+//   inc_window     one CTA per queued block: the exact clamped EDT of its 512 voxels from the site planes
+//                  of the (2 Rb + 1)^3 blocks around it, by three separable passes in shared memory (bit
+//                  scans along x, brute-force minima along y and z over the window) — the "axis
+//                  direction" passes of P:L149, done once instead of iterated to a fixpoint.
+//   Windows wider than 7^3 blocks fall back to the dense passes above with the clamp applied in pass z.
 #include <algorithm>
+#include <cmath>
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <type_traits>
 
 #include "submap.h"
 
@@ -23,9 +50,10 @@ namespace {
 constexpr unsigned kNone16 = 0xffffu;
 constexpr unsigned kInf32 = 0xffffffffu;
 constexpr long long kInfF = 1ll << 62;
+constexpr int kPlaneWords = 48;   // per slot: observed[16] | negative[16] | site[16] (bit l = local index l)
 
-// slot of every block of the AABB (-1 = not allocated) and, per (bx, by) column, whether any block of
-// the column is allocated (pass z skips empty columns: they hold no voxel to write)
+// slot of every block of the AABB (-1 = not allocated) and, per (bx, by) column / (by, bz) row, whether
+// any block of it is allocated (pass z skips empty columns: they hold no voxel to write)
 __global__ void block_grid_kernel(const Counters* ctr, const int4* coords, int max_blocks, int* grid,
                                   unsigned char* colmask, unsigned char* rowmask, int lx, int ly, int lz, int nbx,
                                   int nby) {
@@ -33,14 +61,26 @@ __global__ void block_grid_kernel(const Counters* ctr, const int4* coords, int m
   for (int sIdx = blockIdx.x * blockDim.x + threadIdx.x; sIdx < nb; sIdx += gridDim.x * blockDim.x) {
     int4 c = coords[sIdx];
     grid[((long long)(c.z - lz) * nby + (c.y - ly)) * nbx + (c.x - lx)] = sIdx;
-    colmask[(long long)(c.y - ly) * nbx + (c.x - lx)] = 1;
-    rowmask[(long long)(c.z - lz) * nby + (c.y - ly)] = 1;
+    if (colmask) colmask[(long long)(c.y - ly) * nbx + (c.x - lx)] = 1;
+    if (rowmask) rowmask[(long long)(c.z - lz) * nby + (c.y - ly)] = 1;
+  }
+}
+
+// O10 / R4: the site test on D rounded to fp32 (the value cvx_export_blocks returns), compared in fp64
+__device__ __forceinline__ void classify_voxel(longlong2 sw, double thr, bool& obs, bool& neg, bool& site) {
+  obs = sw.y > 0;
+  neg = false;
+  site = false;
+  if (obs) {
+    const float D = (float)((double)sw.x / (double)sw.y);
+    neg = D < 0.0f;
+    site = fabs((double)D) <= thr;
   }
 }
 
 struct XParams {
   const long long* sums;
-  float* esdf;
+  unsigned* planes;
   const int* grid;
   const unsigned char* rowmask;   // (by, bz) block rows with allocated blocks
   unsigned short* g1;
@@ -54,10 +94,10 @@ struct XParams {
 constexpr int kXCh = CVX_XCH;   // chunks (32 voxels each) whose loads a warp issues together in pass x
 
 __global__ void __launch_bounds__(128) pass_x_kernel(const __grid_constant__ XParams p) {
-  extern __shared__ unsigned smem[];
+  extern __shared__ __align__(1024) unsigned char dsmem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nch = (p.nx + 31) >> 5;
-  unsigned* msk = smem + warp * 3 * nch;
+  unsigned* msk = reinterpret_cast<unsigned*>(dsmem) + warp * 3 * nch;
   int* prv = reinterpret_cast<int*>(msk + nch);
   int* nxt = prv + nch;
   const long long rows = (long long)p.ny * p.nz;
@@ -71,7 +111,8 @@ __global__ void __launch_bounds__(128) pass_x_kernel(const __grid_constant__ XPa
     }
     const int* grow = p.grid + ((long long)(z >> 3) * p.nby + (y >> 3)) * p.nbx;
     const int lyz = 8 * (y & 7) + 64 * (z & 7);
-    // 1) sites of the row -> one 32-bit mask per chunk; E placeholder (sign of D, NaN if unobserved).
+    const int prow = (y & 7) + 8 * (z & 7);   // byte of the block's 64-byte planes holding this x-row
+    // 1) sites of the row -> one 32-bit mask per chunk; the block's observed / sign / site plane bytes.
     //    kXCh chunks per round: their slot look-ups, then their TSDF loads, are issued back to back so
     //    every warp keeps kXCh 512-byte requests in flight (the row loop is otherwise latency-bound).
     for (int c0 = 0; c0 < nch; c0 += kXCh) {
@@ -89,21 +130,18 @@ __global__ void __launch_bounds__(128) pass_x_kernel(const __grid_constant__ XPa
       }
 #pragma unroll
       for (int u = 0; u < kXCh; ++u) {
-        bool site = false;
-        if (slot[u] >= 0) {
-          const long long vi = (long long)slot[u] * kBlockVox + (lane & 7) + lyz;
-          float ph;
-          if (sw[u].y > 0) {
-            const float D = (float)((double)sw[u].x / (double)sw[u].y);   // exported D (stage-isolated parity)
-            site = fabs((double)D) <= p.site_thr;                          // O10
-            ph = D < 0.0f ? -0.0f : 0.0f;
-          } else {
-            ph = __int_as_float(0x7fc00000);                              // unobserved -> NaN (O11)
-          }
-          p.esdf[vi] = ph;
+        bool obs, neg, site;
+        classify_voxel(sw[u], p.site_thr, obs, neg, site);
+        const unsigned bs = __ballot_sync(0xffffffffu, site);
+        const unsigned bo = __ballot_sync(0xffffffffu, obs);
+        const unsigned bn = __ballot_sync(0xffffffffu, neg);
+        if (lane == 0 && c0 + u < nch) msk[c0 + u] = bs;
+        if ((lane & 7) == 0 && slot[u] >= 0) {   // one lane per block: its row bytes of the three planes
+          unsigned char* pl = reinterpret_cast<unsigned char*>(p.planes + (long long)slot[u] * kPlaneWords);
+          pl[prow] = (unsigned char)(bo >> lane);
+          pl[64 + prow] = (unsigned char)(bn >> lane);
+          pl[128 + prow] = (unsigned char)(bs >> lane);
         }
-        const unsigned b = __ballot_sync(0xffffffffu, site);
-        if (lane == 0 && c0 + u < nch) msk[c0 + u] = b;
       }
     }
     __syncwarp();
@@ -151,205 +189,501 @@ __global__ void __launch_bounds__(128) pass_x_kernel(const __grid_constant__ XPa
   }
 }
 
-struct LineParams {
-  const void* fin;          // pass y: uint16 1-D distances; pass z: uint32 squared distances
-  unsigned* gout;           // pass y output (uint32 squared distances)
-  void* meta;               // per pushed voxel q — pass z: u64 envelope state below q {f: hi 32, t: 16,
-                            // prev: lo 16}; pass y: u32 {t_q: hi 16, prev: lo 16}
-  float* esdf;              // pass z output (ESDF blocks)
-  const int* grid;
-  const unsigned char* colmask;   // (bx, by) columns with allocated blocks
-  int nx, ny, nz, nbx, nby;
-  float s;
-};
-
-__device__ __forceinline__ long long floordiv(long long a, long long b) {  // b > 0
-  return a >= 0 ? a / b : -((-a + b - 1) / b);
+// ------------------------------------------------------------------------------ TMA / mbarrier helpers
+__device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile("{\n\t.reg .pred p;\n"
+               "WAIT_%=:\n\t"
+               "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+               "@!p bra WAIT_%=;\n\t}" :: "r"(smem_addr(bar)), "r"(phase) : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int c0, int c1, int c2,
+                                            unsigned long long* bar) {
+  asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+               :: "r"(smem_addr(dst)), "l"(reinterpret_cast<unsigned long long>(tm)), "r"(c0), "r"(c1), "r"(c2),
+                  "r"(smem_addr(bar)) : "memory");
 }
 
-// Lower envelope along one line of length m; element q lives at base + q*stride.
-// kSplit = 2 (pass y, whose line count nx*nz is small): the two halves of a line go to lanes l and l+16
-// of one warp; each builds the envelope of the sites in its half and evaluates it over the whole line,
-// and the two results are combined with one shuffle per position (2x the evaluation work, 2x the
-// threads in flight for a latency-bound pass).
-#ifndef CVX_META64Y
-#define CVX_META64Y 0
-#endif
-constexpr bool kMeta64Y = CVX_META64Y;
-#ifndef CVX_EDT_LAYOUT
-#define CVX_EDT_LAYOUT 0
-#endif
+// floor(num / den) for den > 0, |num| <= 2^35, den <= 2^17: the correctly rounded fp64 quotient is
+// within half an ulp (<= 2^-18) of num/den, whose fractional part is 0 or >= 1/den >= 2^-17 away from
+// the next integer, so its floor is the exact integer floor.
+__device__ __forceinline__ long long floordiv_exact(long long num, long long den) {
+  return (long long)floor((double)num / (double)den);
+}
 
-template <bool kZ, int kSplit>
-__global__ void __launch_bounds__(256) pass_line_kernel(const __grid_constant__ LineParams p) {
-  const long long nlines = kZ ? (long long)p.nx * p.ny : (long long)p.nx * p.nz;
-  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const int lane = threadIdx.x & 31;
-  const int half = kSplit == 2 ? (lane >> 4) : 0;
-  const long long line = kSplit == 2 ? (tid >> 5) * 16 + (lane & 15) : tid;
-  const bool valid = line < nlines;
-  if (kSplit == 1 && !valid) return;
-  if (kSplit == 2 && ((tid >> 5) * 16) >= nlines) return;   // whole warp beyond the lines
-  const int x = valid ? (int)(line % p.nx) : 0;
-  const int o2 = valid ? (int)(line / p.nx) : 0;      // pass y: z ; pass z: y
-  const int m = kZ ? p.nz : p.ny;
-  const long long stride = kZ ? (long long)p.nx * p.ny : (long long)p.nx;
-  const long long base = kZ ? (long long)o2 * p.nx + x : (long long)o2 * p.nx * p.ny + x;
-  if (kZ && !p.colmask[(long long)(o2 >> 3) * p.nbx + (x >> 3)]) return;   // no allocated voxel in this line
-  auto f_at = [&](int q) -> long long {
-    if (kZ) {
-      unsigned v = static_cast<const unsigned*>(p.fin)[base + q * stride];
-      return v == kInf32 ? kInfF : (long long)v;
-    } else {
-      unsigned v = static_cast<const unsigned short*>(p.fin)[base + q * stride];
-      return v == kNone16 ? kInfF : (long long)v * v;
+struct PbaParams {
+  unsigned* g2;                   // pass y output: 2-D squared distances (u32, x-fastest dense AABB)
+  float* esdf;                    // pass z output: ESDF blocks
+  const int* grid;                // dense slot grid over the AABB
+  const unsigned char* colmask;   // (bx, by) columns with allocated blocks
+  const unsigned* planes;         // per-slot observed / negative / site bit-planes (pass x)
+  int nx, ny, nz, nbx, nby;
+  int m;                          // line length (ny for pass y, nz for pass z)
+  int tx;                         // lines per tile (consecutive x)
+  int nbands, lb;                 // bands per line (power of two <= 32) and band length
+  int rows;                       // staged positions per line (nbox * box_h >= m)
+  int box_h, nbox;                // TMA box height and boxes per tile
+  int tiles_x;
+  double s;
+  int capped;                     // f1 fallback: E clamped at dmax
+  double dmax;
+};
+
+// Shared memory of one tile: f [rows][tx] (TMA destination), envelope site q and start t [rows][tx]
+// (u16; the stack of band b lives in rows [b lb, b lb + size)), band ranges lo / hi [nbands][tx], mbarrier.
+size_t pba_smem_bytes(int rows, int tx, int nbands, size_t esize) {
+  size_t b = (size_t)rows * tx * esize + (size_t)rows * tx * 4 + (size_t)nbands * tx * 4;
+  return ((b + 15) & ~(size_t)15) + 16;
+}
+
+template <bool kZ>
+__global__ void __launch_bounds__(256) pba_line_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                       const __grid_constant__ PbaParams p) {
+  using Elem = typename std::conditional<kZ, unsigned, unsigned short>::type;
+  extern __shared__ __align__(1024) unsigned char dsmem[];
+  unsigned char* smem = dsmem;
+  const int tx = p.tx, B = p.nbands, m = p.m, rows = p.rows, lb = p.lb;
+  Elem* fb = reinterpret_cast<Elem*>(smem);
+  unsigned short* sq = reinterpret_cast<unsigned short*>(smem + (size_t)rows * tx * sizeof(Elem));
+  unsigned short* stt = sq + (size_t)rows * tx;
+  unsigned short* blo = stt + (size_t)rows * tx;
+  unsigned short* bhi = blo + B * tx;
+  unsigned long long* mbar = reinterpret_cast<unsigned long long*>(
+      smem + (((size_t)rows * tx * sizeof(Elem) + (size_t)rows * tx * 4 + (size_t)B * tx * 4 + 15) & ~(size_t)15));
+
+  const int xt = blockIdx.x % p.tiles_x, o2 = blockIdx.x / p.tiles_x;   // o2: z (pass y) or y (pass z)
+  const int x0 = xt * tx;
+  const int xend = min(p.nx, x0 + tx);
+  if (kZ) {   // a tile whose columns hold no allocated block has no voxel to write
+    bool any = false;
+    for (int bx = x0 >> 3; bx < (xend + 7) >> 3; ++bx) any |= p.colmask[(long long)(o2 >> 3) * p.nbx + bx] != 0;
+    if (!any) return;
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(mbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(mbar, (unsigned)((size_t)rows * tx * sizeof(Elem)));
+    for (int k = 0; k < p.nbox; ++k) {
+      Elem* dst = fb + (size_t)k * p.box_h * tx;
+      if (kZ) tma_load_3d(dst, &tmap, x0, o2, k * p.box_h, mbar);
+      else tma_load_3d(dst, &tmap, x0, k * p.box_h, o2, mbar);
     }
+  }
+  const int xl = threadIdx.x % tx, b = threadIdx.x / tx;
+  const bool valid = (x0 + xl < p.nx) && (b < B);
+  auto F = [&](int q) -> long long {
+    const Elem v = fb[(size_t)q * tx + xl];
+    if (kZ) return v == kInf32 ? kInfF : (long long)v;
+    return v == kNone16 ? kInfF : (long long)v * v;
   };
-  const int qa = kSplit == 2 ? half * (m >> 1) : 0, qb = kSplit == 2 ? qa + (m >> 1) : m;
-  int top = -1, t_top = 0;
-  long long f_top = 0;
-  // Stack links.  Pass z stores with every pushed q the full state of the element below it, so a pop
-  // is ONE load; pass y (u16 input, re-read cheaply) keeps 4-byte links {t_q, prev} and re-reads f —
-  // measured: the 8-byte form costs pass y more in bytes than it saves in latency, pass z the opposite.
-  // forward: build the envelope (Meijster phase 2 with a linked stack) of the sites in [qa, qb).  The
-  // line is read in chunks of 8 independent loads so each thread keeps 8 requests in flight.
-  for (int q0 = qa; q0 < qb; q0 += 8) {
-    long long fv[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) fv[u] = (valid && q0 + u < qb) ? f_at(q0 + u) : kInfF;
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int q = q0 + u;
-      const long long fq = fv[u];
+  auto SQ = [&](int r) -> unsigned short& { return sq[(size_t)r * tx + xl]; };
+  auto ST = [&](int r) -> unsigned short& { return stt[(size_t)r * tx + xl]; };
+  auto LO = [&](int bb) -> unsigned short& { return blo[bb * tx + xl]; };
+  auto HI = [&](int bb) -> unsigned short& { return bhi[bb * tx + xl]; };
+  mbar_wait(mbar, 0);
+
+  // ---- 1) band envelopes: Meijster's stack over the sites of [q0, q1), envelope over the whole line
+  const int q0 = b * lb, q1 = min(m, q0 + lb);
+  if (valid) {
+    int size = 0, top = -1, t_top = 0;
+    long long f_top = 0;
+    for (int q = q0; q < q1; ++q) {
+      const long long fq = F(q);
       if (fq >= kInfF) continue;
-      while (top >= 0) {
-        const long long a = (long long)(t_top - top), b = (long long)(t_top - q);
-        if (a * a + f_top > b * b + fq) {                 // q beats top already at top's start: pop
-          if constexpr (kZ || kMeta64Y) {   // one load restores the whole state below top
-            const unsigned long long mt = static_cast<const unsigned long long*>(p.meta)[base + (long long)top * stride];
-            const int pr = (int)(mt & 0xffffu);
-            if (pr == 0xffff) { top = -1; break; }
-            top = pr; t_top = (int)((mt >> 16) & 0xffffu); f_top = (long long)(mt >> 32);
-          } else {
-            const unsigned mt = static_cast<const unsigned*>(p.meta)[base + (long long)top * stride];
-            const int pr = (int)(mt & 0xffffu);
-            if (pr == 0xffff) { top = -1; break; }
-            top = pr;
-            t_top = (int)(static_cast<const unsigned*>(p.meta)[base + (long long)top * stride] >> 16);
-            f_top = f_at(top);
-          }
+      while (size > 0) {
+        const long long a = t_top - top, c = t_top - q;
+        if (a * a + f_top > c * c + fq) {            // q beats top already at top's start: pop
+          --size;
+          if (size > 0) { top = SQ(q0 + size - 1); t_top = ST(q0 + size - 1); f_top = F(top); }
         } else {
           break;
         }
       }
-      int tq;
-      if (top < 0) {
-        tq = 0;
-      } else {
-        const long long num = (long long)q * q - (long long)top * top + fq - f_top;
-        const long long sep = floordiv(num, 2ll * (q - top));   // last position where top is <= q
-        if (sep + 1 >= m) continue;                             // q never wins inside the line
+      int tq = 0;
+      if (size > 0) {
+        const long long sep = floordiv_exact((long long)q * q - (long long)top * top + fq - f_top, 2ll * (q - top));
+        if (sep + 1 >= m) continue;                   // q never wins inside the line
         tq = (int)(sep + 1);
       }
-      if constexpr (kZ || kMeta64Y)
-        static_cast<unsigned long long*>(p.meta)[base + (long long)q * stride] = top < 0 ? 0xffffull
-            : ((unsigned long long)f_top << 32) | ((unsigned long long)t_top << 16) | (unsigned long long)top;
-      else
-        static_cast<unsigned*>(p.meta)[base + (long long)q * stride] =
-            ((unsigned)tq << 16) | (unsigned)(top < 0 ? 0xffff : top);
+      SQ(q0 + size) = (unsigned short)q;
+      ST(q0 + size) = (unsigned short)tq;
+      ++size;
       top = q; t_top = tq; f_top = fq;
     }
+    LO(b) = (unsigned short)q0;
+    HI(b) = (unsigned short)(q0 + size);
   }
-  // backward: read the envelope from the right, one 8-voxel chunk (= one block along the line) at a
-  // time; pass z prefetches the chunk's sign/observed placeholders before evaluating it.
-  const int bx = x >> 3;
-  for (int q0 = m - 8; q0 >= 0; q0 -= 8) {
-    int slot = -1;
-    float ph[8];
-    if (kZ) {
-      slot = p.grid[((long long)(q0 >> 3) * p.nby + (o2 >> 3)) * p.nbx + bx];
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        ph[u] = slot >= 0 ? p.esdf[(long long)slot * kBlockVox + (x & 7) + 8 * (o2 & 7) + 64 * u]
-                          : __int_as_float(0x7fc00000);
-    }
-#pragma unroll
-    for (int u = 7; u >= 0; --u) {
-      const int q = q0 + u;
-      long long d2 = kInfF;
-      if (top >= 0) {
-        const long long dq = (long long)(q - top);
-        d2 = dq * dq + f_top;
-      }
-      if (kSplit == 2) d2 = min(d2, __shfl_xor_sync(0xffffffffu, d2, 16));
-      if (!kZ) {
-        if (valid && half == 0) p.gout[base + (long long)q * stride] = d2 >= kInfF ? kInf32 : (unsigned)d2;
-      } else if (!isnan(ph[u])) {
-        float e;
-        if (d2 >= kInfF) e = __int_as_float(0x7f800000);             // S empty -> +inf (O11)
-        else e = copysignf((float)((double)p.s * sqrt((double)d2)), ph[u]);
-        p.esdf[(long long)slot * kBlockVox + (x & 7) + 8 * (o2 & 7) + 64 * u] = e;
-      }
-      if (top >= 0 && q == t_top) {
-        if constexpr (kZ || kMeta64Y) {
-          const unsigned long long mt = static_cast<const unsigned long long*>(p.meta)[base + (long long)top * stride];
-          const int pr = (int)(mt & 0xffffu);
-          if (pr == 0xffff) { top = -1; }
-          else { top = pr; t_top = (int)((mt >> 16) & 0xffffu); f_top = (long long)(mt >> 32); }
-        } else {
-          const unsigned* mm = static_cast<const unsigned*>(p.meta);
-          const int pr = (int)(mm[base + (long long)top * stride] & 0xffffu);
-          if (pr == 0xffff) { top = -1; }
-          else { top = pr; t_top = (int)(mm[base + (long long)top * stride] >> 16); f_top = f_at(top); }
+  __syncthreads();
+  // ---- 2) pairwise merges: groups [g, g + w) and [g + w, g + 2w) -> one envelope, log2(B) levels
+  for (int w = 1; w < B; w <<= 1) {
+    if (valid && (b & (2 * w - 1)) == w) {
+      const int L0 = b - w, R0 = b, R1 = b + w;
+      int jl = R0 - 1;
+      while (jl >= L0 && LO(jl) == HI(jl)) --jl;
+      int jr = R0;
+      while (jr < R1 && LO(jr) == HI(jr)) ++jr;
+      while (jl >= L0 && jr < R1) {
+        const int rb = LO(jr);
+        const int qb = SQ(rb);
+        const long long fb_ = F(qb);
+        // pop the left top while the right bottom beats it at the top's start
+        int ra = HI(jl) - 1, qa = SQ(ra), ta = ST(ra);
+        long long fa = F(qa);
+        for (;;) {
+          const long long a = ta - qa, c = ta - qb;
+          if (!(a * a + fa > c * c + fb_)) break;
+          HI(jl) = (unsigned short)ra;
+          if (LO(jl) == HI(jl)) { --jl; while (jl >= L0 && LO(jl) == HI(jl)) --jl; }
+          if (jl < L0) break;
+          ra = HI(jl) - 1; qa = SQ(ra); ta = ST(ra); fa = F(qa);
         }
+        if (jl < L0) { ST(rb) = 0; break; }           // left emptied: the right bottom starts the line
+        const long long sep = floordiv_exact((long long)qb * qb - (long long)qa * qa + fb_ - fa, 2ll * (qb - qa));
+        // the element after the right bottom (same band, or the first of the next non-empty band)
+        int rn = -1;
+        if (rb + 1 < HI(jr)) rn = rb + 1;
+        else for (int k = jr + 1; k < R1; ++k) if (LO(k) < HI(k)) { rn = LO(k); break; }
+        if (sep + 1 >= m || (rn >= 0 && sep + 1 >= (long long)ST(rn))) {   // dominated: drop it, next one
+          LO(jr) = (unsigned short)(rb + 1);
+          if (LO(jr) == HI(jr)) { ++jr; while (jr < R1 && LO(jr) == HI(jr)) ++jr; }
+          continue;
+        }
+        ST(rb) = (unsigned short)(sep + 1);
+        break;
       }
+    }
+    __syncthreads();
+  }
+  // ---- 3) every band writes its own positions from the merged envelope
+  if (!valid || q0 >= m) return;
+  int cb = -1;
+  for (int c = B - 1; c >= 0; --c)
+    if (LO(c) < HI(c) && ST(LO(c)) <= q0) { cb = c; break; }
+  const int x = x0 + xl;
+  int cr = -1, q = 0, nb_ = -1, nr = -1, tn = 0x7fffffff;
+  long long fq = kInfF;
+  auto find_next = [&]() {   // the envelope element after (cb, cr)
+    nb_ = -1; nr = -1; tn = 0x7fffffff;
+    if (cr + 1 < HI(cb)) { nb_ = cb; nr = cr + 1; }
+    else for (int k = cb + 1; k < B; ++k) if (LO(k) < HI(k)) { nb_ = k; nr = LO(k); break; }
+    if (nr >= 0) tn = ST(nr);
+  };
+  if (cb >= 0) {
+    cr = LO(cb);
+    while (cr + 1 < HI(cb) && ST(cr + 1) <= q0) ++cr;
+    q = SQ(cr); fq = F(q);
+    find_next();
+  }
+  int slot = -1, slot_bz = -1;
+  for (int pp = q0; pp < q1; ++pp) {
+    while (nr >= 0 && tn <= pp) { cb = nb_; cr = nr; q = SQ(cr); fq = F(q); find_next(); }
+    long long d2 = kInfF;
+    if (cb >= 0) { const long long d = pp - q; d2 = d * d + fq; }
+    if (!kZ) {
+      if (p.colmask[(long long)(pp >> 3) * p.nbx + (x >> 3)])   // only columns pass z will read
+        p.g2[((long long)o2 * p.ny + pp) * p.nx + x] = d2 >= kInfF ? kInf32 : (unsigned)d2;
+    } else {
+      if ((pp >> 3) != slot_bz) {
+        slot_bz = pp >> 3;
+        slot = p.grid[((long long)slot_bz * p.nby + (o2 >> 3)) * p.nbx + (x >> 3)];
+      }
+      if (slot < 0) continue;
+      const int l = (x & 7) + 8 * (o2 & 7) + 64 * (pp & 7);
+      const unsigned* pl = p.planes + (long long)slot * kPlaneWords;
+      const bool obs = (pl[l >> 5] >> (l & 31)) & 1u, neg = (pl[16 + (l >> 5)] >> (l & 31)) & 1u;
+      float e;
+      if (!obs) e = __int_as_float(0x7fc00000);                           // unobserved -> NaN (O11)
+      else if (p.capped) {
+        const double md = d2 >= kInfF ? p.dmax : fmin(p.s * sqrt((double)d2), p.dmax);
+        e = (float)(neg ? -md : md);
+      } else if (d2 >= kInfF) e = __int_as_float(0x7f800000);            // S empty -> +inf (O11)
+      else {
+        const double md = p.s * sqrt((double)d2);
+        e = (float)(neg ? -md : md);
+      }
+      p.esdf[(long long)slot * kBlockVox + l] = e;
     }
   }
 }
 
-}  // namespace
+// ------------------------------------------------------------------------------- incremental (f1)
+struct IncParams {
+  const long long* sums;
+  const unsigned* prev;       // bit-planes of the previous update (slots < nb_prev)
+  unsigned* cur;              // bit-planes of this update
+  unsigned char* flags;       // per slot: bit 0 site plane changed (source), bit 1 recompute
+  int* list;
+  int* cnt;
+  const int* grid;            // dense slot grid over the AABB
+  const int4* coords;
+  float* esdf;
+  int lo0, lo1, lo2, nbx, nby, nbz;
+  int nb, nb_prev;
+  double site_thr;
+  double s, dmax;
+  int r, rb, win;             // window radius (voxels), block radius, window side 8 + 2 r
+};
 
-cudaError_t launch_finalize(cvx_submap* sm, int n_blocks, const int lo[3], const int hi[3], cudaStream_t st) {
-  if (n_blocks <= 0) return cudaSuccess;
+__device__ __forceinline__ int grid_slot(const IncParams& p, int bx, int by, int bz) {
+  bx -= p.lo0; by -= p.lo1; bz -= p.lo2;
+  if (bx < 0 || by < 0 || bz < 0 || bx >= p.nbx || by >= p.nby || bz >= p.nbz) return -1;
+  return p.grid[((long long)bz * p.nby + by) * p.nbx + bx];
+}
+
+// one warp per 32 voxels (= one plane word of one block)
+__global__ void inc_classify(const __grid_constant__ IncParams p) {
+  const long long n = (long long)p.nb * kBlockVox;
+  const int lane = threadIdx.x & 31;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i - lane < n; i += (long long)gridDim.x * blockDim.x) {
+    const bool in = i < n;
+    bool obs = false, neg = false, site = false;
+    if (in) classify_voxel(reinterpret_cast<const longlong2*>(p.sums)[i], p.site_thr, obs, neg, site);
+    const unsigned bo = __ballot_sync(0xffffffffu, obs), bn = __ballot_sync(0xffffffffu, neg),
+                   bs = __ballot_sync(0xffffffffu, site);
+    if (lane == 0 && in) {
+      const int slot = (int)(i >> 9), w = (int)((i & 511) >> 5);
+      unsigned* c = p.cur + (long long)slot * kPlaneWords;
+      c[w] = bo; c[16 + w] = bn; c[32 + w] = bs;
+      unsigned char fl = 0;
+      if (slot >= p.nb_prev) fl = (bs ? 1 : 0) | 2;    // new block: its sites are sources, it is written
+      else {
+        const unsigned* q = p.prev + (long long)slot * kPlaneWords;
+        if (q[32 + w] != bs) fl = 3;
+        else if (q[w] != bo || q[16 + w] != bn) fl = 2;
+      }
+      if (fl) atomicOr(reinterpret_cast<unsigned*>(p.flags + (slot & ~3)), (unsigned)fl << (8 * (slot & 3)));
+    }
+  }
+}
+
+// queue every block within rb blocks (per axis) of a source block
+__global__ void inc_dilate(const __grid_constant__ IncParams p) {
+  const int k = 2 * p.rb + 1, k3 = k * k * k;
+  const long long n = (long long)p.nb * k3;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int slot = (int)(i / k3), o = (int)(i % k3);
+    if (!(p.flags[slot] & 1)) continue;
+    const int4 c = p.coords[slot];
+    const int ns = grid_slot(p, c.x + o % k - p.rb, c.y + (o / k) % k - p.rb, c.z + o / (k * k) - p.rb);
+    if (ns >= 0 && !(p.flags[ns] & 2))
+      atomicOr(reinterpret_cast<unsigned*>(p.flags + (ns & ~3)), 2u << (8 * (ns & 3)));
+  }
+}
+
+__global__ void inc_compact(const __grid_constant__ IncParams p) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < p.nb; b += gridDim.x * blockDim.x) {
+    const bool q = (p.flags[b] & 2) != 0;
+    const unsigned m = __ballot_sync(__activemask(), q);
+    if (!q) continue;
+    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(p.cnt, __popc(m));
+    base = __shfl_sync(m, base, leader);
+    p.list[base + __popc(m & ((1u << lane) - 1u))] = b;
+  }
+}
+
+// exact clamped EDT of one queued block from the site planes of the (2 rb + 1)^3 blocks around it.
+// Window: voxels [8 b - r, 8 b + 8 + r) per axis (W = 8 + 2 r <= 56 so an x-row is one u64).  Distances
+// are exact below C = (r + 1)^2 and >= C otherwise (a saturated row distance r + 1 is <= the true one,
+// and r >= d_max / s makes every value >= C clamp to d_max).
+__global__ void __launch_bounds__(256) inc_window(const __grid_constant__ IncParams p) {
+  extern __shared__ __align__(1024) unsigned char dsmem[];
+  unsigned char* smem = dsmem;
+  const int k = 2 * p.rb + 1, k3 = k * k * k, W = p.win, r = p.r;
+  unsigned* nbp = reinterpret_cast<unsigned*>(smem);                                 // [k3][16] site planes
+  unsigned long long* rowm = reinterpret_cast<unsigned long long*>(smem + (size_t)k3 * 64);   // [W][W] (z, y)
+  unsigned char* g1 = reinterpret_cast<unsigned char*>(rowm + (size_t)W * W);        // [W z][W y][8 x]
+  unsigned short* g2 = reinterpret_cast<unsigned short*>(g1 + (size_t)W * W * 8);    // [W z][8 y][8 x]
+  __shared__ int s_slot;
+  const int nq = *(volatile const int*)p.cnt;
+  const int off = 8 * p.rb - r;   // window origin inside the neighbourhood (voxels)
+  const unsigned C = (unsigned)((r + 1) * (r + 1));
+  for (int qi = blockIdx.x; qi < nq; qi += gridDim.x) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_slot = p.list[qi];
+    __syncthreads();
+    const int slot = s_slot;
+    const int4 c = p.coords[slot];
+    for (int i = threadIdx.x; i < k3 * 16; i += blockDim.x) {
+      const int o = i >> 4, w = i & 15;
+      const int ns = grid_slot(p, c.x + o % k - p.rb, c.y + (o / k) % k - p.rb, c.z + o / (k * k) - p.rb);
+      nbp[i] = ns >= 0 ? p.cur[(long long)ns * kPlaneWords + 32 + w] : 0u;
+    }
+    __syncthreads();
+    // x-row bit masks of the window
+    for (int i = threadIdx.x; i < W * W; i += blockDim.x) {
+      const int yw = i % W, zw = i / W;
+      const int yn = yw + off, zn = zw + off;
+      const int by = yn >> 3, bz = zn >> 3, row = (yn & 7) + 8 * (zn & 7);
+      unsigned long long bits = 0;
+      for (int bx = 0; bx < k; ++bx) {
+        const unsigned wd = nbp[((bz * k + by) * k + bx) * 16 + (row >> 2)];
+        bits |= (unsigned long long)((wd >> (8 * (row & 3))) & 0xffu) << (8 * bx);
+      }
+      bits >>= off;
+      if (W < 64) bits &= (1ull << W) - 1ull;
+      rowm[i] = bits;
+    }
+    __syncthreads();
+    // pass x: distance along x to the nearest window site (saturated at r + 1), for the block's 8 columns
+    for (int i = threadIdx.x; i < W * W * 8; i += blockDim.x) {
+      const int x = i & 7, yz = i >> 3;
+      const unsigned long long mk = rowm[yz];
+      const int xw = r + x;
+      int d = r + 1;
+      const unsigned long long lm = mk & ((2ull << xw) - 1ull);
+      if (lm) d = min(d, xw - (63 - __clzll(lm)));
+      const unsigned long long rm = mk >> xw;
+      if (rm) d = min(d, __ffsll(rm) - 1);
+      g1[i] = (unsigned char)d;
+    }
+    __syncthreads();
+    // pass y: min over the window's y of g1^2 + dy^2, for y in the block (saturated at C)
+    for (int i = threadIdx.x; i < W * 64; i += blockDim.x) {
+      const int x = i & 7, y = (i >> 3) & 7, zw = i >> 6;
+      const int yc = r + y;
+      unsigned best = C;
+      const unsigned char* col = g1 + (size_t)zw * W * 8 + x;
+      for (int yw = 0; yw < W; ++yw) {
+        const unsigned g = col[yw * 8];
+        const int dy = yc - yw;
+        best = min(best, g * g + (unsigned)(dy * dy));
+      }
+      g2[i] = (unsigned short)best;
+    }
+    __syncthreads();
+    // pass z + write-back: E = sign(D) min(s sqrt(d^2), d_max), NaN unobserved
+    for (int l = threadIdx.x; l < kBlockVox; l += blockDim.x) {
+      const int xy = l & 63, z = l >> 6;
+      const int zc = r + z;
+      unsigned best = C;
+      for (int zw = 0; zw < W; ++zw) {
+        const int dz = zc - zw;
+        best = min(best, (unsigned)g2[zw * 64 + xy] + (unsigned)(dz * dz));
+      }
+      const unsigned* pl = p.cur + (long long)slot * kPlaneWords;
+      const bool obs = (pl[l >> 5] >> (l & 31)) & 1u, neg = (pl[16 + (l >> 5)] >> (l & 31)) & 1u;
+      float e;
+      if (!obs) e = __int_as_float(0x7fc00000);
+      else {
+        const double md = best >= C ? p.dmax : fmin(p.s * sqrt((double)best), p.dmax);
+        e = (float)(neg ? -md : md);
+      }
+      p.esdf[(long long)slot * kBlockVox + l] = e;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------- host side
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn;
+}
+
+cudaError_t grow_async(void** ptr, int64_t* cap, int64_t need, cudaStream_t st) {
+  if (*cap >= need) return cudaSuccess;
+  if (*ptr) cudaFreeAsync(*ptr, st);
+  *ptr = nullptr;
+  *cap = 0;
+  cudaError_t e = cudaMallocAsync(ptr, (size_t)need, st);
+  if (e == cudaSuccess) *cap = need;
+  return e;
+}
+
+cudaError_t ensure_planes(cvx_submap* sm, cudaStream_t st) {
+  if (sm->planes[0]) return cudaSuccess;
+  const size_t bytes = (size_t)sm->pool.max_blocks * kPlaneWords * 4;
+  cudaError_t e = cudaMallocAsync(&sm->planes[0], bytes, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&sm->planes[1], bytes, st);
+  return e;
+}
+
+// dense slot grid over the AABB (+ optional column / row masks)
+cudaError_t build_grid(cvx_submap* sm, const int lo[3], int nbx, int nby, int nbz, unsigned char* colmask,
+                       unsigned char* rowmask, cudaStream_t st, const char* name) {
+  const long long nblk = (long long)nbx * nby * nbz;
+  void* g = sm->block_grid;
+  cudaError_t e = grow_async(&g, &sm->block_grid_cap, nblk * (long long)sizeof(int), st);
+  sm->block_grid = static_cast<int*>(g);
+  if (e != cudaSuccess) return e;
+  cudaMemsetAsync(sm->block_grid, 0xff, sizeof(int) * (size_t)nblk, st);
+  ProfScope ps_(sm, name, st);
+  block_grid_kernel<<<148 * 4, 256, 0, st>>>(sm->ctr, sm->pool.coords, sm->pool.max_blocks, sm->block_grid, colmask,
+                                             rowmask, lo[0], lo[1], lo[2], nbx, nby);
+  return cudaSuccess;
+}
+
+template <bool kZ>
+cudaError_t launch_pba(cvx_submap* sm, const void* fin, const PbaParams& base, cudaStream_t st) {
+  auto enc = tmap_encoder();
+  if (!enc) return cudaErrorNotSupported;
+  PbaParams p = base;
+  const size_t esize = kZ ? 4 : 2;
+  p.m = kZ ? p.nz : p.ny;
+  p.nbox = (p.m + 255) / 256;
+  p.box_h = ((p.m + p.nbox - 1) / p.nbox + 7) & ~7;   // box bytes a multiple of 128 (TMA smem alignment)
+  p.rows = p.nbox * p.box_h;
+  p.tx = 8;
+  for (int t : {32, 16}) {
+    if (pba_smem_bytes(p.rows, t, 1, esize) <= 100 * 1024 && t <= ((p.nx + 7) & ~7)) { p.tx = t; break; }
+  }
+  int B = 1;
+  while (B * 2 * p.tx <= 256 && B * 2 <= 32 && (p.m + B * 2 - 1) / (B * 2) >= 8) B *= 2;
+  p.nbands = B;
+  p.lb = (p.m + B - 1) / B;
+  p.tiles_x = (p.nx + p.tx - 1) / p.tx;
+  const size_t smem = pba_smem_bytes(p.rows, p.tx, B, esize);
+  CUtensorMap tm;
+  const cuuint64_t dims[3] = {(cuuint64_t)p.nx, (cuuint64_t)p.ny, (cuuint64_t)p.nz};
+  const cuuint64_t strides[2] = {(cuuint64_t)p.nx * esize, (cuuint64_t)p.nx * p.ny * esize};
+  const cuuint32_t box[3] = {(cuuint32_t)p.tx, kZ ? 1u : (cuuint32_t)p.box_h, kZ ? (cuuint32_t)p.box_h : 1u};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult cr = enc(&tm, kZ ? CU_TENSOR_MAP_DATA_TYPE_UINT32 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 3,
+                    const_cast<void*>(fin), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  cudaFuncSetAttribute(pba_line_kernel<kZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const long long tiles = (long long)p.tiles_x * (kZ ? p.ny : p.nz);
+  ProfScope ps_(sm, kZ ? "esdf_pass_z" : "esdf_pass_y", st);
+  pba_line_kernel<kZ><<<(unsigned)tiles, p.tx * B, smem, st>>>(tm, p);
+  return cudaGetLastError();
+}
+
+// the dense exact EDT (finalize; capped = f1 fallback): planes go to sm->planes[sm->cur_planes]
+cudaError_t dense_edt(cvx_submap* sm, const int lo[3], const int hi[3], cudaStream_t st, bool capped, double dmax) {
   const int nbx = hi[0] - lo[0] + 1, nby = hi[1] - lo[1] + 1, nbz = hi[2] - lo[2] + 1;
   const int nx = 8 * nbx, ny = 8 * nby, nz = 8 * nbz;
-  const long long nblk = (long long)nbx * nby * nbz;
   const long long nvox = (long long)nx * ny * nz;
-  cudaError_t e;
-  if (sm->block_grid_cap < nblk) {
-    if (sm->block_grid) cudaFree(sm->block_grid);
-    sm->block_grid = nullptr; sm->block_grid_cap = 0;
-    if ((e = cudaMalloc(&sm->block_grid, sizeof(int) * (size_t)nblk)) != cudaSuccess) return e;
-    sm->block_grid_cap = nblk;
-  }
-  const long long need = nvox * (2 + 4 + 8) + (long long)nbx * nby + (long long)nby * nbz + 256;
-  if (sm->edt_bytes < need) {
-    if (sm->edt) cudaFree(sm->edt);
-    sm->edt = nullptr; sm->edt_bytes = 0;
-    if ((e = cudaMalloc(&sm->edt, (size_t)need)) != cudaSuccess) return e;
-    sm->edt_bytes = need;
-  }
-#if CVX_EDT_LAYOUT == 0
+  cudaError_t e = ensure_planes(sm, st);
+  if (e != cudaSuccess) return e;
+  const long long need = nvox * (4 + 2) + (long long)nbx * nby + (long long)nby * nbz + 256;
+  if ((e = grow_async(&sm->edt, &sm->edt_bytes, need, st)) != cudaSuccess) return e;
   unsigned* g2 = reinterpret_cast<unsigned*>(sm->edt);
-  unsigned long long* meta = reinterpret_cast<unsigned long long*>(g2 + nvox);   // nvox % 512 == 0: aligned
-  unsigned short* g1 = reinterpret_cast<unsigned short*>(meta + nvox);
+  unsigned short* g1 = reinterpret_cast<unsigned short*>(g2 + nvox);   // nvox % 512 == 0: aligned
   unsigned char* colmask = reinterpret_cast<unsigned char*>(g1 + nvox);
-#else
-  unsigned short* g1 = reinterpret_cast<unsigned short*>(sm->edt);
-  unsigned* g2 = reinterpret_cast<unsigned*>(g1 + nvox);
-  unsigned long long* meta = reinterpret_cast<unsigned long long*>(g2 + nvox);
-  unsigned char* colmask = reinterpret_cast<unsigned char*>(meta + nvox);
-#endif
-  cudaMemsetAsync(sm->block_grid, 0xff, sizeof(int) * (size_t)nblk, st);
   unsigned char* rowmask = colmask + (size_t)nbx * nby;
   cudaMemsetAsync(colmask, 0, (size_t)nbx * nby + (size_t)nby * nbz, st);
-  {
-    ProfScope ps_(sm, "esdf_block_grid", st);
-    block_grid_kernel<<<148 * 4, 256, 0, st>>>(sm->ctr, sm->pool.coords, sm->pool.max_blocks, sm->block_grid,
-                                               colmask, rowmask, lo[0], lo[1], lo[2], nbx, nby);
-  }
+  if ((e = build_grid(sm, lo, nbx, nby, nbz, colmask, rowmask, st, "esdf_block_grid")) != cudaSuccess) return e;
+  unsigned* planes = sm->planes[sm->cur_planes];
   XParams xp;
-  xp.sums = sm->pool.sums; xp.esdf = sm->pool.esdf; xp.grid = sm->block_grid; xp.g1 = g1; xp.rowmask = rowmask;
+  xp.sums = sm->pool.sums; xp.planes = planes; xp.grid = sm->block_grid; xp.g1 = g1; xp.rowmask = rowmask;
   xp.nx = nx; xp.ny = ny; xp.nz = nz; xp.nbx = nbx; xp.nby = nby; xp.site_thr = sm->cfg.site_threshold;
   const int nch = (nx + 31) / 32;
   const size_t smem = (size_t)4 * 3 * nch * sizeof(unsigned);
@@ -360,326 +694,97 @@ cudaError_t launch_finalize(cvx_submap* sm, int n_blocks, const int lo[3], const
     ProfScope ps_(sm, "esdf_pass_x", st);
     pass_x_kernel<<<xblocks, 128, smem, st>>>(xp);
   }
-
-  LineParams lp;
-  lp.fin = g1; lp.gout = g2; lp.meta = meta; lp.esdf = sm->pool.esdf; lp.grid = sm->block_grid; lp.colmask = colmask;
-  lp.nx = nx; lp.ny = ny; lp.nz = nz; lp.nbx = nbx; lp.nby = nby; lp.s = (float)sm->cfg.voxel_size;
-  long long nl = (long long)nx * nz;
-  {
-    ProfScope ps_(sm, "esdf_pass_y", st);
-    // (the 2-way split of pass_line_kernel measured no faster on configs[1] and 1.6x slower on configs[4])
-    pass_line_kernel<false, 1><<<(unsigned)((nl + 255) / 256), 256, 0, st>>>(lp);
-  }
-  lp.fin = g2;
-  nl = (long long)nx * ny;
-  {
-    ProfScope ps_(sm, "esdf_pass_z", st);
-    pass_line_kernel<true, 1><<<(unsigned)((nl + 255) / 256), 256, 0, st>>>(lp);
-  }
-  return cudaGetLastError();
-}
-
-}  // namespace cvx
-
-// ================================================================================================
-// Incremental ESDF: keep, per voxel, a pointer to its nearest site
-// (packed offset) and, after new integration, update only what changed:
-//   inc_classify   new / removed sites (site = observed and |D| <= tau_site, R4) per voxel; new blocks
-//                  start without a parent; blocks with changes are queued (one region queue = one block)
-//   inc_invalidate "raise": every voxel whose parent is no longer a site loses it (one direct check per
-//                  voxel instead of a wavefront)
-//   inc_propagate  "lower": per queued block, one CTA relaxes the 8^3 voxels plus the neighbour faces in
-//                  shared memory (sweeps along all axis directions until the block is stable, P:L149
-//                  "process every axis direction within each queued block"), writes back, and queues the
-//                  neighbour blocks whose shared face changed; repeated until no block is queued
-//   inc_write      E = sign(D) s |v - parent| (NaN unobserved, +inf without a site)
-// The fixpoint is the 6-neighbour parent-propagation distance of the paper's scheme, not always the
-// exact EDT; tests/test_gpu_esdf_incremental.py bounds the difference to finalize_esdf.
-namespace cvx {
-namespace {
-
-constexpr unsigned long long kNoPar = 1ull << 63;
-constexpr unsigned long long kFld = (1ull << 21) - 1;
-
-__device__ __forceinline__ unsigned long long pack3(int x, int y, int z) {
-  return ((unsigned long long)(x & (int)kFld) << 42) | ((unsigned long long)(y & (int)kFld) << 21) |
-         (unsigned long long)(z & (int)kFld);
-}
-__device__ __forceinline__ int fld(unsigned long long p, int sh) {
-  return (int)((long long)(p << (43 - sh)) >> 43);   // sign-extend the 21-bit field at bit sh
-}
-
-struct IncParams {
-  const long long* sums;
-  float* esdf;
-  const int4* coords;
-  unsigned long long* par;   // per voxel: packed offset (parent - v), kNoPar = none
-  unsigned* sitebits;        // per block: 16 x 32 bits
-  int* active;               // per block: queued flag
-  int* list;                 // compacted queue
-  int* cnt;                  // queue length
-  const int* grid;           // dense slot grid over the AABB
-  int lo0, lo1, lo2, nbx, nby, nbz;
-  int nb, nb_prev;
-  double site_thr;
-  float s;
-};
-
-__device__ __forceinline__ int grid_slot(const IncParams& p, int bx, int by, int bz) {
-  bx -= p.lo0; by -= p.lo1; bz -= p.lo2;
-  if (bx < 0 || by < 0 || bz < 0 || bx >= p.nbx || by >= p.nby || bz >= p.nbz) return -1;
-  return p.grid[((long long)bz * p.nby + by) * p.nbx + bx];
-}
-
-__device__ __forceinline__ bool is_site(const IncParams& p, long long vi, bool& observed, bool& neg) {
-  const longlong2 sw = reinterpret_cast<const longlong2*>(p.sums)[vi];
-  observed = sw.y > 0;
-  if (!observed) { neg = false; return false; }
-  const float D = (float)((double)sw.x / (double)sw.y);
-  neg = D < 0.0f;
-  return fabs((double)D) <= p.site_thr;
-}
-
-__global__ void inc_classify(const __grid_constant__ IncParams p) {
-  const long long n = (long long)p.nb * kBlockVox;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const int slot = (int)(i >> 9), l = (int)(i & 511);
-    bool obs, neg;
-    const bool site = is_site(p, i, obs, neg);
-    const bool fresh = slot >= p.nb_prev;
-    const bool old = !fresh && ((p.sitebits[(long long)slot * 16 + (l >> 5)] >> (l & 31)) & 1u);
-    if (fresh) p.par[i] = site ? 0ull : kNoPar;
-    else if (site && !old) p.par[i] = 0ull;
-    else if (!site && old) p.par[i] = kNoPar;
-    const unsigned bits = __ballot_sync(0xffffffffu, site);   // 32 consecutive voxels of one block
-    if ((l & 31) == 0) p.sitebits[(long long)slot * 16 + (l >> 5)] = bits;
-    if (fresh || site != old) p.active[slot] = 1;
-  }
-}
-
-__global__ void inc_invalidate(const __grid_constant__ IncParams p) {
-  const long long n = (long long)p.nb_prev * kBlockVox;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const unsigned long long q = p.par[i];
-    if (q == kNoPar || q == 0ull) continue;
-    const int slot = (int)(i >> 9), l = (int)(i & 511);
-    const int4 c = p.coords[slot];
-    const int px = 8 * c.x + (l & 7) + fld(q, 42), py = 8 * c.y + ((l >> 3) & 7) + fld(q, 21),
-              pz = 8 * c.z + (l >> 6) + fld(q, 0);
-    const int ps = grid_slot(p, px >> 3, py >> 3, pz >> 3);
-    const int pl = (px & 7) | ((py & 7) << 3) | ((pz & 7) << 6);
-    const bool alive = ps >= 0 && ((p.sitebits[(long long)ps * 16 + (pl >> 5)] >> (pl & 31)) & 1u);
-    if (!alive) { p.par[i] = kNoPar; p.active[slot] = 1; }
-  }
-}
-
-__global__ void inc_compact(const __grid_constant__ IncParams p) {
-  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < p.nb; b += gridDim.x * blockDim.x)
-    if (p.active[b]) { p.active[b] = 0; p.list[atomicAdd(p.cnt, 1)] = b; }
-}
-
-// squared distance from local voxel (x,y,z) to a parent given relative to the block origin
-__device__ __forceinline__ long long pd2(unsigned long long a, int x, int y, int z) {
-  const long long dx = fld(a, 42) - x, dy = fld(a, 21) - y, dz = fld(a, 0) - z;
-  return dx * dx + dy * dy + dz * dz;
-}
-
-// one 64-thread CTA per queued block (grid-stride over the queue); shared memory holds the block + its 6
-// face neighbours (10^3 halo cube) as parents relative to the block origin.  The block is relaxed by
-// directional sweeps ("process every axis direction within each queued block"): thread t owns
-// line t along the swept axis and carries the best parent forward (then backward) over the 8 voxels;
-// rounds of the six sweeps repeat until no voxel changes, which is the 6-neighbour local fixpoint.
-__global__ void __launch_bounds__(64) inc_propagate(const __grid_constant__ IncParams p) {
-  __shared__ unsigned long long cur[1000];
-  __shared__ int nb_slot[6];
-  __shared__ int face_changed[6];
-  const int qlen = *(volatile const int*)p.cnt;
-  const int t = threadIdx.x;
-  for (int qi = blockIdx.x; qi < qlen; qi += gridDim.x) {
-    __syncthreads();
-    const int slot = p.list[qi];
-    const int4 c = p.coords[slot];
-    if (t < 6) {
-      const int d = (t >> 1), sg = (t & 1) ? 1 : -1;
-      nb_slot[t] = grid_slot(p, c.x + (d == 0) * sg, c.y + (d == 1) * sg, c.z + (d == 2) * sg);
-      face_changed[t] = 0;
-    }
-    __syncthreads();
-    for (int l = t; l < 512; l += 64) {
-      const int x = l & 7, y = (l >> 3) & 7, z = l >> 6;
-      const unsigned long long q = p.par[(long long)slot * kBlockVox + l];
-      cur[(x + 1) + 10 * (y + 1) + 100 * (z + 1)] = q == kNoPar ? kNoPar : pack3(x + fld(q, 42), y + fld(q, 21), z + fld(q, 0));
-    }
-    for (int k = t; k < 384; k += 64) {   // face halo: 6 faces x 64 voxels
-      const int f = k >> 6, a = k & 7, b = (k >> 3) & 7, d = f >> 1, hi = f & 1;
-      const int ns = nb_slot[f];
-      int x, y, z, nl;
-      if (d == 0) { x = hi ? 8 : -1; y = a; z = b; nl = (hi ? 0 : 7) | (a << 3) | (b << 6); }
-      else if (d == 1) { x = a; y = hi ? 8 : -1; z = b; nl = a | ((hi ? 0 : 7) << 3) | (b << 6); }
-      else { x = a; y = b; z = hi ? 8 : -1; nl = a | (b << 3) | ((hi ? 0 : 7) << 6); }
-      unsigned long long v = kNoPar;
-      if (ns >= 0) {
-        const unsigned long long q = *(volatile const unsigned long long*)&p.par[(long long)ns * kBlockVox + nl];
-        if (q != kNoPar) v = pack3(x + fld(q, 42), y + fld(q, 21), z + fld(q, 0));
-      }
-      cur[(x + 1) + 10 * (y + 1) + 100 * (z + 1)] = v;
-    }
-    __syncthreads();
-    const int la = t & 7, lb = t >> 3;   // this thread's line: the two coordinates other than the swept one
-    for (int round = 0; round < 16; ++round) {
-      int changed = 0;
-#pragma unroll 1
-      for (int sw = 0; sw < 6; ++sw) {
-        const int ax = sw >> 1, dir = (sw & 1) ? -1 : 1;
-        const int stride = ax == 0 ? 1 : (ax == 1 ? 10 : 100);
-        int x0, y0, z0;   // first voxel of the line in sweep order (local coords)
-        if (ax == 0) { x0 = dir > 0 ? 0 : 7; y0 = la; z0 = lb; }
-        else if (ax == 1) { x0 = la; y0 = dir > 0 ? 0 : 7; z0 = lb; }
-        else { x0 = la; y0 = lb; z0 = dir > 0 ? 0 : 7; }
-        int ci = (x0 + 1) + 10 * (y0 + 1) + 100 * (z0 + 1);
-        unsigned long long carry = cur[ci - dir * stride];   // halo / previous voxel
-        int x = x0, y = y0, z = z0;
-        for (int st = 0; st < 8; ++st) {
-          unsigned long long best = cur[ci];
-          long long bd = best == kNoPar ? 0x7fffffffffffffffll : pd2(best, x, y, z);
-          if (carry != kNoPar) {
-            const long long d = pd2(carry, x, y, z);
-            if (d < bd || (d == bd && carry < best)) { bd = d; best = carry; cur[ci] = best; changed = 1; }
-          }
-          carry = best;
-          ci += dir * stride;
-          if (ax == 0) x += dir; else if (ax == 1) y += dir; else z += dir;
-        }
-        __syncthreads();
-      }
-      if (!__syncthreads_or(changed)) break;
-    }
-    // write back; a changed face voxel queues the neighbour block across that face
-    for (int l = t; l < 512; l += 64) {
-      const int x = l & 7, y = (l >> 3) & 7, z = l >> 6;
-      const unsigned long long b = cur[(x + 1) + 10 * (y + 1) + 100 * (z + 1)];
-      const unsigned long long nq = b == kNoPar ? kNoPar : pack3(fld(b, 42) - x, fld(b, 21) - y, fld(b, 0) - z);
-      unsigned long long* dst = &p.par[(long long)slot * kBlockVox + l];
-      if (*dst != nq) {
-        *dst = nq;
-        if (x == 0) face_changed[0] = 1;
-        if (x == 7) face_changed[1] = 1;
-        if (y == 0) face_changed[2] = 1;
-        if (y == 7) face_changed[3] = 1;
-        if (z == 0) face_changed[4] = 1;
-        if (z == 7) face_changed[5] = 1;
-      }
-    }
-    __syncthreads();
-    if (t < 6 && face_changed[t] && nb_slot[t] >= 0) p.active[nb_slot[t]] = 1;
-  }
-}
-
-__global__ void inc_write(const __grid_constant__ IncParams p) {
-  const long long n = (long long)p.nb * kBlockVox;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    bool obs, neg;
-    (void)is_site(p, i, obs, neg);
-    float e;
-    const unsigned long long q = p.par[i];
-    if (!obs) e = __int_as_float(0x7fc00000);
-    else if (q == kNoPar) e = __int_as_float(0x7f800000);
-    else {
-      const long long dx = fld(q, 42), dy = fld(q, 21), dz = fld(q, 0);
-      const float m = (float)((double)p.s * sqrt((double)(dx * dx + dy * dy + dz * dz)));
-      e = neg ? -m : m;
-    }
-    p.esdf[i] = e;
-  }
+  PbaParams pp{};
+  pp.g2 = g2; pp.esdf = sm->pool.esdf; pp.grid = sm->block_grid; pp.colmask = colmask; pp.planes = planes;
+  pp.nx = nx; pp.ny = ny; pp.nz = nz; pp.nbx = nbx; pp.nby = nby; pp.s = sm->cfg.voxel_size;
+  pp.capped = capped ? 1 : 0; pp.dmax = dmax;
+  if ((e = launch_pba<false>(sm, g1, pp, st)) != cudaSuccess) return e;
+  return launch_pba<true>(sm, g2, pp, st);
 }
 
 }  // namespace
 
-cudaError_t launch_update_esdf(cvx_submap* sm, int n_blocks, const int lo[3], const int hi[3], cudaStream_t st,
-                               int* iterations) {
-  *iterations = 0;
+cudaError_t launch_finalize(cvx_submap* sm, int n_blocks, const int lo[3], const int hi[3], cudaStream_t st) {
+  sm->inc.nb_prev = 0;   // the uncapped ESDF is not the incremental one: the next update recomputes all
   if (n_blocks <= 0) return cudaSuccess;
-  cudaError_t e;
-  const size_t mb = (size_t)sm->pool.max_blocks;
-  if (!sm->inc.par) {
-    if ((e = cudaMalloc(&sm->inc.par, mb * kBlockVox * 8)) != cudaSuccess ||
-        (e = cudaMalloc(&sm->inc.sitebits, mb * 64)) != cudaSuccess ||
-        (e = cudaMalloc(&sm->inc.active, mb * 4)) != cudaSuccess ||
-        (e = cudaMalloc(&sm->inc.list, mb * 4)) != cudaSuccess ||
-        (e = cudaMallocHost(&sm->inc.cnt_host, 4)) != cudaSuccess ||
-        (e = cudaMalloc(&sm->inc.cnt, 4)) != cudaSuccess)
+  return dense_edt(sm, lo, hi, st, false, 0.0);
+}
+
+cudaError_t launch_update_esdf(cvx_submap* sm, int n_blocks, const int lo[3], const int hi[3], cudaStream_t st,
+                               int* blocks_updated) {
+  *blocks_updated = 0;
+  if (n_blocks <= 0) { sm->inc.nb_prev = 0; return cudaSuccess; }
+  cudaError_t e = ensure_planes(sm, st);
+  if (e != cudaSuccess) return e;
+  const double s = sm->cfg.voxel_size, dmax = sm->cfg.esdf_max_distance;
+  const int r = std::max(1, (int)std::ceil(dmax / s));
+  const int rb = (r + 7) / 8;
+  if (rb > 3) {   // window of more than 7^3 blocks: the dense exact EDT, clamped (same values)
+    sm->cur_planes ^= 1;
+    if ((e = dense_edt(sm, lo, hi, st, true, dmax)) != cudaSuccess) return e;
+    sm->inc.nb_prev = n_blocks;
+    *blocks_updated = n_blocks;
+    return cudaSuccess;
+  }
+  if (!sm->inc.flags) {
+    const size_t mb = (size_t)sm->pool.max_blocks;
+    if ((e = cudaMallocAsync(reinterpret_cast<void**>(&sm->inc.flags), (mb + 3) & ~(size_t)3, st)) != cudaSuccess ||
+        (e = cudaMallocAsync(reinterpret_cast<void**>(&sm->inc.list), mb * 4, st)) != cudaSuccess ||
+        (e = cudaMallocAsync(reinterpret_cast<void**>(&sm->inc.cnt), 4, st)) != cudaSuccess ||
+        (e = cudaMallocHost(&sm->inc.cnt_host, 4)) != cudaSuccess)
       return e;
-    cudaMemsetAsync(sm->inc.active, 0, mb * 4, st);
-    sm->inc.nb_prev = 0;
   }
   const int nbx = hi[0] - lo[0] + 1, nby = hi[1] - lo[1] + 1, nbz = hi[2] - lo[2] + 1;
-  const long long nblk = (long long)nbx * nby * nbz;
-  if (sm->block_grid_cap < nblk) {
-    if (sm->block_grid) cudaFree(sm->block_grid);
-    sm->block_grid = nullptr; sm->block_grid_cap = 0;
-    if ((e = cudaMalloc(&sm->block_grid, sizeof(int) * (size_t)nblk)) != cudaSuccess) return e;
-    sm->block_grid_cap = nblk;
-  }
-  // dense slot grid (the colmask / rowmask side outputs go to a scratch tail of the EDT buffer)
-  const long long mask_bytes = (long long)nbx * nby + (long long)nby * nbz + 256;
-  if (sm->edt_bytes < mask_bytes) {
-    if (sm->edt) cudaFree(sm->edt);
-    sm->edt = nullptr; sm->edt_bytes = 0;
-    if ((e = cudaMalloc(&sm->edt, (size_t)mask_bytes)) != cudaSuccess) return e;
-    sm->edt_bytes = mask_bytes;
-  }
-  unsigned char* colmask = reinterpret_cast<unsigned char*>(sm->edt);
-  cudaMemsetAsync(sm->block_grid, 0xff, sizeof(int) * (size_t)nblk, st);
-  {
-    ProfScope ps_(sm, "inc_block_grid", st);
-    block_grid_kernel<<<148 * 4, 256, 0, st>>>(sm->ctr, sm->pool.coords, sm->pool.max_blocks, sm->block_grid,
-                                               colmask, colmask + (size_t)nbx * nby, lo[0], lo[1], lo[2], nbx, nby);
-  }
+  if ((e = build_grid(sm, lo, nbx, nby, nbz, nullptr, nullptr, st, "inc_block_grid")) != cudaSuccess) return e;
+  const int prev = sm->cur_planes, cur = prev ^ 1;
   IncParams ip;
-  ip.sums = sm->pool.sums; ip.esdf = sm->pool.esdf; ip.coords = sm->pool.coords; ip.par = sm->inc.par;
-  ip.sitebits = sm->inc.sitebits; ip.active = sm->inc.active; ip.list = sm->inc.list; ip.cnt = sm->inc.cnt;
-  ip.grid = sm->block_grid; ip.lo0 = lo[0]; ip.lo1 = lo[1]; ip.lo2 = lo[2]; ip.nbx = nbx; ip.nby = nby; ip.nbz = nbz;
+  ip.sums = sm->pool.sums; ip.prev = sm->planes[prev]; ip.cur = sm->planes[cur];
+  ip.flags = sm->inc.flags; ip.list = sm->inc.list; ip.cnt = sm->inc.cnt; ip.grid = sm->block_grid;
+  ip.coords = sm->pool.coords; ip.esdf = sm->pool.esdf;
+  ip.lo0 = lo[0]; ip.lo1 = lo[1]; ip.lo2 = lo[2]; ip.nbx = nbx; ip.nby = nby; ip.nbz = nbz;
   ip.nb = n_blocks; ip.nb_prev = std::min(sm->inc.nb_prev, n_blocks);
-  ip.site_thr = sm->cfg.site_threshold; ip.s = (float)sm->cfg.voxel_size;
+  ip.site_thr = sm->cfg.site_threshold; ip.s = s; ip.dmax = dmax;
+  ip.r = r; ip.rb = rb; ip.win = 8 + 2 * r;
+  cudaMemsetAsync(sm->inc.flags, 0, ((size_t)n_blocks + 3) & ~(size_t)3, st);
+  cudaMemsetAsync(sm->inc.cnt, 0, 4, st);
   {
     ProfScope ps_(sm, "inc_classify", st);
     inc_classify<<<148 * 8, 256, 0, st>>>(ip);
   }
-  if (ip.nb_prev > 0) {
-    ProfScope ps_(sm, "inc_invalidate", st);
-    inc_invalidate<<<148 * 8, 256, 0, st>>>(ip);
-  }
-  // waves are launched in groups of kWaves between host checks of the queue: a wave whose queue is empty
-  // costs two tiny launches (the propagate grid exits at once), a host round trip costs far more.
-  // Each wave: propagate the queued blocks, then compact the blocks they queued into the next list.
-  constexpr int kWaves = 8;
-  const unsigned pgrid = (unsigned)std::min<long long>(n_blocks, 148ll * 32);
-  auto compact = [&]() {
-    cudaMemsetAsync(sm->inc.cnt, 0, 4, st);
-    ProfScope ps_(sm, "inc_compact", st);
-    inc_compact<<<(n_blocks + 255) / 256, 256, 0, st>>>(ip);
-  };
-  compact();
-  cudaMemcpyAsync(sm->inc.cnt_host, sm->inc.cnt, 4, cudaMemcpyDeviceToHost, st);
-  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
-  for (int group = 0; *sm->inc.cnt_host != 0 && group < 100000; ++group) {
-    for (int w = 0; w < kWaves; ++w) {
-      {
-        ProfScope ps_(sm, "inc_propagate", st);
-        inc_propagate<<<pgrid, 64, 0, st>>>(ip);
-      }
-      compact();
-    }
-    *iterations += kWaves;
-    cudaMemcpyAsync(sm->inc.cnt_host, sm->inc.cnt, 4, cudaMemcpyDeviceToHost, st);
-    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+  {
+    ProfScope ps_(sm, "inc_dilate", st);
+    const long long n = (long long)n_blocks * (2 * rb + 1) * (2 * rb + 1) * (2 * rb + 1);
+    inc_dilate<<<(unsigned)std::min<long long>((n + 255) / 256, 148ll * 16), 256, 0, st>>>(ip);
   }
   {
-    ProfScope ps_(sm, "inc_write", st);
-    inc_write<<<148 * 8, 256, 0, st>>>(ip);
+    ProfScope ps_(sm, "inc_compact", st);
+    inc_compact<<<(n_blocks + 255) / 256, 256, 0, st>>>(ip);
   }
+  const int k = 2 * rb + 1, W = ip.win;
+  const size_t smem = (size_t)k * k * k * 64 + (size_t)W * W * 8 + (size_t)W * W * 8 + (size_t)W * 64 * 2;
+  cudaFuncSetAttribute(inc_window, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    ProfScope ps_(sm, "inc_window", st);
+    inc_window<<<148 * 4, 256, smem, st>>>(ip);
+  }
+  cudaMemcpyAsync(sm->inc.cnt_host, sm->inc.cnt, 4, cudaMemcpyDeviceToHost, st);
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+  *blocks_updated = *sm->inc.cnt_host;
+  sm->cur_planes = cur;
   sm->inc.nb_prev = n_blocks;
   return cudaGetLastError();
+}
+
+void release_esdf(cvx_submap* sm) {
+  if (sm->edt) cudaFree(sm->edt);
+  if (sm->block_grid) cudaFree(sm->block_grid);
+  for (auto& pl : sm->planes) if (pl) cudaFree(pl);
+  if (sm->inc.flags) cudaFree(sm->inc.flags);
+  if (sm->inc.list) cudaFree(sm->inc.list);
+  if (sm->inc.cnt) cudaFree(sm->inc.cnt);
+  if (sm->inc.cnt_host) cudaFreeHost(sm->inc.cnt_host);
+  sm->edt = nullptr; sm->block_grid = nullptr; sm->planes[0] = sm->planes[1] = nullptr;
+  sm->inc = cvx_submap::Inc{};
 }
 
 }  // namespace cvx

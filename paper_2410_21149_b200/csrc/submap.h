@@ -74,21 +74,24 @@ struct cvx_submap {
   long long list_cap_limit = 1ll << 62;   // test knob: cap on the per-ray slot-list buffer (full: walk hashes)
   bool fuse_alloc = false;    // constant weights: ALLOCATE inside walk_cw_kernel (measured 1.4x slower: off)
 
-  // ESDF scratch (grow-only)
-  void* edt = nullptr;        // device: g2 u32 | meta u32 | g1 u16 over the dense AABB
+  // ESDF scratch (grow-only, stream-ordered cudaMallocAsync on the calling stream)
+  void* edt = nullptr;        // device: g2 u32 | g1 u16 over the dense AABB, then the column / row masks
   int64_t edt_bytes = 0;
   int* block_grid = nullptr;  // device int32 [nbz][nby][nbx]
   int64_t block_grid_cap = 0;
+  // per-slot bit-planes of the last ESDF pass (pass x of finalize, or the incremental classify): 48 u32
+  // words per slot = observed | D < 0 | site (O10), bit l = voxel local index l.  Two buffers: the
+  // incremental update compares the new planes with the previous ones.
+  unsigned* planes[2] = {nullptr, nullptr};
+  int cur_planes = 0;
 
-  // incremental ESDF state (allocated on the first cvx_update_esdf)
+  // incremental ESDF state (R11: exact EDT clamped at esdf_max_distance)
   struct Inc {
-    unsigned long long* par = nullptr;  // per voxel: packed offset to the nearest site
-    unsigned* sitebits = nullptr;       // per block: site bitmask at the last update
-    int* active = nullptr;              // per block: queued
-    int* list = nullptr;                // compacted queue
+    unsigned char* flags = nullptr;     // per slot: bit 0 site plane changed, bit 1 block must be recomputed
+    int* list = nullptr;                // compacted queue of the blocks to recompute (one region per block)
     int* cnt = nullptr;
     int* cnt_host = nullptr;            // pinned
-    int nb_prev = 0;                    // blocks covered by the last update
+    int nb_prev = 0;                    // blocks covered by the last update (0: recompute everything)
   } inc;
 
   int* proj_birth = nullptr;  // device [max_blocks + 1]: birth frame per slot, then the block count at the
@@ -128,7 +131,8 @@ cudaError_t launch_export_color(const cvx_submap* sm, int n_blocks, float* rgb, 
 // esdf.cu
 cudaError_t launch_finalize(cvx_submap* sm, int n_blocks, const int lo[3], const int hi[3], cudaStream_t st);
 cudaError_t launch_update_esdf(cvx_submap* sm, int n_blocks, const int lo[3], const int hi[3], cudaStream_t st,
-                               int* iterations);
+                               int* blocks_updated);
+void release_esdf(cvx_submap* sm);   // frees the ESDF scratch, planes and incremental state
 // query.cu
 cudaError_t launch_query(const cvx_submap* sm, const float* pts, int64_t m, float* out, uint8_t* status,
                          cudaStream_t st, float* grad = nullptr);

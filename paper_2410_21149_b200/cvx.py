@@ -33,7 +33,8 @@ class CvxError(RuntimeError):
 class GridConfig(C.Structure):
     _fields_ = [("voxel_size", C.c_double), ("block_side", C.c_int32), ("truncation", C.c_double),
                 ("weighting", C.c_int32), ("weight_range_floor", C.c_double), ("carve", C.c_int32),
-                ("site_threshold", C.c_double), ("max_blocks", C.c_int64), ("color", C.c_int32)]
+                ("site_threshold", C.c_double), ("max_blocks", C.c_int64), ("color", C.c_int32),
+                ("esdf_max_distance", C.c_double)]
 
 
 class SensorModel(C.Structure):
@@ -122,7 +123,8 @@ def grid_config(grid: dict) -> GridConfig:
     return GridConfig(float(grid["voxel_size"]), int(grid.get("block_side", 8)), float(grid["truncation"]),
                       int(grid.get("weighting", 0)), float(grid.get("weight_range_floor", 0.1)),
                       int(grid.get("carve", 1)), float(grid.get("site_threshold", grid["voxel_size"])),
-                      int(grid.get("max_blocks", 1 << 16)), int(grid.get("color", 0)))
+                      int(grid.get("max_blocks", 1 << 16)), int(grid.get("color", 0)),
+                      float(grid.get("esdf_max_distance", 2.0)))
 
 
 def sensor_model(sensor: dict) -> SensorModel:
@@ -267,7 +269,8 @@ class Submap:
         _check(lib().cvx_finalize_esdf(self._h, self._stream()))
 
     def update_esdf(self) -> int:
-        """Incremental ESDF update (cvx_update_esdf); returns the number of propagation waves."""
+        """Incremental ESDF update (cvx_update_esdf): the exact ESDF clamped at grid['esdf_max_distance'];
+        returns the number of blocks recomputed."""
         it = C.c_int32()
         _check(lib().cvx_update_esdf(self._h, self._stream(), C.byref(it)))
         return int(it.value)

@@ -205,7 +205,7 @@ def _grid(voxel_size, truncation, max_blocks, weighting=0, carve=1, site_thresho
     return dict(voxel_size=voxel_size, block_side=8, truncation=truncation, weighting=weighting,
                 weight_range_floor=0.1, carve=carve,
                 site_threshold=voxel_size if site_threshold is None else site_threshold,
-                max_blocks=max_blocks)
+                max_blocks=max_blocks, esdf_max_distance=2.0)
 
 
 def _tiny_scene():

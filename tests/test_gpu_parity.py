@@ -129,6 +129,29 @@ def test_esdf_import_random_tsdf(orc, seed):
     assert_esdf_parity(Eg, Eo, Wg > 0)
 
 
+@pytest.mark.parametrize("seed,p_site", [(0, 2e-4), (1, 3e-3), (2, 0.05)])
+def test_esdf_long_lines_sparse_sites(orc, seed, p_site):
+    """Lines longer than one TMA box (y: 360, z: 320 voxels) with sparse and dense site patterns, holes and
+    a ragged block set: exercises the banded envelopes, empty bands and every merge level of passes y / z."""
+    from paper_2410_21149_b200 import Submap
+    rng = np.random.default_rng(50 + seed)
+    blocks = [(x, y, z) for x in range(0, 3) for y in range(-20, 25) for z in range(-15, 25) if rng.random() < 0.6]
+    b = np.array(blocks, np.int32)
+    nb = len(b)
+    W = ((rng.random((nb, 512)) < 0.9) * rng.uniform(0.5, 4, (nb, 512))).astype(np.float32)
+    D = rng.uniform(0.02, 0.3, (nb, 512)) * np.where(rng.random((nb, 512)) < 0.5, -1, 1)
+    site = rng.random((nb, 512)) < p_site
+    D = (np.where(site, rng.uniform(-0.01, 0.01, (nb, 512)), D) * (W > 0)).astype(np.float32)
+    grid = dict(voxel_size=0.1, truncation=0.3, site_threshold=0.01, max_blocks=nb + 16)
+    sm = Submap(grid)
+    dev = torch.device("cuda", 0)
+    sm.import_tsdf(torch.from_numpy(b).to(dev), torch.from_numpy(D).to(dev), torch.from_numpy(W).to(dev))
+    sm.finalize_esdf()
+    bg, Dg, Wg, Eg = gpu_export_sorted(sm)
+    Eo, _ = orc.esdf(bg, Dg.astype(np.float64), Wg.astype(np.float64), 0.1, 0.01)
+    assert_esdf_parity(Eg, Eo, Wg > 0)
+
+
 def test_esdf_no_sites_and_single_site(orc):
     from paper_2410_21149_b200 import Submap
     dev = torch.device("cuda", 0)
