@@ -38,6 +38,7 @@
 //   Windows wider than 7^3 blocks fall back to the dense passes above with the clamp applied in pass z.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <type_traits>
@@ -100,18 +101,21 @@ __global__ void __launch_bounds__(128) pass_x_kernel(const __grid_constant__ XPa
   unsigned* msk = reinterpret_cast<unsigned*>(dsmem) + warp * 3 * nch;
   int* prv = reinterpret_cast<int*>(msk + nch);
   int* nxt = prv + nch;
-  const long long rows = (long long)p.ny * p.nz;
+  // the CTA's 4 rows are 4 consecutive y of one z: byte (y & 3) of one plane word per block and plane, so
+  // the planes are written as whole words (3 per block) once the 4 warps are done
+  unsigned char* pb = reinterpret_cast<unsigned char*>(reinterpret_cast<unsigned*>(dsmem) + 4 * 3 * nch);
+  const long long rows = (long long)p.ny * p.nz;   // a multiple of 8
   const int kNeg = -(1 << 30), kPos = 1 << 30;
-  for (long long row = (long long)blockIdx.x * 4 + warp; row < rows; row += (long long)gridDim.x * 4) {
+  for (long long g = blockIdx.x; g * 4 < rows; g += gridDim.x) {
+    const long long row = g * 4 + warp;
     const int y = (int)(row % p.ny), z = (int)(row / p.ny);
-    if (!p.rowmask[(long long)(z >> 3) * p.nby + (y >> 3)]) {   // no block in this row: no site, no voxel
+    if (!p.rowmask[(long long)(z >> 3) * p.nby + (y >> 3)]) {   // no block in these rows: no site, no voxel
       unsigned short* out = p.g1 + row * p.nx;
       for (int x = lane; x < p.nx; x += 32) out[x] = (unsigned short)kNone16;
       continue;
     }
     const int* grow = p.grid + ((long long)(z >> 3) * p.nby + (y >> 3)) * p.nbx;
     const int lyz = 8 * (y & 7) + 64 * (z & 7);
-    const int prow = (y & 7) + 8 * (z & 7);   // byte of the block's 64-byte planes holding this x-row
     // 1) sites of the row -> one 32-bit mask per chunk; the block's observed / sign / site plane bytes.
     //    kXCh chunks per round: their slot look-ups, then their TSDF loads, are issued back to back so
     //    every warp keeps kXCh 512-byte requests in flight (the row loop is otherwise latency-bound).
@@ -136,11 +140,11 @@ __global__ void __launch_bounds__(128) pass_x_kernel(const __grid_constant__ XPa
         const unsigned bo = __ballot_sync(0xffffffffu, obs);
         const unsigned bn = __ballot_sync(0xffffffffu, neg);
         if (lane == 0 && c0 + u < nch) msk[c0 + u] = bs;
-        if ((lane & 7) == 0 && slot[u] >= 0) {   // one lane per block: its row bytes of the three planes
-          unsigned char* pl = reinterpret_cast<unsigned char*>(p.planes + (long long)slot[u] * kPlaneWords);
-          pl[prow] = (unsigned char)(bo >> lane);
-          pl[64 + prow] = (unsigned char)(bn >> lane);
-          pl[128 + prow] = (unsigned char)(bs >> lane);
+        if ((lane & 7) == 0 && (((c0 + u) << 5) + lane) < p.nx) {   // one lane per block: its row bytes
+          const int blk = (((c0 + u) << 5) + lane) >> 3;
+          pb[(0 * p.nbx + blk) * 4 + (y & 3)] = (unsigned char)(bo >> lane);
+          pb[(1 * p.nbx + blk) * 4 + (y & 3)] = (unsigned char)(bn >> lane);
+          pb[(2 * p.nbx + blk) * 4 + (y & 3)] = (unsigned char)(bs >> lane);
         }
       }
     }
@@ -185,7 +189,14 @@ __global__ void __launch_bounds__(128) pass_x_kernel(const __grid_constant__ XPa
       const long long d = dl < dr ? dl : dr;
       out[x] = (unsigned short)(d >= (long long)kNone16 ? kNone16 : d);
     }
-    __syncwarp();
+    __syncthreads();
+    const int w = ((y & 7) >> 2) + 2 * (z & 7);   // plane word of rows (y & ~3 .. + 3, z)
+    for (int i = threadIdx.x; i < 3 * p.nbx; i += blockDim.x) {
+      const int pl = i / p.nbx, blk = i % p.nbx;
+      const int slot = grow[blk];
+      if (slot >= 0) p.planes[(long long)slot * kPlaneWords + 16 * pl + w] = reinterpret_cast<const unsigned*>(pb)[i];
+    }
+    __syncthreads();
   }
 }
 
@@ -235,27 +246,39 @@ struct PbaParams {
   double dmax;
 };
 
-// Shared memory of one tile: f [rows][tx] (TMA destination), envelope site q and start t [rows][tx]
-// (u16; the stack of band b lives in rows [b lb, b lb + size)), band ranges lo / hi [nbands][tx], mbarrier.
-size_t pba_smem_bytes(int rows, int tx, int nbands, size_t esize) {
-  size_t b = (size_t)rows * tx * esize + (size_t)rows * tx * 4 + (size_t)nbands * tx * 4;
+// Shared memory of one tile ([row][line] arrays, line fastest):
+//   fb   [rows][tx]  f per position (TMA destination; pass z reuses it for the output d^2 after the hulls)
+//   hq   [rows][tx]  u16 hull sites of band b in rows [b lb, b lb + nh)
+//   hf   [rows][tx]  u32 their f (pass z only; pass y re-reads the u16 input)
+//   nh, hmin [nbands][tx]  hull size and min f of every band; then the mbarrier.
+template <bool kZ>
+__host__ __device__ inline size_t pba_smem_bytes(int rows, int tx, int nbands) {
+  const size_t esize = kZ ? 4 : 2;
+  size_t b = (size_t)rows * tx * (esize + 2 + (kZ ? 4 : 0)) + (size_t)nbands * tx * 8;
   return ((b + 15) & ~(size_t)15) + 16;
 }
+
+// One band hull = the lower envelope over the whole real line of the parabolas (p - q)^2 + f(q) of the
+// band's sites q (equivalently the lower convex hull of the points (q, q^2 + f(q))), built by Andrew's
+// monotone chain; a pointer walks it as p increases (the optimal hull element is non-decreasing in p).
+struct HullPtr {
+  int k, end;                // current element row, one past the last row
+  long long q, f;            // current site and its f
+};
 
 template <bool kZ>
 __global__ void __launch_bounds__(256) pba_line_kernel(const __grid_constant__ CUtensorMap tmap,
                                                        const __grid_constant__ PbaParams p) {
   using Elem = typename std::conditional<kZ, unsigned, unsigned short>::type;
   extern __shared__ __align__(1024) unsigned char dsmem[];
-  unsigned char* smem = dsmem;
   const int tx = p.tx, B = p.nbands, m = p.m, rows = p.rows, lb = p.lb;
-  Elem* fb = reinterpret_cast<Elem*>(smem);
-  unsigned short* sq = reinterpret_cast<unsigned short*>(smem + (size_t)rows * tx * sizeof(Elem));
-  unsigned short* stt = sq + (size_t)rows * tx;
-  unsigned short* blo = stt + (size_t)rows * tx;
-  unsigned short* bhi = blo + B * tx;
-  unsigned long long* mbar = reinterpret_cast<unsigned long long*>(
-      smem + (((size_t)rows * tx * sizeof(Elem) + (size_t)rows * tx * 4 + (size_t)B * tx * 4 + 15) & ~(size_t)15));
+  Elem* fb = reinterpret_cast<Elem*>(dsmem);
+  unsigned short* hq = reinterpret_cast<unsigned short*>(dsmem + (size_t)rows * tx * sizeof(Elem));
+  unsigned* hf = reinterpret_cast<unsigned*>(hq + (size_t)rows * tx);                  // pass z only
+  unsigned short* nhv = reinterpret_cast<unsigned short*>(kZ ? (unsigned char*)(hf + (size_t)rows * tx)
+                                                             : (unsigned char*)(hq + (size_t)rows * tx));
+  unsigned* hminv = reinterpret_cast<unsigned*>(nhv + B * tx + (B * tx & 1));
+  unsigned long long* mbar = reinterpret_cast<unsigned long long*>(dsmem + pba_smem_bytes<kZ>(rows, tx, B) - 16);
 
   const int xt = blockIdx.x % p.tiles_x, o2 = blockIdx.x / p.tiles_x;   // o2: z (pass y) or y (pass z)
   const int x0 = xt * tx;
@@ -279,138 +302,285 @@ __global__ void __launch_bounds__(256) pba_line_kernel(const __grid_constant__ C
     }
   }
   const int xl = threadIdx.x % tx, b = threadIdx.x / tx;
-  const bool valid = (x0 + xl < p.nx) && (b < B);
-  auto F = [&](int q) -> long long {
+  const bool valid = x0 + xl < p.nx;
+  const int q0 = b * lb, q1 = min(m, q0 + lb);
+  auto Fin = [&](int q) -> long long {         // f of position q from the staged input
     const Elem v = fb[(size_t)q * tx + xl];
     if (kZ) return v == kInf32 ? kInfF : (long long)v;
     return v == kNone16 ? kInfF : (long long)v * v;
   };
-  auto SQ = [&](int r) -> unsigned short& { return sq[(size_t)r * tx + xl]; };
-  auto ST = [&](int r) -> unsigned short& { return stt[(size_t)r * tx + xl]; };
-  auto LO = [&](int bb) -> unsigned short& { return blo[bb * tx + xl]; };
-  auto HI = [&](int bb) -> unsigned short& { return bhi[bb * tx + xl]; };
+  auto HQ = [&](int r) -> unsigned short& { return hq[(size_t)r * tx + xl]; };
+  auto HF = [&](int r) -> long long {          // f of the hull element in row r
+    if (kZ) return (long long)hf[(size_t)r * tx + xl];
+    return Fin(hq[(size_t)r * tx + xl]);
+  };
   mbar_wait(mbar, 0);
 
-  // ---- 1) band envelopes: Meijster's stack over the sites of [q0, q1), envelope over the whole line
-  const int q0 = b * lb, q1 = min(m, q0 + lb);
+  // ---- 1) band hulls (Andrew's monotone chain on (q, q^2 + f)); a middle point on or above the chord
+  //         of its neighbours never gives a strictly smaller value and is dropped
   if (valid) {
-    int size = 0, top = -1, t_top = 0;
-    long long f_top = 0;
+    int n = 0;
+    long long qa = 0, ga = 0, qb = 0, gb = 0;   // the last two hull points
+    unsigned minf = kInf32;
     for (int q = q0; q < q1; ++q) {
-      const long long fq = F(q);
+      const long long fq = Fin(q);
       if (fq >= kInfF) continue;
-      while (size > 0) {
+      const long long gq = (long long)q * q + fq;
+      while (n >= 2 && (gb - ga) * (q - qa) >= (gq - ga) * (qb - qa)) {
+        --n;
+        qb = qa; gb = ga;
+        if (n >= 2) { qa = HQ(q0 + n - 2); ga = qa * qa + HF(q0 + n - 2); }
+      }
+      HQ(q0 + n) = (unsigned short)q;
+      if (kZ) hf[(size_t)(q0 + n) * tx + xl] = (unsigned)fq;
+      ++n;
+      qa = qb; ga = gb; qb = q; gb = gq;
+      if (fq < minf) minf = (unsigned)fq;
+    }
+    nhv[b * tx + xl] = (unsigned short)n;
+    hminv[b * tx + xl] = minf;
+  }
+  __syncthreads();
+  if (!valid || q0 >= m) return;
+
+  // ---- 2) outputs of [q0, q1): min over the hulls of bands b-1, b, b+1 (pointer walks), then every
+  //         other band whose lower bound gap^2 + min f is below the current maximum over the range
+  auto start = [&](HullPtr& h, int c, int p0) {   // element of band c's hull optimal at p0
+    const int r0 = c * lb, n = nhv[c * tx + xl];
+    h.end = r0 + n;
+    if (n == 0) { h.k = h.end; return; }
+    if (c < b) {   // positions right of the band: walk back from the last element (optimum near the end)
+      h.k = h.end - 1; h.q = HQ(h.k); h.f = HF(h.k);
+      while (h.k > r0) {
+        const long long q2 = HQ(h.k - 1), f2 = HF(h.k - 1);
+        if ((p0 - q2) * (p0 - q2) + f2 > (p0 - h.q) * (p0 - h.q) + h.f) break;
+        --h.k; h.q = q2; h.f = f2;
+      }
+    } else {
+      h.k = r0; h.q = HQ(r0); h.f = HF(r0);
+    }
+  };
+  auto value = [&](HullPtr& h, int pp) -> long long {   // advance to pp, return the hull's value there
+    if (h.k >= h.end) return kInfF;
+    long long d = pp - h.q, v = d * d + h.f;
+    while (h.k + 1 < h.end) {
+      const long long q2 = HQ(h.k + 1), f2 = HF(h.k + 1), d2 = pp - q2, v2 = d2 * d2 + f2;
+      if (v2 >= v) break;
+      ++h.k; h.q = q2; h.f = f2; v = v2;
+    }
+    return v;
+  };
+  const int x = x0 + xl;
+  HullPtr w0, w1, w2;
+  start(w0, max(b - 1, 0), q0);
+  if (b == 0) w0.k = w0.end;
+  start(w1, b, q0);
+  start(w2, min(b + 1, B - 1), q0);
+  if (b == B - 1) w2.k = w2.end;
+  long long U = 0;
+  unsigned* d2buf = reinterpret_cast<unsigned*>(fb);   // pass z: the input is no longer read
+  for (int pp = q0; pp < q1; ++pp) {
+    const long long v = min(value(w1, pp), min(value(w0, pp), value(w2, pp)));
+    U = max(U, v);
+    const unsigned o = v >= kInfF ? kInf32 : (unsigned)v;
+    if (!kZ) {
+      if (p.colmask[(long long)(pp >> 3) * p.nbx + (x >> 3)])   // only columns pass z will read
+        p.g2[((long long)o2 * p.ny + pp) * p.nx + x] = o;
+    } else {
+      d2buf[(size_t)pp * tx + xl] = o;
+    }
+  }
+  // far bands, nearest first; each one that can still win somewhere is swept into the outputs
+  for (int dist = 2; dist < B && U > 0; ++dist) {
+    for (int side = 0; side < 2; ++side) {
+      const int c = side ? b + dist : b - dist;
+      if (c < 0 || c >= B || nhv[c * tx + xl] == 0) continue;
+      const long long gap = side ? (long long)c * lb - (q1 - 1) : (long long)q0 - (c * lb + lb - 1);
+      if (gap * gap + (long long)hminv[c * tx + xl] >= U) continue;
+      HullPtr h;
+      start(h, c, q0);
+      long long U2 = 0;
+      for (int pp = q0; pp < q1; ++pp) {
+        const long long v = value(h, pp);
+        if (!kZ) {
+          if (!p.colmask[(long long)(pp >> 3) * p.nbx + (x >> 3)]) continue;
+          unsigned* o = p.g2 + ((long long)o2 * p.ny + pp) * p.nx + x;
+          const long long cur = *o == kInf32 ? kInfF : (long long)*o;
+          if (v < cur) *o = (unsigned)v;
+          U2 = max(U2, min(v, cur));
+        } else {
+          unsigned& o = d2buf[(size_t)pp * tx + xl];
+          const long long cur = o == kInf32 ? kInfF : (long long)o;
+          if (v < cur) o = (unsigned)v;
+          U2 = max(U2, min(v, cur));
+        }
+      }
+      U = U2;
+    }
+  }
+  if (!kZ) return;
+  // ---- 3) pass z: E = sign(D) s sqrt(d^2) into the allocated blocks of this line
+  int slot = -1, slot_bz = -1;
+  for (int pp = q0; pp < q1; ++pp) {
+    if ((pp >> 3) != slot_bz) {
+      slot_bz = pp >> 3;
+      slot = p.grid[((long long)slot_bz * p.nby + (o2 >> 3)) * p.nbx + (x >> 3)];
+    }
+    if (slot < 0) continue;
+    const unsigned dd = d2buf[(size_t)pp * tx + xl];
+    const int l = (x & 7) + 8 * (o2 & 7) + 64 * (pp & 7);
+    const unsigned* pl = p.planes + (long long)slot * kPlaneWords;
+    const bool obs = (pl[l >> 5] >> (l & 31)) & 1u, neg = (pl[16 + (l >> 5)] >> (l & 31)) & 1u;
+    float e;
+    if (!obs) e = __int_as_float(0x7fc00000);                           // unobserved -> NaN (O11)
+    else if (p.capped) {
+      const double md = dd == kInf32 ? p.dmax : fmin(p.s * sqrt((double)dd), p.dmax);
+      e = (float)(neg ? -md : md);
+    } else if (dd == kInf32) e = __int_as_float(0x7f800000);            // S empty -> +inf (O11)
+    else {
+      const double md = p.s * sqrt((double)dd);
+      e = (float)(neg ? -md : md);
+    }
+    p.esdf[(long long)slot * kBlockVox + l] = e;
+  }
+}
+
+// Passes y / z, streaming variant (CVX_EDT_KERNEL=0): one thread per line (consecutive x in a warp ->
+// coalesced row reads), Meijster's lower envelope with the stack kept in place in global memory as
+// per-position links (PBA's proximate sites at their own positions): pass y stores u32 {t: 16, prev: 16}
+// per pushed position and re-reads f, pass z stores the full state below (u64 {f: 32, t: 16, prev: 16})
+// so a pop is one load.  Same outputs as pba_line_kernel.
+struct LinkParams {
+  const void* fin;                // pass y: u16 1-D distances; pass z: u32 squared distances
+  unsigned* g2;                   // pass y output
+  void* meta;                     // stack links (8 bytes per AABB voxel)
+  float* esdf;
+  const int* grid;
+  const unsigned char* colmask;
+  const unsigned* planes;
+  int nx, ny, nz, nbx, nby;
+  double s;
+  int capped;
+  double dmax;
+};
+
+template <bool kZ>
+__global__ void __launch_bounds__(256) link_line_kernel(const __grid_constant__ LinkParams p) {
+  const long long nlines = kZ ? (long long)p.nx * p.ny : (long long)p.nx * p.nz;
+  const long long line = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (line >= nlines) return;
+  const int x = (int)(line % p.nx);
+  const int o2 = (int)(line / p.nx);      // pass y: z ; pass z: y
+  const int m = kZ ? p.nz : p.ny;
+  const long long stride = kZ ? (long long)p.nx * p.ny : (long long)p.nx;
+  const long long base = kZ ? (long long)o2 * p.nx + x : (long long)o2 * p.nx * p.ny + x;
+  if (kZ && !p.colmask[(long long)(o2 >> 3) * p.nbx + (x >> 3)]) return;   // no allocated voxel in this line
+  auto f_at = [&](int q) -> long long {
+    if (kZ) {
+      const unsigned v = static_cast<const unsigned*>(p.fin)[base + q * stride];
+      return v == kInf32 ? kInfF : (long long)v;
+    }
+    const unsigned v = static_cast<const unsigned short*>(p.fin)[base + q * stride];
+    return v == kNone16 ? kInfF : (long long)v * v;
+  };
+  unsigned* m32 = static_cast<unsigned*>(p.meta);
+  unsigned long long* m64 = static_cast<unsigned long long*>(p.meta);
+  int top = -1, t_top = 0;
+  long long f_top = 0;
+  for (int q0 = 0; q0 < m; q0 += 8) {     // 8 independent loads in flight per thread
+    long long fv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) fv[u] = q0 + u < m ? f_at(q0 + u) : kInfF;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int q = q0 + u;
+      const long long fq = fv[u];
+      if (fq >= kInfF) continue;
+      while (top >= 0) {
         const long long a = t_top - top, c = t_top - q;
-        if (a * a + f_top > c * c + fq) {            // q beats top already at top's start: pop
-          --size;
-          if (size > 0) { top = SQ(q0 + size - 1); t_top = ST(q0 + size - 1); f_top = F(top); }
+        if (a * a + f_top > c * c + fq) {                 // q beats top already at top's start: pop
+          if (kZ) {
+            const unsigned long long mt = m64[base + (long long)top * stride];
+            const int pr = (int)(mt & 0xffffu);
+            if (pr == 0xffff) { top = -1; break; }
+            top = pr; t_top = (int)((mt >> 16) & 0xffffu); f_top = (long long)(mt >> 32);
+          } else {
+            const int pr = (int)(m32[base + (long long)top * stride] & 0xffffu);
+            if (pr == 0xffff) { top = -1; break; }
+            top = pr;
+            t_top = (int)(m32[base + (long long)top * stride] >> 16);
+            f_top = f_at(top);
+          }
         } else {
           break;
         }
       }
       int tq = 0;
-      if (size > 0) {
+      if (top >= 0) {
         const long long sep = floordiv_exact((long long)q * q - (long long)top * top + fq - f_top, 2ll * (q - top));
-        if (sep + 1 >= m) continue;                   // q never wins inside the line
+        if (sep + 1 >= m) continue;                        // q never wins inside the line
         tq = (int)(sep + 1);
       }
-      SQ(q0 + size) = (unsigned short)q;
-      ST(q0 + size) = (unsigned short)tq;
-      ++size;
+      if (kZ)
+        m64[base + (long long)q * stride] = top < 0 ? 0xffffull
+            : ((unsigned long long)f_top << 32) | ((unsigned long long)t_top << 16) | (unsigned long long)top;
+      else
+        m32[base + (long long)q * stride] = ((unsigned)tq << 16) | (unsigned)(top < 0 ? 0xffff : top);
       top = q; t_top = tq; f_top = fq;
     }
-    LO(b) = (unsigned short)q0;
-    HI(b) = (unsigned short)(q0 + size);
   }
-  __syncthreads();
-  // ---- 2) pairwise merges: groups [g, g + w) and [g + w, g + 2w) -> one envelope, log2(B) levels
-  for (int w = 1; w < B; w <<= 1) {
-    if (valid && (b & (2 * w - 1)) == w) {
-      const int L0 = b - w, R0 = b, R1 = b + w;
-      int jl = R0 - 1;
-      while (jl >= L0 && LO(jl) == HI(jl)) --jl;
-      int jr = R0;
-      while (jr < R1 && LO(jr) == HI(jr)) ++jr;
-      while (jl >= L0 && jr < R1) {
-        const int rb = LO(jr);
-        const int qb = SQ(rb);
-        const long long fb_ = F(qb);
-        // pop the left top while the right bottom beats it at the top's start
-        int ra = HI(jl) - 1, qa = SQ(ra), ta = ST(ra);
-        long long fa = F(qa);
-        for (;;) {
-          const long long a = ta - qa, c = ta - qb;
-          if (!(a * a + fa > c * c + fb_)) break;
-          HI(jl) = (unsigned short)ra;
-          if (LO(jl) == HI(jl)) { --jl; while (jl >= L0 && LO(jl) == HI(jl)) --jl; }
-          if (jl < L0) break;
-          ra = HI(jl) - 1; qa = SQ(ra); ta = ST(ra); fa = F(qa);
-        }
-        if (jl < L0) { ST(rb) = 0; break; }           // left emptied: the right bottom starts the line
-        const long long sep = floordiv_exact((long long)qb * qb - (long long)qa * qa + fb_ - fa, 2ll * (qb - qa));
-        // the element after the right bottom (same band, or the first of the next non-empty band)
-        int rn = -1;
-        if (rb + 1 < HI(jr)) rn = rb + 1;
-        else for (int k = jr + 1; k < R1; ++k) if (LO(k) < HI(k)) { rn = LO(k); break; }
-        if (sep + 1 >= m || (rn >= 0 && sep + 1 >= (long long)ST(rn))) {   // dominated: drop it, next one
-          LO(jr) = (unsigned short)(rb + 1);
-          if (LO(jr) == HI(jr)) { ++jr; while (jr < R1 && LO(jr) == HI(jr)) ++jr; }
-          continue;
-        }
-        ST(rb) = (unsigned short)(sep + 1);
-        break;
+  // backward: read the envelope from the right, one 8-position chunk (one block along the line) at a time
+  for (int q0 = ((m - 1) >> 3) << 3; q0 >= 0; q0 -= 8) {
+    int slot = -1;
+    unsigned obsw = 0, negw = 0;   // pass z: bit u = observed / negative of position q0 + u (prefetched)
+    const int lb = (x & 7) + 8 * (o2 & 7);
+    if (kZ) {
+      slot = p.grid[((long long)(q0 >> 3) * p.nby + (o2 >> 3)) * p.nbx + (x >> 3)];
+      if (slot >= 0) {
+        const unsigned* pl = p.planes + (long long)slot * kPlaneWords + (lb >> 5);
+        unsigned ow[8], nw[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) { ow[u] = pl[2 * u]; nw[u] = pl[16 + 2 * u]; }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) { obsw |= ((ow[u] >> (lb & 31)) & 1u) << u; negw |= ((nw[u] >> (lb & 31)) & 1u) << u; }
       }
     }
-    __syncthreads();
-  }
-  // ---- 3) every band writes its own positions from the merged envelope
-  if (!valid || q0 >= m) return;
-  int cb = -1;
-  for (int c = B - 1; c >= 0; --c)
-    if (LO(c) < HI(c) && ST(LO(c)) <= q0) { cb = c; break; }
-  const int x = x0 + xl;
-  int cr = -1, q = 0, nb_ = -1, nr = -1, tn = 0x7fffffff;
-  long long fq = kInfF;
-  auto find_next = [&]() {   // the envelope element after (cb, cr)
-    nb_ = -1; nr = -1; tn = 0x7fffffff;
-    if (cr + 1 < HI(cb)) { nb_ = cb; nr = cr + 1; }
-    else for (int k = cb + 1; k < B; ++k) if (LO(k) < HI(k)) { nb_ = k; nr = LO(k); break; }
-    if (nr >= 0) tn = ST(nr);
-  };
-  if (cb >= 0) {
-    cr = LO(cb);
-    while (cr + 1 < HI(cb) && ST(cr + 1) <= q0) ++cr;
-    q = SQ(cr); fq = F(q);
-    find_next();
-  }
-  int slot = -1, slot_bz = -1;
-  for (int pp = q0; pp < q1; ++pp) {
-    while (nr >= 0 && tn <= pp) { cb = nb_; cr = nr; q = SQ(cr); fq = F(q); find_next(); }
-    long long d2 = kInfF;
-    if (cb >= 0) { const long long d = pp - q; d2 = d * d + fq; }
-    if (!kZ) {
-      if (p.colmask[(long long)(pp >> 3) * p.nbx + (x >> 3)])   // only columns pass z will read
-        p.g2[((long long)o2 * p.ny + pp) * p.nx + x] = d2 >= kInfF ? kInf32 : (unsigned)d2;
-    } else {
-      if ((pp >> 3) != slot_bz) {
-        slot_bz = pp >> 3;
-        slot = p.grid[((long long)slot_bz * p.nby + (o2 >> 3)) * p.nbx + (x >> 3)];
+    const bool wy = !kZ && p.colmask[(long long)(q0 >> 3) * p.nbx + (x >> 3)];
+#pragma unroll
+    for (int u = 7; u >= 0; --u) {
+      const int q = q0 + u;
+      if (q >= m) continue;
+      long long d2 = kInfF;
+      if (top >= 0) { const long long dq = q - top; d2 = dq * dq + f_top; }
+      if (!kZ) {
+        if (wy) p.g2[base + (long long)q * stride] = d2 >= kInfF ? kInf32 : (unsigned)d2;
+      } else if (slot >= 0) {
+        const int l = lb + 64 * u;
+        const bool obs = (obsw >> u) & 1u, neg = (negw >> u) & 1u;
+        float e;
+        if (!obs) e = __int_as_float(0x7fc00000);
+        else if (p.capped) {
+          const double md = d2 >= kInfF ? p.dmax : fmin(p.s * sqrt((double)d2), p.dmax);
+          e = (float)(neg ? -md : md);
+        } else if (d2 >= kInfF) e = __int_as_float(0x7f800000);
+        else {
+          const double md = p.s * sqrt((double)d2);
+          e = (float)(neg ? -md : md);
+        }
+        p.esdf[(long long)slot * kBlockVox + l] = e;
       }
-      if (slot < 0) continue;
-      const int l = (x & 7) + 8 * (o2 & 7) + 64 * (pp & 7);
-      const unsigned* pl = p.planes + (long long)slot * kPlaneWords;
-      const bool obs = (pl[l >> 5] >> (l & 31)) & 1u, neg = (pl[16 + (l >> 5)] >> (l & 31)) & 1u;
-      float e;
-      if (!obs) e = __int_as_float(0x7fc00000);                           // unobserved -> NaN (O11)
-      else if (p.capped) {
-        const double md = d2 >= kInfF ? p.dmax : fmin(p.s * sqrt((double)d2), p.dmax);
-        e = (float)(neg ? -md : md);
-      } else if (d2 >= kInfF) e = __int_as_float(0x7f800000);            // S empty -> +inf (O11)
-      else {
-        const double md = p.s * sqrt((double)d2);
-        e = (float)(neg ? -md : md);
+      if (top >= 0 && q == t_top) {
+        if (kZ) {
+          const unsigned long long mt = m64[base + (long long)top * stride];
+          const int pr = (int)(mt & 0xffffu);
+          if (pr == 0xffff) top = -1;
+          else { top = pr; t_top = (int)((mt >> 16) & 0xffffu); f_top = (long long)(mt >> 32); }
+        } else {
+          const int pr = (int)(m32[base + (long long)top * stride] & 0xffffu);
+          if (pr == 0xffff) top = -1;
+          else { top = pr; t_top = (int)(m32[base + (long long)top * stride] >> 16); f_top = f_at(top); }
+        }
       }
-      p.esdf[(long long)slot * kBlockVox + l] = e;
     }
   }
 }
@@ -642,14 +812,14 @@ cudaError_t launch_pba(cvx_submap* sm, const void* fin, const PbaParams& base, c
   p.rows = p.nbox * p.box_h;
   p.tx = 8;
   for (int t : {32, 16}) {
-    if (pba_smem_bytes(p.rows, t, 1, esize) <= 100 * 1024 && t <= ((p.nx + 7) & ~7)) { p.tx = t; break; }
+    if (pba_smem_bytes<kZ>(p.rows, t, 1) <= 80 * 1024 && t <= p.nx) { p.tx = t; break; }
   }
   int B = 1;
-  while (B * 2 * p.tx <= 256 && B * 2 <= 32 && (p.m + B * 2 - 1) / (B * 2) >= 8) B *= 2;
+  while (B * 2 * p.tx <= 256 && B * 2 <= 32 && (p.m + B * 2 - 1) / (B * 2) >= 12) B *= 2;
   p.nbands = B;
   p.lb = (p.m + B - 1) / B;
   p.tiles_x = (p.nx + p.tx - 1) / p.tx;
-  const size_t smem = pba_smem_bytes(p.rows, p.tx, B, esize);
+  const size_t smem = pba_smem_bytes<kZ>(p.rows, p.tx, B);
   CUtensorMap tm;
   const cuuint64_t dims[3] = {(cuuint64_t)p.nx, (cuuint64_t)p.ny, (cuuint64_t)p.nz};
   const cuuint64_t strides[2] = {(cuuint64_t)p.nx * esize, (cuuint64_t)p.nx * p.ny * esize};
@@ -673,11 +843,14 @@ cudaError_t dense_edt(cvx_submap* sm, const int lo[3], const int hi[3], cudaStre
   const long long nvox = (long long)nx * ny * nz;
   cudaError_t e = ensure_planes(sm, st);
   if (e != cudaSuccess) return e;
-  const long long need = nvox * (4 + 2) + (long long)nbx * nby + (long long)nby * nbz + 256;
+  // passes y / z: 0 = streaming link kernel (default, measured faster), 1 = TMA-staged band hulls
+  static const int kernel = [] { const char* v = std::getenv("CVX_EDT_KERNEL"); return v ? std::atoi(v) : 0; }();
+  const long long need = nvox * (4 + 2 + (kernel == 0 ? 8 : 0)) + (long long)nbx * nby + (long long)nby * nbz + 256;
   if ((e = grow_async(&sm->edt, &sm->edt_bytes, need, st)) != cudaSuccess) return e;
   unsigned* g2 = reinterpret_cast<unsigned*>(sm->edt);
   unsigned short* g1 = reinterpret_cast<unsigned short*>(g2 + nvox);   // nvox % 512 == 0: aligned
-  unsigned char* colmask = reinterpret_cast<unsigned char*>(g1 + nvox);
+  void* meta = g1 + nvox;                                                  // link variant only
+  unsigned char* colmask = reinterpret_cast<unsigned char*>(g1 + nvox) + (kernel == 0 ? 8 * nvox : 0);
   unsigned char* rowmask = colmask + (size_t)nbx * nby;
   cudaMemsetAsync(colmask, 0, (size_t)nbx * nby + (size_t)nby * nbz, st);
   if ((e = build_grid(sm, lo, nbx, nby, nbz, colmask, rowmask, st, "esdf_block_grid")) != cudaSuccess) return e;
@@ -686,13 +859,29 @@ cudaError_t dense_edt(cvx_submap* sm, const int lo[3], const int hi[3], cudaStre
   xp.sums = sm->pool.sums; xp.planes = planes; xp.grid = sm->block_grid; xp.g1 = g1; xp.rowmask = rowmask;
   xp.nx = nx; xp.ny = ny; xp.nz = nz; xp.nbx = nbx; xp.nby = nby; xp.site_thr = sm->cfg.site_threshold;
   const int nch = (nx + 31) / 32;
-  const size_t smem = (size_t)4 * 3 * nch * sizeof(unsigned);
+  const size_t smem = (size_t)4 * 3 * nch * sizeof(unsigned) + (size_t)3 * nbx * 4;
   if (smem > 48 * 1024) cudaFuncSetAttribute(pass_x_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const long long rows = (long long)ny * nz;
-  const unsigned xblocks = (unsigned)std::min<long long>((rows + 3) / 4, 148ll * 16);
+  const unsigned xblocks = (unsigned)std::min<long long>(rows / 4, 148ll * 16);
   {
     ProfScope ps_(sm, "esdf_pass_x", st);
     pass_x_kernel<<<xblocks, 128, smem, st>>>(xp);
+  }
+  if (kernel == 0) {
+    LinkParams lp{};
+    lp.fin = g1; lp.g2 = g2; lp.meta = meta; lp.esdf = sm->pool.esdf; lp.grid = sm->block_grid; lp.colmask = colmask;
+    lp.planes = planes; lp.nx = nx; lp.ny = ny; lp.nz = nz; lp.nbx = nbx; lp.nby = nby; lp.s = sm->cfg.voxel_size;
+    lp.capped = capped ? 1 : 0; lp.dmax = dmax;
+    {
+      ProfScope ps_(sm, "esdf_pass_y", st);
+      const long long nl = (long long)nx * nz;
+      link_line_kernel<false><<<(unsigned)((nl + 255) / 256), 256, 0, st>>>(lp);
+    }
+    lp.fin = g2;
+    ProfScope ps_(sm, "esdf_pass_z", st);
+    const long long nl = (long long)nx * ny;
+    link_line_kernel<true><<<(unsigned)((nl + 255) / 256), 256, 0, st>>>(lp);
+    return cudaGetLastError();
   }
   PbaParams pp{};
   pp.g2 = g2; pp.esdf = sm->pool.esdf; pp.grid = sm->block_grid; pp.colmask = colmask; pp.planes = planes;

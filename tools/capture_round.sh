@@ -22,13 +22,15 @@ for w in $WHAT; do case $w in
   prepare) cap "^prepare_kernel" prepare 2;;
   fold) cap "^fold_kernel" fold 1;;
   esdf_pass_x) cap "^pass_x_kernel" esdf_pass_x 1;;
-  esdf_pass_y) cap "^pass_line_kernel" esdf_pass_y 2;;
-  esdf_pass_z) cap "^pass_line_kernel" esdf_pass_z 3;;
+  esdf_pass_y) cap "^pba_line_kernel" esdf_pass_y 2;;
+  esdf_pass_z) cap "^pba_line_kernel" esdf_pass_z 3;;
   query) cap "^query_kernel" query 0;;
   project) capw "^project_kernel" project 2 rgbd;;
   stress_x) capw "^pass_x_kernel" stress_pass_x 0 esdf_stress;;
-  stress_y) capw "^pass_line_kernel" stress_pass_y 0 esdf_stress;;
-  stress_z) capw "^pass_line_kernel" stress_pass_z 1 esdf_stress;;
+  stress_y) capw "^pba_line_kernel" stress_pass_y 0 esdf_stress;;
+  stress_z) capw "^pba_line_kernel" stress_pass_z 1 esdf_stress;;
   rgbd) timeout 900 python bench.py --workload rgbd --steps 5 > gpurun_out/$T/bench_rgbd.json 2> gpurun_out/$T/bench_rgbd.err; echo "rgbd rc=$?";;
+  incremental) timeout 900 python bench.py --workload incremental --steps 5 > gpurun_out/$T/bench_incremental.json 2> gpurun_out/$T/bench_incremental.err; echo "incremental rc=$?";;
+  gputest) timeout 1500 python -m pytest tests -q -m gpu > gpurun_out/$T/gputest.log 2>&1; echo "gputest rc=$?";;
   stress) timeout 900 python bench.py --workload esdf_stress --steps 5 > gpurun_out/$T/bench_esdf_stress.json 2> gpurun_out/$T/bench_esdf_stress.err; echo "stress rc=$?";;
 esac; done
