@@ -264,6 +264,27 @@ cvx_status cvx_pack_esdf(const cvx_submap* submap, void* dst, int64_t dst_bytes,
 /* Bytes cvx_pack_esdf needs (synchronising). */
 cvx_status cvx_packed_size(const cvx_submap* submap, int64_t* bytes);
 
+/* Gathered submap ESDFs (SURVEY §8 e / f4; registration queries "between every overlapped
+ * submap" — the consumer of the multi-GPU gather).  `payloads` (device) holds n_submaps cvx_pack_esdf
+ * payloads (e.g. the output of an all-gather), payload k starting at byte offsets[k] (host int64 [n],
+ * 16-byte aligned) inside a buffer of payload_bytes.  The set indexes the records in place: the CALLER keeps
+ * `payloads` alive and unmodified until cvx_esdf_set_destroy.  Each submap keeps its own pose and voxel
+ * size from its header.  Synchronising (reads the headers, builds the index on `stream`).
+ * Errors: CVX_E_INVALID (bad header / offsets, a block listed twice, a payload not from a finalized
+ * submap), CVX_E_OOM, CVX_E_CUDA. */
+typedef struct cvx_esdf_set cvx_esdf_set;
+cvx_status cvx_esdf_set_create(const void* payloads, int64_t payload_bytes, const int64_t* offsets, int32_t n_submaps,
+                               int device, void* stream, cvx_esdf_set** out);
+cvx_status cvx_esdf_set_destroy(cvx_esdf_set* set);
+
+/* Batched look-ups across the set: point i (device fp32 [m][3], world frame) is queried in submap
+ * submap_index[i] (device int32 [m]) exactly as cvx_query_distance_gradient queries that submap (O13 in
+ * the submap's own frame: trilinear / NEAREST / UNKNOWN, world-frame gradient).  out_gradient (device fp32
+ * [m][3]) may be NULL.  An index outside [0, n_submaps) gives UNKNOWN.  Stream-ordered.
+ * Errors: CVX_E_INVALID, CVX_E_CUDA. */
+cvx_status cvx_esdf_set_query(const cvx_esdf_set* set, const int32_t* submap_index, const float* points_world,
+                              int64_t m, float* out_distance, float* out_gradient, uint8_t* out_status, void* stream);
+
 /* Per-kernel timing of this submap's launches with CUDA events recorded on the launching stream
  * (off by default; enabling synchronises the device and clears earlier records).  enable: bit 0 =
  * record, bit 1 = serialise (the integration pipeline's side-stream work runs on the caller's stream,

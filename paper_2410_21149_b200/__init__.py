@@ -4,5 +4,5 @@ exact ESDF, distance queries — hand-written sm_100a CUDA behind the C-ABI in i
 The Python surface is a thin ctypes binding (cvx.py); it never computes any step of the method.
 """
 from .cvx import (  # noqa: F401
-    Submap, CvxError, lib, unpack, STATUS_OK, STATUS_NEAREST, STATUS_UNKNOWN, SIGNATURES,
+    Submap, EsdfSet, CvxError, lib, unpack, payload_bytes, STATUS_OK, STATUS_NEAREST, STATUS_UNKNOWN, SIGNATURES,
 )

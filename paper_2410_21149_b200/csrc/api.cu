@@ -10,6 +10,7 @@
 #include <utility>
 #include <vector>
 
+#include "esdf_set.h"
 #include "submap.h"
 
 namespace {
@@ -577,6 +578,96 @@ cvx_status cvx_pack_esdf(const cvx_submap* sm, void* dst, int64_t dst_bytes, int
   if (e == cudaSuccess) e = cvx::launch_pack(sm, nb, (unsigned char*)dst + 256, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "pack_esdf");
+  return CVX_OK;
+}
+
+cvx_status cvx_esdf_set_create(const void* payloads, int64_t payload_bytes, const int64_t* offsets, int32_t n_submaps,
+                               int device, void* stream, cvx_esdf_set** out) {
+  g_last_error.clear();
+  if (!out) return fail(CVX_E_INVALID, "out is NULL");
+  *out = nullptr;
+  if (n_submaps < 1 || n_submaps >= (1 << 24)) return fail(CVX_E_INVALID, "n_submaps must be in [1, 2^24)");
+  if (!payloads || !offsets || payload_bytes <= 0) return fail(CVX_E_INVALID, "NULL / empty payload buffer");
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+  if (device < 0 || device >= ndev) return fail(CVX_E_INVALID, "device index out of range");
+  DeviceGuard g(device);
+  cudaStream_t st = (cudaStream_t)stream;
+  cvx_esdf_set* set = new cvx_esdf_set();
+  set->device = device;
+  set->n = n_submaps;
+  set->payload = static_cast<const unsigned char*>(payloads);
+  std::vector<unsigned char> hdr((size_t)n_submaps * 256);
+  std::vector<long long> rec(n_submaps);
+  auto bad = [&](cvx_status code, const std::string& msg) {
+    cvx_esdf_set_destroy(set);
+    return fail(code, msg);
+  };
+  for (int k = 0; k < n_submaps; ++k) {
+    if (offsets[k] < 0 || offsets[k] % 16 != 0 || offsets[k] + 256 > payload_bytes)
+      return bad(CVX_E_INVALID, "payload offset out of range or not 16-byte aligned");
+    if ((e = cudaMemcpyAsync(hdr.data() + 256 * (size_t)k, set->payload + offsets[k], 256, cudaMemcpyDeviceToHost, st)) !=
+        cudaSuccess)
+      return bad(CVX_E_CUDA, std::string("reading payload headers: ") + cudaGetErrorString(e));
+  }
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return bad(CVX_E_CUDA, cudaGetErrorString(e));
+  set->T.resize(16 * (size_t)n_submaps);
+  set->s.resize(n_submaps);
+  set->n_blocks.resize(n_submaps);
+  for (int k = 0; k < n_submaps; ++k) {
+    const unsigned char* h = hdr.data() + 256 * (size_t)k;
+    uint32_t magic; int32_t version; int64_t nb; double vs;
+    std::memcpy(&magic, h, 4); std::memcpy(&version, h + 4, 4); std::memcpy(&nb, h + 8, 8); std::memcpy(&vs, h + 16, 8);
+    if (magic != 0x45585643u || version != 1) return bad(CVX_E_INVALID, "not a cvx_pack_esdf payload (magic / version)");
+    if (nb < 0 || offsets[k] + 256 + nb * (16 + 4 * cvx::kBlockVox) > payload_bytes)
+      return bad(CVX_E_INVALID, "payload block count exceeds the buffer");
+    if (!(vs > 0)) return bad(CVX_E_INVALID, "payload voxel size must be > 0");
+    std::memcpy(&set->T[16 * (size_t)k], h + 24, 128);
+    if (!valid_pose(&set->T[16 * (size_t)k])) return bad(CVX_E_INVALID, "payload pose is not a rigid 4x4");
+    set->s[k] = vs;
+    set->n_blocks[k] = nb;
+    rec[k] = offsets[k] + 256;
+  }
+  std::vector<double> Ts(set->T);
+  Ts.insert(Ts.end(), set->s.begin(), set->s.end());
+  if ((e = cudaMalloc(&set->T_dev, sizeof(double) * Ts.size())) != cudaSuccess ||
+      (e = cudaMalloc(&set->rec_off, sizeof(long long) * n_submaps)) != cudaSuccess ||
+      (e = cudaMalloc(&set->err, 4)) != cudaSuccess)
+    return bad(e == cudaErrorMemoryAllocation ? CVX_E_OOM : CVX_E_CUDA, "allocating the set");
+  cudaMemcpyAsync(set->T_dev, Ts.data(), sizeof(double) * Ts.size(), cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(set->rec_off, rec.data(), sizeof(long long) * n_submaps, cudaMemcpyHostToDevice, st);
+  unsigned err = 0;
+  if ((e = cvx::launch_set_build(set, st, &err)) != cudaSuccess)
+    return bad(e == cudaErrorMemoryAllocation ? CVX_E_OOM : CVX_E_CUDA, std::string("building the set: ") + cudaGetErrorString(e));
+  if (err & 2u) return bad(CVX_E_INVALID, "a payload spans >= 8192 blocks along an axis (not a finalized submap)");
+  if (err & 1u) return bad(CVX_E_INVALID, "a payload holds the same block twice");
+  *out = set;
+  return CVX_OK;
+}
+
+cvx_status cvx_esdf_set_destroy(cvx_esdf_set* set) {
+  if (!set) return CVX_OK;
+  DeviceGuard g(set->device);
+  cudaDeviceSynchronize();
+  if (set->T_dev) cudaFree(set->T_dev);
+  if (set->rec_off) cudaFree(set->rec_off);
+  if (set->table) cudaFree(set->table);
+  if (set->err) cudaFree(set->err);
+  delete set;
+  return CVX_OK;
+}
+
+cvx_status cvx_esdf_set_query(const cvx_esdf_set* set, const int32_t* submap_index, const float* points_world,
+                              int64_t m, float* out_distance, float* out_gradient, uint8_t* out_status, void* stream) {
+  g_last_error.clear();
+  if (!set) return fail(CVX_E_INVALID, "set is NULL");
+  if (m < 0) return fail(CVX_E_INVALID, "m < 0");
+  if (m > 0 && (!submap_index || !points_world || !out_distance || !out_status)) return fail(CVX_E_INVALID, "NULL buffer");
+  DeviceGuard g(set->device);
+  cudaError_t e = cvx::launch_set_query(set, submap_index, points_world, m, out_distance, out_gradient, out_status,
+                                        (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "esdf_set_query");
   return CVX_OK;
 }
 

@@ -1,13 +1,10 @@
 // query.cu — distance queries (O13) and the block export / import /
 // pack kernels of the inspection and multi-GPU gather hooks, for sm_100a.
+#include "query_point.cuh"
 #include "submap.h"
 
 namespace cvx {
 namespace {
-
-__device__ __forceinline__ double dm(double a, double b) { return __dmul_rn(a, b); }
-__device__ __forceinline__ double da(double a, double b) { return __dadd_rn(a, b); }
-__device__ __forceinline__ double ds(double a, double b) { return __dsub_rn(a, b); }
 
 struct QueryParams {
   const float* pts;
@@ -21,82 +18,22 @@ struct QueryParams {
   double s;
 };
 
-// Voxel coordinates of the 21-bit block-key domain (O3: |voxel| < 2^23, blocks in [-2^20, 2^20)); a
-// coordinate outside it cannot be allocated, and pack_key would alias it onto an in-range block.
-__device__ __forceinline__ bool in_key_domain(int x, int y, int z) {
-  constexpr int lo = -(1 << 23), hi = (1 << 23) - 1;
-  return x >= lo && x <= hi && y >= lo && y <= hi && z >= lo && z <= hi;
-}
-
-// E of voxel (x,y,z) through the hash (block cached); false if unallocated, outside the key domain or
-// unobserved (NaN).
-__device__ __forceinline__ bool voxel_e(const QueryParams& p, int x, int y, int z, unsigned long long& ckey,
-                                        int& cslot, float* e) {
-  if (!in_key_domain(x, y, z)) return false;
-  const unsigned long long key = pack_key(x >> 3, y >> 3, z >> 3);
-  if (key != ckey) { ckey = key; cslot = hash_find(p.hash, key); }
-  if (cslot < 0) return false;
-  const float v = p.esdf[(long long)cslot * kBlockVox + (x & 7) + 8 * (y & 7) + 64 * (z & 7)];
-  if (isnan(v)) return false;
-  *e = v;
-  return true;
-}
-
 __global__ void __launch_bounds__(256) query_kernel(const __grid_constant__ QueryParams p) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= p.m) return;
-  const double x[3] = {p.pts[3 * i], p.pts[3 * i + 1], p.pts[3 * i + 2]};
-  double xs[3], f[3];
-  int i0[3];
-  bool ok = true;
-  for (int a = 0; a < 3; ++a) {   // x_s = T_WS^-1 x  (O13), same operation order as the oracle
-    xs[a] = da(da(dm(p.T[0 * 4 + a], ds(x[0], p.T[3])), dm(p.T[1 * 4 + a], ds(x[1], p.T[7]))),
-               dm(p.T[2 * 4 + a], ds(x[2], p.T[11])));
-    const double g = ds(__ddiv_rn(xs[a], p.s), 0.5);
-    const double fl = floor(g);
-    if (!(fabs(fl) < 1073741824.0)) ok = false;
-    i0[a] = ok ? (int)fl : 0;
-    f[a] = ds(g, fl);
-  }
-  unsigned long long ckey = ~0ull;
+  unsigned long long ckey = ~0ull;   // block of the last look-up (the 8 corners mostly share one)
   int cslot = -1;
-  const float qnan = __int_as_float(0x7fc00000);
-  if (ok) {
-    double acc = 0.0, gs[3] = {0.0, 0.0, 0.0};
-    bool all = true;
-    for (int c = 0; c < 8; ++c) {
-      const int dx = c & 1, dy = (c >> 1) & 1, dz = (c >> 2) & 1;
-      float e;
-      if (!voxel_e(p, i0[0] + dx, i0[1] + dy, i0[2] + dz, ckey, cslot, &e)) { all = false; break; }
-      const double wx = dx ? f[0] : ds(1.0, f[0]), wy = dy ? f[1] : ds(1.0, f[1]), wz = dz ? f[2] : ds(1.0, f[2]);
-      const double wgt = dm(dm(wx, wy), wz);
-      if (wgt > 0) acc = da(acc, dm(wgt, (double)e));
-      if (p.grad) {   // d/df of the trilinear weights (f4: value + gradient look-ups for registration)
-        gs[0] += (dx ? 1.0 : -1.0) * wy * wz * (double)e;
-        gs[1] += (dy ? 1.0 : -1.0) * wx * wz * (double)e;
-        gs[2] += (dz ? 1.0 : -1.0) * wx * wy * (double)e;
-      }
-    }
-    if (all) {
-      p.out[i] = (float)acc;
-      p.status[i] = 0;
-      if (p.grad)   // dE/dx_world = R_WS dE/dx_s, dE/dx_s = (dE/df) / s
-        for (int a = 0; a < 3; ++a)
-          p.grad[3 * i + a] = (float)((p.T[4 * a] * gs[0] + p.T[4 * a + 1] * gs[1] + p.T[4 * a + 2] * gs[2]) / p.s);
-      return;
-    }
-    if (p.grad) { p.grad[3 * i] = qnan; p.grad[3 * i + 1] = qnan; p.grad[3 * i + 2] = qnan; }
-    int v[3];
-    for (int a = 0; a < 3; ++a) {
-      const double fv = floor(__ddiv_rn(xs[a], p.s));
-      v[a] = fabs(fv) < 1073741824.0 ? (int)fv : (1 << 30);   // |v| >= 2^30: outside the key domain
-    }
-    float e;
-    if (voxel_e(p, v[0], v[1], v[2], ckey, cslot, &e)) { p.out[i] = e; p.status[i] = 1; return; }
-  }
-  if (p.grad && !ok) { p.grad[3 * i] = qnan; p.grad[3 * i + 1] = qnan; p.grad[3 * i + 2] = qnan; }
-  p.out[i] = qnan;
-  p.status[i] = 2;
+  auto lookup = [&](int x, int y, int z, float* e) -> bool {
+    if (!in_key_domain(x, y, z)) return false;
+    const unsigned long long key = pack_key(x >> 3, y >> 3, z >> 3);
+    if (key != ckey) { ckey = key; cslot = hash_find(p.hash, key); }
+    if (cslot < 0) return false;
+    const float v = p.esdf[(long long)cslot * kBlockVox + (x & 7) + 8 * (y & 7) + 64 * (z & 7)];
+    if (isnan(v)) return false;
+    *e = v;
+    return true;
+  };
+  query_point(p.T, p.s, p.pts + 3 * i, lookup, p.out + i, p.grad ? p.grad + 3 * i : nullptr, p.status + i);
 }
 
 __global__ void export_kernel(const long long* sums, const float* esdf, const int4* coords, int nb,

@@ -82,6 +82,9 @@ SIGNATURES = {
     "cvx_import_tsdf_blocks": (C.c_int32, [_P, _P, _P, _P, C.c_int64, _P]),
     "cvx_pack_esdf": (C.c_int32, [_P, _P, C.c_int64, C.POINTER(C.c_int64), _P]),
     "cvx_packed_size": (C.c_int32, [_P, C.POINTER(C.c_int64)]),
+    "cvx_esdf_set_create": (C.c_int32, [_P, C.c_int64, _P, C.c_int32, C.c_int, _P, C.POINTER(_P)]),
+    "cvx_esdf_set_destroy": (C.c_int32, [_P]),
+    "cvx_esdf_set_query": (C.c_int32, [_P, _P, _P, C.c_int64, _P, _P, _P, _P]),
     "cvx_profile_enable": (C.c_int32, [_P, C.c_int32]),
     "cvx_profile_report": (C.c_int32, [_P, C.c_char_p, C.c_int64]),
     "cvx_last_error": (C.c_char_p, []),
@@ -399,3 +402,57 @@ def unpack(buf: torch.Tensor):
     hdr = rec[:, :16].copy().view("<i4").reshape(nb, 4)
     E = rec[:, 16:].copy().view("<f4").reshape(nb, 512)
     return dict(T_world_submap=T.copy(), voxel_size=float(vs), bxyz=hdr[:, :3].copy(), E=E)
+
+
+class EsdfSet:
+    """Gathered submap ESDFs (cvx_esdf_set): `payloads` is a CUDA uint8 buffer holding cvx_pack_esdf
+    payloads at byte `offsets` (e.g. the all-gathered ESDFs of every rank); queries name a submap per point.
+    The set indexes the buffer in place, so it keeps a reference to the tensor."""
+
+    def __init__(self, payloads: torch.Tensor, offsets, device: int | None = None):
+        if not (payloads.is_cuda and payloads.dtype == torch.uint8 and payloads.is_contiguous()):
+            raise ValueError("payloads must be a contiguous CUDA uint8 tensor")
+        self.device = payloads.device.index if device is None else int(device)
+        self._buf = payloads
+        off = np.ascontiguousarray(np.asarray(offsets, dtype=np.int64))
+        self.n = int(off.shape[0])
+        h = C.c_void_p()
+        st = C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+        _check(lib().cvx_esdf_set_create(C.c_void_p(payloads.data_ptr()), payloads.numel(), _ptr(off), self.n,
+                                         self.device, st, C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().cvx_esdf_set_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def query(self, submap_index: torch.Tensor, points_world: torch.Tensor, gradient: bool = False):
+        """(distance [m], status [m]) or, with gradient=True, (distance, gradient [m,3], status)."""
+        m = points_world.shape[0]
+        dev = points_world.device
+        for t, dt, name in ((submap_index, torch.int32, "submap_index"), (points_world, torch.float32, "points")):
+            if not (t.is_cuda and t.dtype == dt and t.is_contiguous()):
+                raise ValueError(f"{name} must be a contiguous CUDA {dt} tensor")
+        if submap_index.numel() != m:
+            raise ValueError("one submap index per point")
+        out = torch.empty(m, dtype=torch.float32, device=dev)
+        status = torch.empty(m, dtype=torch.uint8, device=dev)
+        grad = torch.empty((m, 3), dtype=torch.float32, device=dev) if gradient else None
+        st = C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+        _check(lib().cvx_esdf_set_query(self._h, C.c_void_p(submap_index.data_ptr()), C.c_void_p(points_world.data_ptr()),
+                                        m, C.c_void_p(out.data_ptr()),
+                                        C.c_void_p(grad.data_ptr()) if grad is not None else None,
+                                        C.c_void_p(status.data_ptr()), st))
+        return (out, grad, status) if gradient else (out, status)
+
+
+def payload_bytes(n_blocks: int) -> int:
+    """Size of one cvx_pack_esdf payload of n_blocks blocks (header + records)."""
+    return HEADER_BYTES + int(n_blocks) * RECORD_BYTES

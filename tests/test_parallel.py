@@ -81,3 +81,42 @@ def test_gather_packed_gloo_world2():
         assert [r[2] for r in res] == [0.0, 1.0]                   # submap poses intact
         assert res[0][3] == 2.0 and res[1][3] == 104.0             # last record's E
         assert res[1][4] == [1] * 5
+
+
+def _worker_esdfs(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2410_21149_b200.cvx import unpack
+        from paper_2410_21149_b200.parallel import gather_esdfs
+        mine = [_payload(10 * rank + j, 2 + j + rank) for j in range(rank + 1)]   # rank r: r + 1 payloads
+        buf, offsets, counts = gather_esdfs(mine, max_per_rank=2)
+        res = []
+        for o in offsets:
+            nb = int(np.frombuffer(buf[o + 8:o + 16].numpy().tobytes(), np.int64)[0])
+            d = unpack(buf[o:o + 256 + nb * 2064])
+            res.append((float(d["T_world_submap"][0, 3]), d["bxyz"].shape[0], float(d["E"][-1, 0])))
+        q.put((rank, (counts, [o % 16 for o in offsets], res)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gather_esdfs_gloo_world2():
+    """gather_esdfs: uneven payload counts per rank, one size exchange, one gather; every rank
+    gets every payload at the returned offsets (16-byte aligned, as cvx_esdf_set_create needs)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_esdfs, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = [(0.0, 2, 1.0), (10.0, 3, 1002.0), (11.0, 4, 1103.0)]
+    for rank in (0, 1):
+        counts, align, res = out[rank]
+        assert counts == [1, 2] and align == [0, 0, 0]
+        assert res == want
