@@ -111,10 +111,21 @@ def init_pg(dev):
         dist.init_process_group(backend)
 
 
+def esdf_alg_bytes(va: int, n: int) -> dict:
+    """Algorithmic HBM bytes per launch of the ESDF passes: va allocated voxels, n dense AABB
+    voxels.  pass x: the 16-byte sums of every allocated voxel + 2-byte 1-D distances + 3 bit-planes
+    (3/8 byte per allocated voxel); pass y: 2-byte in + 4-byte out per dense voxel; pass z: 4-byte in per
+    dense voxel + 4-byte E out + 2 bit-planes per allocated voxel."""
+    return {"esdf_pass_x": int(16 * va + 2 * n + 3 * va // 8),
+            "esdf_pass_y": int(6 * n),
+            "esdf_pass_z": int(4 * n + 4 * va + va // 4)}
+
+
 def make_workload(rank: int, device: torch.device):
     import synth
-    seed = 1 + 1000 * rank        # rank 0: the canonical configs[1] scene; other ranks: their own submap
-    cfg = synth.make_config("lidar", device=device, seed=seed)
+    # weak scaling: every rank builds the configs[1] submap (same seed, so identical per-rank work and the
+    # max over ranks measures scaling, not scene imbalance)
+    cfg = synth.make_config("lidar", device=device)
     data = torch.stack([cfg["frames"][k]["data"] for k in range(N_SCANS)]).contiguous()
     poses = np.stack([cfg["frames"][k]["T_world_sensor"] for k in range(N_SCANS)])
     return cfg, data, poses
@@ -271,7 +282,7 @@ def run_mav(args, world, rank, local):
     -> pack); the packed ESDFs of all ranks are then all-gathered (NCCL when N > 1)."""
     import paper_2410_21149_b200 as cvx
     import synth
-    from paper_2410_21149_b200.parallel import gather_packed, shard_submaps
+    from paper_2410_21149_b200.parallel import gather_esdfs, shard_submaps
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     pg = None
@@ -281,8 +292,15 @@ def run_mav(args, world, rank, local):
         pg = dist
     cfg = synth.make_config("mav", frames=[], device=dev)
     subs = cfg["submaps"]
-    # work estimate per submap from the trajectory alone (same on every rank): scans x 1 (uniform)
-    mine = shard_submaps([len(sm["frames"]) for sm in subs], world)[rank]
+    # work estimate per submap (rays x mean range), identical on every rank: sum of the ray
+    # lengths of every 10th scan of the submap, times 10 (input statistics from the seeded generator)
+    from paper_2410_21149_b200.parallel import scan_work
+    sample = sorted(k for sm_ in subs for k in sm_["frames"][::10])
+    cfs = synth.make_config("mav", frames=sample, device=dev)
+    work = [10.0 * scan_work(torch.stack([cfs["frames"][k]["data"] for k in sm_["frames"][::10]])) for sm_ in subs]
+    del cfs
+    assign = shard_submaps(work, world)
+    mine = assign[rank]
     frames = sorted(k for i in mine for k in subs[i]["frames"])
     cfgf = synth.make_config("mav", frames=frames, device=dev)
     data = {i: torch.stack([cfgf["frames"][k]["data"] for k in subs[i]["frames"]]).contiguous() for i in mine}
@@ -293,6 +311,12 @@ def run_mav(args, world, rank, local):
     builders = [cvx.Submap(grid, subs[i]["T_world_submap"], local) for i in mine[:2]]
     stream = torch.cuda.current_stream(dev)
     streams = [stream, torch.cuda.Stream(dev)]
+
+    gathered = [0]
+    gq = torch.Generator(device=dev).manual_seed(11)
+    set_pts = (torch.rand((1 << 16, 3), device=dev, generator=gq) * torch.tensor([200.0, 120.0, 10.0], device=dev)
+               - torch.tensor([100.0, 60.0, 0.0], device=dev)).contiguous()
+    set_idx = torch.randint(0, len(subs), (1 << 16,), device=dev, generator=gq, dtype=torch.int32)
 
     def step():
         payloads = []
@@ -314,9 +338,12 @@ def run_mav(args, world, rank, local):
         if pending is not None:
             take(pending)
         stream.wait_stream(streams[1])
-        if pg is not None:
-            blob = torch.cat(payloads) if payloads else torch.zeros(0, dtype=torch.uint8, device=dev)
-            gather_packed(blob)
+        if pg is not None:   # every rank gets every submap's ESDF and indexes them for registration look-ups
+            buf, offsets, _ = gather_esdfs(payloads, max_per_rank=max(len(a) for a in assign))
+            gathered[0] = int(buf.numel())
+            es = cvx.EsdfSet(buf, offsets)
+            es.query(set_idx, set_pts)
+            es.close()
         return payloads
 
     for _ in range(args.warmup):
@@ -324,6 +351,8 @@ def run_mav(args, world, rank, local):
     if pg is not None:
         pg.barrier()
     torch.cuda.synchronize()
+    for b_ in builders:
+        b_.profile(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         e0.record(stream)
@@ -333,6 +362,11 @@ def run_mav(args, world, rank, local):
         e1.record(stream)
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
+    kms = {}
+    for b_ in builders:
+        for k_, v_ in b_.profile_report().items():
+            kms[k_] = kms.get(k_, 0.0) + v_["ms"] / args.steps
+        b_.profile(False)
     if pg is not None:
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
@@ -342,15 +376,40 @@ def run_mav(args, world, rank, local):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32+i64", "data": "synthetic",
             "config": {"workload": "mav_400m_flight_2000scans_40submaps_0.2m (BJ configs[3])",
-                       "submaps": len(subs), "submaps_per_rank_max": max(len(x) for x in shard_submaps([1] * len(subs), world)),
+                       "submaps": len(subs), "submaps_per_rank_max": max(len(x) for x in assign),
+                       "lpt_work": "sum of ray lengths of every 10th scan x 10 (rays x mean range, SURVEY §8e)",
+                       "work_imbalance": max(sum(work[i] for i in a) for a in assign) / (sum(work) / world),
                        "parallelism": f"submap-sharded x{world} (LPT)",
                        "pipeline": "2 submaps in flight (ESDF of submap j overlaps integration of submap j+1)"},
             "clocks": clk.summary()}
+    line["kernel_ms_per_step"] = kms
+    if world > 1:
+        line["gather_bytes_per_step"] = gathered[0]
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = mav_cpu_baseline(cfgf, subs[mine[0]], n=8)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if pg is not None:
         pg.barrier()
         pg.destroy_process_group()
+
+
+def mav_cpu_baseline(cfg, sub, n=8):
+    """The oracle as it stands, single-threaded, on the first n scans of submap 0 of configs[3] + the
+    exact ESDF of that partial submap."""
+    import oracle
+    g = cfg["grid"]
+    o = oracle.OracleSubmap(g, sub["T_world_submap"])
+    t0 = time.perf_counter()
+    for k in sub["frames"][:n]:
+        o.integrate(cfg["frames"][k]["data"].cpu().numpy(), cfg["frames"][k]["T_world_sensor"], cfg["sensor"])
+    t1 = time.perf_counter()
+    b, D, W = o.export()
+    oracle.esdf(b, D, W, g["voxel_size"], g["site_threshold"])
+    t2 = time.perf_counter()
+    return {"value": n / (t2 - t0), "unit": "scans/s", "cores": 1, "kind": "oracle",
+            "sample": f"first {n} of the 50 scans of submap 0 integrated + exact ESDF of that {b.shape[0]}-block "
+                      "partial submap", "integrate_scans_per_s": n / (t1 - t0), "seconds": t2 - t0}
 
 
 def run_color(args, world, rank, local):
@@ -509,7 +568,7 @@ def run_esdf_stress(args, world, rank, local):
     prof = sm.profile_report()
     per = {k: v["ms"] / args.steps for k, v in prof.items()}
     hbm, hbm_src, _ = peaks()
-    alg = {"esdf_pass_x": 20 * va + 2 * N, "esdf_pass_y": 6 * N, "esdf_pass_z": 4 * N + 8 * va}
+    alg = esdf_alg_bytes(va, N)
     dom = max(alg, key=lambda k: per.get(k, 0.0))
     ach = alg[dom] / (per[dom] / 1e3) / 1e9
     tot_alg = sum(alg.values()) / (sum(per[k] for k in alg) / 1e3) / 1e9
@@ -523,9 +582,41 @@ def run_esdf_stress(args, world, rank, local):
                          "frac": ach / hbm, "traffic": (ncu_traffic(dom, "esdf_stress") or {}).get("bytes_per_launch"),
                          "traffic_source": (ncu_traffic(dom, "esdf_stress") or {}).get("source"), "peak_source": hbm_src,
                          "all_passes_gbs": tot_alg},
-            "gpu_launches": sum(v["n"] for v in prof.values()), "clocks": clk.summary()}
+            "gpu_launches": sum(v["n"] for v in prof.values()), "clocks": clk.summary(),
+            "esdf_roofline": {k: {"ms": per[k], "alg_bytes": alg[k], "achieved_gbs": alg[k] / (per[k] / 1e3) / 1e9,
+                                  "frac": alg[k] / (per[k] / 1e3) / 1e9 / hbm} for k in alg if per.get(k)}}
+    del sm
+    torch.cuda.empty_cache()
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = stress_cpu_baseline(s, tau, dev)
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def stress_cpu_baseline(s, tau, dev, sub=(48, 48, 25)):
+    """The oracle's exact ESDF (single-threaded, stage-isolated: the same analytic TSDF) on a sub-volume of
+    configs[4]: the blocks with (bx, by, bz - bz0) < sub, i.e. 384 x 384 x 200 voxels (SURVEY §8(d) plans a
+    1000 x 1000 x 250 sub-volume; this one keeps the CPU leg to ~10-30 s)."""
+    import oracle
+    import synth.scenes as S
+    keep_b, keep_D, keep_W = [], [], []
+    bz0 = None
+    for b, D, W in S.esdf_stress_blocks(voxel_size=s, truncation=tau, device=dev):
+        if bz0 is None:
+            bz0 = int(b[:, 2].min())
+        m = (b[:, 0] < sub[0]) & (b[:, 1] < sub[1]) & (b[:, 2] - bz0 < sub[2])
+        if m.any():
+            keep_b.append(b[m].cpu()); keep_D.append(D[m].cpu()); keep_W.append(W[m].cpu())
+    b = torch.cat(keep_b).numpy()
+    D = torch.cat(keep_D).double().numpy()
+    W = torch.cat(keep_W).double().numpy()
+    t0 = time.perf_counter()
+    oracle.esdf(b, D, W, s, s)
+    dt = time.perf_counter() - t0
+    va = b.shape[0] * 512
+    return {"value": va / 1e6 / dt, "unit": "Mvox/s", "cores": 1, "kind": "oracle",
+            "sample": f"exact ESDF of a {sub[0] * 8} x {sub[1] * 8} x {sub[2] * 8}-voxel sub-volume of configs[4] "
+                      f"({b.shape[0]} blocks), same analytic TSDF (stage-isolated)", "seconds": dt}
 
 
 def rgbd_cpu_baseline(cfg, sub, depth, poses, n=2):
@@ -764,13 +855,28 @@ def main():
     qout = torch.empty(args.queries, dtype=torch.float32, device=dev)
     qst = torch.empty(args.queries, dtype=torch.uint8, device=dev)
     gather_bytes = [0]
+    gather_ms = []
+    set_queries = torch.zeros((1 << 16, 3), dtype=torch.float32, device=dev)
+    set_idx = (torch.arange(1 << 16, device=dev, dtype=torch.int32) % world).contiguous()
+    set_queries.copy_(queries[:1 << 16])
 
     def gather(m):
+        """N > 1: all-gather every rank's packed ESDF (one size exchange + one NCCL all-gather), index the
+        gathered payloads as a cvx_esdf_set and run 64 k cross-submap look-ups on it (the registration
+        consumer, SURVEY §8 e / f4)."""
         if pg is None:
             return
-        from paper_2410_21149_b200.parallel import gather_packed
-        parts = gather_packed(m.pack())
-        gather_bytes[0] = sum(p.numel() for p in parts)
+        from paper_2410_21149_b200.parallel import gather_esdfs
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        cur = torch.cuda.current_stream(dev)
+        e0.record(cur)
+        buf, offsets, _ = gather_esdfs([m.pack()], max_per_rank=1)
+        e1.record(cur)
+        gather_ms.append((e0, e1))
+        gather_bytes[0] = int(buf.numel())
+        es = cvx.EsdfSet(buf, offsets)
+        es.query(set_idx, set_queries)
+        es.close()
 
     # Two submaps in flight (the paper's frontend/backend queues): step i builds submap i on builder i % 2
     # and its own stream.  Its front half (reset + integration) is enqueued first, then the back half
@@ -791,8 +897,10 @@ def main():
         while backlog:
             backlog.pop()()
 
+    order = os.environ.get("CVX_BENCH_ORDER", "1") != "0"   # test knob: integrations of consecutive steps ordered
+
     def after_previous_integration(k):
-        if last_integrated[0] is not None:
+        if order and last_integrated[0] is not None:
             streams[k].wait_event(last_integrated[0])
 
     def mark_integrated(k):
@@ -940,12 +1048,8 @@ def main():
     launches = sum(v["n"] for v in prof.values())
     va = nb * 512
     # algorithmic bytes per launch
-    alg_bytes = {
-        "esdf_pass_x": 16 * va + 4 * va + 2 * nvox_dense,
-        "esdf_pass_y": 2 * nvox_dense + 4 * nvox_dense,
-        "esdf_pass_z": 4 * nvox_dense + 8 * va,
-        "reset_zero_blocks": 16 * va,
-    }
+    alg_bytes = esdf_alg_bytes(va, nvox_dense)
+    alg_bytes["reset_zero_blocks"] = 16 * va
     n_rays_launch = st["rays_in"] / max(1, prof.get("ray_prepare", {"n": 1})["n"] / K)
     alg_bytes["ray_prepare"] = int(n_rays_launch * (12 + 96))
     dom = max(per_step, key=per_step.get)
@@ -962,17 +1066,23 @@ def main():
         roofline = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
                     "frac": ach / hbm, "traffic": None, "peak_source": hbm_src, "launches_per_step": n_l}
     else:
-        # ray_walk_update: bound by issue (ALU); algorithmic lane-ops per voxel update = 13,
-        # peak = 148 SM x 128 lanes x SM clock.
+        # ray_walk_update: bound by issue (ALU).  Algorithmic work per voxel update = SURVEY §8(d)'s 25-30
+        # int/fp32 lane-ops (DDA step, sdf, weight, address, merge); `achieved` uses the low end (25), the
+        # 30-op and this build's own 13-op count are reported beside it.  peak = SMs (from
+        # the device properties) x 128 lanes x the SM clock sampled during the timed region.
         clk_mhz = (clk.summary().get("sm_mhz") or 1965.0)
-        peak_tops = 148 * 128 * clk_mhz * 1e6 / 1e12
+        n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+        peak_tops = n_sm * 128 * clk_mhz * 1e6 / 1e12
         avg_ms = walk["ms"] / walk["n"]
         upd_launch = updates_per_step / (walk["n"] / K)
-        ach = 13 * upd_launch / (avg_ms / 1e3) / 1e12
+        ups = upd_launch / (avg_ms / 1e3)
+        ach = 25 * ups / 1e12
         roofline = {"kernel": dom, "bound": "alu", "achieved": ach, "peak": peak_tops, "unit": "Tops/s",
                     "frac": ach / peak_tops, "traffic": None,
-                    "updates_per_s": upd_launch / (avg_ms / 1e3), "ops_per_update": 13,
-                    "peak_source": f"148 SM x 128 lanes x {clk_mhz:.0f} MHz (median under load)"}
+                    "updates_per_s": ups, "ops_per_update": 25, "ops_per_update_source": "SURVEY §8(d) (25-30)",
+                    "frac_at_30_ops": 30 * ups / 1e12 / peak_tops, "frac_at_13_ops": 13 * ups / 1e12 / peak_tops,
+                    "peak_source": f"{n_sm} SMs (device properties) x 128 lanes x {clk_mhz:.0f} MHz "
+                                   "(SM clock sampled during the timed region)"}
     tr = ncu_traffic(dom)
     roofline["traffic"] = tr["bytes_per_launch"] if tr else None   # DRAM bytes per launch (ncu)
     roofline["traffic_source"] = tr["source"] if tr else None
@@ -1004,8 +1114,23 @@ def main():
         "clocks": clk.summary(),
         "e2e": e2e,
     }
+    # the ESDF passes against the HBM roofline (solo times of the serialised pass)
+    line["esdf_roofline"] = {
+        k: {"ms": per_step_serial[k], "alg_bytes": alg_bytes[k],
+            "achieved_gbs": alg_bytes[k] / (per_step_serial[k] / 1e3) / 1e9,
+            "frac": alg_bytes[k] / (per_step_serial[k] / 1e3) / 1e9 / hbm}
+        for k in ("esdf_pass_x", "esdf_pass_y", "esdf_pass_z") if per_step_serial.get(k)}
+    line["esdf_roofline"]["peak_gbs"] = hbm
+    line["esdf_roofline"]["peak_source"] = hbm_src
     if world > 1:
-        line["gather_bytes_per_step"] = gather_bytes[0]
+        torch.cuda.synchronize()
+        g_ms = [a.elapsed_time(b) for a, b in gather_ms[-args.steps:]] or [0.0]
+        g_avg = sum(g_ms) / len(g_ms)
+        line["gather"] = {"bytes_per_step": gather_bytes[0], "ms": g_avg,
+                          "algbw_gbs": gather_bytes[0] / (g_avg / 1e3) / 1e9 if g_avg else None,
+                          "busbw_gbs": gather_bytes[0] * (world - 1) / world / (g_avg / 1e3) / 1e9 if g_avg else None,
+                          "note": "all-gather of every rank's packed ESDF + cvx_esdf_set over it + 64 k look-ups; "
+                                  "time = size exchange + all_gather_into_tensor on the rank's stream"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_sample(cfg, data, poses)
     if rank == 0:

@@ -71,11 +71,11 @@ cvx_status check_sensor(const cvx_sensor_model* s, int64_t n_per_frame) {
   return CVX_OK;
 }
 
-// Counter read-back.  With a caller stream the read is ordered after that stream's work; the
-// stream-less synchronising calls (get_stats / get_block_count / get_aabb / packed_size) wait for the
-// whole device first, so work on non-blocking streams (e.g. torch's pool streams) is included.
-cvx_status read_counters(const cvx_submap* sm, cudaStream_t st, cvx::Counters* out) {
-  if (st == nullptr) {
+// Counter read-back.  Calls that take a stream read after that stream's work; the stream-less
+// synchronising calls (get_stats / get_block_count / get_aabb / packed_size) pass whole_device and wait for
+// the whole device first, so work on non-blocking streams (e.g. torch's pool streams) is included.
+cvx_status read_counters(const cvx_submap* sm, cudaStream_t st, cvx::Counters* out, bool whole_device = false) {
+  if (whole_device) {
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return cuda_fail(e, "synchronising before the counter read");
   }
@@ -392,7 +392,7 @@ cvx_status cvx_get_stats(const cvx_submap* sm, cvx_integrate_stats* out) {
   if (!sm || !out) return fail(CVX_E_INVALID, "NULL argument");
   DeviceGuard g(sm->device);
   cvx::Counters c;
-  cvx_status rc = read_counters(sm, 0, &c);
+  cvx_status rc = read_counters(sm, 0, &c, true);
   if (rc != CVX_OK) return rc;
   fill_stats(c, sm->pool.max_blocks, out);
   return sticky(c);
@@ -403,7 +403,7 @@ cvx_status cvx_get_block_count(const cvx_submap* sm, int64_t* out) {
   if (!sm || !out) return fail(CVX_E_INVALID, "NULL argument");
   DeviceGuard g(sm->device);
   cvx::Counters c;
-  cvx_status rc = read_counters(sm, 0, &c);
+  cvx_status rc = read_counters(sm, 0, &c, true);
   if (rc != CVX_OK) return rc;
   *out = c.n_blocks < sm->pool.max_blocks ? c.n_blocks : sm->pool.max_blocks;
   return sticky(c);
@@ -414,7 +414,7 @@ cvx_status cvx_get_aabb(const cvx_submap* sm, int32_t* lo, int32_t* hi) {
   if (!sm || !lo || !hi) return fail(CVX_E_INVALID, "NULL argument");
   DeviceGuard g(sm->device);
   cvx::Counters c;
-  cvx_status rc = read_counters(sm, 0, &c);
+  cvx_status rc = read_counters(sm, 0, &c, true);
   if (rc != CVX_OK) return rc;
   for (int a = 0; a < 3; ++a) { lo[a] = c.aabb_lo[a]; hi[a] = c.aabb_hi[a]; }
   return CVX_OK;
