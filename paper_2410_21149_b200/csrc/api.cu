@@ -113,6 +113,7 @@ void free_all(cvx_submap* sm) {
   if (sm->pool.cacc) cudaFree(sm->pool.cacc);
   if (sm->pool.esdf) cudaFree(sm->pool.esdf);
   if (sm->pool.coords) cudaFree(sm->pool.coords);
+  if (sm->pool.grid) cudaFree(sm->pool.grid);
   if (sm->ctr) cudaFree(sm->ctr);
   if (sm->ctr_host) cudaFreeHost(sm->ctr_host);
   for (auto& B : sm->buf) {
@@ -177,6 +178,7 @@ cvx_status cvx_create_submap(const cvx_grid_config* cfg, const double* T_world_s
   sm->prof = new cvx::Prof();
   if (const char* ag = std::getenv("CVX_AGGREGATE")) sm->aggregate = ag[0] != '0';  // tuning knob
   if (const char* b2 = std::getenv("CVX_BW2")) sm->bw2 = b2[0] != '0';              // tuning knob
+  if (const char* b3 = std::getenv("CVX_BW3")) sm->bw3 = b3[0] != '0';              // tuning knob
   if (const char* wc = std::getenv("CVX_WALK_CW")) sm->walk_cw = wc[0] != '0';     // tuning knob
   if (const char* fa = std::getenv("CVX_FUSE_ALLOC")) sm->fuse_alloc = fa[0] != '0'; // tuning knob
   if (const char* lc = std::getenv("CVX_LIST_CAP")) sm->list_cap_limit = std::atoll(lc);  // test knob
@@ -195,6 +197,7 @@ cvx_status cvx_create_submap(const cvx_grid_config* cfg, const double* T_world_s
       (e = cudaMalloc(&sm->pool.acc, (nb + cvx::kTrashBlocks) * cvx::kBlockVox * 8)) != cudaSuccess ||
       (e = cudaMalloc(&sm->pool.esdf, nb * cvx::kBlockVox * 4)) != cudaSuccess ||
       (e = cudaMalloc(&sm->pool.coords, nb * 16)) != cudaSuccess ||
+      (e = cudaMalloc(&sm->pool.grid, sizeof(int) * cvx::kGridX * cvx::kGridY * cvx::kGridZ)) != cudaSuccess ||
       (e = cudaMalloc(&sm->ctr, sizeof(cvx::Counters))) != cudaSuccess ||
       (e = cudaMallocHost(&sm->ctr_host, sizeof(cvx::Counters))) != cudaSuccess ||
       (e = cudaMalloc(&sm->buf[0].frame_T, sizeof(double) * 16 * cvx::kMaxBatch)) != cudaSuccess ||
@@ -217,6 +220,7 @@ cvx_status cvx_create_submap(const cvx_grid_config* cfg, const double* T_world_s
   cudaMemset(sm->pool.sums, 0, nb * cvx::kBlockVox * 16);
   cudaMemset(sm->pool.acc, 0, (nb + cvx::kTrashBlocks) * cvx::kBlockVox * 8);   // + the trash region (cvx_internal.cuh)
   cudaMemset(sm->pool.esdf, 0, nb * cvx::kBlockVox * 4);
+  cudaMemset(sm->pool.grid, 0xff, sizeof(int) * cvx::kGridX * cvx::kGridY * cvx::kGridZ);   // all unknown
   if (cfg->color) {
     cudaMemset(sm->pool.csum, 0, nb * cvx::kBlockVox * 32);
     cudaMemset(sm->pool.cacc, 0, (nb + cvx::kTrashBlocks) * cvx::kBlockVox * 16);

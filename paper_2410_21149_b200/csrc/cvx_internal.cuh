@@ -55,6 +55,7 @@ struct PoolView {
   float* esdf;             // [max_blocks*512]
   int4* coords;            // [max_blocks]
   int max_blocks;
+  int* grid;               // [kGridZ][kGridY][kGridX] dense slot cache of ALLOCATE
 };
 
 // 21-bit two's-complement fields per axis; never equals kEmptyKey.
@@ -160,6 +161,17 @@ inline int packed_q(double tau) {
 // Longest dense EDT axis (voxels, multiple of 8): 2 (n - 1)^2 < 2^32 - 1, so the 2-D squared distances
 // of the ESDF's second pass fit uint32 with 0xffffffff left as the "no site" marker.
 constexpr long long kMaxEdtAxis = 46336;
+
+// Dense slot cache of ALLOCATE (a3): a fixed window of 256 x 256 x 64 blocks around the submap origin
+// (block (0, 0, 0)), entry = the block's pool slot or -1 (not known yet).  The hash table stays the
+// authority: a -1 (or a block outside the window) goes through hash_activate, whose slot is then cached.
+// Entries only ever go -1 -> slot between resets, so a stale -1 is merely a slower path.
+constexpr int kGridX = 256, kGridY = 256, kGridZ = 64;
+__host__ __device__ inline int grid_cache_index(int bx, int by, int bz) {
+  const unsigned ux = (unsigned)(bx + kGridX / 2), uy = (unsigned)(by + kGridY / 2), uz = (unsigned)(bz + kGridZ / 2);
+  if (ux >= (unsigned)kGridX || uy >= (unsigned)kGridY || uz >= (unsigned)kGridZ) return -1;
+  return (int)((uz * kGridY + uy) * kGridX + ux);
+}
 
 // Floor division / modulo by 8 on int32 voxel coordinates (S:L200-207 floor semantics).
 __host__ __device__ inline int bdiv(int v) { return v >> 3; }

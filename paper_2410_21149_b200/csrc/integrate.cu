@@ -475,6 +475,115 @@ __global__ void __launch_bounds__(256) block_walk2_kernel(const __grid_constant_
   }
 }
 
+// ALLOCATE through the dense slot cache (default): every lane walks its own ray at block granularity (no
+// lockstep, no shuffles) and reads the slot of each block from the cache, the entry of step j+1 loaded
+// before step j's is consumed; only an unknown block (-1) or one outside the cache window goes through
+// hash_activate (insert-if-absent + slot bump), and its slot is then cached.  Same block
+// sets and slot lists as block_walk2_kernel (the slots are the hash's).
+#ifndef CVX_GRID_LD
+#define CVX_GRID_LD(ptr) (*(ptr))   // L1-cacheable: a stale -1 only takes the hash path
+#endif
+template <bool k32>
+__global__ void __launch_bounds__(256) block_walk3_kernel(const __grid_constant__ WalkParams p) {
+  using DT = typename std::conditional<k32, unsigned, unsigned long long>::type;
+  using ST = typename std::conditional<k32, int, long long>::type;
+  const int n_rays = p.lcnt[0];
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n_rays) return;
+  const RayRec r = p.rays[idx];
+  long long R[3], AD[3];
+  int bb[3], st[3], kk[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    bb[a] = (int)(r.A[a] >> 19);
+    const int be = (int)(r.B[a] >> 19);
+    const long long D = r.B[a] - r.A[a];
+    kk[a] = be > bb[a] ? be - bb[a] : bb[a] - be;
+    if (D > 0) { st[a] = 1; R[a] = (((long long)bb[a] + 1) << 19) - r.A[a]; }
+    else { st[a] = -1; R[a] = r.A[a] - ((long long)bb[a] << 19); }
+    AD[a] = D < 0 ? -D : D;
+  }
+  int b0 = bb[0], b1 = bb[1], b2 = bb[2], k0 = kk[0], k1 = kk[1], k2 = kk[2];
+  const int s0 = st[0], s1 = st[1], s2 = st[2];
+  const int nb = 1 + k0 + k1 + k2;
+  DT D01, D02, D12, I0, I1, I2;
+  {
+    const long long C01 = R[0] * AD[1] - R[1] * AD[0];
+    const long long C02 = R[0] * AD[2] - R[2] * AD[0];
+    const long long C12 = R[1] * AD[2] - R[2] * AD[1];
+    if (k32) {
+      D01 = (DT)(-((-C01) >> 19)); D02 = (DT)(-((-C02) >> 19)); D12 = (DT)(-((-C12) >> 19));
+      I0 = (DT)AD[0]; I1 = (DT)AD[1]; I2 = (DT)AD[2];
+    } else {
+      D01 = (DT)C01; D02 = (DT)C02; D12 = (DT)C12;
+      I0 = (DT)(AD[0] << 19); I1 = (DT)(AD[1] << 19); I2 = (DT)(AD[2] << 19);
+    }
+  }
+  int* const list = r.list_off >= 0 ? p.slots + r.list_off : nullptr;
+  const int* const grid = p.pool.grid;
+#if CVX_BW3_AHEAD2
+  // entries of steps j+1 and j+2 in flight while step j is consumed
+  auto adv = [&]() {
+    const bool g0 = k0 > 0, g1 = k1 > 0, g2 = k2 > 0;
+    const bool yf = g1 & (!g0 | ((ST)D01 > 0));
+    const bool zf = g2 & (yf ? ((ST)D12 > 0) : (!g0 | ((ST)D02 > 0)));
+    if (zf) { b2 += s2; --k2; D02 -= I0; D12 -= I1; }
+    else if (yf) { b1 += s1; --k1; D01 -= I0; D12 += I2; }
+    else { b0 += s0; --k0; D01 += I1; D02 += I2; }
+  };
+  int c0 = b0, c1 = b1, c2 = b2, cgi = grid_cache_index(b0, b1, b2);
+  int ent = cgi >= 0 ? CVX_GRID_LD(grid + cgi) : -1;
+  int n0 = 0, n1 = 0, n2 = 0, ngi = -1, entn = -1;
+  if (nb > 1) {
+    adv();
+    n0 = b0; n1 = b1; n2 = b2; ngi = grid_cache_index(b0, b1, b2);
+    entn = ngi >= 0 ? CVX_GRID_LD(grid + ngi) : -1;
+  }
+  for (int j = 0; j < nb; ++j) {
+    int ent2 = -1, gi2 = -1;
+    if (j + 2 < nb) {
+      adv();
+      gi2 = grid_cache_index(b0, b1, b2);
+      if (gi2 >= 0) ent2 = CVX_GRID_LD(grid + gi2);
+    }
+    int slot = ent;
+    if (slot < 0) {
+      slot = hash_activate(p.hash, p.pool, p.ctr, pack_key(c0, c1, c2), c0, c1, c2);
+      if (slot >= 0 && cgi >= 0) p.pool.grid[cgi] = slot;
+    }
+    if (list) list[j] = slot;
+    c0 = n0; c1 = n1; c2 = n2; cgi = ngi; ent = entn;
+    n0 = b0; n1 = b1; n2 = b2; ngi = gi2; entn = ent2;
+  }
+#else
+  int gi = grid_cache_index(b0, b1, b2);
+  int ent = gi >= 0 ? CVX_GRID_LD(grid + gi) : -1;
+  for (int j = 0; j < nb; ++j) {
+    const int c0 = b0, c1 = b1, c2 = b2, cgi = gi;
+    // advance the DDA to step j + 1 (O4 at block granularity: earliest crossing, ties x < y < z) and
+    // load its cache entry before consuming step j's
+    int entn = -1;
+    if (j + 1 < nb) {
+      const bool g0 = k0 > 0, g1 = k1 > 0, g2 = k2 > 0;
+      const bool yf = g1 & (!g0 | ((ST)D01 > 0));
+      const bool zf = g2 & (yf ? ((ST)D12 > 0) : (!g0 | ((ST)D02 > 0)));
+      if (zf) { b2 += s2; --k2; D02 -= I0; D12 -= I1; }
+      else if (yf) { b1 += s1; --k1; D01 -= I0; D12 += I2; }
+      else { b0 += s0; --k0; D01 += I1; D02 += I2; }
+      gi = grid_cache_index(b0, b1, b2);
+      if (gi >= 0) entn = CVX_GRID_LD(grid + gi);
+    }
+    int slot = ent;
+    if (slot < 0) {
+      slot = hash_activate(p.hash, p.pool, p.ctr, pack_key(c0, c1, c2), c0, c1, c2);
+      if (slot >= 0 && cgi >= 0) p.pool.grid[cgi] = slot;
+    }
+    if (list) list[j] = slot;
+    ent = entn;
+  }
+#endif
+}
+
 // k32: the crossing-order differences fit 32 bits.  With r_i = rho_i + m_i 2^16 (m_i crossings done),
 // E_ij = X_ij - X_ji = C_ij + 2^16 F_ij with C_ij = rho_i a_j - rho_j a_i and F_ij = m_i a_j - m_j a_i, so
 // E_ij > 0  <=>  H_ij = F_ij - floor(-C_ij / 2^16) > 0; H_ij moves by a_j / -a_i per step like E_ij by
@@ -1108,6 +1217,16 @@ __global__ void zero_blocks_kernel(Counters* ctr, long long* sums, unsigned long
   }
 }
 
+// reset: the dense slot cache entries of the used blocks go back to unknown
+__global__ void clear_grid_kernel(Counters* ctr, const int4* coords, int* grid, int max_blocks) {
+  const int nb = min(*(volatile int*)&ctr->n_blocks, max_blocks);
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < nb; s += gridDim.x * blockDim.x) {
+    const int4 c = coords[s];
+    const int gi = grid_cache_index(c.x, c.y, c.z);
+    if (gi >= 0) grid[gi] = -1;
+  }
+}
+
 __global__ void zero_color_kernel(Counters* ctr, long long* csum, unsigned long long* cacc, int max_blocks) {
   const int nb = min(*(volatile int*)&ctr->n_blocks, max_blocks);
   const long long nv = (long long)nb * kBlockVox;
@@ -1241,6 +1360,10 @@ cudaError_t launch_reset(cvx_submap* sm, cudaStream_t st) {
   if (sm->pool.csum) {
     ProfScope ps_(sm, "reset_zero_color", st);
     zero_color_kernel<<<148 * 8, 256, 0, st>>>(sm->ctr, sm->pool.csum, sm->pool.cacc, sm->pool.max_blocks);
+  }
+  {
+    ProfScope ps_(sm, "reset_grid", st);
+    clear_grid_kernel<<<148 * 2, 256, 0, st>>>(sm->ctr, sm->pool.coords, sm->pool.grid, sm->pool.max_blocks);
   }
   {
     ProfScope ps_(sm, "reset_counters", st);
@@ -1397,7 +1520,10 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     const bool fuse = sm->fuse_alloc && cw && sm->aggregate && sm->walk_cw && !rgb && !trig;
     if (!fuse) {
       ProfScope ps_(sm, "block_walk_allocate", side);
-      if (sm->bw2) {
+      if (sm->bw3) {
+        if (k32) block_walk3_kernel<true><<<blocks, 256, 0, side>>>(wp);
+        else block_walk3_kernel<false><<<blocks, 256, 0, side>>>(wp);
+      } else if (sm->bw2) {
         if (k32) block_walk2_kernel<true><<<blocks, 256, 0, side>>>(wp);
         else block_walk2_kernel<false><<<blocks, 256, 0, side>>>(wp);
       } else {

@@ -330,7 +330,7 @@ def test_block_count_trigger_matches_frame_by_frame(tiny):
     assert c.integrate_until(data, poses, tiny["sensor"], tiny["grid"]["max_blocks"]) == len(frames)
 
 
-@pytest.mark.parametrize("knob", ["CVX_FUSE_ALLOC=1", "CVX_BW2=0", "CVX_WALK_CW=0", "CVX_LIST_CAP=2000"])
+@pytest.mark.parametrize("knob", ["CVX_FUSE_ALLOC=1", "CVX_BW3=0", "CVX_BW3=0,CVX_BW2=0", "CVX_WALK_CW=0", "CVX_LIST_CAP=2000"])
 def test_walk_variants_bitexact(tiny, orc, monkeypatch, knob):
     """The tuning variants of the integrate path (ALLOCATE fused into the walk, the first block walk,
     the general walk kernel; a slot-list buffer capped so most rays find their blocks by hash lookup in
@@ -338,8 +338,9 @@ def test_walk_variants_bitexact(tiny, orc, monkeypatch, knob):
     sums) and match the oracle."""
     frames = [0, 3, 6, 9]
     ref, _ = gpu_build(tiny, frames, batch=True, finalize=False)
-    k, v = knob.split("=")
-    monkeypatch.setenv(k, v)
+    for kv in knob.split(","):
+        k, v = kv.split("=")
+        monkeypatch.setenv(k, v)
     var, _ = gpu_build(tiny, frames, batch=True, finalize=False)
     a, b = gpu_export_sorted(ref), gpu_export_sorted(var)
     assert np.array_equal(a[0], b[0])

@@ -1,4 +1,4 @@
 cd "$(dirname "$0")/.."
-for r in 1 2; do for o in 1 0; do
-CVX_BENCH_ORDER=$o python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('order=$o', round(d['ms_per_step'],3), round(d['one_submap_in_flight']['ms_per_step'],3))"
+for r in 1 2; do for spec in "1 1" "0 1" "0 0"; do set -- $spec
+CVX_BENCH_ORDER=$1 CVX_WALK_ORDER=$2 python bench.py --steps 10 --warmup 3 --no-cpu-baseline 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('bench_order=$1 walk_order=$2', round(d['ms_per_step'],3), 'e2e', round(d['e2e']['ms_per_step'],3), 'one', round(d['one_submap_in_flight']['ms_per_step'],3))"
 done; done

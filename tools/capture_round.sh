@@ -18,7 +18,7 @@ for w in $WHAT; do case $w in
       -k regex:_ZN3cvx --csv --log-file gpurun_out/$T/launches.csv python bench.py --steps 1 --warmup 1 \
       --no-cpu-baseline --no-e2e > gpurun_out/$T/launches_bench.json 2>&1; echo "launches rc=$?";;
   walk) cap "^walk_(cw_)?kernel" walk 2;;   # one walk launch per configs[1] submap
-  block_walk) cap "^block_walk2?_kernel" block_walk 2;;
+  block_walk) cap "^block_walk[23]?_kernel" block_walk 2;;
   prepare) cap "^prepare_kernel" prepare 2;;
   fold) cap "^fold_kernel" fold 1;;
   esdf_pass_x) cap "^pass_x_kernel" esdf_pass_x 1;;
