@@ -1,6 +1,7 @@
 """Full-size parity: BASELINE.json configs[1] (200 OS1-64 scans, 0.2 m voxels) in the launch
-configuration bench.py times (one integrate_batch of 200 scans = 4 launches of 50), checked on sampled outputs the oracle can
-compute one by one and on properties that hold at any size.
+configuration bench.py times (one integrate_batch of 200 scans = one walk launch of 2^24 - 1 rays at most),
+checked element by element against the oracle's full 200-scan build (TSDF and the stage-isolated exact
+ESDF), on sampled outputs the oracle computes one by one, and on properties that hold at any size.
 """
 import numpy as np
 import pytest
@@ -11,7 +12,7 @@ from helpers import TOL_E, assert_tsdf_parity, gpu_export_sorted, oracle_build, 
 
 pytestmark = pytest.mark.gpu
 
-BATCH = 200  # bench.py default (one integrate_batch call; the library launches 4 x 50 scans)
+BATCH = 200  # bench.py default (one integrate_batch call; the library runs one walk launch of 200 scans)
 
 
 @pytest.fixture(scope="module")
@@ -125,3 +126,22 @@ def test_fullsize_queries_sampled(lidar, built, orc):
     m = so != 2
     assert np.allclose(dist[m], vo[m], atol=1e-4, rtol=0)
     assert (so == 0).sum() > 1000
+
+
+def test_fullsize_all_200_scans_parity_vs_oracle(lidar, built, orc):
+    """The bench's submap state (200 scans, one launch) element by element against the oracle integrating
+    all 200 scans (O1-O8; ~90 s single-threaded): block sets and observed sets bit-exact, |dD| <= 1e-4 m,
+    |dW| <= 1e-3 max(1, W); then the oracle's exact EDT (O10-O12) over the GPU's exported TSDF equals the
+    GPU ESDF on every voxel (stage-isolated, R4)."""
+    cfg, data, poses = lidar
+    sm, (b, D, W, E), st = built
+    sub = dict(cfg)
+    sub["frames"] = {k: dict(data=data[k].cpu(), T_world_sensor=poses[k]) for k in range(200)}
+    o, _ = oracle_build(sub, range(200))
+    rep = assert_tsdf_parity((b, D, W, E), o.export())
+    assert rep["blocks"] == st["total_blocks"] and rep["observed"] > 5_000_000
+    g = cfg["grid"]
+    Eo, _ = orc.esdf(b, D.astype(np.float64), W.astype(np.float64), g["voxel_size"], g["site_threshold"])
+    assert np.array_equal(np.isnan(E), np.isnan(Eo))
+    fin = np.isfinite(Eo)
+    assert np.abs(E[fin].astype(np.float64) - Eo[fin]).max() <= TOL_E
