@@ -85,12 +85,47 @@ __device__ __forceinline__ double dm(double a, double b) { return __dmul_rn(a, b
 __device__ __forceinline__ double da(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double ds(double a, double b) { return __dsub_rn(a, b); }
 
-// O3: q(x) = floor((x / s) * 2^16), rejected outside |voxel| < 2^23.
-__device__ __forceinline__ bool quantise(double x, double s, long long* q) {
-  double a = dm(__ddiv_rn(x, s), 65536.0);
+// x / s correctly rounded (IEEE, identical to __ddiv_rn and to the oracle's x / s) for s > 0, given any
+// approximation rs of 1/s: Markstein's final step q = q0 + (x - q0 s) rs, then an exact check — the
+// remainder r = x - q s is computed exactly by the FMA when q is within a few ulps, and |r| < s ulp(q) / 2
+// proves q = RN(x / s) (RN is monotone, so a rounded remainder below the bound is a true one below it).
+// Anything unproven (a power-of-two q, whose lower half-ulp is smaller; tiny / huge exponents; or a
+// failed check) takes the IEEE division.  Replaces the Newton iteration of a reciprocal per division.
+#ifndef CVX_FAST_DIV
+#define CVX_FAST_DIV 1
+#endif
+__device__ __forceinline__ double div_rn(double x, double s, double rs) {
+#if CVX_FAST_DIV
+  const double q0 = __dmul_rn(x, rs);
+  const double q = __fma_rn(__fma_rn(-q0, s, x), rs, q0);
+  const double r = __fma_rn(-q, s, x);
+  const int hi = __double2hiint(q), lo = __double2loint(q);
+  const int e = (hi >> 20) & 0x7ff;
+  if (e > 54 && e < 2046 && ((hi & 0xfffff) | lo) != 0) {
+    const double h = __hiloint2double((e - 53) << 20, 0);   // ulp(q) / 2
+    if (fabs(r) < __dmul_rn(h, s)) return q;
+  }
+#endif
+  return __ddiv_rn(x, s);
+}
+
+// O3: q(x) = floor((x / s) * 2^16), rejected outside |voxel| < 2^23.  rs ~ 1/s (see div_rn).
+__device__ __forceinline__ bool quantise(double x, double s, long long* q, double rs) {
+  double a = dm(div_rn(x, s, rs), 65536.0);
   if (!(fabs(a) < 549755813888.0)) return false;
   *q = (long long)floor(a);
   return true;
+}
+__device__ __forceinline__ bool quantise(double x, double s, long long* q) {
+  return quantise(x, s, q, __drcp_rn(s));
+}
+
+// n / d for n < 2^32, 0 < d < 2^32 given rd = RN(1/d): the truncated fp64 product is the quotient or one
+// less (its absolute error (n/d) 2^-52 is below the 1/d gap to the next integer), fixed by one compare.
+__device__ __forceinline__ unsigned udiv_fast(unsigned n, unsigned d, double rd) {
+  unsigned q = __double2uint_rz(__dmul_rn((double)n, rd));
+  if (n - q * d >= d) ++q;
+  return q;
 }
 
 // O1: R_SC[i][j] = ((Rws[0][i] Rwc[0][j] + Rws[1][i] Rwc[1][j]) + Rws[2][i] Rwc[2][j]),
@@ -122,6 +157,8 @@ struct PrepParams {
   float fx, fy, cx, cy;
   double rmin, rmax, s, tau, rfloor;
   double sdf_scale;   // 2^(q + kSdfF)
+  double rs;          // RN(1 / s) (fast correctly rounded divisions by s, div_rn)
+  double r_npf, r_width, r_pcols;   // RN(1 / n_per_frame), RN(1 / width), RN(1 / (width / patch cols))
   int weighting, carve;
   int height;
   const double* frame_T;
@@ -143,15 +180,17 @@ __global__ void __launch_bounds__(256) prepare_kernel(const __grid_constant__ Pr
   int status = -1;  // -1 no thread, 0 used, 1 invalid, 2 range, 3 domain
   RayRec rec;
   if (idx < p.total) {
-    const long long f = idx / p.n_per_frame;
-    long long i = idx - f * p.n_per_frame;
+    // (index arithmetic in 32 bits: a launch holds < 2^31 rays; divisions by multiplication, udiv_fast)
+    const unsigned f = udiv_fast((unsigned)idx, (unsigned)p.n_per_frame, p.r_npf);
+    unsigned i = (unsigned)idx - f * (unsigned)p.n_per_frame;
     constexpr int PR = CVX_PATCH_ROWS, PC = 32 / CVX_PATCH_ROWS;
     if (p.kind != 0 && p.width > 0 && p.height > 0 && p.width % PC == 0 && p.height % PR == 0) {
       // organised sensor: warp = PR rows x PC columns patch (spatially coherent rays per warp)
-      const long long pt = i >> 5, l = i & 31, pcols = p.width / PC;
-      const long long rr = l / PC, cc = (rr & 1) ? PC - 1 - (l % PC) : (l % PC);   // serpentine: lane l+1 neighbours lane l
-      const long long row = (pt / pcols) * PR + rr, col = (pt % pcols) * PC + cc;
-      i = row * p.width + col;
+      const unsigned pt = i >> 5, l = i & 31, pcols = (unsigned)p.width / PC;
+      const unsigned rr = l / PC, cc = (rr & 1) ? PC - 1 - (l % PC) : (l % PC);   // serpentine: lane l+1 neighbours lane l
+      const unsigned prow = udiv_fast(pt, pcols, p.r_pcols);
+      const unsigned row = prow * PR + rr, col = (pt - prow * pcols) * PC + cc;
+      i = row * (unsigned)p.width + col;
     }
     const long long src = f * p.n_per_frame + i;
     const double* T = p.frame_T + kFrameRec * f;
@@ -160,7 +199,8 @@ __global__ void __launch_bounds__(256) prepare_kernel(const __grid_constant__ Pr
     if (p.kind == 1) {  // O2: pinhole depth -> point in fp32 exactly as written, integer pixel (Q24)
       float z = p.data[src];
       if (!(z > 0.0f) || !isfinite(z)) status = 1;
-      float u = (float)(int)(i % p.width), v = (float)(int)(i / p.width);
+      const unsigned vi = udiv_fast(i, (unsigned)p.width, p.r_width);
+      float u = (float)(int)(i - vi * (unsigned)p.width), v = (float)(int)vi;
       pc[0] = (double)__fdiv_rn(__fmul_rn(z, __fsub_rn(u, p.cx)), p.fx);
       pc[1] = (double)__fdiv_rn(__fmul_rn(z, __fsub_rn(v, p.cy)), p.fy);
       pc[2] = (double)z;
@@ -179,13 +219,14 @@ __global__ void __launch_bounds__(256) prepare_kernel(const __grid_constant__ Pr
       if (!(L >= p.rmin && L <= p.rmax) || !(L > 0.0)) status = 2;  // Q10
       if (status == 0) {
         if (p.carve && T[15] == 0.0) status = 3;
+        const double rL = __drcp_rn(L);
         for (int a = 0; a < 3 && status == 0; ++a) {
-          double ext = __ddiv_rn(dm(p.tau, d[a]), L);
+          double ext = div_rn(dm(p.tau, d[a]), L, rL);
           double e = da(pw[a], ext);                         // tau behind the point
           bool okA = true;
           if (p.carve) rec.A[a] = __double_as_longlong(T[12 + a]);   // from the optical centre (Q2)
-          else okA = quantise(ds(pw[a], ext), p.s, &rec.A[a]);
-          if (!okA || !quantise(e, p.s, &rec.B[a])) status = 3;
+          else okA = quantise(ds(pw[a], ext), p.s, &rec.A[a], p.rs);
+          if (!okA || !quantise(e, p.s, &rec.B[a], p.rs)) status = 3;
           else {
             long long span = (rec.B[a] >> 16) - (rec.A[a] >> 16);
             if (span >= 32768 || span <= -32768) status = 3;
@@ -195,7 +236,7 @@ __global__ void __launch_bounds__(256) prepare_kernel(const __grid_constant__ Pr
           // O5 in fixed point: sdf of the first voxel v_A, then an exact per-axis decrement s |u_a| per
           // step (stepping axis a moves the voxel centre by s sign(u_a) e_a)
           double u[3], sdf0 = 0.0;
-          const double inv_l = __drcp_rn(L);
+          const double inv_l = rL;
           for (int a = 0; a < 3; ++a) {
             u[a] = d[a] * inv_l;
             const double c = ((double)(rec.A[a] >> 16) + 0.5) * p.s;
@@ -1373,6 +1414,14 @@ cudaError_t launch_reset(cvx_submap* sm, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+static void set_divisors(PrepParams& pp, const cvx_sensor_model& sensor) {
+  constexpr int PC = 32 / CVX_PATCH_ROWS;
+  pp.rs = 1.0 / pp.s;
+  pp.r_npf = 1.0 / (double)pp.n_per_frame;
+  pp.r_width = sensor.width > 0 ? 1.0 / (double)sensor.width : 0.0;
+  pp.r_pcols = sensor.width >= PC ? 1.0 / (double)(sensor.width / PC) : 0.0;
+}
+
 static cudaError_t grow(void** ptr, int64_t* cap, int64_t need, size_t elem) {
   if (*cap >= need) return cudaSuccess;
   if (*ptr) cudaFree(*ptr);
@@ -1493,6 +1542,7 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     pp.s = sm->cfg.voxel_size; pp.tau = sm->cfg.truncation; pp.rfloor = sm->cfg.weight_range_floor;
     pp.weighting = sm->cfg.weighting; pp.carve = sm->cfg.carve;
     pp.sdf_scale = std::ldexp(1.0, q + kSdfF);
+    set_divisors(pp, sensor);
     pp.height = sensor.height;
     pp.frame_T = B.frame_T; pp.rays = (RayRec*)B.rays; pp.ctr = sm->ctr; pp.lcnt = B.lcnt;
     // one spare entry: walk_cw_kernel prefetches the entry after a ray's last block unconditionally
@@ -1613,6 +1663,7 @@ cudaError_t launch_integrate_projective(cvx_submap* sm, const float* depth, int6
       pp.s = sm->cfg.voxel_size; pp.tau = sm->cfg.truncation; pp.rfloor = sm->cfg.weight_range_floor;
       pp.weighting = sm->cfg.weighting; pp.carve = sm->cfg.carve;
       pp.sdf_scale = std::ldexp(1.0, q + kSdfF);
+      set_divisors(pp, sensor);
       pp.height = sensor.height;
       pp.frame_T = B.frame_T; pp.rays = (RayRec*)B.rays; pp.ctr = sm->ctr; pp.lcnt = B.lcnt;
       pp.list_cap = (int)std::min<long long>(B.slot_cap - 1, 0x7fffffffll);
