@@ -524,8 +524,18 @@ __global__ void __launch_bounds__(256) block_walk2_kernel(const __grid_constant_
 #ifndef CVX_GRID_LD
 #define CVX_GRID_LD(ptr) (*(ptr))   // L1-cacheable: a stale -1 only takes the hash path
 #endif
+#ifndef CVX_BW3_MINB
+#define CVX_BW3_MINB 1
+#endif
+// the rare miss path out of line: the walk loop keeps few registers (more resident warps hide the cache
+// entry's L2 latency)
+__device__ __noinline__ int activate_cached(const WalkParams& p, int c0, int c1, int c2, int cgi) {
+  const int slot = hash_activate(p.hash, p.pool, p.ctr, pack_key(c0, c1, c2), c0, c1, c2);
+  if (slot >= 0 && cgi >= 0) p.pool.grid[cgi] = slot;
+  return slot;
+}
 template <bool k32>
-__global__ void __launch_bounds__(256) block_walk3_kernel(const __grid_constant__ WalkParams p) {
+__global__ void __launch_bounds__(256, CVX_BW3_MINB) block_walk3_kernel(const __grid_constant__ WalkParams p) {
   using DT = typename std::conditional<k32, unsigned, unsigned long long>::type;
   using ST = typename std::conditional<k32, int, long long>::type;
   const int n_rays = p.lcnt[0];
@@ -614,11 +624,7 @@ __global__ void __launch_bounds__(256) block_walk3_kernel(const __grid_constant_
       gi = grid_cache_index(b0, b1, b2);
       if (gi >= 0) entn = CVX_GRID_LD(grid + gi);
     }
-    int slot = ent;
-    if (slot < 0) {
-      slot = hash_activate(p.hash, p.pool, p.ctr, pack_key(c0, c1, c2), c0, c1, c2);
-      if (slot >= 0 && cgi >= 0) p.pool.grid[cgi] = slot;
-    }
+    const int slot = ent >= 0 ? ent : activate_cached(p, c0, c1, c2, cgi);
     if (list) list[j] = slot;
     ent = entn;
   }
