@@ -843,14 +843,14 @@ cudaError_t dense_edt(cvx_submap* sm, const int lo[3], const int hi[3], cudaStre
   const long long nvox = (long long)nx * ny * nz;
   cudaError_t e = ensure_planes(sm, st);
   if (e != cudaSuccess) return e;
-  // passes y / z: 0 = streaming link kernel (default, measured faster), 1 = TMA-staged band hulls
+  // passes y / z: 0 = streaming Meijster link kernel (default, measured fastest), 1 = TMA-staged band hulls
   static const int kernel = [] { const char* v = std::getenv("CVX_EDT_KERNEL"); return v ? std::atoi(v) : 0; }();
-  const long long need = nvox * (4 + 2 + (kernel == 0 ? 8 : 0)) + (long long)nbx * nby + (long long)nby * nbz + 256;
+  const long long need = nvox * (4 + 2 + (kernel != 1 ? 8 : 0)) + (long long)nbx * nby + (long long)nby * nbz + 256;
   if ((e = grow_async(&sm->edt, &sm->edt_bytes, need, st)) != cudaSuccess) return e;
   unsigned* g2 = reinterpret_cast<unsigned*>(sm->edt);
   unsigned short* g1 = reinterpret_cast<unsigned short*>(g2 + nvox);   // nvox % 512 == 0: aligned
   void* meta = g1 + nvox;                                                  // link variant only
-  unsigned char* colmask = reinterpret_cast<unsigned char*>(g1 + nvox) + (kernel == 0 ? 8 * nvox : 0);
+  unsigned char* colmask = reinterpret_cast<unsigned char*>(g1 + nvox) + (kernel != 1 ? 8 * nvox : 0);
   unsigned char* rowmask = colmask + (size_t)nbx * nby;
   cudaMemsetAsync(colmask, 0, (size_t)nbx * nby + (size_t)nby * nbz, st);
   if ((e = build_grid(sm, lo, nbx, nby, nbz, colmask, rowmask, st, "esdf_block_grid")) != cudaSuccess) return e;
