@@ -119,6 +119,8 @@ void free_all(cvx_submap* sm) {
   for (auto& B : sm->buf) {
     if (B.frame_T) cudaFree(B.frame_T);
     if (B.rays) cudaFree(B.rays);
+    if (B.rgbs) cudaFree(B.rgbs);
+    if (B.ws) cudaFree(B.ws);
     if (B.slot_lists) cudaFree(B.slot_lists);
     if (B.lcnt) cudaFree(B.lcnt);
     if (B.staging) cudaFree(B.staging);

@@ -35,17 +35,30 @@ namespace {
 // Fixed-point sdf along a ray: units of 2^-(q+kSdfF) metres, q = packed_q(tau).
 constexpr int kSdfF = 20;
 
+// Per used ray, written by prepare_kernel, read by the block walk and the update walk (48 B, SURVEY
+// §8(a1) "<= 48 B/ray"): the fixed-point start A relative to the frame's fixed-point origin O (0 in
+// carve mode), the end B relative to A, the first voxel's sdf with the frame index in its low 13 bits,
+// the per-step sdf decrements (in units of 4) and the ray's block-slot list offset.  Colour and general
+// weights live in per-ray side arrays, allocated only for those modes.
 struct __align__(16) RayRec {
-  long long A[3];   // fixed-point (2^-16 voxel) start of the updated segment (O3)
-  long long B[3];   // fixed-point end: p + tau*u
-  long long S0;     // projective sdf (p - c_v).u of the first voxel, fixed point (kSdfF)
-  long long U[3];   // sdf decrement per voxel step along axis a: s |u_a|, fixed point (>= 0)
-  float w;          // weight (O6)
-  int n_vox;        // closed-form voxel count (COUNT)
-  int list_off;     // offset of the ray's block-slot list, -1 if the list buffer was full
-  unsigned rgb;     // colour of the point r | g << 8 | b << 16 (TSDF + Color)
+  int dA[3];          // A - O, fixed point 2^-16 voxel (O = q(t_SC) of the frame, compose_kernel)
+  int dB[3];          // B - A (a span < 2^15 voxels per axis, O3)
+  long long S0f;      // S0 << kFrameBits | frame, S0 = projective sdf of the first voxel (fixed point kSdfF)
+  unsigned U[3];      // sdf decrement per voxel step along axis a, >> kUShift (>= 0)
+  int list_off;       // offset of the ray's block-slot list, -1 if the list buffer was full
 };
-static_assert(sizeof(RayRec) == 96, "RayRec layout");
+static_assert(sizeof(RayRec) == 48, "RayRec layout");
+constexpr int kFrameBits = 13;      // frame index within a launch (< kMaxBatch)
+constexpr int kUShift = 2;          // U <= s 2^(q + kSdfF) <= 2^34 (tau >= 2 s): U >> 2 fits 32 bits
+
+// The ray as the kernels use it (expanded from RayRec + the frame records + the side arrays).
+struct RayView {
+  long long A[3], B[3];
+  long long S0, U[3];
+  float w;
+  int n_vox, list_off, frame;
+  unsigned rgb;
+};
 
 struct ComposeParams {
   double Tws[16];
@@ -59,9 +72,6 @@ struct ComposeParams {
 constexpr int kFrameRec = 16;
 
 // Organised-sensor patch one warp's rays come from: CVX_PATCH_ROWS rows x 32 / CVX_PATCH_ROWS columns.
-#ifndef CVX_TIGHT
-#define CVX_TIGHT 0
-#endif
 #ifndef CVX_BAND2
 #define CVX_BAND2 1
 #endif
@@ -163,14 +173,14 @@ struct PrepParams {
   int height;
   const double* frame_T;
   RayRec* rays;
+  unsigned* rgbs;   // nullable: per used ray colour r | g << 8 | b << 16 (TSDF + Color)
+  float* ws;        // nullable: per used ray weight (weighting != 0)
   Counters* ctr;
   int* lcnt;        // {n_rays, n_slots} of this launch (8-byte aligned)
   int list_cap;
   const int* trig;  // nullable: {threshold, hit, consumed}; a hit submap takes no further frames
   const unsigned char* rgb;   // nullable: per-point colour [total][3]
   int count_vox;    // add the raycast voxel counts to ctr->voxel_updates (0: projection mapping)
-  int frame_tag;    // projection mapping: store frame_base + frame index in RayRec::rgb (birth frames)
-  int frame_base;
 };
 
 __global__ void __launch_bounds__(256) prepare_kernel(const __grid_constant__ PrepParams p) {
@@ -178,10 +188,12 @@ __global__ void __launch_bounds__(256) prepare_kernel(const __grid_constant__ Pr
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   int status = -1;  // -1 no thread, 0 used, 1 invalid, 2 range, 3 domain
-  RayRec rec;
+  RayView rec;
+  unsigned f_used = 0;
   if (idx < p.total) {
     // (index arithmetic in 32 bits: a launch holds < 2^31 rays; divisions by multiplication, udiv_fast)
     const unsigned f = udiv_fast((unsigned)idx, (unsigned)p.n_per_frame, p.r_npf);
+    f_used = f;
     unsigned i = (unsigned)idx - f * (unsigned)p.n_per_frame;
     constexpr int PR = CVX_PATCH_ROWS, PC = 32 / CVX_PATCH_ROWS;
     if (p.kind != 0 && p.width > 0 && p.height > 0 && p.width % PC == 0 && p.height % PR == 0) {
@@ -230,6 +242,8 @@ __global__ void __launch_bounds__(256) prepare_kernel(const __grid_constant__ Pr
           else {
             long long span = (rec.B[a] >> 16) - (rec.A[a] >> 16);
             if (span >= 32768 || span <= -32768) status = 3;
+          const long long dA = rec.A[a] - __double_as_longlong(T[12 + a]);   // band mode: A - O in int32
+          if (dA >= (1ll << 31) || dA < -(1ll << 31)) status = 3;
           }
         }
         if (status == 0) {
@@ -244,6 +258,7 @@ __global__ void __launch_bounds__(256) prepare_kernel(const __grid_constant__ Pr
             rec.U[a] = __double2ll_rn(fabs(u[a]) * p.s * p.sdf_scale);
           }
           rec.S0 = __double2ll_rn(sdf0 * p.sdf_scale);
+          if (rec.S0 >= (1ll << 49) || rec.S0 < -(1ll << 49)) status = 3;   // (|sdf| / tau < 2^14: never)
         }
         if (p.weighting == 0) rec.w = 1.0f;                  // O6
         else { const float r = (float)fmax(L, p.rfloor); rec.w = __frcp_rn(r * r); }
@@ -253,7 +268,7 @@ __global__ void __launch_bounds__(256) prepare_kernel(const __grid_constant__ Pr
           rec.n_vox += (int)(dv < 0 ? -dv : dv);             // a2: n_r = 1 + sum |dv| (O4)
         }
         rec.list_off = -1;
-        rec.rgb = p.frame_tag ? (unsigned)(p.frame_base + (int)f) : 0u;
+        rec.rgb = 0u;
         if (p.rgb) {
           const unsigned char* c = p.rgb + 3 * src;
           rec.rgb = (unsigned)c[0] | ((unsigned)c[1] << 8) | ((unsigned)c[2] << 16);
@@ -313,12 +328,28 @@ __global__ void __launch_bounds__(256) prepare_kernel(const __grid_constant__ Pr
     const long long off = (long long)(unsigned)(s_base >> 32) + s_w[warp][1] + incl - nb;
     rec.list_off = (off + nb <= p.list_cap) ? (int)off : -1;   // full buffer: the walk hashes instead
     const int pos = (int)(unsigned)(s_base & 0xffffffffu) + (int)s_w[warp][0] + __popc(used & ((1u << lane) - 1u));
-    p.rays[pos] = rec;
+    RayRec out;
+    const double* T = p.frame_T + kFrameRec * f_used;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      out.dA[a] = (int)(rec.A[a] - __double_as_longlong(T[12 + a]));
+      out.dB[a] = (int)(rec.B[a] - rec.A[a]);
+      out.U[a] = (unsigned)min((rec.U[a] + (1ll << (kUShift - 1))) >> kUShift, 0xffffffffll);
+    }
+    out.S0f = (long long)((unsigned long long)rec.S0 << kFrameBits) | (long long)f_used;
+    out.list_off = rec.list_off;
+    p.rays[pos] = out;
+    if (p.rgbs) p.rgbs[pos] = rec.rgb;
+    if (p.ws) p.ws[pos] = rec.w;
   }
 }
 
 struct WalkParams {
   const RayRec* rays;
+  const double* frame_T;   // compose_kernel records of the launch's frames (ray origins)
+  const unsigned* rgbs;    // nullable: per ray colour (TSDF + Color)
+  const float* ws;         // nullable: per ray weight (weighting != 0)
+  int frame_base;          // projection mapping: call-relative index of the launch's first frame
   Counters* ctr;
   HashView hash;
   PoolView pool;
@@ -330,6 +361,27 @@ struct WalkParams {
   long long band;   // colour band |S| < band, S in the fixed-point sdf units 2^-(q+kSdfF) m (= tau)
   int* birth;       // projection mapping: per slot, first frame (RayRec::rgb) whose rays touch the block
 };
+
+__device__ __forceinline__ RayView load_ray(const WalkParams& p, int idx) {
+  const RayRec r = p.rays[idx];
+  RayView v;
+  v.frame = (int)(r.S0f & ((1ll << kFrameBits) - 1));
+  const double* T = p.frame_T + kFrameRec * v.frame;
+  v.n_vox = 1;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    v.A[a] = __double_as_longlong(T[12 + a]) + r.dA[a];
+    v.B[a] = v.A[a] + r.dB[a];
+    v.U[a] = (long long)r.U[a] << kUShift;
+    const long long dv = (v.B[a] >> 16) - (v.A[a] >> 16);
+    v.n_vox += (int)(dv < 0 ? -dv : dv);                 // a2: n_r = 1 + sum |dv| (O4)
+  }
+  v.S0 = r.S0f >> kFrameBits;
+  v.list_off = r.list_off;
+  v.w = p.ws ? p.ws[idx] : 1.0f;
+  v.rgb = p.rgbs ? p.rgbs[idx] : 0u;
+  return v;
+}
 
 // Segmented sum over lanes with equal `peers` groups (log-depth shuffle tree); result valid at the
 // lowest lane of each group.  All lanes of `m` must call it.
@@ -365,7 +417,7 @@ __global__ void __launch_bounds__(256) block_walk_kernel(const __grid_constant__
   DT D01 = 0, D02 = 0, D12 = 0, I0 = 0, I1 = 0, I2 = 0;
   int* list = nullptr;
   if (have) {
-    const RayRec r = p.rays[idx];
+    const RayView r = load_ray(p, idx);
     long long R[3], AD[3];
     int bb[3], st[3], kk[3];
 #pragma unroll
@@ -438,8 +490,8 @@ __global__ void __launch_bounds__(256) block_walk2_kernel(const __grid_constant_
   int* list = nullptr;
   int frame = 0x7fffffff;
   if (have) {
-    const RayRec r = p.rays[idx];
-    if (kBirth) frame = (int)r.rgb;
+    const RayView r = load_ray(p, idx);
+    if (kBirth) frame = p.frame_base + r.frame;
     long long R[3], AD[3];
     int bb[3], st[3], kk[3];
 #pragma unroll
@@ -541,7 +593,7 @@ __global__ void __launch_bounds__(256, CVX_BW3_MINB) block_walk3_kernel(const __
   const int n_rays = p.lcnt[0];
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= n_rays) return;
-  const RayRec r = p.rays[idx];
+  const RayView r = load_ray(p, idx);
   long long R[3], AD[3];
   int bb[3], st[3], kk[3];
 #pragma unroll
@@ -659,7 +711,7 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_kernel(const __grid_cons
   long long w_fx = 0;
   float w = 0.0f;
   if (have) {
-    const RayRec r = p.rays[idx];
+    const RayView r = load_ray(p, idx);
     long long R[3], AD[3];
     int va[3], st[3], kk[3];
     nblk = 1;
@@ -842,43 +894,7 @@ __device__ __forceinline__ unsigned run_len(unsigned above, int lane) {
 // exactly afterwards, so no IEEE slow path is needed).
 __device__ __forceinline__ float rcp_approx(float x) { float y; asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
 
-#if CVX_TIGHT
-__device__ __forceinline__ float rsqrt_approx(float x) { float y; asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
-// Exact free prefix of a ray from a crossing count (checked in the walk's own integer arithmetic).
-// Take a segment fraction f = F / 2^20; the crossings strictly before f are C_a = #boundaries of axis a
-// strictly between A_a and X_a = A_a + f D_a, and the walk takes exactly those first (crossing-time
-// order), so after i_f = sum C_a steps its sdf is S_f = S - sum U_a C_a exactly.  S never grows, so if
-// S_f >= thr every voxel 0..i_f is clamped free space: returns i_f + 1 (<= n - 1), else 0.  f only
-// needs to be a good guess: the sdf falls by ~1 m per metre of segment; back off one voxel diagonal
-// (sum U_a) for the voxel centres.
-__device__ __forceinline__ int tight_free_prefix(const RayRec* rp, long long S, long long thr, int n, float s, int q) {
-  const RayRec& r = *rp;
-  const long long U[3] = {r.U[0], r.U[1], r.U[2]};
-  const long long su = U[0] + U[1] + U[2];
-  const float d0 = (float)(r.B[0] - r.A[0]), d1 = (float)(r.B[1] - r.A[1]), d2 = (float)(r.B[2] - r.A[2]);
-  // segment length in sdf units: |B - A| 2^-16 voxels * s * 2^(q + kSdfF) (a guess: fp32 is plenty)
-  const float l2 = d0 * d0 + d1 * d1 + d2 * d2;
-  const float seg = l2 * rsqrt_approx(l2) * (s * exp2f((float)(q + kSdfF - 16)));
-  const float f = ((float)(S - thr - su - (su >> 4)) - 64.0f) * rcp_approx(seg);
-  if (!(f > 0.0f) || !(seg > 0.0f)) return 0;
-  const long long F = (long long)fminf(floorf(f * 1048576.0f), 1048575.0f);
-  int i_f = 0;
-  long long Sf = S;
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    const long long D = r.B[a] - r.A[a];
-    const long long va = r.A[a] >> 16;
-    const long long X = (r.A[a] << 20) + F * D;         // 2^-36 voxel units, exact
-    long long c = 0;
-    if (D > 0) c = (-((-X) >> 36)) - 1 - va;
-    else if (D < 0) c = va - (X >> 36);
-    c = c < 0 ? 0 : c;
-    i_f += (int)c;
-    Sf -= U[a] * c;
-  }
-  return (Sf >= thr && i_f + 1 <= n - 1) ? i_f + 1 : 0;
-}
-#endif
+
 
 // Constant-weight walk with the voxel address carried incrementally (same decisions as walk_kernel
 // <true, true, k32, kColor>; see there for O4/O5).  Per step only the stepped axis' crossing count,
@@ -908,9 +924,8 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
   int n = 0, nblk = 0, off = -1;
   unsigned rgb = 0, cexp = 0, addr = 0;
   int v0 = 0, v1 = 0, v2 = 0;
-  int mtight = 0;
   if (have) {
-    const RayRec r = p.rays[idx];
+    const RayView r = load_ray(p, idx);
     long long R[3], AD[3];
     int va[3], vb[3], st[3], kk[3];
     nblk = 1;
@@ -945,13 +960,6 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
     n = r.n_vox;
     off = r.list_off;
     rgb = r.rgb;
-#if CVX_TIGHT
-    {
-      long long thr = (long long)(2 * p.tq) << kSdfF;
-      if (kColor) thr = max(thr, (1ll << (kSdfF - 1)) + ((long long)p.tq << kSdfF) + p.band);
-      mtight = tight_free_prefix(p.rays + idx, S, thr, n, p.s, p.q);
-    }
-#endif
   }
   const int maxn = (int)__reduce_max_sync(0xffffffffu, (unsigned)n);
   const int* list = off >= 0 ? p.slots + off : nullptr;
@@ -1056,7 +1064,6 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
       while (m < n - 1 && (m + 1) * umax <= num) ++m;
       mfree = (int)m;
     }
-    mfree = max(mfree, mtight);
   }
   const int mw = (int)__reduce_min_sync(0xffffffffu, (unsigned)mfree);
   // General band step (TSDF + Color: colour sums need the per-lane band test; and CVX_BAND2 = 0): finished
@@ -1465,6 +1472,10 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
   const long long cap_rays = (long long)per * n_per_frame;
   for (int b = 0; b < 2; ++b) {
     cudaError_t e = grow(&sm->buf[b].rays, &sm->buf[b].ray_cap, cap_rays, sizeof(RayRec));
+    if (e == cudaSuccess && rgb)
+      e = grow(reinterpret_cast<void**>(&sm->buf[b].rgbs), &sm->buf[b].rgbs_cap, cap_rays, sizeof(unsigned));
+    if (e == cudaSuccess && sm->cfg.weighting != 0)
+      e = grow(reinterpret_cast<void**>(&sm->buf[b].ws), &sm->buf[b].ws_cap, cap_rays, sizeof(float));
     if (e == cudaSuccess) e = grow(reinterpret_cast<void**>(&sm->buf[b].slot_lists), &sm->buf[b].slot_cap,
                                    cap_rays * kSlotsPerRay + 1024, sizeof(int));
     if (e == cudaSuccess && host_data)
@@ -1555,9 +1566,9 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     pp.list_cap = (int)std::min<long long>(std::min<long long>(B.slot_cap - 1, sm->list_cap_limit), 0x7fffffffll);
     pp.trig = trig;
     pp.rgb = rgb ? rgb + (long long)f0 * n_per_frame * 3 : nullptr;
+    pp.rgbs = rgb ? B.rgbs : nullptr;
+    pp.ws = sm->cfg.weighting != 0 ? B.ws : nullptr;
     pp.count_vox = 1;
-    pp.frame_tag = 0;
-    pp.frame_base = 0;
     {
       ProfScope ps_(sm, "ray_prepare", side);
       prepare_kernel<<<blocks, 256, 0, side>>>(pp);
@@ -1571,6 +1582,7 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     wp.q = q;
     wp.band = std::llround(std::ldexp(sm->cfg.truncation, q + kSdfF));
     wp.birth = nullptr;
+    wp.frame_T = B.frame_T; wp.rgbs = pp.rgbs; wp.ws = pp.ws; wp.frame_base = 0;
     const bool cw = cw_ok && total <= launch_rays;
     // constant weights, no colour, no block-count trigger: ALLOCATE runs inside the update walk
     const bool fuse = sm->fuse_alloc && cw && sm->aggregate && sm->walk_cw && !rgb && !trig;
@@ -1675,9 +1687,9 @@ cudaError_t launch_integrate_projective(cvx_submap* sm, const float* depth, int6
       pp.list_cap = (int)std::min<long long>(B.slot_cap - 1, 0x7fffffffll);
       pp.trig = nullptr;
       pp.rgb = nullptr;
+      pp.rgbs = nullptr;
+      pp.ws = nullptr;
       pp.count_vox = 0;   // voxel_updates counts the projective updates instead
-      pp.frame_tag = 1;
-      pp.frame_base = f0;
       {
         ProfScope ps_(sm, "ray_prepare", st);
         prepare_kernel<<<blocks, 256, 0, st>>>(pp);
@@ -1690,6 +1702,7 @@ cudaError_t launch_integrate_projective(cvx_submap* sm, const float* depth, int6
       wp.q = q;
       wp.band = 0;
       wp.birth = sm->proj_birth;
+      wp.frame_T = B.frame_T; wp.rgbs = nullptr; wp.ws = nullptr; wp.frame_base = f0;   // birth = f0 + frame
       {
         ProfScope ps_(sm, "block_walk_allocate", st);
         if (k32) block_walk2_kernel<true, true><<<blocks, 256, 0, st>>>(wp);

@@ -53,6 +53,10 @@ struct cvx_submap {
     double* frame_T = nullptr;  // device [kMaxBatch][16]: R_SC, t_SC, q(t_SC), flag per frame
     void* rays = nullptr;       // device RayRec [ray_cap]
     int64_t ray_cap = 0;
+    unsigned* rgbs = nullptr;   // device per-ray colour (TSDF + Color only)
+    int64_t rgbs_cap = 0;
+    float* ws = nullptr;        // device per-ray weight (weighting != 0 only)
+    int64_t ws_cap = 0;
     int* slot_lists = nullptr;  // device block-slot lists of the rays of one launch
     int64_t slot_cap = 0;
     int* lcnt = nullptr;        // device {n_rays, n_slots, -, -} of the launch using this buffer
