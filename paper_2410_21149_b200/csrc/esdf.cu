@@ -666,6 +666,9 @@ __global__ void inc_compact(const __grid_constant__ IncParams p) {
 // Window: voxels [8 b - r, 8 b + 8 + r) per axis (W = 8 + 2 r <= 56 so an x-row is one u64).  Distances
 // are exact below C = (r + 1)^2 and >= C otherwise (a saturated row distance r + 1 is <= the true one,
 // and r >= d_max / s makes every value >= C clamp to d_max).
+#ifndef CVX_INC_CTAS
+#define CVX_INC_CTAS 16
+#endif
 __global__ void __launch_bounds__(256) inc_window(const __grid_constant__ IncParams p) {
   extern __shared__ __align__(1024) unsigned char dsmem[];
   unsigned char* smem = dsmem;
@@ -954,7 +957,7 @@ cudaError_t launch_update_esdf(cvx_submap* sm, int n_blocks, const int lo[3], co
   cudaFuncSetAttribute(inc_window, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   {
     ProfScope ps_(sm, "inc_window", st);
-    inc_window<<<148 * 4, 256, smem, st>>>(ip);
+    inc_window<<<148 * CVX_INC_CTAS, 256, smem, st>>>(ip);
   }
   cudaMemcpyAsync(sm->inc.cnt_host, sm->inc.cnt, 4, cudaMemcpyDeviceToHost, st);
   if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
