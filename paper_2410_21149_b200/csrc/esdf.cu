@@ -610,27 +610,36 @@ __device__ __forceinline__ int grid_slot(const IncParams& p, int bx, int by, int
 }
 
 // one warp per 32 voxels (= one plane word of one block)
+// one warp per 4 plane words (128 consecutive voxels of one block) per step: the 4 loads of a lane are
+// issued before any is classified
 __global__ void inc_classify(const __grid_constant__ IncParams p) {
-  const long long n = (long long)p.nb * kBlockVox;
+  const long long nw = (long long)p.nb * 16;                     // plane words
   const int lane = threadIdx.x & 31;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i - lane < n; i += (long long)gridDim.x * blockDim.x) {
-    const bool in = i < n;
-    bool obs = false, neg = false, site = false;
-    if (in) classify_voxel(reinterpret_cast<const longlong2*>(p.sums)[i], p.site_thr, obs, neg, site);
-    const unsigned bo = __ballot_sync(0xffffffffu, obs), bn = __ballot_sync(0xffffffffu, neg),
-                   bs = __ballot_sync(0xffffffffu, site);
-    if (lane == 0 && in) {
-      const int slot = (int)(i >> 9), w = (int)((i & 511) >> 5);
-      unsigned* c = p.cur + (long long)slot * kPlaneWords;
-      c[w] = bo; c[16 + w] = bn; c[32 + w] = bs;
-      unsigned char fl = 0;
-      if (slot >= p.nb_prev) fl = (bs ? 1 : 0) | 2;    // new block: its sites are sources, it is written
-      else {
-        const unsigned* q = p.prev + (long long)slot * kPlaneWords;
-        if (q[32 + w] != bs) fl = 3;
-        else if (q[w] != bo || q[16 + w] != bn) fl = 2;
+  const long long warp0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long w0 = warp0 * 4; w0 < nw; w0 += nwarps * 4) {   // nb * 16 is a multiple of 4
+    longlong2 sw[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) sw[u] = reinterpret_cast<const longlong2*>(p.sums)[(w0 + u) * 32 + lane];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      bool obs, neg, site;
+      classify_voxel(sw[u], p.site_thr, obs, neg, site);
+      const unsigned bo = __ballot_sync(0xffffffffu, obs), bn = __ballot_sync(0xffffffffu, neg),
+                     bs = __ballot_sync(0xffffffffu, site);
+      if (lane == u) {
+        const int slot = (int)((w0 + u) >> 4), w = (int)((w0 + u) & 15);
+        unsigned* c = p.cur + (long long)slot * kPlaneWords;
+        c[w] = bo; c[16 + w] = bn; c[32 + w] = bs;
+        unsigned char fl = 0;
+        if (slot >= p.nb_prev) fl = (bs ? 1 : 0) | 2;    // new block: its sites are sources, it is written
+        else {
+          const unsigned* q = p.prev + (long long)slot * kPlaneWords;
+          if (q[32 + w] != bs) fl = 3;
+          else if (q[w] != bo || q[16 + w] != bn) fl = 2;
+        }
+        if (fl) atomicOr(reinterpret_cast<unsigned*>(p.flags + (slot & ~3)), (unsigned)fl << (8 * (slot & 3)));
       }
-      if (fl) atomicOr(reinterpret_cast<unsigned*>(p.flags + (slot & ~3)), (unsigned)fl << (8 * (slot & 3)));
     }
   }
 }
@@ -678,6 +687,7 @@ __global__ void __launch_bounds__(256) inc_window(const __grid_constant__ IncPar
   unsigned char* g1 = reinterpret_cast<unsigned char*>(rowm + (size_t)W * W);        // [W z][W y][8 x]
   unsigned short* g2 = reinterpret_cast<unsigned short*>(g1 + (size_t)W * W * 8);    // [W z][8 y][8 x]
   __shared__ int s_slot;
+  __shared__ int s_nbs[343];      // slot of every block of the (2 Rb + 1)^3 neighbourhood (Rb <= 3)
   const int nq = *(volatile const int*)p.cnt;
   const int off = 8 * p.rb - r;   // window origin inside the neighbourhood (voxels)
   const unsigned C = (unsigned)((r + 1) * (r + 1));
@@ -687,15 +697,19 @@ __global__ void __launch_bounds__(256) inc_window(const __grid_constant__ IncPar
     __syncthreads();
     const int slot = s_slot;
     const int4 c = p.coords[slot];
+    for (int o = threadIdx.x; o < k3; o += blockDim.x)
+      s_nbs[o] = grid_slot(p, c.x + o % k - p.rb, c.y + (o / k) % k - p.rb, c.z + o / (k * k) - p.rb);
+    __syncthreads();
     for (int i = threadIdx.x; i < k3 * 16; i += blockDim.x) {
-      const int o = i >> 4, w = i & 15;
-      const int ns = grid_slot(p, c.x + o % k - p.rb, c.y + (o / k) % k - p.rb, c.z + o / (k * k) - p.rb);
-      nbp[i] = ns >= 0 ? p.cur[(long long)ns * kPlaneWords + 32 + w] : 0u;
+      const int ns = s_nbs[i >> 4];
+      nbp[i] = ns >= 0 ? p.cur[(long long)ns * kPlaneWords + 32 + (i & 15)] : 0u;
     }
     __syncthreads();
-    // x-row bit masks of the window
-    for (int i = threadIdx.x; i < W * W; i += blockDim.x) {
-      const int yw = i % W, zw = i / W;
+    // x-row bit masks of the window (row index i = zw W + yw kept incrementally: no divisions)
+    const int dz_step = (int)blockDim.x / W, dy_step = (int)blockDim.x % W;
+    int yw = (int)threadIdx.x % W, zw = (int)threadIdx.x / W;
+    for (int i = threadIdx.x; i < W * W; i += blockDim.x, yw += dy_step, zw += dz_step) {
+      if (yw >= W) { yw -= W; ++zw; }
       const int yn = yw + off, zn = zw + off;
       const int by = yn >> 3, bz = zn >> 3, row = (yn & 7) + 8 * (zn & 7);
       unsigned long long bits = 0;
