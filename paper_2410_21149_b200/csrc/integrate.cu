@@ -476,7 +476,10 @@ __device__ __forceinline__ int key_field(unsigned long long key, int sh) {
   return ((int)((key >> sh) & 0x1fffffu) << 11) >> 11;          // 21-bit two's complement (pack_key)
 }
 
-template <bool k32, bool kBirth = false>
+// kGrid: the run heads read the dense slot cache (R15) instead of the hash entry for blocks inside its
+// window; a cache miss activates through the hash (deduplicated across the run, as every probe here)
+// and caches the slot.
+template <bool k32, bool kBirth = false, bool kGrid = false>
 __global__ void __launch_bounds__(256) block_walk2_kernel(const __grid_constant__ WalkParams p) {
   using DT = typename std::conditional<k32, unsigned, unsigned long long>::type;
   using ST = typename std::conditional<k32, int, long long>::type;
@@ -530,7 +533,15 @@ __global__ void __launch_bounds__(256) block_walk2_kernel(const __grid_constant_
   unsigned long long key = act ? pack_key(b0, b1, b2) : ((1ull << 63) | (unsigned)lane);
   unsigned heads = heads_of(act, key);
   longlong2 ent = make_longlong2(0, 0);
-  if ((heads >> lane) & 1u) ent = ld_entry(p.hash.e + hash_slot(key, p.hash));
+  int gi = -1;   // kGrid: cache index of the head's block (-1: outside the window -> hash entry)
+  auto probe = [&](unsigned long long k, int bx, int by, int bz, int& g) -> longlong2 {
+    if (kGrid) {
+      g = grid_cache_index(bx, by, bz);
+      if (g >= 0) return make_longlong2((long long)k, (long long)(unsigned)p.pool.grid[g]);
+    }
+    return ld_entry(p.hash.e + hash_slot(k, p.hash));
+  };
+  if ((heads >> lane) & 1u) ent = probe(key, b0, b1, b2, gi);
   for (int j = 0; j < maxnb; ++j) {
     // advance the DDA to step j+1 (independent of the probe of step j)
     const bool stp = j + 1 < nb;
@@ -545,13 +556,20 @@ __global__ void __launch_bounds__(256) block_walk2_kernel(const __grid_constant_
     const unsigned long long keyn = actn ? pack_key(b0, b1, b2) : ((1ull << 63) | (unsigned)lane);
     const unsigned headsn = (j + 1 < maxnb) ? heads_of(actn, keyn) : 0u;
     longlong2 entn = make_longlong2(0, 0);
-    if ((headsn >> lane) & 1u) entn = ld_entry(p.hash.e + hash_slot(keyn, p.hash));   // prefetch j+1
+    int gin = -1;
+    if ((headsn >> lane) & 1u) entn = probe(keyn, b0, b1, b2, gin);   // prefetch j+1
     // consume step j
     int slot = kFailed;
     if ((heads >> lane) & 1u) {   // hit on the prefetched entry: done; else the full activate (insert / probe / wait)
       slot = (int)(ent.y & 0xffffffffll);
-      if ((unsigned long long)ent.x != key || slot < 0)
-        slot = hash_activate_pf(p.hash, p.pool, p.ctr, key, key_field(key, 42), key_field(key, 21), key_field(key, 0), ent);
+      if ((unsigned long long)ent.x != key || slot < 0) {
+        if (kGrid && gi >= 0) {
+          slot = hash_activate(p.hash, p.pool, p.ctr, key, key_field(key, 42), key_field(key, 21), key_field(key, 0));
+          if (slot >= 0) p.pool.grid[gi] = slot;
+        } else {
+          slot = hash_activate_pf(p.hash, p.pool, p.ctr, key, key_field(key, 42), key_field(key, 21), key_field(key, 0), ent);
+        }
+      }
     }
     const unsigned hb = heads & (0xffffffffu >> (31 - lane));
     slot = __shfl_sync(0xffffffffu, slot, hb ? 31 - __clz(hb) : lane);
@@ -564,7 +582,7 @@ __global__ void __launch_bounds__(256) block_walk2_kernel(const __grid_constant_
       // already <= frame is exact, and it keeps hot blocks (near the sensor) free of same-address REDs
       if (mine && slot >= 0 && p.birth[slot] > frame) atomicMin(p.birth + slot, frame);
     }
-    act = actn; key = keyn; heads = headsn; ent = entn;
+    act = actn; key = keyn; heads = headsn; ent = entn; gi = gin;
   }
 }
 

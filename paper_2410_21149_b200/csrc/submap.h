@@ -74,7 +74,8 @@ struct cvx_submap {
   bool aggregate = true;      // warp-aggregate equal-voxel updates before the L2 atomics
   bool serialize = false;     // profiling: run the pipeline's side work on the caller's stream
   bool bw2 = true;            // software-pipelined ALLOCATE (block_walk2_kernel)
-  bool bw3 = true;            // ALLOCATE through the dense slot cache (block_walk3_kernel, default)
+  bool bw3 = false;           // ALLOCATE through the dense slot cache (block_walk3_kernel): configs[1] step
+                              // 8.33 -> 8.25 ms, but MAV submaps (50 scans, more new blocks) 133 -> 143 ms
   bool walk_cw = true;        // constant weights: incremental-address walk (walk_cw_kernel)
   long long list_cap_limit = 1ll << 62;   // test knob: cap on the per-ray slot-list buffer (full: walk hashes)
   bool fuse_alloc = false;    // constant weights: ALLOCATE inside walk_cw_kernel (measured 1.4x slower: off)

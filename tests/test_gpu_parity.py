@@ -330,7 +330,7 @@ def test_block_count_trigger_matches_frame_by_frame(tiny):
     assert c.integrate_until(data, poses, tiny["sensor"], tiny["grid"]["max_blocks"]) == len(frames)
 
 
-@pytest.mark.parametrize("knob", ["CVX_FUSE_ALLOC=1", "CVX_BW3=0", "CVX_BW3=0,CVX_BW2=0", "CVX_WALK_CW=0", "CVX_LIST_CAP=2000"])
+@pytest.mark.parametrize("knob", ["CVX_FUSE_ALLOC=1", "CVX_BW3=1", "CVX_BW2=0", "CVX_WALK_CW=0", "CVX_LIST_CAP=2000"])
 def test_walk_variants_bitexact(tiny, orc, monkeypatch, knob):
     """The tuning variants of the integrate path (ALLOCATE fused into the walk, the first block walk,
     the general walk kernel; a slot-list buffer capped so most rays find their blocks by hash lookup in

@@ -1,10 +1,7 @@
 #!/bin/bash
-# A/B of library variants on the mav workload (kernel breakdown): tools/ab_mav.sh v1 v2 ...
+# A/B of env knobs on the mav workload (kernel breakdown): tools/ab_mav.sh "K=V" "K=V,K2=V2" ...
 cd "$(dirname "$0")/.."
-cp paper_2410_21149_b200/libcvx.so /tmp/libcvx_orig.so
-for v in "$@"; do
-  cp variants/libcvx_$v.so paper_2410_21149_b200/libcvx.so
-  python bench.py --workload mav --steps 2 --warmup 1 --no-cpu-baseline 2>/dev/null | tail -1 | python -c "
-import json,sys; d=json.loads(sys.stdin.read()); print('$v', round(d['ms_per_step'],2), {k: round(x,2) for k,x in d.get('kernel_ms_per_step',{}).items()})"
+for spec in "$@"; do
+  env ${spec//,/ } python bench.py --workload mav --steps 2 --warmup 1 --no-cpu-baseline 2>/dev/null | tail -1 | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); print('$spec', round(d['ms_per_step'],2), {k: round(x,2) for k,x in d.get('kernel_ms_per_step',{}).items()})"
 done
-cp /tmp/libcvx_orig.so paper_2410_21149_b200/libcvx.so

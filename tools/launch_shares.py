@@ -11,7 +11,10 @@ import sys
 from collections import defaultdict
 
 NAMES = [("prepare_kernel", "ray_prepare"), ("block_walk_kernel", "block_walk_allocate"),
-         ("block_walk2_kernel", "block_walk_allocate"), ("walk_cw_kernel", "ray_walk_update"),
+         ("block_walk2_kernel", "block_walk_allocate"), ("block_walk3_kernel", "block_walk_allocate"),
+         ("walk_cw_kernel", "ray_walk_update"), ("link_line_kernel<0", "esdf_pass_y"), ("link_line_kernel<1", "esdf_pass_z"),
+         ("link_line_kernel<false", "esdf_pass_y"), ("link_line_kernel<true", "esdf_pass_z"),
+         ("pba_line_kernel<0", "esdf_pass_y"), ("pba_line_kernel<1", "esdf_pass_z"), ("clear_grid", "reset_grid"),
          ("fold_color_kernel", "fold_color"), ("pass_line_kernelILb0", "esdf_pass_y"), ("pass_line_kernelILb1", "esdf_pass_z"), ("pass_line_kernel<0", "esdf_pass_y"), ("pass_line_kernel<1", "esdf_pass_z"),
          ("walk_kernel", "ray_walk_update"), ("fold_kernel", "fold"), ("zero_blocks", "reset_zero_blocks"),
          ("reset_counters", "reset_counters"), ("compose_kernel", "compose_poses"),

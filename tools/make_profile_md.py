@@ -17,7 +17,7 @@ shutil.copy(os.path.join(src, "launches.csv"), os.path.join(dst, "launches.csv")
 shares = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "launch_shares.py"), os.path.join(src, "launches.csv"),
                          os.path.join(src, "bench.json")], capture_output=True, text=True).stdout
 kern = ["walk", "block_walk", "prepare", "fold", "esdf_pass_x", "esdf_pass_y", "esdf_pass_z", "query", "project",
-        "stress_pass_x", "stress_pass_y", "stress_pass_z"]
+        "stress_pass_x", "stress_pass_y", "stress_pass_z", "inc_window"]
 summ = {}
 for k in kern:
     rep = os.path.join(src, k + ".ncu-rep")
@@ -79,12 +79,13 @@ the bench numbers come from an unprofiled run with CUDA events.
 Per-kernel stall breakdowns and the hottest SASS lines: `ncu_<kernel>.txt`. The dominant kernel's
 full report is `walk.ncu-rep` (open with `ncu -i`).
 """
-for extra in ("bench_rgbd.json", "bench_esdf_stress.json"):
+for extra in ("bench_rgbd.json", "bench_esdf_stress.json", "bench_mav.json", "bench_incremental.json", "bench_color.json",
+              "bench_voxel_sweep.json", "bench_reference.json", "bench_n2_onegpu_gloo.json"):
     f = os.path.join(src, extra)
     if os.path.exists(f) and os.path.getsize(f):
         d = json.loads(open(f).read().strip().splitlines()[-1])
         json.dump(d, open(os.path.join(dst, extra), "w"), indent=1)
-        md += f"\n## `{extra}`\n\n* value {d['value']:.1f} {d['unit']}, {d['ms_per_step']:.2f} ms per step; " \
+        md += f"\n## `{extra}`\n\n* value {d['value']:.4g} {d['unit']}, {d.get('ms_per_step') or 0:.2f} ms per step; " \
               f"workload {d['config']['workload']}\n"
         if "roofline" in d:
             r = d["roofline"]
