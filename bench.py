@@ -351,8 +351,9 @@ def run_mav(args, world, rank, local):
     if pg is not None:
         pg.barrier()
     torch.cuda.synchronize()
+    mav_prof = os.environ.get("CVX_BENCH_MAV_PROFILE", "0") == "1"   # per-kernel events perturb the pipeline
     for b_ in builders:
-        b_.profile(True)
+        b_.profile(mav_prof)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         e0.record(stream)
@@ -364,8 +365,9 @@ def run_mav(args, world, rank, local):
     ms = e0.elapsed_time(e1) / args.steps
     kms = {}
     for b_ in builders:
-        for k_, v_ in b_.profile_report().items():
-            kms[k_] = kms.get(k_, 0.0) + v_["ms"] / args.steps
+        if mav_prof:
+            for k_, v_ in b_.profile_report().items():
+                kms[k_] = kms.get(k_, 0.0) + v_["ms"] / args.steps
         b_.profile(False)
     if pg is not None:
         t = torch.tensor([ms], device=dev, dtype=torch.float64)

@@ -254,14 +254,16 @@ cvx_status cvx_export_blocks(const cvx_submap* submap, int32_t* bxyz, float* D, 
 cvx_status cvx_import_tsdf_blocks(cvx_submap* submap, const int32_t* bxyz, const float* D,
                                   const float* W, int64_t n_blocks, void* stream);
 
-/* Pack the finalized ESDF for the multi-GPU gather (synchronising): dst (device) receives a
+/* Pack the finalized ESDF for the multi-GPU gather (synchronises `stream`): dst (device) receives a
  * 256-byte header {u32 magic 'CVXE', i32 version 1, i64 n_blocks, f64 voxel_size, f64 T_world_submap[16],
  * zero padding} followed by n_blocks records {i32 bx, by, bz, slot; f32 E[512]} (2064 B each).
- * *used = bytes written.  Errors: CVX_E_STATE before finalize, CVX_E_CAPACITY if dst_bytes too small. */
+ * *used = bytes written.  dst = NULL: only *used = the bytes needed (ordered after `stream`'s work, unlike
+ * cvx_packed_size, which synchronises the whole device).  Errors: CVX_E_STATE before finalize,
+ * CVX_E_CAPACITY if dst_bytes too small. */
 cvx_status cvx_pack_esdf(const cvx_submap* submap, void* dst, int64_t dst_bytes, int64_t* used,
                          void* stream);
 
-/* Bytes cvx_pack_esdf needs (synchronising). */
+/* Bytes cvx_pack_esdf needs (synchronises the whole device; see cvx_pack_esdf with dst = NULL). */
 cvx_status cvx_packed_size(const cvx_submap* submap, int64_t* bytes);
 
 /* Gathered submap ESDFs (SURVEY §8 e / f4; registration queries "between every overlapped

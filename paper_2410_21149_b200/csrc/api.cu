@@ -559,7 +559,7 @@ cvx_status cvx_packed_size(const cvx_submap* sm, int64_t* bytes) {
 
 cvx_status cvx_pack_esdf(const cvx_submap* sm, void* dst, int64_t dst_bytes, int64_t* used, void* stream) {
   g_last_error.clear();
-  if (!sm || !dst || !used) return fail(CVX_E_INVALID, "NULL argument");
+  if (!sm || !used) return fail(CVX_E_INVALID, "NULL argument");
   if (!sm->finalized) return fail(CVX_E_STATE, "pack before finalize_esdf");
   DeviceGuard g(sm->device);
   cudaStream_t st = (cudaStream_t)stream;
@@ -569,6 +569,7 @@ cvx_status cvx_pack_esdf(const cvx_submap* sm, void* dst, int64_t dst_bytes, int
   const int nb = c.n_blocks < sm->pool.max_blocks ? c.n_blocks : sm->pool.max_blocks;
   const int64_t need = 256 + (int64_t)nb * (16 + 4 * cvx::kBlockVox);
   *used = need;
+  if (!dst) return CVX_OK;   // size query, ordered on `stream` only
   if (dst_bytes < need) return fail(CVX_E_CAPACITY, "pack buffer too small");
   unsigned char hdr[256];
   std::memset(hdr, 0, sizeof(hdr));

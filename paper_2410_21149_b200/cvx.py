@@ -381,7 +381,9 @@ class Submap:
         return int(n.value)
 
     def pack(self, dst: torch.Tensor | None = None) -> torch.Tensor:
-        need = self.packed_size()
+        used0 = C.c_int64()   # size query ordered on the current stream only (no device-wide sync)
+        _check(lib().cvx_pack_esdf(self._h, None, 0, C.byref(used0), self._stream()))
+        need = int(used0.value)
         if dst is None:
             dst = torch.empty(need, dtype=torch.uint8, device=torch.device("cuda", self.device))
         used = C.c_int64()
