@@ -795,7 +795,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="cvx", choices=["cvx", "reference"])
-    ap.add_argument("--batch", type=int, default=200, help="scans per integrate_batch call (the library splits them into equal launches of <= 2^22 rays)")
+    ap.add_argument("--batch", type=int, default=200, help="scans per integrate_batch call (the library splits them into equal launches of <= 2^24 - 1 rays and <= 200 frames: one launch for 200 OS1-64 scans)")
     ap.add_argument("--queries", type=int, default=1 << 20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
