@@ -1453,12 +1453,14 @@ static void set_divisors(PrepParams& pp, const cvx_sensor_model& sensor) {
   pp.r_pcols = sensor.width >= PC ? 1.0 / (double)(sensor.width / PC) : 0.0;
 }
 
-static cudaError_t grow(void** ptr, int64_t* cap, int64_t need, size_t elem) {
+// Grow-only scratch, stream-ordered (cudaMallocAsync / cudaFreeAsync on `st`): the caller
+// orders `st` after every earlier user of the buffer before growing it.
+static cudaError_t grow(void** ptr, int64_t* cap, int64_t need, size_t elem, cudaStream_t st) {
   if (*cap >= need) return cudaSuccess;
-  if (*ptr) cudaFree(*ptr);
+  if (*ptr) cudaFreeAsync(*ptr, st);
   *ptr = nullptr;
   *cap = 0;
-  cudaError_t e = cudaMalloc(ptr, elem * (size_t)need);
+  cudaError_t e = cudaMallocAsync(ptr, elem * (size_t)need, st);
   if (e == cudaSuccess) *cap = need;
   return e;
 }
@@ -1488,17 +1490,28 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
   }
   const int per = *std::max_element(plan.begin(), plan.end());
   const long long cap_rays = (long long)per * n_per_frame;
+  // scratch growth is stream-ordered on the side stream, after the walk that last read the buffer
+  const cudaStream_t gs = sm->serialize ? st : sm->side;
   for (int b = 0; b < 2; ++b) {
-    cudaError_t e = grow(&sm->buf[b].rays, &sm->buf[b].ray_cap, cap_rays, sizeof(RayRec));
+    const bool need_grow = sm->buf[b].ray_cap < cap_rays || sm->buf[b].slot_cap < cap_rays * kSlotsPerRay + 1024 ||
+                           (rgb && sm->buf[b].rgbs_cap < cap_rays) || (sm->cfg.weighting != 0 && sm->buf[b].ws_cap < cap_rays) ||
+                           (host_data && sm->buf[b].staging_cap < (long long)per * elems_per_frame);
+    if (need_grow) {
+      cudaEventRecord(sm->ev_entry, st);     // the caller's earlier work on the buffers, then their last walk
+      cudaStreamWaitEvent(gs, sm->ev_entry, 0);
+      cudaStreamWaitEvent(gs, sm->ev_free[b], 0);
+      if (sm->copy) cudaStreamWaitEvent(gs, sm->ev_stage_free[b], 0);
+    }
+    cudaError_t e = grow(&sm->buf[b].rays, &sm->buf[b].ray_cap, cap_rays, sizeof(RayRec), gs);
     if (e == cudaSuccess && rgb)
-      e = grow(reinterpret_cast<void**>(&sm->buf[b].rgbs), &sm->buf[b].rgbs_cap, cap_rays, sizeof(unsigned));
+      e = grow(reinterpret_cast<void**>(&sm->buf[b].rgbs), &sm->buf[b].rgbs_cap, cap_rays, sizeof(unsigned), gs);
     if (e == cudaSuccess && sm->cfg.weighting != 0)
-      e = grow(reinterpret_cast<void**>(&sm->buf[b].ws), &sm->buf[b].ws_cap, cap_rays, sizeof(float));
+      e = grow(reinterpret_cast<void**>(&sm->buf[b].ws), &sm->buf[b].ws_cap, cap_rays, sizeof(float), gs);
     if (e == cudaSuccess) e = grow(reinterpret_cast<void**>(&sm->buf[b].slot_lists), &sm->buf[b].slot_cap,
-                                   cap_rays * kSlotsPerRay + 1024, sizeof(int));
+                                   cap_rays * kSlotsPerRay + 1024, sizeof(int), gs);
     if (e == cudaSuccess && host_data)
       e = grow(reinterpret_cast<void**>(&sm->buf[b].staging), &sm->buf[b].staging_cap, (long long)per * elems_per_frame,
-               sizeof(float));
+               sizeof(float), gs);
     if (e != cudaSuccess) return e;
   }
   const int q = packed_q(sm->cfg.truncation);
@@ -1659,12 +1672,13 @@ cudaError_t launch_integrate_projective(cvx_submap* sm, const float* depth, int6
   if (n_per_frame <= 0 || n_frames <= 0) return cudaSuccess;
   const int lim = (int)std::max<long long>(1, std::min<long long>(kMaxBatch, kLaunchRays / n_per_frame));
   cvx_submap::Buf& B = sm->buf[0];
-  cudaError_t e = grow(&B.rays, &B.ray_cap, (long long)lim * n_per_frame, sizeof(RayRec));
+  cudaStreamWaitEvent(st, sm->ev_free[0], 0);   // the walk that last read buffer 0 (stream-ordered growth)
+  cudaError_t e = grow(&B.rays, &B.ray_cap, (long long)lim * n_per_frame, sizeof(RayRec), st);
   if (e == cudaSuccess)
     e = grow(reinterpret_cast<void**>(&B.slot_lists), &B.slot_cap, (long long)lim * n_per_frame * kSlotsPerRay + 1024,
-             sizeof(int));
+             sizeof(int), st);
   if (e == cudaSuccess && !sm->proj_birth) {
-    e = cudaMalloc(&sm->proj_birth, sizeof(int) * ((size_t)sm->pool.max_blocks + 1));
+    e = cudaMallocAsync(reinterpret_cast<void**>(&sm->proj_birth), sizeof(int) * ((size_t)sm->pool.max_blocks + 1), st);
     if (e == cudaSuccess) sm->proj_start = sm->proj_birth + sm->pool.max_blocks;
   }
   if (e != cudaSuccess) return e;

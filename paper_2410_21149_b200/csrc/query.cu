@@ -119,10 +119,10 @@ cudaError_t launch_import(cvx_submap* sm, const int32_t* bxyz, const float* D, c
   // caller's stream after any integrate work on it, so the buffer is free
   cvx_submap::Buf& B = sm->buf[0];
   cudaStreamWaitEvent(st, sm->ev_free[0], 0);
-  if (B.slot_cap < n) {
-    if (B.slot_lists) cudaFree(B.slot_lists);
+  if (B.slot_cap < n) {   // stream-ordered growth (st already waits for buffer 0's last walk)
+    if (B.slot_lists) cudaFreeAsync(B.slot_lists, st);
     B.slot_lists = nullptr; B.slot_cap = 0;
-    cudaError_t e = cudaMalloc(&B.slot_lists, sizeof(int) * (size_t)n);
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&B.slot_lists), sizeof(int) * (size_t)n, st);
     if (e != cudaSuccess) return e;
     B.slot_cap = n;
   }
