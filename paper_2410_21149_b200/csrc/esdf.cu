@@ -67,15 +67,22 @@ __global__ void block_grid_kernel(const Counters* ctr, const int4* coords, int m
   }
 }
 
-// O10 / R4: the site test on D rounded to fp32 (the value cvx_export_blocks returns), compared in fp64
+// O10 / R4: the site test on D rounded to fp32 (the value cvx_export_blocks returns), compared in fp64.
+// Without the division where it cannot matter: with W > 0, sign(D) = sign(sum w d) (a non-zero quotient
+// never rounds to zero in fp32 at these magnitudes), and |D| <= thr is decided by |sum w d| vs thr W
+// unless they are within 2^-20 of each other (fp32 rounding of D and the fp64 products move them by less
+// than 2^-23), where the exact rounded quotient decides.
 __device__ __forceinline__ void classify_voxel(longlong2 sw, double thr, bool& obs, bool& neg, bool& site) {
   obs = sw.y > 0;
-  neg = false;
+  neg = obs && sw.x < 0;
   site = false;
   if (obs) {
-    const float D = (float)((double)sw.x / (double)sw.y);
-    neg = D < 0.0f;
-    site = fabs((double)D) <= thr;
+    const double a = fabs((double)sw.x), b = thr * (double)sw.y;
+    if (a < b * (1.0 - 0x1p-20)) site = true;
+    else if (a <= b * (1.0 + 0x1p-20)) {
+      const float D = (float)((double)sw.x / (double)sw.y);
+      site = fabs((double)D) <= thr;
+    }
   }
 }
 
