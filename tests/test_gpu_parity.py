@@ -72,6 +72,24 @@ def test_lidar_subset_parity(orc):
     assert rep["blocks"] > 5000
 
 
+@pytest.mark.parametrize("isub,min_blocks", [(2, 5000), (7, 100)])   # outdoors; inside the building
+def test_mav_submap_parity(orc, isub, min_blocks):
+    """BASELINE.json configs[3]: one MAV submap (its own pose, the disaster-site scene) over 4 scans with
+    range weighting — TSDF parity and the stage-isolated exact ESDF on every voxel."""
+    base = synth.make_config("mav", frames=[])
+    sub = base["submaps"][isub]
+    ks = sub["frames"][:40:10]
+    cfg = synth.make_config("mav", frames=ks)
+    g = dict(cfg["grid"], weighting=1, max_blocks=1 << 16)
+    sm, _ = gpu_build(cfg, ks, grid=g, T_ws=sub["T_world_submap"], batch=True)
+    o, _ = oracle_build(cfg, ks, grid=g, T_ws=sub["T_world_submap"])
+    b, D, W, E = gpu_export_sorted(sm)
+    rep = assert_tsdf_parity((b, D, W, E), o.export())
+    assert rep["blocks"] > min_blocks
+    Eo, _ = orc.esdf(b, D.astype(np.float64), W.astype(np.float64), g["voxel_size"], g["site_threshold"])
+    assert_esdf_parity(E, Eo, W > 0)
+
+
 def test_rgbd_subset_parity(orc):
     cfg = synth.make_config("rgbd", frames=[0, 37])
     sm, _ = gpu_build(cfg, [0, 37], grid=dict(cfg["grid"], weighting=1), finalize=False)
