@@ -592,6 +592,152 @@ __global__ void __launch_bounds__(256) link_line_kernel(const __grid_constant__ 
   }
 }
 
+// Passes y / z, ring variant (default when every quantity fits 24 bits, see ring_fits): one thread per
+// line as above, but Meijster's stack is an explicit array per line in HBM ([line][k], contiguous per
+// thread) whose top kRing entries live in a shared-memory ring:
+//   * entries {f: 32, t: 16, s: 16} (site s, start t of its interval, f(s)); pops read the ring only
+//     (a pop below the ring's window refills it from the array: rare);
+//   * an entry is written to HBM only when a push displaces it from the ring (it has survived kRing
+//     later pushes), so entries popped while young never leave the SM;
+//   * the backward sweep takes the entries still in the ring, then the older ones from the array with
+//     cp.async kAhead entries ahead into their ring slots (no dependent load chain);
+//   * 32-bit arithmetic: with m^2 + max f < 2^24 every separator numerator is exact in fp32, and
+//     floor(num / den) = the fp32 reciprocal estimate corrected by the exact integer remainder.
+// Same outputs as link_line_kernel / pba_line_kernel (bit for bit: the envelope is unique and the
+// output is its value).
+constexpr int kRing = 16, kAhead = 12, kRingThreads = 128;
+
+__device__ __forceinline__ float rcp_approx32(float x) { float y; asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+
+__device__ __forceinline__ int floordiv24(int num, int den) {   // den in [2, 2^17], |num| < 2^24
+  int q = __float2int_rd((float)num * rcp_approx32((float)den));
+  int r = num - q * den;
+  while (r < 0) { --q; r += den; }
+  while (r >= den) { ++q; r -= den; }
+  return q;
+}
+
+template <bool kZ>
+__global__ void __launch_bounds__(kRingThreads, 8) ring_line_kernel(const __grid_constant__ LinkParams p) {
+  __shared__ unsigned long long ring[kRing][kRingThreads];
+  const long long nlines = kZ ? (long long)p.nx * p.ny : (long long)p.nx * p.nz;
+  const long long line = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (line >= nlines) return;
+  const int x = (int)(line % p.nx);
+  const int o2 = (int)(line / p.nx);      // pass y: z ; pass z: y
+  const int m = kZ ? p.nz : p.ny;
+  const long long stride = kZ ? (long long)p.nx * p.ny : (long long)p.nx;
+  const long long base = kZ ? (long long)o2 * p.nx + x : (long long)o2 * p.nx * p.ny + x;
+  if (kZ && !p.colmask[(long long)(o2 >> 3) * p.nbx + (x >> 3)]) return;   // no allocated voxel in this line
+  unsigned long long* const gst = static_cast<unsigned long long*>(p.meta) + line * m;
+  unsigned long long* const rg = &ring[0][threadIdx.x];   // ring slot j of this thread: rg[j * kRingThreads]
+  auto f_at = [&](int q) -> unsigned {    // kInf32 = no site in the line's slice
+    if (kZ) return static_cast<const unsigned*>(p.fin)[base + q * stride];
+    const unsigned v = static_cast<const unsigned short*>(p.fin)[base + q * stride];
+    return v == kNone16 ? kInf32 : v * v;
+  };
+  int k = -1, lo = 0;                      // stack [0, k]; indices < lo valid in gst, [lo, k] in the ring
+  int s_top = 0, t_top = 0;
+  unsigned f_top = 0;
+  for (int q0 = 0; q0 < m; q0 += 8) {
+    unsigned fv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) fv[u] = q0 + u < m ? f_at(q0 + u) : kInf32;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int q = q0 + u;
+      const unsigned fq = fv[u];
+      if (fq == kInf32) continue;
+      while (k >= 0) {
+        const int a = t_top - s_top, c = t_top - q;
+        if ((unsigned)(a * a) + f_top <= (unsigned)(c * c) + fq) break;   // q does not beat top at top's start
+        if (--k < 0) break;
+        if (k < lo) {                      // below the ring's window: refill kRing entries from the array
+          const int j0 = max(0, k - (kRing - 1));
+          for (int j = j0; j <= k; ++j) rg[(j & (kRing - 1)) * kRingThreads] = gst[j];
+          lo = j0;
+        }
+        const unsigned long long e = rg[(k & (kRing - 1)) * kRingThreads];
+        s_top = (int)(e & 0xffffu); t_top = (int)((e >> 16) & 0xffffu); f_top = (unsigned)(e >> 32);
+      }
+      int tq = 0;
+      if (k >= 0) {
+        const int sep = floordiv24(q * q - s_top * s_top + (int)fq - (int)f_top, 2 * (q - s_top));
+        if (sep + 1 >= m) continue;        // q never wins inside the line
+        tq = sep + 1;
+      }
+      ++k;
+      unsigned long long* slot = rg + (k & (kRing - 1)) * kRingThreads;
+      if (k - kRing >= lo) { gst[k - kRing] = *slot; lo = k - kRing + 1; }   // displaced: write back
+      *slot = ((unsigned long long)fq << 32) | ((unsigned)tq << 16) | (unsigned)q;
+      s_top = q; t_top = tq; f_top = fq;
+    }
+  }
+  // backward: the entries below the top in decreasing index order; entry j < lo is copied into its ring
+  // slot by cp.async kAhead pops before it is needed (one commit group per pop, empty when j >= lo)
+  auto issue = [&](int j) {
+    if (j >= 0 && j < lo) {
+      const unsigned sa = smem_addr(rg + (j & (kRing - 1)) * kRingThreads);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(sa), "l"(gst + j) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if (k >= 0) {
+#pragma unroll 1
+    for (int i = 1; i <= kAhead; ++i) issue(k - i);
+  }
+  for (int q0 = ((m - 1) >> 3) << 3; q0 >= 0; q0 -= 8) {
+    int slot = -1;
+    unsigned obsw = 0, negw = 0;   // pass z: bit u = observed / negative of position q0 + u (prefetched)
+    const int lb = (x & 7) + 8 * (o2 & 7);
+    if (kZ) {
+      slot = p.grid[((long long)(q0 >> 3) * p.nby + (o2 >> 3)) * p.nbx + (x >> 3)];
+      if (slot >= 0) {
+        const unsigned* pl = p.planes + (long long)slot * kPlaneWords + (lb >> 5);
+        unsigned ow[8], nw[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) { ow[u] = pl[2 * u]; nw[u] = pl[16 + 2 * u]; }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) { obsw |= ((ow[u] >> (lb & 31)) & 1u) << u; negw |= ((nw[u] >> (lb & 31)) & 1u) << u; }
+      }
+    }
+    const bool wy = !kZ && p.colmask[(long long)(q0 >> 3) * p.nbx + (x >> 3)];
+#pragma unroll
+    for (int u = 7; u >= 0; --u) {
+      const int q = q0 + u;
+      if (q >= m) continue;
+      unsigned d2 = kInf32;
+      if (k >= 0) { const int dq = q - s_top; d2 = (unsigned)(dq * dq) + f_top; }
+      if (!kZ) {
+        if (wy) p.g2[base + (long long)q * stride] = d2;
+      } else if (slot >= 0) {
+        const int l = lb + 64 * u;
+        const bool obs = (obsw >> u) & 1u, neg = (negw >> u) & 1u;
+        float e;
+        if (!obs) e = __int_as_float(0x7fc00000);
+        else if (p.capped) {
+          const double md = d2 == kInf32 ? p.dmax : fmin(p.s * sqrt((double)d2), p.dmax);
+          e = (float)(neg ? -md : md);
+        } else if (d2 == kInf32) e = __int_as_float(0x7f800000);
+        else {
+          const double md = p.s * sqrt((double)d2);
+          e = (float)(neg ? -md : md);
+        }
+        p.esdf[(long long)slot * kBlockVox + l] = e;
+      }
+      if (k >= 0 && q == t_top) {          // pop: the entry below takes over left of t_top
+        if (--k >= 0) {
+          if (k < lo) asm volatile("cp.async.wait_group %0;" :: "n"(kAhead - 1) : "memory");
+          const unsigned long long e = *(volatile unsigned long long*)(rg + (k & (kRing - 1)) * kRingThreads);
+          s_top = (int)(e & 0xffffu); t_top = (int)((e >> 16) & 0xffffu); f_top = (unsigned)(e >> 32);
+          issue(k - kAhead);
+        }
+      }
+    }
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 // ------------------------------------------------------------------------------- incremental (f1)
 struct IncParams {
   const long long* sums;
@@ -867,7 +1013,8 @@ cudaError_t dense_edt(cvx_submap* sm, const int lo[3], const int hi[3], cudaStre
   const long long nvox = (long long)nx * ny * nz;
   cudaError_t e = ensure_planes(sm, st);
   if (e != cudaSuccess) return e;
-  // passes y / z: 0 = streaming Meijster link kernel (default, measured fastest), 1 = TMA-staged band hulls
+  // passes y / z: 0 = ring kernel where it fits 24 bits, else the link kernel (default); 2 = the streaming
+  // Meijster link kernel; 1 = TMA-staged band hulls
   static const int kernel = [] { const char* v = std::getenv("CVX_EDT_KERNEL"); return v ? std::atoi(v) : 0; }();
   const long long need = nvox * (4 + 2 + (kernel != 1 ? 8 : 0)) + (long long)nbx * nby + (long long)nby * nbz + 256;
   if ((e = grow_async(&sm->edt, &sm->edt_bytes, need, st)) != cudaSuccess) return e;
@@ -891,7 +1038,10 @@ cudaError_t dense_edt(cvx_submap* sm, const int lo[3], const int hi[3], cudaStre
     ProfScope ps_(sm, "esdf_pass_x", st);
     pass_x_kernel<<<xblocks, 128, smem, st>>>(xp);
   }
-  if (kernel == 0) {
+  // ring kernel: every separator numerator and squared distance below 2^24 (exact in fp32 / int32)
+  const long long mx2 = (long long)(nx - 1) * (nx - 1), my2 = (long long)(ny - 1) * (ny - 1);
+  const bool ring_y = (long long)ny * ny + mx2 < (1ll << 24), ring_z = (long long)nz * nz + mx2 + my2 < (1ll << 24);
+  if (kernel == 0 || kernel == 2) {
     LinkParams lp{};
     lp.fin = g1; lp.g2 = g2; lp.meta = meta; lp.esdf = sm->pool.esdf; lp.grid = sm->block_grid; lp.colmask = colmask;
     lp.planes = planes; lp.nx = nx; lp.ny = ny; lp.nz = nz; lp.nbx = nbx; lp.nby = nby; lp.s = sm->cfg.voxel_size;
@@ -899,12 +1049,14 @@ cudaError_t dense_edt(cvx_submap* sm, const int lo[3], const int hi[3], cudaStre
     {
       ProfScope ps_(sm, "esdf_pass_y", st);
       const long long nl = (long long)nx * nz;
-      link_line_kernel<false><<<(unsigned)((nl + 255) / 256), 256, 0, st>>>(lp);
+      if (kernel == 0 && ring_y) ring_line_kernel<false><<<(unsigned)((nl + kRingThreads - 1) / kRingThreads), kRingThreads, 0, st>>>(lp);
+      else link_line_kernel<false><<<(unsigned)((nl + 255) / 256), 256, 0, st>>>(lp);
     }
     lp.fin = g2;
     ProfScope ps_(sm, "esdf_pass_z", st);
     const long long nl = (long long)nx * ny;
-    link_line_kernel<true><<<(unsigned)((nl + 255) / 256), 256, 0, st>>>(lp);
+    if (kernel == 0 && ring_z) ring_line_kernel<true><<<(unsigned)((nl + kRingThreads - 1) / kRingThreads), kRingThreads, 0, st>>>(lp);
+    else link_line_kernel<true><<<(unsigned)((nl + 255) / 256), 256, 0, st>>>(lp);
     return cudaGetLastError();
   }
   PbaParams pp{};
