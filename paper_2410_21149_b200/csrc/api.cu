@@ -115,6 +115,8 @@ void free_all(cvx_submap* sm) {
   if (sm->pool.coords) cudaFree(sm->pool.coords);
   if (sm->pool.grid) cudaFree(sm->pool.grid);
   if (sm->ctr) cudaFree(sm->ctr);
+  if (sm->acc_dirty) cudaFree(sm->acc_dirty);
+  if (sm->dacc) cudaFree(sm->dacc);
   if (sm->ctr_host) cudaFreeHost(sm->ctr_host);
   for (auto& B : sm->buf) {
     if (B.frame_T) cudaFree(B.frame_T);
@@ -123,6 +125,7 @@ void free_all(cvx_submap* sm) {
     if (B.ws) cudaFree(B.ws);
     if (B.slot_lists) cudaFree(B.slot_lists);
     if (B.lcnt) cudaFree(B.lcnt);
+    if (B.cta_box) cudaFree(B.cta_box);
     if (B.staging) cudaFree(B.staging);
   }
   if (sm->side) cudaStreamDestroy(sm->side);
@@ -184,6 +187,9 @@ cvx_status cvx_create_submap(const cvx_grid_config* cfg, const double* T_world_s
   if (const char* wc = std::getenv("CVX_WALK_CW")) sm->walk_cw = wc[0] != '0';     // tuning knob
   if (const char* fa = std::getenv("CVX_FUSE_ALLOC")) sm->fuse_alloc = fa[0] != '0'; // tuning knob
   if (const char* lc = std::getenv("CVX_LIST_CAP")) sm->list_cap_limit = std::atoll(lc);  // test knob
+  if (const char* dn = std::getenv("CVX_DENSE")) sm->dense_on = dn[0] != '0';         // R19 knob
+  if (const char* db = std::getenv("CVX_DENSE_BLOCKS"))                                 // R19 capacity knob
+    sm->dense_cap = std::max(1ll, std::min(std::atoll(db), 1ll << 22));
   sm->cfg = *cfg;
   std::memcpy(sm->T_ws, T_world_submap, sizeof(sm->T_ws));
   sm->device = device;
@@ -204,7 +210,8 @@ cvx_status cvx_create_submap(const cvx_grid_config* cfg, const double* T_world_s
       (e = cudaMallocHost(&sm->ctr_host, sizeof(cvx::Counters))) != cudaSuccess ||
       (e = cudaMalloc(&sm->buf[0].frame_T, sizeof(double) * 16 * cvx::kMaxBatch)) != cudaSuccess ||
       (e = cudaMalloc(&sm->buf[1].frame_T, sizeof(double) * 16 * cvx::kMaxBatch)) != cudaSuccess ||
-      (e = cudaMalloc(&sm->buf[0].lcnt, 16)) != cudaSuccess || (e = cudaMalloc(&sm->buf[1].lcnt, 16)) != cudaSuccess ||
+      (e = cudaMalloc(&sm->buf[0].lcnt, 64)) != cudaSuccess || (e = cudaMalloc(&sm->buf[1].lcnt, 64)) != cudaSuccess ||
+      (e = cudaMalloc(&sm->acc_dirty, sizeof(int))) != cudaSuccess ||
       (e = cudaStreamCreateWithFlags(&sm->side, cudaStreamNonBlocking)) != cudaSuccess ||
       (e = cudaEventCreateWithFlags(&sm->ev_entry, cudaEventDisableTiming)) != cudaSuccess ||
       (e = cudaEventCreateWithFlags(&sm->ev_prepared[0], cudaEventDisableTiming)) != cudaSuccess ||
@@ -219,6 +226,7 @@ cvx_status cvx_create_submap(const cvx_grid_config* cfg, const double* T_world_s
   }
   // zero-initialised pool (a3 zero-init happens once here; reset re-zeroes only the used blocks)
   cudaMemset(sm->ctr, 0, sizeof(cvx::Counters));
+  cudaMemset(sm->acc_dirty, 0, sizeof(int));
   cudaMemset(sm->pool.sums, 0, nb * cvx::kBlockVox * 16);
   cudaMemset(sm->pool.acc, 0, (nb + cvx::kTrashBlocks) * cvx::kBlockVox * 8);   // + the trash region (cvx_internal.cuh)
   cudaMemset(sm->pool.esdf, 0, nb * cvx::kBlockVox * 4);

@@ -605,6 +605,9 @@ __global__ void __launch_bounds__(256) link_line_kernel(const __grid_constant__ 
 //     floor(num / den) = the fp32 reciprocal estimate corrected by the exact integer remainder.
 // Same outputs as link_line_kernel / pba_line_kernel (bit for bit: the envelope is unique and the
 // output is its value).
+#ifndef CVX_RING_MINB
+#define CVX_RING_MINB 7
+#endif
 constexpr int kRing = 16, kAhead = 12, kRingThreads = 128;
 
 __device__ __forceinline__ float rcp_approx32(float x) { float y; asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
@@ -617,8 +620,23 @@ __device__ __forceinline__ int floordiv24(int num, int den) {   // den in [2, 2^
   return q;
 }
 
+// (float)(s * sqrt(d2)) correctly rounded as in fp64 (O11, the value the oracle computes), d2 < 2^24: an
+// fp32 square root refined once in fp64 (relative error < 2^-44), rounded to fp32; only when the fp64
+// value lies within 2^-40 (relative) of an fp32 rounding boundary is the IEEE fp64 sqrt taken.
+__device__ __forceinline__ float esdf_value(double s, unsigned d2) {
+  const float df = (float)d2;                               // exact (< 2^24)
+  const float r = sqrtf(df);                                // |r - sqrt(d2)| <= ~1 ulp (fp32)
+  if (r == 0.f) return 0.f;
+  const double rd = (double)r;
+  const double y = rd + ((double)d2 - rd * rd) * (0.5 / rd);   // one Newton step: error ~ 2^-46 relative
+  const double v = s * y;
+  const float lo = (float)(v * (1.0 - 0x1p-40)), hi = (float)(v * (1.0 + 0x1p-40));
+  if (lo == hi) return lo;
+  return (float)(s * sqrt((double)d2));
+}
+
 template <bool kZ>
-__global__ void __launch_bounds__(kRingThreads, 8) ring_line_kernel(const __grid_constant__ LinkParams p) {
+__global__ void __launch_bounds__(kRingThreads, CVX_RING_MINB) ring_line_kernel(const __grid_constant__ LinkParams p) {
   __shared__ unsigned long long ring[kRing][kRingThreads];
   const long long nlines = kZ ? (long long)p.nx * p.ny : (long long)p.nx * p.nz;
   const long long line = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -631,22 +649,28 @@ __global__ void __launch_bounds__(kRingThreads, 8) ring_line_kernel(const __grid
   if (kZ && !p.colmask[(long long)(o2 >> 3) * p.nbx + (x >> 3)]) return;   // no allocated voxel in this line
   unsigned long long* const gst = static_cast<unsigned long long*>(p.meta) + line * m;
   unsigned long long* const rg = &ring[0][threadIdx.x];   // ring slot j of this thread: rg[j * kRingThreads]
-  auto f_at = [&](int q) -> unsigned {    // kInf32 = no site in the line's slice
+  // raw input (pass y: u16 1-D distance, pass z: u32 squared distance) and its f (kInf32 = no site)
+  auto raw_at = [&](int q) -> unsigned {
     if (kZ) return static_cast<const unsigned*>(p.fin)[base + q * stride];
-    const unsigned v = static_cast<const unsigned short*>(p.fin)[base + q * stride];
-    return v == kNone16 ? kInf32 : v * v;
+    return static_cast<const unsigned short*>(p.fin)[base + q * stride];
   };
+  auto f_of = [](unsigned v) -> unsigned { return kZ ? v : (v == kNone16 ? kInf32 : v * v); };
   int k = -1, lo = 0;                      // stack [0, k]; indices < lo valid in gst, [lo, k] in the ring
   int s_top = 0, t_top = 0;
   unsigned f_top = 0;
-  for (int q0 = 0; q0 < m; q0 += 8) {
-    unsigned fv[8];
+  // forward (m is a multiple of 8): the loads of batch q0 + 8 are issued before batch q0 is consumed
+  unsigned fa[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) fv[u] = q0 + u < m ? f_at(q0 + u) : kInf32;
+  for (int u = 0; u < 8; ++u) fa[u] = raw_at(u);
+  for (int q0 = 0; q0 < m; q0 += 8) {
+    unsigned fb[8];
+    const int qn = q0 + 8 < m ? q0 + 8 : q0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) fb[u] = raw_at(qn + u);
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int q = q0 + u;
-      const unsigned fq = fv[u];
+      const unsigned fq = f_of(fa[u]);
       if (fq == kInf32) continue;
       while (k >= 0) {
         const int a = t_top - s_top, c = t_top - q;
@@ -672,6 +696,8 @@ __global__ void __launch_bounds__(kRingThreads, 8) ring_line_kernel(const __grid
       *slot = ((unsigned long long)fq << 32) | ((unsigned)tq << 16) | (unsigned)q;
       s_top = q; t_top = tq; f_top = fq;
     }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) fa[u] = fb[u];
   }
   // backward: the entries below the top in decreasing index order; entry j < lo is copied into its ring
   // slot by cp.async kAhead pops before it is needed (one commit group per pop, empty when j >= lo)
@@ -686,44 +712,54 @@ __global__ void __launch_bounds__(kRingThreads, 8) ring_line_kernel(const __grid
 #pragma unroll 1
     for (int i = 1; i <= kAhead; ++i) issue(k - i);
   }
-  for (int q0 = ((m - 1) >> 3) << 3; q0 >= 0; q0 -= 8) {
-    int slot = -1;
-    unsigned obsw = 0, negw = 0;   // pass z: bit u = observed / negative of position q0 + u (prefetched)
-    const int lb = (x & 7) + 8 * (o2 & 7);
-    if (kZ) {
-      slot = p.grid[((long long)(q0 >> 3) * p.nby + (o2 >> 3)) * p.nbx + (x >> 3)];
-      if (slot >= 0) {
-        const unsigned* pl = p.planes + (long long)slot * kPlaneWords + (lb >> 5);
-        unsigned ow[8], nw[8];
+  const int lb = (x & 7) + 8 * (o2 & 7);
+  // per 8-position chunk: pass y whether its block column holds an allocated block; pass z the block's
+  // slot and this column's observed / negative plane words (8 each).  Loaded one chunk ahead.
+  auto chunk_slot = [&](int c0) -> int {
+    if (c0 < 0) return -1;
+    if (kZ) return p.grid[((long long)(c0 >> 3) * p.nby + (o2 >> 3)) * p.nbx + (x >> 3)];
+    return p.colmask[(long long)(c0 >> 3) * p.nbx + (x >> 3)] ? 0 : -1;
+  };
+  unsigned ow[8], nw[8];
+  auto load_planes = [&](int sl) {
+    if (kZ && sl >= 0) {
+      const unsigned* pl = p.planes + (long long)sl * kPlaneWords + (lb >> 5);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) { ow[u] = pl[2 * u]; nw[u] = pl[16 + 2 * u]; }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) { obsw |= ((ow[u] >> (lb & 31)) & 1u) << u; negw |= ((nw[u] >> (lb & 31)) & 1u) << u; }
-      }
+      for (int u = 0; u < 8; ++u) { ow[u] = pl[2 * u]; nw[u] = pl[16 + 2 * u]; }
     }
-    const bool wy = !kZ && p.colmask[(long long)(q0 >> 3) * p.nbx + (x >> 3)];
+  };
+  const int qlast = ((m - 1) >> 3) << 3;
+  int slot = chunk_slot(qlast);
+  load_planes(slot);
+  int nslot = chunk_slot(qlast - 8);
+  for (int q0 = qlast; q0 >= 0; q0 -= 8) {
+    unsigned obsw = 0, negw = 0;   // pass z: bit u = observed / negative of position q0 + u
+    if (kZ && slot >= 0) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) { obsw |= ((ow[u] >> (lb & 31)) & 1u) << u; negw |= ((nw[u] >> (lb & 31)) & 1u) << u; }
+    }
+    const int cur = slot;
+    slot = nslot;
+    load_planes(slot);                     // chunk q0 - 8
+    nslot = chunk_slot(q0 - 16);
 #pragma unroll
     for (int u = 7; u >= 0; --u) {
       const int q = q0 + u;
-      if (q >= m) continue;
       unsigned d2 = kInf32;
       if (k >= 0) { const int dq = q - s_top; d2 = (unsigned)(dq * dq) + f_top; }
       if (!kZ) {
-        if (wy) p.g2[base + (long long)q * stride] = d2;
-      } else if (slot >= 0) {
-        const int l = lb + 64 * u;
+        if (cur >= 0) p.g2[base + (long long)q * stride] = d2;
+      } else if (cur >= 0) {
         const bool obs = (obsw >> u) & 1u, neg = (negw >> u) & 1u;
         float e;
         if (!obs) e = __int_as_float(0x7fc00000);
-        else if (p.capped) {
-          const double md = d2 == kInf32 ? p.dmax : fmin(p.s * sqrt((double)d2), p.dmax);
-          e = (float)(neg ? -md : md);
-        } else if (d2 == kInf32) e = __int_as_float(0x7f800000);
+        else if (d2 == kInf32) e = p.capped ? (float)(neg ? -p.dmax : p.dmax) : __int_as_float(0x7f800000);
         else {
-          const double md = p.s * sqrt((double)d2);
-          e = (float)(neg ? -md : md);
+          e = esdf_value(p.s, d2);
+          if (p.capped && (double)e > p.dmax) e = (float)p.dmax;
+          if (neg) e = -e;
         }
-        p.esdf[(long long)slot * kBlockVox + l] = e;
+        p.esdf[(long long)cur * kBlockVox + lb + 64 * u] = e;
       }
       if (k >= 0 && q == t_top) {          // pop: the entry below takes over left of t_top
         if (--k >= 0) {

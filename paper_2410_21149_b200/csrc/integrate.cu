@@ -181,6 +181,7 @@ struct PrepParams {
   const int* trig;  // nullable: {threshold, hit, consumed}; a hit submap takes no further frames
   const unsigned char* rgb;   // nullable: per-point colour [total][3]
   int count_vox;    // add the raycast voxel counts to ctr->voxel_updates (0: projection mapping)
+  int* box;         // nullable: per CTA {lo[3], hi[3]} block box of its rays (dense-window path, R19)
 };
 
 __global__ void __launch_bounds__(256) prepare_kernel(const __grid_constant__ PrepParams p) {
@@ -282,7 +283,21 @@ __global__ void __launch_bounds__(256) prepare_kernel(const __grid_constant__ Pr
   // and the block-slot list space — no hot global counter per warp.
   __shared__ unsigned long long s_base;
   __shared__ unsigned s_w[8][7];   // per warp: used, slots, in, invalid, range, domain, voxels
+  __shared__ int s_box[8][6];      // per warp: block box of its used rays (dense-window path)
   const int warp = threadIdx.x >> 5;
+  if (p.box) {   // R19: the block box of every voxel the launch's rays traverse = that of the blocks of A and B
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      int lo = 0x7fffffff, hi = (int)0x80000000;
+      if (status == 0) {
+        const int ba = (int)(rec.A[a] >> 19), bb = (int)(rec.B[a] >> 19);
+        lo = min(ba, bb); hi = max(ba, bb);
+      }
+      lo = __reduce_min_sync(0xffffffffu, lo);
+      hi = __reduce_max_sync(0xffffffffu, hi);
+      if (lane == 0) { s_box[warp][a] = lo; s_box[warp][3 + a] = hi; }
+    }
+  }
   const unsigned used = __ballot_sync(0xffffffffu, status == 0);
   int nb = 0;                      // block-slot list length: closed form 1 + sum |db| (a2)
   if (status == 0) {
@@ -323,6 +338,12 @@ __global__ void __launch_bounds__(256) prepare_kernel(const __grid_constant__ Pr
     if (c[5]) { atomicAdd(&p.ctr->skipped_domain, c[5]); atomicOr(&p.ctr->err, (unsigned)kErrRange); }
     if (c[6] && p.count_vox) atomicAdd(&p.ctr->voxel_updates, c[6]);
   }
+  if (p.box && threadIdx.x < 6) {   // the CTA's box component -> its slot (box_reduce_kernel combines them)
+    const int a = threadIdx.x;
+    int v = a < 3 ? 0x7fffffff : (int)0x80000000;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v = a < 3 ? min(v, s_box[w][a]) : max(v, s_box[w][a]);
+    p.box[6ll * blockIdx.x + a] = v;
+  }
   __syncthreads();
   if (status == 0) {
     const long long off = (long long)(unsigned)(s_base >> 32) + s_w[warp][1] + incl - nb;
@@ -360,7 +381,20 @@ struct WalkParams {
   int q;            // sdf quantum 2^-q m
   long long band;   // colour band |S| < band, S in the fixed-point sdf units 2^-(q+kSdfF) m (= tau)
   int* birth;       // projection mapping: per slot, first frame (RayRec::rgb) whose rays touch the block
+  // dense-window path (R19): accumulators over the launch's block box, block-major; nullable dbox = off
+  unsigned long long* dacc;
+  const int* dbox;  // {lo[3], hi[3]} written by prepare_kernel
+  long long dcap;   // capacity of dacc in blocks (excluding the trash region)
+  int* acc_dirty;   // set when a dense-eligible launch falls back to the pool accumulators
 };
+
+// R19: dims of the dense window of the launch; false if it does not fit the buffer (the launch then takes
+// the slot-list path: block walk + walk_cw_kernel + fold_kernel).
+__device__ __forceinline__ bool dense_dims(const int* box, long long cap, int& nbx, int& nby, int& nbz) {
+  nbx = box[3] - box[0] + 1; nby = box[4] - box[1] + 1; nbz = box[5] - box[2] + 1;
+  if (nbx <= 0 || nby <= 0 || nbz <= 0) { nbx = nby = nbz = 0; return true; }   // no used ray
+  return (long long)nbx * nby * nbz <= cap;
+}
 
 __device__ __forceinline__ RayView load_ray(const WalkParams& p, int idx) {
   const RayRec r = p.rays[idx];
@@ -483,6 +517,7 @@ template <bool k32, bool kBirth = false, bool kGrid = false>
 __global__ void __launch_bounds__(256) block_walk2_kernel(const __grid_constant__ WalkParams p) {
   using DT = typename std::conditional<k32, unsigned, unsigned long long>::type;
   using ST = typename std::conditional<k32, int, long long>::type;
+  if (p.dbox) { int a, b, c; if (dense_dims(p.dbox, p.dcap, a, b, c)) return; }   // R19: the dense window runs
   const int n_rays = p.lcnt[0];
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
@@ -931,6 +966,11 @@ template <bool k32, bool kColor, bool kFuse = false>
 __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_constant__ WalkParams p) {
   using DT = typename std::conditional<k32, unsigned, unsigned long long>::type;
   using ST = typename std::conditional<k32, int, long long>::type;
+  if (p.dbox) {   // R19: the dense window runs this launch unless its box exceeds the buffer
+    int a, b, c;
+    if (dense_dims(p.dbox, p.dcap, a, b, c)) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *p.acc_dirty = 1;   // fold_kernel has work
+  }
   const int n_rays = p.lcnt[0];
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
@@ -1229,6 +1269,211 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
   for (; it < maxn; ++it) band_body(it);
 }
 
+// R19: the launch's block box = the union of prepare_kernel's per-CTA boxes
+__global__ void __launch_bounds__(256) box_reduce_kernel(const int* cta_box, int n, int* box) {
+  int v[6] = {0x7fffffff, 0x7fffffff, 0x7fffffff, (int)0x80000000, (int)0x80000000, (int)0x80000000};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int a = 0; a < 6; ++a) v[a] = a < 3 ? min(v[a], cta_box[6ll * i + a]) : max(v[a], cta_box[6ll * i + a]);
+  }
+#pragma unroll
+  for (int a = 0; a < 6; ++a) v[a] = a < 3 ? __reduce_min_sync(0xffffffffu, v[a]) : __reduce_max_sync(0xffffffffu, v[a]);
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) { atomicMin(box + a, v[a]); atomicMax(box + 3 + a, v[3 + a]); }
+  }
+}
+
+// Dense-window walk (R19; constant weights, no colour): walk_cw_kernel's exact DDA, sdf and run merging,
+// with the accumulators of the launch's block box laid out block-major (dense block index
+// (bz - lz) nby nbx + (by - ly) nbx + (bx - lx), 512 voxels each).  Entering the next block along axis a is
+// then pure arithmetic — the step wrapped the local field of a, -8 da undoes the carry and the block
+// stride moves to the neighbour block: addr += s_a (block stride_a - 8 |da_a|) — so the walk has no slot
+// lists, no prefetch and no divergent block-entry branch.  ALLOCATE runs afterwards (dense_fold_kernel)
+// for the blocks the walk touched.
+template <bool k32>
+__global__ void __launch_bounds__(128, CVX_V_MINB) walk_dw_kernel(const __grid_constant__ WalkParams p) {
+  using DT = typename std::conditional<k32, unsigned, unsigned long long>::type;
+  using ST = typename std::conditional<k32, int, long long>::type;
+  int nbx, nby, nbz;
+  if (!dense_dims(p.dbox, p.dcap, nbx, nby, nbz)) return;   // the slot-list path runs this launch
+  const int n_rays = p.lcnt[0];
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  if ((idx & ~31) >= n_rays) return;
+  const bool have = idx < n_rays;
+  // per-warp trash spots after the buffer's capacity (never inside any launch's box, never folded)
+  const unsigned trash = (unsigned)(p.dcap * kBlockVox);
+  int s0 = 1, s1 = 1, s2 = 1, k0 = 0, k1 = 0, k2 = 0;
+  DT D01 = 0, D02 = 0, D12 = 0, I0 = 0, I1 = 0, I2 = 0;
+  long long S = 0, U0 = 0, U1 = 0, U2 = 0;
+  int n = 0;
+  unsigned cexp = 0, addr = trash;
+  if (have) {
+    const RayView r = load_ray(p, idx);
+    long long R[3], AD[3];
+    int va[3], st[3], kk[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      va[a] = (int)(r.A[a] >> 16);
+      const int vb = (int)(r.B[a] >> 16);
+      const long long D = r.B[a] - r.A[a];
+      kk[a] = vb > va[a] ? vb - va[a] : va[a] - vb;
+      if (D > 0) { st[a] = 1; R[a] = (((long long)va[a] + 1) << 16) - r.A[a]; }
+      else { st[a] = -1; R[a] = r.A[a] - ((long long)va[a] << 16); }
+      AD[a] = D < 0 ? -D : D;
+    }
+    s0 = st[0]; s1 = st[1]; s2 = st[2]; k0 = kk[0]; k1 = kk[1]; k2 = kk[2];
+    cexp = (s0 > 0 ? 0u : 7u) | ((s1 > 0 ? 0u : 7u) << 3) | ((s2 > 0 ? 0u : 7u) << 6);
+    const long long C01 = R[0] * AD[1] - R[1] * AD[0];
+    const long long C02 = R[0] * AD[2] - R[2] * AD[0];
+    const long long C12 = R[1] * AD[2] - R[2] * AD[1];
+    if (k32) {
+      D01 = (DT)(-((-C01) >> 16)); D02 = (DT)(-((-C02) >> 16)); D12 = (DT)(-((-C12) >> 16));
+      I0 = (DT)AD[0]; I1 = (DT)AD[1]; I2 = (DT)AD[2];
+    } else {
+      D01 = (DT)C01; D02 = (DT)C02; D12 = (DT)C12;
+      I0 = (DT)(AD[0] << 16); I1 = (DT)(AD[1] << 16); I2 = (DT)(AD[2] << 16);
+    }
+    S = r.S0 + (1ll << (kSdfF - 1)) + ((long long)p.tq << kSdfF);
+    U0 = r.U[0]; U1 = r.U[1]; U2 = r.U[2];
+    n = r.n_vox;
+    const unsigned blk = (unsigned)((((va[2] >> 3) - p.dbox[2]) * nby + ((va[1] >> 3) - p.dbox[1])) * nbx + ((va[0] >> 3) - p.dbox[0]));
+    addr = blk * 512u + (unsigned)((va[0] & 7) | ((va[1] & 7) << 3) | ((va[2] & 7) << 6));
+  }
+  const int maxn = (int)__reduce_max_sync(0xffffffffu, (unsigned)n);
+  if (!have) { k0 = 0x3fffffff; s0 = 0; cexp = 1u; }   // parked idle lane (x step of 0, never a block entry)
+  const int da0 = s0, da1 = 8 * s1, da2 = 64 * s2;
+  // block entry along axis a: addr += e_a (the neighbour block's base minus the local field's carry)
+  const unsigned e0 = (unsigned)(s0 * (512 - 8)), e1 = (unsigned)((long long)s1 * (512ll * nbx - 64)),
+                 e2 = (unsigned)((long long)s2 * (512ll * nbx * nby - 512));
+  const int tq2 = 2 * p.tq;
+  unsigned long long* const acc = p.dacc;
+  int mfree = 0x7fffffff;
+  const int K0 = k0, K1 = k1, K2 = k2;
+  if (have) {
+    const long long thr = (long long)tq2 << kSdfF;
+    const long long umax = max(U0, max(U1, U2));
+    mfree = 0;
+    if (S > thr && umax > 0) {
+      const long long num = S - thr;
+      long long m = (long long)fminf((float)num * rcp_approx((float)umax), (float)(n - 1));
+      while (m > 0 && m * umax > num) --m;
+      while (m < n - 1 && (m + 1) * umax <= num) ++m;
+      mfree = (int)m;
+    }
+  }
+  const int mw = (int)__reduce_min_sync(0xffffffffu, (unsigned)mfree);
+  const unsigned above_mask = 0xfffffffeu << lane;
+  const bool lane0 = lane == 0;
+  int it = 0;
+  {
+    // free prefix (see walk_cw_kernel): every lane's update is the clamped one, merged over runs
+    const unsigned utq2 = (unsigned)tq2;
+    for (; it < mw; ++it) {
+      const unsigned prev = __shfl_up_sync(0xffffffffu, addr, 1);
+      const bool head = lane0 | (prev != addr);
+      const unsigned stops = __ballot_sync(0xffffffffu, head);
+      const unsigned len = run_len(stops & above_mask, lane);
+      const unsigned long long val = ((unsigned long long)(len << (kCntShift - 32)) << 32) | (len * utq2);
+      asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.relaxed.gpu.global.add.u64 [%0], %1;\n\t}"
+                   :: "l"(acc + addr), "l"(val), "r"((unsigned)head) : "memory");
+      const bool g0 = k0 > 0, g1 = k1 > 0, g2 = k2 > 0;
+      const bool yf = g1 & (!g0 | ((ST)D01 > 0));
+      const bool zf = g2 & (yf ? ((ST)D12 > 0) : (!g0 | ((ST)D02 > 0)));
+      const bool by = yf & !zf, bx = !yf & !zf;
+      if (bx) { addr += da0; --k0; D01 += I1; D02 += I2; }
+      if (by) { addr += da1; --k1; D01 -= I0; D12 += I2; }
+      if (zf) { addr += da2; --k2; D02 -= I0; D12 -= I1; }
+      const unsigned m = zf ? 0x1c0u : (yf ? 0x38u : 7u);
+      const unsigned e = zf ? e2 : (yf ? e1 : e0);
+      addr += ((addr ^ cexp) & m) == 0u ? e : 0u;   // entered the next block of the ray
+    }
+  }
+  S -= U0 * (K0 - k0) + U1 * (K1 - k1) + U2 * (K2 - k2);
+  {
+    // rest of the rays (see walk_cw_kernel): a finished lane parks on its warp's trash spot
+    const unsigned spot = trash + ((((unsigned)idx >> 5) & 4095u) << 3);
+    int dx0 = da0;
+    unsigned ex0 = e0;
+    if (it >= n) { addr = spot; k0 = 0x3fffffff; k1 = 0; k2 = 0; dx0 = 0; cexp = 1u; S = (long long)tq2 << (kSdfF + 1); U0 = 0; n = 0x7fffffff; }
+    for (; it < maxn; ++it) {
+      const int dpi = min(max((int)(S >> kSdfF), 0), tq2);   // round(sdf 2^q) + tq, clamped (O5, Q4)
+      const unsigned key = dpi == tq2 ? addr : 0xffffffffu;     // only clamped updates merge
+      const unsigned prev = __shfl_up_sync(0xffffffffu, key, 1);
+      const bool head = lane0 | (prev != key) | (key == 0xffffffffu);
+      const unsigned stops = __ballot_sync(0xffffffffu, head);
+      const unsigned len = run_len(stops & above_mask, lane);
+      const unsigned long long val = ((unsigned long long)(len << (kCntShift - 32)) << 32) | (len * (unsigned)dpi);
+      asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.relaxed.gpu.global.add.u64 [%0], %1;\n\t}"
+                   :: "l"(acc + addr), "l"(val), "r"((unsigned)head) : "memory");
+      if (it + 1 >= n) {   // that was the ray's last voxel: park
+        addr = spot; k0 = 0x3fffffff; k1 = 0; k2 = 0; dx0 = 0; cexp = 1u; S = (long long)tq2 << (kSdfF + 1); U0 = 0;
+        n = 0x7fffffff; ex0 = 0u;
+      }
+      const bool g0 = k0 > 0, g1 = k1 > 0, g2 = k2 > 0;
+      const bool yf = g1 & (!g0 | ((ST)D01 > 0));
+      const bool zf = g2 & (yf ? ((ST)D12 > 0) : (!g0 | ((ST)D02 > 0)));
+      const bool by = yf & !zf, bx = !yf & !zf;
+      if (bx) { addr += dx0; --k0; D01 += I1; D02 += I2; S -= U0; }
+      if (by) { addr += da1; --k1; D01 -= I0; D12 += I2; S -= U1; }
+      if (zf) { addr += da2; --k2; D02 -= I0; D12 -= I1; S -= U2; }
+      const unsigned m = zf ? 0x1c0u : (yf ? 0x38u : 7u);
+      const unsigned e = zf ? e2 : (yf ? e1 : ex0);
+      addr += ((addr ^ cexp) & m) == 0u ? e : 0u;   // entered the next block of the ray
+    }
+  }
+}
+
+// R19 ALLOCATE + FOLD of a dense-window launch, one warp per block of the box: a block whose accumulators
+// are not all zero was traversed by a ray (every traversed voxel receives a count >= 1), so it is
+// activated in the hash table (insert-if-absent + slot bump, P:L85, P:L124 — the same block set as the
+// block walk) and its accumulators are folded into the exact sums (fold_kernel's arithmetic) and zeroed.
+__global__ void __launch_bounds__(256) dense_fold_kernel(const __grid_constant__ WalkParams p) {
+  int nbx, nby, nbz;
+  if (!dense_dims(p.dbox, p.dcap, nbx, nby, nbz)) return;
+  const long long nblk = (long long)nbx * nby * nbz;
+  const int lane = threadIdx.x & 31;
+  const long long w0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int shift = 30 - p.q;
+  for (long long b = w0; b < nblk; b += nw) {
+    ulonglong2* src = reinterpret_cast<ulonglong2*>(p.dacc + b * kBlockVox);
+    ulonglong2 v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = src[lane + 32 * i];
+    unsigned long long any = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) any |= v[i].x | v[i].y;
+    if (!__any_sync(0xffffffffu, any != 0ull)) continue;
+    int slot = kFailed;
+    if (lane == 0) {
+      const int bx = p.dbox[0] + (int)(b % nbx), by = p.dbox[1] + (int)((b / nbx) % nby), bz = p.dbox[2] + (int)(b / ((long long)nbx * nby));
+      slot = hash_activate(p.hash, p.pool, p.ctr, pack_key(bx, by, bz), bx, by, bz);
+    }
+    slot = __shfl_sync(0xffffffffu, slot, 0);
+    longlong2* s2 = reinterpret_cast<longlong2*>(p.pool.sums) + (long long)(slot < 0 ? 0 : slot) * kBlockVox;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if ((v[i].x | v[i].y) == 0ull) continue;
+      const int e = lane + 32 * i;   // voxels 2e, 2e + 1
+      if (slot >= 0) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const unsigned long long a = h ? v[i].y : v[i].x;
+          if (!a) continue;
+          const long long cnt = (long long)(a >> kCntShift), sd = (long long)(a & ((1ull << kCntShift) - 1));
+          longlong2 x = s2[2 * e + h];
+          x.x += (sd - cnt * p.tq) << shift;
+          x.y += cnt << 30;
+          s2[2 * e + h] = x;
+        }
+      }
+      src[e] = make_ulonglong2(0ull, 0ull);
+    }
+  }
+}
+
 // Block-count submap trigger: after the ALLOCATE phase of frame k, fire once the
 // submap holds >= threshold blocks; frame k is the last one it takes.
 __global__ void trigger_check_kernel(const Counters* ctr, int* trig, int frame) {
@@ -1257,7 +1502,9 @@ __global__ void fold_color_kernel(const Counters* ctr, unsigned long long* cacc,
 // a5 FOLD of the packed per-launch accumulators into the exact sums: sum(w d) += (sum d' - n tq) 2^(30-q),
 // sum(w) += n 2^30 (w = 1).  Every update contributes exactly round(d 2^q) 2^(30-q), so the result does
 // not depend on how frames are grouped into launches.
-__global__ void fold_kernel(const Counters* ctr, unsigned long long* acc, long long* sums, int max_blocks, int tq, int shift) {
+__global__ void fold_kernel(const Counters* ctr, unsigned long long* acc, long long* sums, int max_blocks, int tq, int shift,
+                            const int* dirty) {
+  if (dirty && !*dirty) return;   // R19: every launch since the last fold ran in its dense window
   const int nb = min(ctr->n_blocks, max_blocks);
   const long long nv2 = (long long)nb * (kBlockVox / 2);
   ulonglong2* a2 = reinterpret_cast<ulonglong2*>(acc);
@@ -1493,7 +1740,7 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
   // scratch growth is stream-ordered on the side stream, after the walk that last read the buffer
   const cudaStream_t gs = sm->serialize ? st : sm->side;
   for (int b = 0; b < 2; ++b) {
-    const bool need_grow = sm->buf[b].ray_cap < cap_rays || sm->buf[b].slot_cap < cap_rays * kSlotsPerRay + 1024 ||
+    const bool need_grow = sm->buf[b].ray_cap < cap_rays || (sm->dense_on && sm->buf[b].cta_box_cap < 6 * ((cap_rays + 255) / 256)) || sm->buf[b].slot_cap < cap_rays * kSlotsPerRay + 1024 ||
                            (rgb && sm->buf[b].rgbs_cap < cap_rays) || (sm->cfg.weighting != 0 && sm->buf[b].ws_cap < cap_rays) ||
                            (host_data && sm->buf[b].staging_cap < (long long)per * elems_per_frame);
     if (need_grow) {
@@ -1509,6 +1756,8 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
       e = grow(reinterpret_cast<void**>(&sm->buf[b].ws), &sm->buf[b].ws_cap, cap_rays, sizeof(float), gs);
     if (e == cudaSuccess) e = grow(reinterpret_cast<void**>(&sm->buf[b].slot_lists), &sm->buf[b].slot_cap,
                                    cap_rays * kSlotsPerRay + 1024, sizeof(int), gs);
+    if (e == cudaSuccess && sm->dense_on)
+      e = grow(reinterpret_cast<void**>(&sm->buf[b].cta_box), &sm->buf[b].cta_box_cap, 6 * ((cap_rays + 255) / 256), sizeof(int), gs);
     if (e == cudaSuccess && host_data)
       e = grow(reinterpret_cast<void**>(&sm->buf[b].staging), &sm->buf[b].staging_cap, (long long)per * elems_per_frame,
                sizeof(float), gs);
@@ -1519,13 +1768,50 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
   // every ray spans < 2^12 voxels per axis if (max_range + tau) / s + 2 < 4096 (domain check O3 bounds
   // the rest): then the crossing-order differences fit 32 bits (see walk_kernel)
   const bool k32 = ((double)sensor.max_range + sm->cfg.truncation) / sm->cfg.voxel_size + 2.0 < 4096.0;
+  // R19: the dense-window path (constant weights, no colour, no trigger, default ALLOCATE kernels): the
+  // accumulator buffer covers a conservative box of the call (balls of radius max_range + tau around the
+  // frames' sensor origins), capped at dense_cap blocks; each launch uses the exact box of its rays
+  // (prepare_kernel) and falls back to the slot-list path on the device if that box exceeds the buffer.
+  const bool dense = cw_ok && sm->dense_on && sm->walk_cw && sm->bw2 && !sm->bw3 && !sm->fuse_alloc && !rgb && !trig;
+  long long dcap = 0;
+  if (dense) {
+    const double* W = sm->T_ws;
+    const double R = (double)sensor.max_range + sm->cfg.truncation, sv = sm->cfg.voxel_size;
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+    for (int f = 0; f < n_frames; ++f) {
+      const double* C = T_world_sensor + 16 * f;
+      for (int i = 0; i < 3; ++i) {
+        const double o = W[0 * 4 + i] * (C[3] - W[3]) + W[1 * 4 + i] * (C[7] - W[7]) + W[2 * 4 + i] * (C[11] - W[11]);
+        lo[i] = std::min(lo[i], o); hi[i] = std::max(hi[i], o);
+      }
+    }
+    long long nblk = 1;
+    for (int i = 0; i < 3; ++i) {
+      const double b0 = std::floor((lo[i] - R) / sv / 8.0) - 1.0, b1 = std::floor((hi[i] + R) / sv / 8.0) + 1.0;
+      nblk = (long long)std::min(1e15, (double)nblk * (b1 - b0 + 1.0));
+    }
+    dcap = std::min(nblk, sm->dense_cap);
+    if (sm->dacc_blocks < dcap) {   // grow-only, zeroed once; the dense folds keep it zero
+      if (sm->dacc) cudaFreeAsync(sm->dacc, st);
+      sm->dacc = nullptr;
+      sm->dacc_blocks = 0;
+      const size_t bytes = (size_t)(dcap + kTrashBlocks) * kBlockVox * sizeof(unsigned long long);
+      cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&sm->dacc), bytes, st);
+      if (e != cudaSuccess) return e;
+      cudaMemsetAsync(sm->dacc, 0, bytes, st);
+      sm->dacc_blocks = dcap;
+    }
+    dcap = sm->dacc_blocks;
+  }
   long long pending = 0;                             // rays in the packed accumulators since the last fold
   auto fold = [&]() {
     if (pending == 0) return;
     {
       ProfScope ps_(sm, "fold", st);
-      fold_kernel<<<148 * 8, 256, 0, st>>>(sm->ctr, sm->pool.acc, sm->pool.sums, sm->pool.max_blocks, tq, 30 - q);
+      fold_kernel<<<148 * 8, 256, 0, st>>>(sm->ctr, sm->pool.acc, sm->pool.sums, sm->pool.max_blocks, tq, 30 - q,
+                                           dense ? sm->acc_dirty : nullptr);
     }
+    if (dense) cudaMemsetAsync(sm->acc_dirty, 0, sizeof(int), st);
     if (rgb) {
       ProfScope ps_(sm, "fold_color", st);
       fold_color_kernel<<<148 * 8, 256, 0, st>>>(sm->ctr, sm->pool.cacc, sm->pool.csum, sm->pool.max_blocks);
@@ -1580,6 +1866,10 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
       compose_kernel<<<1, kMaxBatch, 0, side>>>(cp, B.frame_T);
     }
     cudaMemsetAsync(B.lcnt, 0, 4 * sizeof(int), side);
+    if (dense) {   // box {lo[3], hi[3]} = {0x7f7f7f7f x3, 0x80808080 x3}: beyond any block coordinate (< 2^20)
+      cudaMemsetAsync(B.lcnt + 8, 0x7f, 3 * sizeof(int), side);
+      cudaMemsetAsync(B.lcnt + 11, 0x80, 3 * sizeof(int), side);
+    }
     if (host_data && cstream != side) cudaStreamWaitEvent(side, sm->ev_staged[b], 0);
     PrepParams pp;
     pp.data = chunk;
@@ -1600,12 +1890,14 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     pp.rgbs = rgb ? B.rgbs : nullptr;
     pp.ws = sm->cfg.weighting != 0 ? B.ws : nullptr;
     pp.count_vox = 1;
+    pp.box = dense ? B.cta_box : nullptr;
     {
       ProfScope ps_(sm, "ray_prepare", side);
       prepare_kernel<<<blocks, 256, 0, side>>>(pp);
     }
+    if (dense) box_reduce_kernel<<<32, 256, 0, side>>>(B.cta_box, (int)blocks, B.lcnt + 8);
     if (host_data && cstream != side) cudaEventRecord(sm->ev_stage_free[b], side);   // staging[b] consumed
-    WalkParams wp;
+    WalkParams wp{};
     wp.rays = (const RayRec*)B.rays; wp.ctr = sm->ctr; wp.hash = sm->hash; wp.pool = sm->pool;
     wp.slots = B.slot_lists; wp.lcnt = B.lcnt;
     wp.s = (float)sm->cfg.voxel_size; wp.tau = (float)sm->cfg.truncation;
@@ -1614,6 +1906,7 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     wp.band = std::llround(std::ldexp(sm->cfg.truncation, q + kSdfF));
     wp.birth = nullptr;
     wp.frame_T = B.frame_T; wp.rgbs = pp.rgbs; wp.ws = pp.ws; wp.frame_base = 0;
+    wp.dacc = sm->dacc; wp.dbox = dense ? B.lcnt + 8 : nullptr; wp.dcap = dcap; wp.acc_dirty = sm->acc_dirty;
     const bool cw = cw_ok && total <= launch_rays;
     // constant weights, no colour, no block-count trigger: ALLOCATE runs inside the update walk
     const bool fuse = sm->fuse_alloc && cw && sm->aggregate && sm->walk_cw && !rgb && !trig;
@@ -1641,7 +1934,11 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
       if (cw && sm->aggregate && sm->walk_cw) {
         if (rgb) { if (k32) walk_cw_kernel<true, true><<<wblocks, 128, 0, st>>>(wp); else walk_cw_kernel<false, true><<<wblocks, 128, 0, st>>>(wp); }
         else if (fuse) { if (k32) walk_cw_kernel<true, false, true><<<wblocks, 128, 0, st>>>(wp); else walk_cw_kernel<false, false, true><<<wblocks, 128, 0, st>>>(wp); }
-        else { if (k32) walk_cw_kernel<true, false><<<wblocks, 128, 0, st>>>(wp); else walk_cw_kernel<false, false><<<wblocks, 128, 0, st>>>(wp); }
+        else {
+          if (dense) { if (k32) walk_dw_kernel<true><<<wblocks, 128, 0, st>>>(wp); else walk_dw_kernel<false><<<wblocks, 128, 0, st>>>(wp); }
+          // (dense: runs only if this launch's box exceeds the dense buffer)
+          if (k32) walk_cw_kernel<true, false><<<wblocks, 128, 0, st>>>(wp); else walk_cw_kernel<false, false><<<wblocks, 128, 0, st>>>(wp);
+        }
       } else if (rgb) {
         if (cw) { if (k32) walk_kernel<true, true, true, true><<<wblocks, 128, 0, st>>>(wp); else walk_kernel<true, true, false, true><<<wblocks, 128, 0, st>>>(wp); }
         else { if (k32) walk_kernel<true, false, true, true><<<wblocks, 128, 0, st>>>(wp); else walk_kernel<true, false, false, true><<<wblocks, 128, 0, st>>>(wp); }
@@ -1651,6 +1948,10 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
       } else {
         walk_kernel<false, false, false><<<wblocks, 128, 0, st>>>(wp);
       }
+    }
+    if (dense) {
+      ProfScope ps_(sm, "dense_fold_allocate", st);
+      dense_fold_kernel<<<148 * 8, 256, 0, st>>>(wp);
     }
     if (cw) pending += total;
     cudaEventRecord(sm->ev_free[b], st);
@@ -1726,7 +2027,7 @@ cudaError_t launch_integrate_projective(cvx_submap* sm, const float* depth, int6
         ProfScope ps_(sm, "ray_prepare", st);
         prepare_kernel<<<blocks, 256, 0, st>>>(pp);
       }
-      WalkParams wp;
+      WalkParams wp{};
       wp.rays = (const RayRec*)B.rays; wp.ctr = sm->ctr; wp.hash = sm->hash; wp.pool = sm->pool;
       wp.slots = B.slot_lists; wp.lcnt = B.lcnt;
       wp.s = (float)sm->cfg.voxel_size; wp.tau = (float)sm->cfg.truncation;

@@ -59,7 +59,9 @@ struct cvx_submap {
     int64_t ws_cap = 0;
     int* slot_lists = nullptr;  // device block-slot lists of the rays of one launch
     int64_t slot_cap = 0;
-    int* lcnt = nullptr;        // device {n_rays, n_slots, -, -} of the launch using this buffer
+    int* lcnt = nullptr;        // device {n_rays, n_slots, -, -, 4 spare, box lo[3], hi[3]} of the launch
+    int* cta_box = nullptr;     // device per-CTA block boxes of prepare_kernel (dense-window path, R19)
+    int64_t cta_box_cap = 0;
     float* staging = nullptr;   // device copy of host frames (cvx_integrate_batch_host)
     int64_t staging_cap = 0;
   } buf[2];
@@ -79,6 +81,12 @@ struct cvx_submap {
   bool walk_cw = true;        // constant weights: incremental-address walk (walk_cw_kernel)
   long long list_cap_limit = 1ll << 62;   // test knob: cap on the per-ray slot-list buffer (full: walk hashes)
   bool fuse_alloc = false;    // constant weights: ALLOCATE inside walk_cw_kernel (measured 1.4x slower: off)
+  // dense-window path (R19): block-major accumulators over the launch's block box, ALLOCATE after the walk
+  bool dense_on = true;
+  long long dense_cap = 1ll << 20;          // blocks (4 GiB of u64 accumulators)
+  unsigned long long* dacc = nullptr;       // device [(dacc_blocks + kTrashBlocks) * 512], zero between folds
+  long long dacc_blocks = 0;
+  int* acc_dirty = nullptr;                 // device: a dense-eligible launch fell back to the pool accumulators
 
   // ESDF scratch (grow-only, stream-ordered cudaMallocAsync on the calling stream)
   void* edt = nullptr;        // device: g2 u32 | g1 u16 over the dense AABB, then the column / row masks

@@ -22,8 +22,8 @@ for w in $WHAT; do case $w in
   prepare) cap "^prepare_kernel" prepare 2;;
   fold) cap "^fold_kernel" fold 1;;
   esdf_pass_x) cap "^pass_x_kernel" esdf_pass_x 1;;
-  esdf_pass_y) cap "^(link|pba)_line_kernel" esdf_pass_y 2;;
-  esdf_pass_z) cap "^(link|pba)_line_kernel" esdf_pass_z 3;;
+  esdf_pass_y) cap "^(link|pba|ring)_line_kernel" esdf_pass_y 2;;
+  esdf_pass_z) cap "^(link|pba|ring)_line_kernel" esdf_pass_z 3;;
   query) cap "^query_kernel" query 0;;
   project) capw "^project_kernel" project 2 rgbd;;
   inc_window) capw "^inc_window" inc_window 3 incremental;;
@@ -33,8 +33,8 @@ for w in $WHAT; do case $w in
   voxel_sweep) timeout 900 python bench.py --workload voxel_sweep --steps 5 > gpurun_out/$T/bench_voxel_sweep.json 2> gpurun_out/$T/bench_voxel_sweep.err; echo "voxel_sweep rc=$?";;
   n2) CVX_BENCH_ONE_GPU=1 CVX_BENCH_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29513 bench.py --gpus 2 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/$T/bench_n2_onegpu_gloo.json 2> gpurun_out/$T/bench_n2_onegpu_gloo.err; echo "n2 rc=$?";;
   stress_x) capw "^pass_x_kernel" stress_pass_x 0 esdf_stress;;
-  stress_y) capw "^(link|pba)_line_kernel" stress_pass_y 0 esdf_stress;;
-  stress_z) capw "^(link|pba)_line_kernel" stress_pass_z 1 esdf_stress;;
+  stress_y) capw "^(link|pba|ring)_line_kernel" stress_pass_y 0 esdf_stress;;
+  stress_z) capw "^(link|pba|ring)_line_kernel" stress_pass_z 1 esdf_stress;;
   rgbd) timeout 900 python bench.py --workload rgbd --steps 5 > gpurun_out/$T/bench_rgbd.json 2> gpurun_out/$T/bench_rgbd.err; echo "rgbd rc=$?";;
   incremental) timeout 900 python bench.py --workload incremental --steps 5 > gpurun_out/$T/bench_incremental.json 2> gpurun_out/$T/bench_incremental.err; echo "incremental rc=$?";;
   gputest) timeout 1500 python -m pytest tests -q -m gpu > gpurun_out/$T/gputest.log 2>&1; echo "gputest rc=$?";;
