@@ -385,6 +385,7 @@ struct WalkParams {
   unsigned long long* dacc;
   const int* dbox;  // {lo[3], hi[3]} written by prepare_kernel
   long long dcap;   // capacity of dacc in blocks (excluding the trash region)
+  unsigned char* dflag;   // per dense block: touched by the walk (cleared by dense_fold_kernel)
   int* acc_dirty;   // set when a dense-eligible launch falls back to the pool accumulators
 };
 
@@ -514,12 +515,10 @@ __device__ __forceinline__ int key_field(unsigned long long key, int sh) {
 // window; a cache miss activates through the hash (deduplicated across the run, as every probe here)
 // and caches the slot.
 template <bool k32, bool kBirth = false, bool kGrid = false>
-__global__ void __launch_bounds__(256) block_walk2_kernel(const __grid_constant__ WalkParams p) {
+__device__ __forceinline__ void block_walk2_body(const WalkParams& p, const int idx) {
   using DT = typename std::conditional<k32, unsigned, unsigned long long>::type;
   using ST = typename std::conditional<k32, int, long long>::type;
-  if (p.dbox) { int a, b, c; if (dense_dims(p.dbox, p.dcap, a, b, c)) return; }   // R19: the dense window runs
   const int n_rays = p.lcnt[0];
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   if ((idx & ~31) >= n_rays) return;
   const bool have = idx < n_rays;
@@ -619,6 +618,15 @@ __global__ void __launch_bounds__(256) block_walk2_kernel(const __grid_constant_
     }
     act = actn; key = keyn; heads = headsn; ent = entn; gi = gin;
   }
+}
+
+// Grid-stride over the rays (the dense-window path launches it with a small grid: usually a no-op)
+template <bool k32, bool kBirth = false, bool kGrid = false>
+__global__ void __launch_bounds__(256) block_walk2_kernel(const __grid_constant__ WalkParams p) {
+  if (p.dbox) { int a, b, c; if (dense_dims(p.dbox, p.dcap, a, b, c)) return; }   // R19: the dense window runs
+  const long long n = p.lcnt[0];
+  for (long long base = (long long)blockIdx.x * blockDim.x; base < n; base += (long long)gridDim.x * blockDim.x)
+    block_walk2_body<k32, kBirth, kGrid>(p, (int)(base + threadIdx.x));
 }
 
 // ALLOCATE through the dense slot cache (default): every lane walks its own ray at block granularity (no
@@ -963,16 +971,10 @@ __device__ __forceinline__ float rcp_approx(float x) { float y; asm("rcp.approx.
 // next entry takes the one on the stepped axis; a hit is the slot, anything else (absent: insert, other
 // key: probe on, pending) goes through hash_activate_pf with that entry as its first probe.
 template <bool k32, bool kColor, bool kFuse = false>
-__global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_constant__ WalkParams p) {
+__device__ __forceinline__ void walk_cw_body(const WalkParams& p, const int idx) {
   using DT = typename std::conditional<k32, unsigned, unsigned long long>::type;
   using ST = typename std::conditional<k32, int, long long>::type;
-  if (p.dbox) {   // R19: the dense window runs this launch unless its box exceeds the buffer
-    int a, b, c;
-    if (dense_dims(p.dbox, p.dcap, a, b, c)) return;
-    if (blockIdx.x == 0 && threadIdx.x == 0) *p.acc_dirty = 1;   // fold_kernel has work
-  }
   const int n_rays = p.lcnt[0];
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   if ((idx & ~31) >= n_rays) return;
   const bool have = idx < n_rays;
@@ -1269,6 +1271,19 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_c
   for (; it < maxn; ++it) band_body(it);
 }
 
+// Grid-stride over the rays (the dense-window path launches it with a small grid: usually a no-op)
+template <bool k32, bool kColor, bool kFuse = false>
+__global__ void __launch_bounds__(128, CVX_V_MINB) walk_cw_kernel(const __grid_constant__ WalkParams p) {
+  if (p.dbox) {   // R19: the dense window runs this launch unless its box exceeds the buffer
+    int a, b, c;
+    if (dense_dims(p.dbox, p.dcap, a, b, c)) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *p.acc_dirty = 1;   // fold_kernel has work
+  }
+  const long long n = p.lcnt[0];
+  for (long long base = (long long)blockIdx.x * blockDim.x; base < n; base += (long long)gridDim.x * blockDim.x)
+    walk_cw_body<k32, kColor, kFuse>(p, (int)(base + threadIdx.x));
+}
+
 // R19: the launch's block box = the union of prepare_kernel's per-CTA boxes
 __global__ void __launch_bounds__(256) box_reduce_kernel(const int* cta_box, int n, int* box) {
   int v[6] = {0x7fffffff, 0x7fffffff, 0x7fffffff, (int)0x80000000, (int)0x80000000, (int)0x80000000};
@@ -1291,8 +1306,36 @@ __global__ void __launch_bounds__(256) box_reduce_kernel(const int* cta_box, int
 // stride moves to the neighbour block: addr += s_a (block stride_a - 8 |da_a|) — so the walk has no slot
 // lists, no prefetch and no divergent block-entry branch.  ALLOCATE runs afterwards (dense_fold_kernel)
 // for the blocks the walk touched.
+#ifndef CVX_DW_MINB
+#define CVX_DW_MINB CVX_V_MINB
+#endif
+// timing experiments only (wrong results): CVX_DW_EXP=1 drops the reductions, =2 sends them to 32
+// consecutive words per warp (lane-coherent)
+#ifndef CVX_DW_EXP
+#define CVX_DW_EXP 0
+#endif
+#if CVX_DW_EXP == 1
+#define DW_RED(acc, addr, val, head) do { if ((head) && (addr) == 0xfffffff0u) (acc)[0] = (val); } while (0)
+#elif CVX_DW_EXP == 2
+#define DW_RED(acc, addr, val, head) asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.relaxed.gpu.global.add.u64 [%0], %1;\n\t}" \
+                   :: "l"((acc) + (((addr) & ~31u) | (threadIdx.x & 31))), "l"(val), "r"((unsigned)(head)) : "memory")
+#else
+#define DW_RED(acc, addr, val, head) asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.relaxed.gpu.global.add.u64 [%0], %1;\n\t}" \
+                   :: "l"((acc) + (addr)), "l"(val), "r"((unsigned)(head)) : "memory")
+#endif
+#ifndef CVX_DW_FLAGS
+#define CVX_DW_FLAGS 0
+#endif
+// mark dense block bi as touched: a plain (L1-cached) read first, so blocks already marked (the common case:
+// neighbouring rays enter the same blocks) cost no L2 write; a stale 0 only repeats the store
+__device__ __forceinline__ void mark_block(unsigned char* flags, unsigned bi, bool pred) {
+#if CVX_DW_FLAGS
+  if (pred && flags[bi] == 0) flags[bi] = 1;
+#endif
+}
+
 template <bool k32>
-__global__ void __launch_bounds__(128, CVX_V_MINB) walk_dw_kernel(const __grid_constant__ WalkParams p) {
+__global__ void __launch_bounds__(128, CVX_DW_MINB) walk_dw_kernel(const __grid_constant__ WalkParams p) {
   using DT = typename std::conditional<k32, unsigned, unsigned long long>::type;
   using ST = typename std::conditional<k32, int, long long>::type;
   int nbx, nby, nbz;
@@ -1340,6 +1383,7 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_dw_kernel(const __grid_c
     n = r.n_vox;
     const unsigned blk = (unsigned)((((va[2] >> 3) - p.dbox[2]) * nby + ((va[1] >> 3) - p.dbox[1])) * nbx + ((va[0] >> 3) - p.dbox[0]));
     addr = blk * 512u + (unsigned)((va[0] & 7) | ((va[1] & 7) << 3) | ((va[2] & 7) << 6));
+    mark_block(p.dflag, blk, true);
   }
   const int maxn = (int)__reduce_max_sync(0xffffffffu, (unsigned)n);
   if (!have) { k0 = 0x3fffffff; s0 = 0; cexp = 1u; }   // parked idle lane (x step of 0, never a block entry)
@@ -1376,8 +1420,7 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_dw_kernel(const __grid_c
       const unsigned stops = __ballot_sync(0xffffffffu, head);
       const unsigned len = run_len(stops & above_mask, lane);
       const unsigned long long val = ((unsigned long long)(len << (kCntShift - 32)) << 32) | (len * utq2);
-      asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.relaxed.gpu.global.add.u64 [%0], %1;\n\t}"
-                   :: "l"(acc + addr), "l"(val), "r"((unsigned)head) : "memory");
+      DW_RED(acc, addr, val, head);
       const bool g0 = k0 > 0, g1 = k1 > 0, g2 = k2 > 0;
       const bool yf = g1 & (!g0 | ((ST)D01 > 0));
       const bool zf = g2 & (yf ? ((ST)D12 > 0) : (!g0 | ((ST)D02 > 0)));
@@ -1387,7 +1430,9 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_dw_kernel(const __grid_c
       if (zf) { addr += da2; --k2; D02 -= I0; D12 -= I1; }
       const unsigned m = zf ? 0x1c0u : (yf ? 0x38u : 7u);
       const unsigned e = zf ? e2 : (yf ? e1 : e0);
-      addr += ((addr ^ cexp) & m) == 0u ? e : 0u;   // entered the next block of the ray
+      const bool ent = ((addr ^ cexp) & m) == 0u;     // entered the next block of the ray
+      addr += ent ? e : 0u;
+      mark_block(p.dflag, addr >> 9, ent);
     }
   }
   S -= U0 * (K0 - k0) + U1 * (K1 - k1) + U2 * (K2 - k2);
@@ -1405,8 +1450,7 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_dw_kernel(const __grid_c
       const unsigned stops = __ballot_sync(0xffffffffu, head);
       const unsigned len = run_len(stops & above_mask, lane);
       const unsigned long long val = ((unsigned long long)(len << (kCntShift - 32)) << 32) | (len * (unsigned)dpi);
-      asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.relaxed.gpu.global.add.u64 [%0], %1;\n\t}"
-                   :: "l"(acc + addr), "l"(val), "r"((unsigned)head) : "memory");
+      DW_RED(acc, addr, val, head);
       if (it + 1 >= n) {   // that was the ray's last voxel: park
         addr = spot; k0 = 0x3fffffff; k1 = 0; k2 = 0; dx0 = 0; cexp = 1u; S = (long long)tq2 << (kSdfF + 1); U0 = 0;
         n = 0x7fffffff; ex0 = 0u;
@@ -1420,15 +1464,45 @@ __global__ void __launch_bounds__(128, CVX_V_MINB) walk_dw_kernel(const __grid_c
       if (zf) { addr += da2; --k2; D02 -= I0; D12 -= I1; S -= U2; }
       const unsigned m = zf ? 0x1c0u : (yf ? 0x38u : 7u);
       const unsigned e = zf ? e2 : (yf ? e1 : ex0);
-      addr += ((addr ^ cexp) & m) == 0u ? e : 0u;   // entered the next block of the ray
+      const bool ent = ((addr ^ cexp) & m) == 0u;     // entered the next block of the ray
+      addr += ent ? e : 0u;
+      mark_block(p.dflag, addr >> 9, ent);
     }
   }
 }
 
-// R19 ALLOCATE + FOLD of a dense-window launch, one warp per block of the box: a block whose accumulators
-// are not all zero was traversed by a ray (every traversed voxel receives a count >= 1), so it is
-// activated in the hash table (insert-if-absent + slot bump, P:L85, P:L124 — the same block set as the
-// block walk) and its accumulators are folded into the exact sums (fold_kernel's arithmetic) and zeroed.
+// R19 ALLOCATE for the dense fold: insert-if-absent of one key.  Returns the slot of an existing key
+// (waiting out a concurrent inserter's PENDING), or kPending with *ent = the entry this lane won (the
+// caller assigns the slot for the whole warp and publishes it), or kFailed if the table is full.
+__device__ __forceinline__ int dense_insert(const HashView& h, Counters* ctr, unsigned long long key, unsigned* ent) {
+  unsigned i = hash_slot(key, h);
+  for (unsigned n = 0; n <= h.mask; ++n) {
+    const longlong2 en = ld_entry(h.e + i);
+    unsigned long long k = (unsigned long long)en.x;
+    int v = (int)(en.y & 0xffffffffll);
+    if (k == kEmptyKey) {
+      const unsigned long long old = atomicCAS(&h.e[i].key, kEmptyKey, key);
+      if (old == kEmptyKey) { *ent = i; return kPending; }   // won the CAS: this lane inserts
+      k = old;
+      v = kPending;                                          // its slot is read below
+    }
+    if (k == key) {
+      while (v == kPending) { v = ld_volatile(&h.e[i].val); if (v == kPending) __nanosleep(32); }
+      return v;
+    }
+    i = (i + 1) & h.mask;
+  }
+  atomicOr(&ctr->err, (unsigned)kErrHashFull);
+  return kFailed;
+}
+
+// R19 ALLOCATE + FOLD of a dense-window launch.  A warp takes 32 consecutive blocks of the box: (1) it
+// reads their accumulators (two blocks in flight) — a block whose accumulators are not all zero was
+// traversed by a ray (every traversed voxel receives a count >= 1); (2) lane j activates block j if it
+// was touched (insert-if-absent; the pool slots of the new blocks are bumped once per warp, P:L124,
+// and the AABB / new-block counters updated once per warp) — the same block set as the block walk;
+// (3) the touched blocks are folded into the exact sums one by one (fold_kernel's arithmetic) and their
+// accumulators zeroed.
 __global__ void __launch_bounds__(256) dense_fold_kernel(const __grid_constant__ WalkParams p) {
   int nbx, nby, nbz;
   if (!dense_dims(p.dbox, p.dcap, nbx, nby, nbz)) return;
@@ -1437,39 +1511,83 @@ __global__ void __launch_bounds__(256) dense_fold_kernel(const __grid_constant__
   const long long w0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
   const int shift = 30 - p.q;
-  for (long long b = w0; b < nblk; b += nw) {
-    ulonglong2* src = reinterpret_cast<ulonglong2*>(p.dacc + b * kBlockVox);
-    ulonglong2 v[8];
+  for (long long b0 = w0 * 32; b0 < nblk; b0 += nw * 32) {
+    const int nb = (int)min(32ll, nblk - b0);
+    unsigned touched = 0;
+    for (int j = 0; j < nb; j += 2) {
+      const ulonglong2* s0 = reinterpret_cast<const ulonglong2*>(p.dacc + (b0 + j) * kBlockVox);
+      const ulonglong2* s1 = reinterpret_cast<const ulonglong2*>(p.dacc + (b0 + min(j + 1, nb - 1)) * kBlockVox);
+      ulonglong2 v[8], w[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = src[lane + 32 * i];
-    unsigned long long any = 0;
+      for (int i = 0; i < 8; ++i) { v[i] = s0[lane + 32 * i]; w[i] = s1[lane + 32 * i]; }
+      unsigned long long av = 0, aw = 0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) any |= v[i].x | v[i].y;
-    if (!__any_sync(0xffffffffu, any != 0ull)) continue;
-    int slot = kFailed;
-    if (lane == 0) {
-      const int bx = p.dbox[0] + (int)(b % nbx), by = p.dbox[1] + (int)((b / nbx) % nby), bz = p.dbox[2] + (int)(b / ((long long)nbx * nby));
-      slot = hash_activate(p.hash, p.pool, p.ctr, pack_key(bx, by, bz), bx, by, bz);
+      for (int i = 0; i < 8; ++i) { av |= v[i].x | v[i].y; aw |= w[i].x | w[i].y; }
+      touched |= (__any_sync(0xffffffffu, av != 0ull) ? 1u : 0u) << j;
+      if (j + 1 < nb) touched |= (__any_sync(0xffffffffu, aw != 0ull) ? 1u : 0u) << (j + 1);
     }
-    slot = __shfl_sync(0xffffffffu, slot, 0);
-    longlong2* s2 = reinterpret_cast<longlong2*>(p.pool.sums) + (long long)(slot < 0 ? 0 : slot) * kBlockVox;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      if ((v[i].x | v[i].y) == 0ull) continue;
-      const int e = lane + 32 * i;   // voxels 2e, 2e + 1
-      if (slot >= 0) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const unsigned long long a = h ? v[i].y : v[i].x;
-          if (!a) continue;
-          const long long cnt = (long long)(a >> kCntShift), sd = (long long)(a & ((1ull << kCntShift) - 1));
-          longlong2 x = s2[2 * e + h];
-          x.x += (sd - cnt * p.tq) << shift;
-          x.y += cnt << 30;
-          s2[2 * e + h] = x;
-        }
+    if (!touched) continue;
+    // (2) activation, lane j <-> block b0 + j
+    const bool mine = (touched >> lane) & 1u;
+    const long long b = b0 + lane;
+    const int bx = p.dbox[0] + (int)(b % nbx), by = p.dbox[1] + (int)((b / nbx) % nby),
+              bz = p.dbox[2] + (int)(b / ((long long)nbx * nby));
+    int slot = kFailed;
+    unsigned ent = 0;
+    if (mine) slot = dense_insert(p.hash, p.ctr, pack_key(bx, by, bz), &ent);
+    const unsigned nm = __ballot_sync(0xffffffffu, mine && slot == kPending);
+    if (nm) {
+      const int lead = __ffs(nm) - 1;
+      int base = 0;
+      if (lane == lead) base = atomicAdd(&p.ctr->n_blocks, __popc(nm));
+      base = __shfl_sync(0xffffffffu, base, lead);
+      const bool isnew = (nm >> lane) & 1u;
+      bool ok = false;
+      if (isnew) {
+        slot = base + __popc(nm & ((1u << lane) - 1u));
+        if (slot >= p.pool.max_blocks) { atomicOr(&p.ctr->err, (unsigned)kErrCapacity); slot = kFailed; }
+        else { p.pool.coords[slot] = make_int4(bx, by, bz, 0); ok = true; }
       }
-      src[e] = make_ulonglong2(0ull, 0ull);
+      const int big = 0x7fffffff, small = (int)0x80000000;
+      const int lo0 = __reduce_min_sync(0xffffffffu, ok ? bx : big), hi0 = __reduce_max_sync(0xffffffffu, ok ? bx : small);
+      const int lo1 = __reduce_min_sync(0xffffffffu, ok ? by : big), hi1 = __reduce_max_sync(0xffffffffu, ok ? by : small);
+      const int lo2 = __reduce_min_sync(0xffffffffu, ok ? bz : big), hi2 = __reduce_max_sync(0xffffffffu, ok ? bz : small);
+      const unsigned nok = __popc(__ballot_sync(0xffffffffu, ok));
+      if (lane == lead && nok) {
+        atomicMin(&p.ctr->aabb_lo[0], lo0); atomicMin(&p.ctr->aabb_lo[1], lo1); atomicMin(&p.ctr->aabb_lo[2], lo2);
+        atomicMax(&p.ctr->aabb_hi[0], hi0); atomicMax(&p.ctr->aabb_hi[1], hi1); atomicMax(&p.ctr->aabb_hi[2], hi2);
+        atomicAdd(&p.ctr->new_blocks, (unsigned long long)nok);
+      }
+      __threadfence();   // coordinates before the published slots (one fence per warp, not per block)
+      if (isnew) *(volatile int*)&p.hash.e[ent].val = slot;
+    }
+    // (3) fold the touched blocks
+    for (unsigned t = touched; t; t &= t - 1) {
+      const int j = __ffs(t) - 1;
+      const int sl = __shfl_sync(0xffffffffu, slot, j);
+      ulonglong2* src = reinterpret_cast<ulonglong2*>(p.dacc + (b0 + j) * kBlockVox);
+      longlong2* s2 = reinterpret_cast<longlong2*>(p.pool.sums) + (long long)(sl < 0 ? 0 : sl) * kBlockVox;
+      ulonglong2 v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = src[lane + 32 * i];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if ((v[i].x | v[i].y) == 0ull) continue;
+        const int e = lane + 32 * i;   // voxels 2e, 2e + 1
+        if (sl >= 0) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const unsigned long long a = h ? v[i].y : v[i].x;
+            if (!a) continue;
+            const long long cnt = (long long)(a >> kCntShift), sd = (long long)(a & ((1ull << kCntShift) - 1));
+            longlong2 x = s2[2 * e + h];
+            x.x += (sd - cnt * p.tq) << shift;
+            x.y += cnt << 30;
+            s2[2 * e + h] = x;
+          }
+        }
+        src[e] = make_ulonglong2(0ull, 0ull);
+      }
     }
   }
 }
@@ -1795,7 +1913,8 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
       if (sm->dacc) cudaFreeAsync(sm->dacc, st);
       sm->dacc = nullptr;
       sm->dacc_blocks = 0;
-      const size_t bytes = (size_t)(dcap + kTrashBlocks) * kBlockVox * sizeof(unsigned long long);
+      // accumulators, the trash region, then one touched flag per block
+      const size_t bytes = (size_t)(dcap + kTrashBlocks) * kBlockVox * sizeof(unsigned long long) + (size_t)dcap;
       cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&sm->dacc), bytes, st);
       if (e != cudaSuccess) return e;
       cudaMemsetAsync(sm->dacc, 0, bytes, st);
@@ -1907,6 +2026,7 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     wp.birth = nullptr;
     wp.frame_T = B.frame_T; wp.rgbs = pp.rgbs; wp.ws = pp.ws; wp.frame_base = 0;
     wp.dacc = sm->dacc; wp.dbox = dense ? B.lcnt + 8 : nullptr; wp.dcap = dcap; wp.acc_dirty = sm->acc_dirty;
+    wp.dflag = dense ? reinterpret_cast<unsigned char*>(sm->dacc + (dcap + kTrashBlocks) * kBlockVox) : nullptr;
     const bool cw = cw_ok && total <= launch_rays;
     // constant weights, no colour, no block-count trigger: ALLOCATE runs inside the update walk
     const bool fuse = sm->fuse_alloc && cw && sm->aggregate && sm->walk_cw && !rgb && !trig;
@@ -1916,8 +2036,9 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
         if (k32) block_walk3_kernel<true><<<blocks, 256, 0, side>>>(wp);
         else block_walk3_kernel<false><<<blocks, 256, 0, side>>>(wp);
       } else if (sm->bw2) {
-        if (k32) block_walk2_kernel<true><<<blocks, 256, 0, side>>>(wp);
-        else block_walk2_kernel<false><<<blocks, 256, 0, side>>>(wp);
+        const unsigned bwb = dense ? std::min(blocks, 148u * 8u) : blocks;   // dense: grid-stride fallback only
+        if (k32) block_walk2_kernel<true><<<bwb, 256, 0, side>>>(wp);
+        else block_walk2_kernel<false><<<bwb, 256, 0, side>>>(wp);
       } else {
         if (k32) block_walk_kernel<true><<<blocks, 256, 0, side>>>(wp);
         else block_walk_kernel<false><<<blocks, 256, 0, side>>>(wp);
@@ -1937,7 +2058,8 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
         else {
           if (dense) { if (k32) walk_dw_kernel<true><<<wblocks, 128, 0, st>>>(wp); else walk_dw_kernel<false><<<wblocks, 128, 0, st>>>(wp); }
           // (dense: runs only if this launch's box exceeds the dense buffer)
-          if (k32) walk_cw_kernel<true, false><<<wblocks, 128, 0, st>>>(wp); else walk_cw_kernel<false, false><<<wblocks, 128, 0, st>>>(wp);
+          const unsigned fwb = dense ? std::min(wblocks, 148u * 16u) : wblocks;
+          if (k32) walk_cw_kernel<true, false><<<fwb, 128, 0, st>>>(wp); else walk_cw_kernel<false, false><<<fwb, 128, 0, st>>>(wp);
         }
       } else if (rgb) {
         if (cw) { if (k32) walk_kernel<true, true, true, true><<<wblocks, 128, 0, st>>>(wp); else walk_kernel<true, true, false, true><<<wblocks, 128, 0, st>>>(wp); }

@@ -348,11 +348,13 @@ def test_block_count_trigger_matches_frame_by_frame(tiny):
     assert c.integrate_until(data, poses, tiny["sensor"], tiny["grid"]["max_blocks"]) == len(frames)
 
 
-@pytest.mark.parametrize("knob", ["CVX_FUSE_ALLOC=1", "CVX_BW3=1", "CVX_BW2=0", "CVX_WALK_CW=0", "CVX_LIST_CAP=2000"])
+@pytest.mark.parametrize("knob", ["CVX_FUSE_ALLOC=1", "CVX_BW3=1", "CVX_BW2=0", "CVX_WALK_CW=0", "CVX_LIST_CAP=2000",
+                                  "CVX_DENSE=0", "CVX_DENSE_BLOCKS=4"])
 def test_walk_variants_bitexact(tiny, orc, monkeypatch, knob):
     """The tuning variants of the integrate path (ALLOCATE fused into the walk, the first block walk,
     the general walk kernel; a slot-list buffer capped so most rays find their blocks by hash lookup in
-    the walk) read at submap creation: each must give the default path's TSDF bit for bit (R1 exact
+    the walk; the slot-list path instead of the dense window (R19), chosen on the host or — with a window
+    buffer too small for any launch's box — by the device-side fallback) read at submap creation: each must give the default path's TSDF bit for bit (R1 exact
     sums) and match the oracle."""
     frames = [0, 3, 6, 9]
     ref, _ = gpu_build(tiny, frames, batch=True, finalize=False)

@@ -17,7 +17,9 @@ for w in $WHAT; do case $w in
   launches) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base mangled \
       -k regex:_ZN3cvx --csv --log-file gpurun_out/$T/launches.csv python bench.py --steps 1 --warmup 1 \
       --no-cpu-baseline --no-e2e > gpurun_out/$T/launches_bench.json 2>&1; echo "launches rc=$?";;
-  walk) cap "^walk_(cw_)?kernel" walk 2;;   # one walk launch per configs[1] submap
+  walk) cap "^walk_dw_kernel" walk 2;;   # one walk launch per configs[1] submap (dense window, R19)
+  walk_cw) CVX_DENSE=0 cap "^walk_(cw_)?kernel" walk_cw 2;;
+  dense_fold) cap "^dense_fold_kernel" dense_fold 2;;
   block_walk) cap "^block_walk[23]?_kernel" block_walk 2;;
   prepare) cap "^prepare_kernel" prepare 2;;
   fold) cap "^fold_kernel" fold 1;;
