@@ -608,6 +608,19 @@ __global__ void __launch_bounds__(256) link_line_kernel(const __grid_constant__ 
 #ifndef CVX_RING_MINB
 #define CVX_RING_MINB 7
 #endif
+#ifndef CVX_RING_BPF
+#define CVX_RING_BPF 1      // backward: masks / planes of the next chunk loaded one chunk ahead
+#endif
+#ifndef CVX_RING_EFAST
+#define CVX_RING_EFAST 0    // 1: E = (float)(s sqrt(d2)) by an fp32 root refined in fp64 (esdf_value; measured slower)
+#endif
+#ifndef CVX_RING_BUNROLL
+#define CVX_RING_BUNROLL 1  // unroll of the backward sweep over the 8 positions of a chunk (1 measured best: code size)
+#endif
+constexpr int kRingBUnroll = CVX_RING_BUNROLL;
+#ifndef CVX_RING_FSMEM
+#define CVX_RING_FSMEM 0    // 1: the forward batch goes through shared memory (rolled loop, smaller code)
+#endif
 constexpr int kRing = 16, kAhead = 12, kRingThreads = 128;
 
 __device__ __forceinline__ float rcp_approx32(float x) { float y; asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
@@ -623,7 +636,7 @@ __device__ __forceinline__ int floordiv24(int num, int den) {   // den in [2, 2^
 // (float)(s * sqrt(d2)) correctly rounded as in fp64 (O11, the value the oracle computes), d2 < 2^24: an
 // fp32 square root refined once in fp64 (relative error < 2^-44), rounded to fp32; only when the fp64
 // value lies within 2^-40 (relative) of an fp32 rounding boundary is the IEEE fp64 sqrt taken.
-__device__ __forceinline__ float esdf_value(double s, unsigned d2) {
+[[maybe_unused]] __device__ __forceinline__ float esdf_value(double s, unsigned d2) {
   const float df = (float)d2;                               // exact (< 2^24)
   const float r = sqrtf(df);                                // |r - sqrt(d2)| <= ~1 ulp (fp32)
   if (r == 0.f) return 0.f;
@@ -662,15 +675,28 @@ __global__ void __launch_bounds__(kRingThreads, CVX_RING_MINB) ring_line_kernel(
   unsigned fa[8];
 #pragma unroll
   for (int u = 0; u < 8; ++u) fa[u] = raw_at(u);
+#if CVX_RING_FSMEM
+  __shared__ unsigned fsm[8][kRingThreads];
+#endif
   for (int q0 = 0; q0 < m; q0 += 8) {
     unsigned fb[8];
     const int qn = q0 + 8 < m ? q0 + 8 : q0;
 #pragma unroll
     for (int u = 0; u < 8; ++u) fb[u] = raw_at(qn + u);
+#if CVX_RING_FSMEM
 #pragma unroll
+    for (int u = 0; u < 8; ++u) fsm[u][threadIdx.x] = fa[u];
+#pragma unroll 1
+#else
+#pragma unroll
+#endif
     for (int u = 0; u < 8; ++u) {
       const int q = q0 + u;
+#if CVX_RING_FSMEM
+      const unsigned fq = f_of(fsm[u][threadIdx.x]);
+#else
       const unsigned fq = f_of(fa[u]);
+#endif
       if (fq == kInf32) continue;
       while (k >= 0) {
         const int a = t_top - s_top, c = t_top - q;
@@ -729,20 +755,28 @@ __global__ void __launch_bounds__(kRingThreads, CVX_RING_MINB) ring_line_kernel(
     }
   };
   const int qlast = ((m - 1) >> 3) << 3;
+#if CVX_RING_BPF
   int slot = chunk_slot(qlast);
   load_planes(slot);
   int nslot = chunk_slot(qlast - 8);
+#endif
   for (int q0 = qlast; q0 >= 0; q0 -= 8) {
     unsigned obsw = 0, negw = 0;   // pass z: bit u = observed / negative of position q0 + u
+#if !CVX_RING_BPF
+    const int slot = chunk_slot(q0);
+    load_planes(slot);
+#endif
     if (kZ && slot >= 0) {
 #pragma unroll
       for (int u = 0; u < 8; ++u) { obsw |= ((ow[u] >> (lb & 31)) & 1u) << u; negw |= ((nw[u] >> (lb & 31)) & 1u) << u; }
     }
     const int cur = slot;
+#if CVX_RING_BPF
     slot = nslot;
     load_planes(slot);                     // chunk q0 - 8
     nslot = chunk_slot(q0 - 16);
-#pragma unroll
+#endif
+#pragma unroll kRingBUnroll
     for (int u = 7; u >= 0; --u) {
       const int q = q0 + u;
       unsigned d2 = kInf32;
@@ -755,7 +789,11 @@ __global__ void __launch_bounds__(kRingThreads, CVX_RING_MINB) ring_line_kernel(
         if (!obs) e = __int_as_float(0x7fc00000);
         else if (d2 == kInf32) e = p.capped ? (float)(neg ? -p.dmax : p.dmax) : __int_as_float(0x7f800000);
         else {
+#if CVX_RING_EFAST
           e = esdf_value(p.s, d2);
+#else
+          e = (float)(p.s * sqrt((double)d2));
+#endif
           if (p.capped && (double)e > p.dmax) e = (float)p.dmax;
           if (neg) e = -e;
         }
