@@ -96,10 +96,27 @@ struct XParams {
   double site_thr;
 };
 
+__device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
 #ifndef CVX_XCH
 #define CVX_XCH 4
 #endif
 constexpr int kXCh = CVX_XCH;   // chunks (32 voxels each) whose loads a warp issues together in pass x
+#ifndef CVX_XPIPE
+#define CVX_XPIPE 0             // pass x: 1 = cp.async ring of kXDepth chunks per warp instead of kXCh batches (measured: no gain)
+#endif
+#ifndef CVX_XDEPTH
+#define CVX_XDEPTH 8
+#endif
+constexpr int kXDepth = CVX_XDEPTH;
+// dynamic shared memory of pass_x_kernel: per warp msk / prv / nxt [nch], the CTA's plane bytes [3][nbx][4],
+// then (CVX_XPIPE) per warp a ring of kXDepth chunks x 32 lanes x 16 bytes
+__host__ __device__ inline size_t xring_off(int nch, int nbx) {
+  return (((size_t)4 * 3 * nch * 4 + (size_t)3 * nbx * 4) + 15) & ~(size_t)15;
+}
+__host__ __device__ inline size_t xsmem_bytes(int nch, int nbx) {
+  return xring_off(nch, nbx) + (CVX_XPIPE ? (size_t)4 * kXDepth * 32 * 16 : 0);
+}
 
 __global__ void __launch_bounds__(128) pass_x_kernel(const __grid_constant__ XParams p) {
   extern __shared__ __align__(1024) unsigned char dsmem[];
@@ -126,6 +143,50 @@ __global__ void __launch_bounds__(128) pass_x_kernel(const __grid_constant__ XPa
     // 1) sites of the row -> one 32-bit mask per chunk; the block's observed / sign / site plane bytes.
     //    kXCh chunks per round: their slot look-ups, then their TSDF loads, are issued back to back so
     //    every warp keeps kXCh 512-byte requests in flight (the row loop is otherwise latency-bound).
+#if CVX_XPIPE
+    // cp.async pipeline: the TSDF sums of chunk c + kXDepth are copied into this warp's shared ring while
+    // chunk c is classified (the slot of the chunk after that is loaded one chunk ahead, in a register)
+    {
+      longlong2* ring = reinterpret_cast<longlong2*>(dsmem + xring_off(nch, p.nbx)) + warp * kXDepth * 32;
+      auto slot_of = [&](int c) -> int {
+        const int x = (c << 5) + lane;
+        return (c < nch && x < p.nx) ? grow[x >> 3] : -1;
+      };
+      auto issue = [&](int c, int sl) {
+        longlong2* dst = ring + (c % kXDepth) * 32 + lane;
+        if (sl >= 0) {
+          const longlong2* src = reinterpret_cast<const longlong2*>(p.sums) + (long long)sl * kBlockVox + (lane & 7) + lyz;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(smem_addr(dst)), "l"(src) : "memory");
+        } else {
+          *dst = make_longlong2(0, 0);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      };
+      for (int c = 0; c < kXDepth; ++c) issue(c, slot_of(c));
+      int nsl = slot_of(kXDepth);
+      for (int c = 0; c < nch; ++c) {
+        asm volatile("cp.async.wait_group %0;" :: "n"(kXDepth - 1) : "memory");
+        const volatile long long* rv = reinterpret_cast<volatile long long*>(ring + (c % kXDepth) * 32 + lane);
+        const longlong2 sw = make_longlong2(rv[0], rv[1]);
+        const int sl = nsl;
+        nsl = slot_of(c + kXDepth + 1);
+        issue(c + kXDepth, sl);
+        bool obs, neg, site;
+        classify_voxel(sw, p.site_thr, obs, neg, site);
+        const unsigned bs = __ballot_sync(0xffffffffu, site);
+        const unsigned bo = __ballot_sync(0xffffffffu, obs);
+        const unsigned bn = __ballot_sync(0xffffffffu, neg);
+        if (lane == 0) msk[c] = bs;
+        if ((lane & 7) == 0 && ((c << 5) + lane) < p.nx) {   // one lane per block: its row bytes
+          const int blk = ((c << 5) + lane) >> 3;
+          pb[(0 * p.nbx + blk) * 4 + (y & 3)] = (unsigned char)(bo >> lane);
+          pb[(1 * p.nbx + blk) * 4 + (y & 3)] = (unsigned char)(bn >> lane);
+          pb[(2 * p.nbx + blk) * 4 + (y & 3)] = (unsigned char)(bs >> lane);
+        }
+      }
+      asm volatile("cp.async.wait_all;" ::: "memory");
+    }
+#else
     for (int c0 = 0; c0 < nch; c0 += kXCh) {
       int slot[kXCh];
 #pragma unroll
@@ -155,6 +216,7 @@ __global__ void __launch_bounds__(128) pass_x_kernel(const __grid_constant__ XPa
         }
       }
     }
+#endif
     __syncwarp();
     // 2) nearest site strictly before / after each chunk (warp scans over groups of 32 chunks)
     int carry = kNeg;
@@ -208,7 +270,6 @@ __global__ void __launch_bounds__(128) pass_x_kernel(const __grid_constant__ XPa
 }
 
 // ------------------------------------------------------------------------------ TMA / mbarrier helpers
-__device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_addr(bar)), "r"(count) : "memory");
 }
@@ -1104,7 +1165,7 @@ cudaError_t dense_edt(cvx_submap* sm, const int lo[3], const int hi[3], cudaStre
   xp.sums = sm->pool.sums; xp.planes = planes; xp.grid = sm->block_grid; xp.g1 = g1; xp.rowmask = rowmask;
   xp.nx = nx; xp.ny = ny; xp.nz = nz; xp.nbx = nbx; xp.nby = nby; xp.site_thr = sm->cfg.site_threshold;
   const int nch = (nx + 31) / 32;
-  const size_t smem = (size_t)4 * 3 * nch * sizeof(unsigned) + (size_t)3 * nbx * 4;
+  const size_t smem = xsmem_bytes(nch, nbx);
   if (smem > 48 * 1024) cudaFuncSetAttribute(pass_x_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const long long rows = (long long)ny * nz;
   const unsigned xblocks = (unsigned)std::min<long long>(rows / 4, 148ll * 16);

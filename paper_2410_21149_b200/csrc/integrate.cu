@@ -1416,11 +1416,11 @@ __global__ void __launch_bounds__(128, CVX_DW_MINB) walk_dw_kernel(const __grid_
     const unsigned utq2 = (unsigned)tq2;
     for (; it < mw; ++it) {
       const unsigned prev = __shfl_up_sync(0xffffffffu, addr, 1);
-      const bool head = lane0 | (prev != addr);
+      const bool head = lane0 | (prev != addr) | !have;   // an idle lane is its own run ...
       const unsigned stops = __ballot_sync(0xffffffffu, head);
       const unsigned len = run_len(stops & above_mask, lane);
       const unsigned long long val = ((unsigned long long)(len << (kCntShift - 32)) << 32) | (len * utq2);
-      DW_RED(acc, addr, val, head);
+      DW_RED(acc, addr, val, head & have);                 // ... and issues no reduction
       const bool g0 = k0 > 0, g1 = k1 > 0, g2 = k2 > 0;
       const bool yf = g1 & (!g0 | ((ST)D01 > 0));
       const bool zf = g2 & (yf ? ((ST)D12 > 0) : (!g0 | ((ST)D02 > 0)));
@@ -1441,19 +1441,20 @@ __global__ void __launch_bounds__(128, CVX_DW_MINB) walk_dw_kernel(const __grid_
     const unsigned spot = trash + ((((unsigned)idx >> 5) & 4095u) << 3);
     int dx0 = da0;
     unsigned ex0 = e0;
-    if (it >= n) { addr = spot; k0 = 0x3fffffff; k1 = 0; k2 = 0; dx0 = 0; cexp = 1u; S = (long long)tq2 << (kSdfF + 1); U0 = 0; n = 0x7fffffff; }
+    bool parked = it >= n;
+    if (parked) { addr = spot; k0 = 0x3fffffff; k1 = 0; k2 = 0; dx0 = 0; cexp = 1u; S = (long long)tq2 << (kSdfF + 1); U0 = 0; n = 0x7fffffff; }
     for (; it < maxn; ++it) {
       const int dpi = min(max((int)(S >> kSdfF), 0), tq2);   // round(sdf 2^q) + tq, clamped (O5, Q4)
       const unsigned key = dpi == tq2 ? addr : 0xffffffffu;     // only clamped updates merge
       const unsigned prev = __shfl_up_sync(0xffffffffu, key, 1);
-      const bool head = lane0 | (prev != key) | (key == 0xffffffffu);
+      const bool head = lane0 | (prev != key) | (key == 0xffffffffu) | parked;   // a parked lane is its own run ...
       const unsigned stops = __ballot_sync(0xffffffffu, head);
       const unsigned len = run_len(stops & above_mask, lane);
       const unsigned long long val = ((unsigned long long)(len << (kCntShift - 32)) << 32) | (len * (unsigned)dpi);
-      DW_RED(acc, addr, val, head);
+      DW_RED(acc, addr, val, head & !parked);                  // ... and issues no reduction
       if (it + 1 >= n) {   // that was the ray's last voxel: park
         addr = spot; k0 = 0x3fffffff; k1 = 0; k2 = 0; dx0 = 0; cexp = 1u; S = (long long)tq2 << (kSdfF + 1); U0 = 0;
-        n = 0x7fffffff; ex0 = 0u;
+        n = 0x7fffffff; ex0 = 0u; parked = true;
       }
       const bool g0 = k0 > 0, g1 = k1 > 0, g2 = k2 > 0;
       const bool yf = g1 & (!g0 | ((ST)D01 > 0));
