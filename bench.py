@@ -196,6 +196,7 @@ def cpu_baseline_sample(cfg, data, poses, n=20):
 
 
 NCU_FILES = {"ray_walk_update": "ncu_walk.txt", "block_walk_allocate": "ncu_block_walk.txt",
+             "dense_fold_allocate": "ncu_dense_fold.txt",
              "ray_prepare": "ncu_prepare.txt", "esdf_pass_x": "ncu_esdf_pass_x.txt",
              "esdf_pass_y": "ncu_esdf_pass_y.txt", "esdf_pass_z": "ncu_esdf_pass_z.txt", "fold": "ncu_fold.txt"}
 
@@ -1053,11 +1054,12 @@ def main():
     alg_bytes = esdf_alg_bytes(va, nvox_dense)
     alg_bytes["reset_zero_blocks"] = 16 * va
     n_rays_launch = st["rays_in"] / max(1, prof.get("ray_prepare", {"n": 1})["n"] / K)
-    alg_bytes["ray_prepare"] = int(n_rays_launch * (12 + 96))
+    alg_bytes["ray_prepare"] = int(n_rays_launch * (12 + 48))   # 12 B point in, 48 B ray record out
     dom = max(per_step, key=per_step.get)
     esdf_ms = sum(v for k, v in per_step_serial.items() if k.startswith("esdf_"))
     integ_ms = sum(v for k, v in per_step_serial.items()
-                   if k in ("compose_poses", "ray_prepare", "block_walk_allocate", "ray_walk_update", "fold"))
+                   if k in ("compose_poses", "ray_prepare", "block_walk_allocate", "ray_walk_update", "fold",
+                            "dense_fold_allocate"))
     walk = prof.get("ray_walk_update", {"ms": 0.0, "n": 1})
     updates_per_step = st["voxel_updates"]
     roofline = {}
@@ -1089,8 +1091,9 @@ def main():
     roofline["traffic"] = tr["bytes_per_launch"] if tr else None   # DRAM bytes per launch (ncu)
     roofline["traffic_source"] = tr["source"] if tr else None
     if dom == "ray_walk_update":
-        # the walk's real ceiling is the issue rate (one warp instruction per SMSP per clock): ncu's issue
-        # utilisation of the same kernel says how close the instruction stream is to it
+        # what binds the walk: with the dense window (R19) its instruction stream alone would
+        # run in ~3.7 ms (reductions removed, CVX_DW_EXP=1); the L2 reductions are the rest — ncu's issue
+        # utilisation and the RED sector rate against the measured L2 reduction ceiling say how close each is
         roofline["ncu_issue_slots_busy"] = ncu_metric(dom, "Issue Slots Busy")
         roofline["l2_red"] = l2_red_view(dom)
     line = {

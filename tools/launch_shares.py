@@ -10,7 +10,9 @@ import re
 import sys
 from collections import defaultdict
 
-NAMES = [("prepare_kernel", "ray_prepare"), ("block_walk_kernel", "block_walk_allocate"),
+NAMES = [("prepare_kernel", "ray_prepare"), ("box_reduce_kernel", "ray_prepare"), ("walk_dw_kernel", "ray_walk_update"),
+         ("dense_fold_kernel", "dense_fold_allocate"), ("ring_line_kernel<0", "esdf_pass_y"), ("ring_line_kernel<1", "esdf_pass_z"),
+         ("ring_line_kernel<false", "esdf_pass_y"), ("ring_line_kernel<true", "esdf_pass_z"), ("block_walk_kernel", "block_walk_allocate"),
          ("block_walk2_kernel", "block_walk_allocate"), ("block_walk3_kernel", "block_walk_allocate"),
          ("walk_cw_kernel", "ray_walk_update"), ("link_line_kernel<0", "esdf_pass_y"), ("link_line_kernel<1", "esdf_pass_z"),
          ("link_line_kernel<false", "esdf_pass_y"), ("link_line_kernel<true", "esdf_pass_z"),

@@ -16,7 +16,7 @@ json.dump(bench, open(os.path.join(dst, "bench.json"), "w"), indent=1)
 shutil.copy(os.path.join(src, "launches.csv"), os.path.join(dst, "launches.csv"))
 shares = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "launch_shares.py"), os.path.join(src, "launches.csv"),
                          os.path.join(src, "bench.json")], capture_output=True, text=True).stdout
-kern = ["walk", "block_walk", "prepare", "fold", "esdf_pass_x", "esdf_pass_y", "esdf_pass_z", "query", "project",
+kern = ["walk", "walk_cw", "dense_fold", "block_walk", "prepare", "fold", "esdf_pass_x", "esdf_pass_y", "esdf_pass_z", "query", "project",
         "stress_pass_x", "stress_pass_y", "stress_pass_z", "inc_window"]
 summ = {}
 for k in kern:
