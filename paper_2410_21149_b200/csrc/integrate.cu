@@ -1497,7 +1497,14 @@ __device__ __forceinline__ int dense_insert(const HashView& h, Counters* ctr, un
   return kFailed;
 }
 
-// R19 ALLOCATE + FOLD of a dense-window launch.  A warp takes 32 consecutive blocks of the box: (1) it
+// blocks of the box per warp pass of dense_fold_kernel (<= 32): small groups spread the touched blocks of
+// dense regions over more warps (each touched block is folded by its warp one after the other)
+#ifndef CVX_FOLD_GROUP
+#define CVX_FOLD_GROUP 4
+#endif
+constexpr int kFoldGroup = CVX_FOLD_GROUP;
+
+// R19 ALLOCATE + FOLD of a dense-window launch.  A warp takes kFoldGroup consecutive blocks of the box: (1) it
 // reads their accumulators (two blocks in flight) — a block whose accumulators are not all zero was
 // traversed by a ray (every traversed voxel receives a count >= 1); (2) lane j activates block j if it
 // was touched (insert-if-absent; the pool slots of the new blocks are bumped once per warp, P:L124,
@@ -1512,8 +1519,8 @@ __global__ void __launch_bounds__(256) dense_fold_kernel(const __grid_constant__
   const long long w0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
   const int shift = 30 - p.q;
-  for (long long b0 = w0 * 32; b0 < nblk; b0 += nw * 32) {
-    const int nb = (int)min(32ll, nblk - b0);
+  for (long long b0 = w0 * kFoldGroup; b0 < nblk; b0 += nw * kFoldGroup) {
+    const int nb = (int)min((long long)kFoldGroup, nblk - b0);
     unsigned touched = 0;
     for (int j = 0; j < nb; j += 2) {
       const ulonglong2* s0 = reinterpret_cast<const ulonglong2*>(p.dacc + (b0 + j) * kBlockVox);
@@ -1529,7 +1536,7 @@ __global__ void __launch_bounds__(256) dense_fold_kernel(const __grid_constant__
     }
     if (!touched) continue;
     // (2) activation, lane j <-> block b0 + j
-    const bool mine = (touched >> lane) & 1u;
+    const bool mine = lane < kFoldGroup && ((touched >> lane) & 1u);
     const long long b = b0 + lane;
     const int bx = p.dbox[0] + (int)(b % nbx), by = p.dbox[1] + (int)((b / nbx) % nby),
               bz = p.dbox[2] + (int)(b / ((long long)nbx * nby));
