@@ -1323,6 +1323,9 @@ __global__ void __launch_bounds__(256) box_reduce_kernel(const int* cta_box, int
 #define DW_RED(acc, addr, val, head) asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.relaxed.gpu.global.add.u64 [%0], %1;\n\t}" \
                    :: "l"((acc) + (addr)), "l"(val), "r"((unsigned)(head)) : "memory")
 #endif
+#ifndef CVX_DW_UNIFORM
+#define CVX_DW_UNIFORM 0   // 1: free prefix takes a warp-uniform path when no two adjacent lanes share a voxel (measured slower)
+#endif
 #ifndef CVX_DW_FLAGS
 #define CVX_DW_FLAGS 0
 #endif
@@ -1418,9 +1421,19 @@ __global__ void __launch_bounds__(128, CVX_DW_MINB) walk_dw_kernel(const __grid_
       const unsigned prev = __shfl_up_sync(0xffffffffu, addr, 1);
       const bool head = lane0 | (prev != addr) | !have;   // an idle lane is its own run ...
       const unsigned stops = __ballot_sync(0xffffffffu, head);
+#if CVX_DW_UNIFORM
+      if (stops == 0xffffffffu) {                          // every lane its own run (far field): len = 1
+        DW_RED(acc, addr, (1ull << kCntShift) | utq2, have);
+      } else {
+        const unsigned len = run_len(stops & above_mask, lane);
+        const unsigned long long val = ((unsigned long long)(len << (kCntShift - 32)) << 32) | (len * utq2);
+        DW_RED(acc, addr, val, head & have);               // ... and issues no reduction
+      }
+#else
       const unsigned len = run_len(stops & above_mask, lane);
       const unsigned long long val = ((unsigned long long)(len << (kCntShift - 32)) << 32) | (len * utq2);
       DW_RED(acc, addr, val, head & have);                 // ... and issues no reduction
+#endif
       const bool g0 = k0 > 0, g1 = k1 > 0, g2 = k2 > 0;
       const bool yf = g1 & (!g0 | ((ST)D01 > 0));
       const bool zf = g2 & (yf ? ((ST)D12 > 0) : (!g0 | ((ST)D02 > 0)));
