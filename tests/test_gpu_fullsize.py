@@ -54,6 +54,24 @@ def test_fullsize_count_identity_and_batch_independence(lidar, built):
     assert np.array_equal(D7.view(np.uint32), D.view(np.uint32)) and np.array_equal(W7.view(np.uint32), W.view(np.uint32))
 
 
+@pytest.mark.parametrize("knob", ["CVX_DENSE=0", "CVX_DENSE_BLOCKS=100000"])
+def test_fullsize_dense_window_equals_slot_list_path(lidar, built, monkeypatch, knob):
+    """DESIGN.md R19 at full size: the default dense-window path (ALLOCATE after the walk) and the slot-list
+    path — chosen on the host (CVX_DENSE=0) or by the device-side fallback, with a window buffer (1e5
+    blocks) smaller than the launch's box (~2.3e5 blocks) — give the same blocks and the same TSDF bit for
+    bit."""
+    cfg, data, poses = lidar
+    _, (b, D, W, _), st = built
+    k, v = knob.split("=")
+    monkeypatch.setenv(k, v)
+    sm = _build(cfg, data, poses, BATCH, finalize=False)
+    b2, D2, W2, _ = gpu_export_sorted(sm)
+    assert np.array_equal(b2, b)
+    assert np.array_equal(D2.view(np.uint32), D.view(np.uint32)) and np.array_equal(W2.view(np.uint32), W.view(np.uint32))
+    st2 = sm.stats()
+    assert st2["voxel_updates"] == st["voxel_updates"] and st2["total_blocks"] == st["total_blocks"]
+
+
 def test_fold_inside_one_call_is_exact(lidar):
     """300 scans in one call pass the packed-accumulator limit (2^24 - 1 rays, R6/R7), so the library folds
     inside the call; the state must equal two separate calls bit for bit."""
