@@ -519,6 +519,7 @@ __global__ void __launch_bounds__(256) pba_line_kernel(const __grid_constant__ C
 // per pushed position and re-reads f, pass z stores the full state below (u64 {f: 32, t: 16, prev: 16})
 // so a pop is one load.  Same outputs as pba_line_kernel.
 struct LinkParams {
+  const unsigned char* rowmask;   // ring kernel, pass y: (by, bz) block rows with allocated blocks
   const void* fin;                // pass y: u16 1-D distances; pass z: u32 squared distances
   unsigned* g2;                   // pass y output
   void* meta;                     // stack links (8 bytes per AABB voxel)
@@ -679,6 +680,9 @@ __global__ void __launch_bounds__(256) link_line_kernel(const __grid_constant__ 
 #define CVX_RING_BUNROLL 1  // unroll of the backward sweep over the 8 positions of a chunk (1 measured best: code size)
 #endif
 constexpr int kRingBUnroll = CVX_RING_BUNROLL;
+#ifndef CVX_RING_ROWSKIP
+#define CVX_RING_ROWSKIP 1  // pass y: skip the y batches of block rows without allocated blocks
+#endif
 #ifndef CVX_RING_FSMEM
 #define CVX_RING_FSMEM 0    // 1: the forward batch goes through shared memory (rolled loop, smaller code)
 #endif
@@ -733,17 +737,30 @@ __global__ void __launch_bounds__(kRingThreads, CVX_RING_MINB) ring_line_kernel(
   int s_top = 0, t_top = 0;
   unsigned f_top = 0;
   // forward (m is a multiple of 8): the loads of batch q0 + 8 are issued before batch q0 is consumed
+  // pass y: an x-row block row (by, bz) without allocated blocks has no site, so f = inf on its 8 y
+  // positions: such batches are neither loaded nor scanned (sparse AABBs: LiDAR / MAV submaps)
+  auto row_has = [&](int q) -> bool {
+    return kZ || !CVX_RING_ROWSKIP || p.rowmask[(long long)(o2 >> 3) * p.nby + (q >> 3)] != 0;
+  };
   unsigned fa[8];
+  bool ha = row_has(0);
 #pragma unroll
-  for (int u = 0; u < 8; ++u) fa[u] = raw_at(u);
+  for (int u = 0; u < 8; ++u) fa[u] = ha ? raw_at(u) : kNone16;
 #if CVX_RING_FSMEM
   __shared__ unsigned fsm[8][kRingThreads];
 #endif
   for (int q0 = 0; q0 < m; q0 += 8) {
     unsigned fb[8];
     const int qn = q0 + 8 < m ? q0 + 8 : q0;
+    const bool hb = row_has(qn);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) fb[u] = raw_at(qn + u);
+    for (int u = 0; u < 8; ++u) fb[u] = hb ? raw_at(qn + u) : kNone16;
+    if (!ha) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) fa[u] = fb[u];
+      ha = hb;
+      continue;
+    }
 #if CVX_RING_FSMEM
 #pragma unroll
     for (int u = 0; u < 8; ++u) fsm[u][threadIdx.x] = fa[u];
@@ -785,6 +802,7 @@ __global__ void __launch_bounds__(kRingThreads, CVX_RING_MINB) ring_line_kernel(
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) fa[u] = fb[u];
+    ha = hb;
   }
   // backward: the entries below the top in decreasing index order; entry j < lo is copied into its ring
   // slot by cp.async kAhead pops before it is needed (one commit group per pop, empty when j >= lo)
@@ -1179,6 +1197,7 @@ cudaError_t dense_edt(cvx_submap* sm, const int lo[3], const int hi[3], cudaStre
   if (kernel == 0 || kernel == 2) {
     LinkParams lp{};
     lp.fin = g1; lp.g2 = g2; lp.meta = meta; lp.esdf = sm->pool.esdf; lp.grid = sm->block_grid; lp.colmask = colmask;
+    lp.rowmask = rowmask;
     lp.planes = planes; lp.nx = nx; lp.ny = ny; lp.nz = nz; lp.nbx = nbx; lp.nby = nby; lp.s = sm->cfg.voxel_size;
     lp.capped = capped ? 1 : 0; lp.dmax = dmax;
     {
