@@ -680,6 +680,9 @@ __global__ void __launch_bounds__(256) link_line_kernel(const __grid_constant__ 
 #define CVX_RING_BUNROLL 1  // unroll of the backward sweep over the 8 positions of a chunk (1 measured best: code size)
 #endif
 constexpr int kRingBUnroll = CVX_RING_BUNROLL;
+#ifndef CVX_RING_BSKIP
+#define CVX_RING_BSKIP 0    // 1: backward of pass z skips chunks no lane of the warp writes (measured: no gain; pass y slower)
+#endif
 #ifndef CVX_RING_ROWSKIP
 #define CVX_RING_ROWSKIP 1  // pass y: skip the y batches of block rows without allocated blocks
 #endif
@@ -854,6 +857,19 @@ __global__ void __launch_bounds__(kRingThreads, CVX_RING_MINB) ring_line_kernel(
     slot = nslot;
     load_planes(slot);                     // chunk q0 - 8
     nslot = chunk_slot(q0 - 16);
+#endif
+#if CVX_RING_BSKIP
+    if (kZ && __all_sync(__activemask(), cur < 0)) {   // no lane writes this chunk: only its pops (t strictly
+      while (k >= 0 && t_top >= q0) {            // decreases down the stack)
+        if (--k >= 0) {
+          if (k < lo) asm volatile("cp.async.wait_group %0;" :: "n"(kAhead - 1) : "memory");
+          const unsigned long long e = *(volatile unsigned long long*)(rg + (k & (kRing - 1)) * kRingThreads);
+          s_top = (int)(e & 0xffffu); t_top = (int)((e >> 16) & 0xffffu); f_top = (unsigned)(e >> 32);
+          issue(k - kAhead);
+        }
+      }
+      continue;
+    }
 #endif
 #pragma unroll kRingBUnroll
     for (int u = 7; u >= 0; --u) {
