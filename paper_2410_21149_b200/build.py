@@ -47,5 +47,19 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+BOUNDS_LIB = os.path.join(HERE, "libcvx_bounds.so")
+
+
+def build_bounds(force: bool = False) -> str:
+    """The same library with the device-side bounds checks of CVX_BOUNDS=1 (cvx_internal.cuh)."""
+    if not force and os.path.exists(BOUNDS_LIB) and all(os.path.getmtime(d) <= os.path.getmtime(BOUNDS_LIB) for d in deps()):
+        return BOUNDS_LIB
+    nvcc = os.environ.get("NVCC", "nvcc")
+    cmd = [nvcc, *NVCC_FLAGS, "-DCVX_BOUNDS=1", "-I", os.path.join(ROOT, "include"), "-o", BOUNDS_LIB + ".tmp", *sources()]
+    subprocess.check_call(cmd)
+    os.replace(BOUNDS_LIB + ".tmp", BOUNDS_LIB)
+    return BOUNDS_LIB
+
+
 if __name__ == "__main__":
     print(build(force=True, verbose=True))

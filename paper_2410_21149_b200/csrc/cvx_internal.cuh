@@ -14,6 +14,26 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// Bounds-checked build (CVX_BOUNDS=1, tests/test_gpu_bounds.py): the hot kernels check the indices of
+// their global writes / reductions and trap with a message on a violation (compute-sanitizer's memcheck
+// is not available on every GPU pool).  Compiled out otherwise.
+#ifndef CVX_BOUNDS
+#define CVX_BOUNDS 0
+#endif
+#if CVX_BOUNDS
+#include <cstdio>
+#define CVX_CHECK(cond, what)                                                                       \
+  do {                                                                                              \
+    if (!(cond)) {                                                                                  \
+      printf("cvx bounds check failed: %s (%s:%d) block %d thread %d\n", what, __FILE__, __LINE__,   \
+             (int)blockIdx.x, (int)threadIdx.x);                                                    \
+      __trap();                                                                                     \
+    }                                                                                               \
+  } while (0)
+#else
+#define CVX_CHECK(cond, what) do { } while (0)
+#endif
+
 namespace cvx {
 
 constexpr int kBlockSide = 8;

@@ -94,6 +94,7 @@ struct XParams {
   unsigned short* g1;
   int nx, ny, nz, nbx, nby;
   double site_thr;
+  int max_blocks;
 };
 
 __device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -246,6 +247,7 @@ __global__ void __launch_bounds__(128) pass_x_kernel(const __grid_constant__ XPa
     __syncwarp();
     // 3) exact 1-D distance along x
     unsigned short* out = p.g1 + row * p.nx;
+    CVX_CHECK(row < (long long)p.ny * p.nz, "pass x row");
     for (int c = 0; c < nch; ++c) {
       const int x = (c << 5) + lane;
       if (x >= p.nx) break;
@@ -263,6 +265,7 @@ __global__ void __launch_bounds__(128) pass_x_kernel(const __grid_constant__ XPa
     for (int i = threadIdx.x; i < 3 * p.nbx; i += blockDim.x) {
       const int pl = i / p.nbx, blk = i % p.nbx;
       const int slot = grow[blk];
+      CVX_CHECK(slot < p.max_blocks, "pass x plane slot");
       if (slot >= 0) p.planes[(long long)slot * kPlaneWords + 16 * pl + w] = reinterpret_cast<const unsigned*>(pb)[i];
     }
     __syncthreads();
@@ -785,6 +788,7 @@ __global__ void __launch_bounds__(kRingThreads, CVX_RING_MINB) ring_line_kernel(
         if (--k < 0) break;
         if (k < lo) {                      // below the ring's window: refill kRing entries from the array
           const int j0 = max(0, k - (kRing - 1));
+          CVX_CHECK(j0 >= 0 && k < lo && k < m, "ring refill range");
           for (int j = j0; j <= k; ++j) rg[(j & (kRing - 1)) * kRingThreads] = gst[j];
           lo = j0;
         }
@@ -799,6 +803,7 @@ __global__ void __launch_bounds__(kRingThreads, CVX_RING_MINB) ring_line_kernel(
       }
       ++k;
       unsigned long long* slot = rg + (k & (kRing - 1)) * kRingThreads;
+      CVX_CHECK(k < m, "ring stack depth <= line length");
       if (k - kRing >= lo) { gst[k - kRing] = *slot; lo = k - kRing + 1; }   // displaced: write back
       *slot = ((unsigned long long)fq << 32) | ((unsigned)tq << 16) | (unsigned)q;
       s_top = q; t_top = tq; f_top = fq;
@@ -876,6 +881,7 @@ __global__ void __launch_bounds__(kRingThreads, CVX_RING_MINB) ring_line_kernel(
       const int q = q0 + u;
       unsigned d2 = kInf32;
       if (k >= 0) { const int dq = q - s_top; d2 = (unsigned)(dq * dq) + f_top; }
+      CVX_CHECK(base + (long long)q * stride < (long long)p.nx * p.ny * p.nz, "line pass output index");
       if (!kZ) {
         if (cur >= 0) p.g2[base + (long long)q * stride] = d2;
       } else if (cur >= 0) {
@@ -1198,6 +1204,7 @@ cudaError_t dense_edt(cvx_submap* sm, const int lo[3], const int hi[3], cudaStre
   XParams xp;
   xp.sums = sm->pool.sums; xp.planes = planes; xp.grid = sm->block_grid; xp.g1 = g1; xp.rowmask = rowmask;
   xp.nx = nx; xp.ny = ny; xp.nz = nz; xp.nbx = nbx; xp.nby = nby; xp.site_thr = sm->cfg.site_threshold;
+  xp.max_blocks = sm->pool.max_blocks;
   const int nch = (nx + 31) / 32;
   const size_t smem = xsmem_bytes(nch, nbx);
   if (smem > 48 * 1024) cudaFuncSetAttribute(pass_x_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

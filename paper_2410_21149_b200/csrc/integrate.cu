@@ -1140,6 +1140,7 @@ __device__ __forceinline__ void walk_cw_body(const WalkParams& p, const int idx)
       const unsigned len = run_len(stops & (0xfffffffeu << lane), lane);
       // len * (2^40 | dpi) as two 32-bit halves: hi = len << 8, lo = len * dpi (< 2^22, no carry)
       const unsigned long long val = ((unsigned long long)(len << (kCntShift - 32)) << 32) | (len * (unsigned)dpi);
+      CVX_CHECK(!head || (long long)addr < ((long long)p.pool.max_blocks + kTrashBlocks) * kBlockVox, "pool accumulator address");
       asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.relaxed.gpu.global.add.u64 [%0], %1;\n\t}"
                    :: "l"(acc + addr), "l"(val), "r"((unsigned)head) : "memory");
     }
@@ -1184,6 +1185,7 @@ __device__ __forceinline__ void walk_cw_body(const WalkParams& p, const int idx)
       const unsigned stops = __ballot_sync(0xffffffffu, head);
       const unsigned len = run_len(stops & above_mask, lane);
       const unsigned long long val = ((unsigned long long)(len << (kCntShift - 32)) << 32) | (len * utq2);
+      CVX_CHECK(!head || (long long)addr < ((long long)p.pool.max_blocks + kTrashBlocks) * kBlockVox, "pool accumulator address");
       asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.relaxed.gpu.global.add.u64 [%0], %1;\n\t}"
                    :: "l"(acc + addr), "l"(val), "r"((unsigned)head) : "memory");
       const bool g0 = k0 > 0, g1 = k1 > 0, g2 = k2 > 0;
@@ -1229,6 +1231,7 @@ __device__ __forceinline__ void walk_cw_body(const WalkParams& p, const int idx)
       const unsigned stops = __ballot_sync(0xffffffffu, head);
       const unsigned len = run_len(stops & above_mask, lane);
       const unsigned long long val = ((unsigned long long)(len << (kCntShift - 32)) << 32) | (len * (unsigned)dpi);
+      CVX_CHECK(!head || (long long)addr < ((long long)p.pool.max_blocks + kTrashBlocks) * kBlockVox, "pool accumulator address");
       asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.relaxed.gpu.global.add.u64 [%0], %1;\n\t}"
                    :: "l"(acc + addr), "l"(val), "r"((unsigned)head) : "memory");
       if (kColor && S > band_lo && S < band_hi) {   // TSDF + Color: band updates carry the point's colour (R13)
@@ -1320,8 +1323,10 @@ __global__ void __launch_bounds__(256) box_reduce_kernel(const int* cta_box, int
 #define DW_RED(acc, addr, val, head) asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.relaxed.gpu.global.add.u64 [%0], %1;\n\t}" \
                    :: "l"((acc) + (((addr) & ~31u) | (threadIdx.x & 31))), "l"(val), "r"((unsigned)(head)) : "memory")
 #else
-#define DW_RED(acc, addr, val, head) asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.relaxed.gpu.global.add.u64 [%0], %1;\n\t}" \
-                   :: "l"((acc) + (addr)), "l"(val), "r"((unsigned)(head)) : "memory")
+#define DW_RED(acc, addr, val, head) do { \
+    CVX_CHECK(!(head) || (long long)(addr) < (p.dcap + kTrashBlocks) * kBlockVox, "dense accumulator address"); \
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.relaxed.gpu.global.add.u64 [%0], %1;\n\t}" \
+                   :: "l"((acc) + (addr)), "l"(val), "r"((unsigned)(head)) : "memory"); } while (0)
 #endif
 #ifndef CVX_DW_UNIFORM
 #define CVX_DW_UNIFORM 0   // 1: free prefix takes a warp-uniform path when no two adjacent lanes share a voxel (measured slower)
@@ -1384,6 +1389,8 @@ __global__ void __launch_bounds__(128, CVX_DW_MINB) walk_dw_kernel(const __grid_
     S = r.S0 + (1ll << (kSdfF - 1)) + ((long long)p.tq << kSdfF);
     U0 = r.U[0]; U1 = r.U[1]; U2 = r.U[2];
     n = r.n_vox;
+    CVX_CHECK((va[0] >> 3) >= p.dbox[0] && (va[0] >> 3) <= p.dbox[3] && (va[1] >> 3) >= p.dbox[1] && (va[1] >> 3) <= p.dbox[4] &&
+              (va[2] >> 3) >= p.dbox[2] && (va[2] >> 3) <= p.dbox[5], "ray start inside the launch's block box");
     const unsigned blk = (unsigned)((((va[2] >> 3) - p.dbox[2]) * nby + ((va[1] >> 3) - p.dbox[1])) * nbx + ((va[0] >> 3) - p.dbox[0]));
     addr = blk * 512u + (unsigned)((va[0] & 7) | ((va[1] & 7) << 3) | ((va[2] & 7) << 6));
     mark_block(p.dflag, blk, true);
@@ -1587,6 +1594,7 @@ __global__ void __launch_bounds__(256) dense_fold_kernel(const __grid_constant__
       const int j = __ffs(t) - 1;
       const int sl = __shfl_sync(0xffffffffu, slot, j);
       ulonglong2* src = reinterpret_cast<ulonglong2*>(p.dacc + (b0 + j) * kBlockVox);
+      CVX_CHECK(sl < p.pool.max_blocks && b0 + j < p.dcap, "dense fold slot / block");
       longlong2* s2 = reinterpret_cast<longlong2*>(p.pool.sums) + (long long)(sl < 0 ? 0 : sl) * kBlockVox;
       ulonglong2 v[8];
 #pragma unroll

@@ -14,7 +14,8 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcvx.so")
+# CVX_LIB_PATH: load another build of the same library (the bounds-checked build of tests/test_gpu_bounds.py)
+LIB_PATH = os.environ.get("CVX_LIB_PATH") or os.path.join(_HERE, "libcvx.so")
 
 OK, E_INVALID, E_OOM, E_CAPACITY, E_STATE, E_CUDA, E_RANGE = 0, -1, -2, -3, -4, -5, -6
 _NAMES = {E_INVALID: "CVX_E_INVALID", E_OOM: "CVX_E_OOM", E_CAPACITY: "CVX_E_CAPACITY",
