@@ -119,7 +119,11 @@ __host__ __device__ inline size_t xsmem_bytes(int nch, int nbx) {
   return xring_off(nch, nbx) + (CVX_XPIPE ? (size_t)4 * kXDepth * 32 * 16 : 0);
 }
 
+#ifdef CVX_PX_MINB
+__global__ void __launch_bounds__(128, CVX_PX_MINB) pass_x_kernel(const __grid_constant__ XParams p) {
+#else
 __global__ void __launch_bounds__(128) pass_x_kernel(const __grid_constant__ XParams p) {
+#endif
   extern __shared__ __align__(1024) unsigned char dsmem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nch = (p.nx + 31) >> 5;
