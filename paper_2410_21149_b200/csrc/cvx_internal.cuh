@@ -170,7 +170,7 @@ constexpr long long kMaxPackedRays = (1ll << 24) - 1;
 constexpr long long kLaunchRays = (1ll << CVX_LAUNCH_LOG2) - 1;   // rays per walk launch (pipelining granularity)
 static_assert(CVX_LAUNCH_LOG2 <= 24, "the fold runs once per 2^24 rays; a launch must not exceed it");
 #ifndef CVX_HOST_LAUNCH_LOG2
-#define CVX_HOST_LAUNCH_LOG2 23
+#define CVX_HOST_LAUNCH_LOG2 24   // dense window (R19): one launch per configs[1] submap, e2e 6.59 -> 6.51 ms (2^23: two launches, two box folds)
 #endif
 constexpr long long kLaunchRaysHost = (1ll << CVX_HOST_LAUNCH_LOG2) - 1;   // host frames (copy pipelining)
 inline int packed_q(double tau) {
