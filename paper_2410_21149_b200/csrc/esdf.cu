@@ -690,6 +690,9 @@ constexpr int kRingBUnroll = CVX_RING_BUNROLL;
 #ifndef CVX_RING_BSKIP
 #define CVX_RING_BSKIP 0    // 1: backward of pass z skips chunks no lane of the warp writes (measured: no gain; pass y slower)
 #endif
+#ifndef CVX_RING_INFSKIP
+#define CVX_RING_INFSKIP 0  // 1: a batch of 8 positions without any site is skipped as a whole (per lane)
+#endif
 #ifndef CVX_RING_ROWSKIP
 #define CVX_RING_ROWSKIP 1  // pass y: skip the y batches of block rows without allocated blocks
 #endif
@@ -765,7 +768,16 @@ __global__ void __launch_bounds__(kRingThreads, CVX_RING_MINB) ring_line_kernel(
     const bool hb = row_has(qn);
 #pragma unroll
     for (int u = 0; u < 8; ++u) fb[u] = hb ? raw_at(qn + u) : kNone16;
-    if (!ha) {
+    bool skip = !ha;
+#if CVX_RING_INFSKIP
+    {   // the 8 positions of the batch hold no site of this line (raw all-ones = none / inf)
+      unsigned a = fa[0];
+#pragma unroll
+      for (int u = 1; u < 8; ++u) a &= fa[u];
+      skip |= a == (kZ ? kInf32 : kNone16);
+    }
+#endif
+    if (skip) {
 #pragma unroll
       for (int u = 0; u < 8; ++u) fa[u] = fb[u];
       ha = hb;
