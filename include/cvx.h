@@ -115,9 +115,10 @@ cvx_status cvx_set_submap_pose(cvx_submap* submap, const double* T_world_submap)
  * ray records (48 B per ray) and, with constant weights and no colour, the dense-window accumulators of
  * DESIGN.md R19 — block-major u64 over the block box of each launch's rays, sized on the first call to a
  * conservative box of the call's frames (balls of radius max_range + truncation around the sensor
- * origins) capped at 2^20 blocks = 4 GiB (environment CVX_DENSE_BLOCKS at submap creation; CVX_DENSE=0
- * disables the path); a launch whose box exceeds the buffer takes the slot-list path on the device, with
- * the same results.  ALLOCATE then runs after the update walk (same block set).
+ * origins) capped at 2^19 blocks = 2 GiB (environment CVX_DENSE_BLOCKS at submap creation; CVX_DENSE=0
+ * disables the path); a launch whose box exceeds the buffer takes the slot-list path on the device, and a
+ * call whose buffer cannot be allocated takes it on the host — same results either way.  ALLOCATE then
+ * runs after the update walk (same block set).  The buffer lives until cvx_destroy_submap.
  * Errors: CVX_E_INVALID, CVX_E_STATE (after finalize), CVX_E_CUDA (also CVX_E_OOM-class CUDA errors when
  * the scratch cannot be allocated); with stats also CVX_E_CAPACITY / CVX_E_RANGE from the sticky flags. */
 cvx_status cvx_integrate_pointcloud(cvx_submap* submap, const float* data, int64_t n,

@@ -1922,7 +1922,7 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
   // accumulator buffer covers a conservative box of the call (balls of radius max_range + tau around the
   // frames' sensor origins), capped at dense_cap blocks; each launch uses the exact box of its rays
   // (prepare_kernel) and falls back to the slot-list path on the device if that box exceeds the buffer.
-  const bool dense = cw_ok && sm->dense_on && sm->walk_cw && sm->bw2 && !sm->bw3 && !sm->fuse_alloc && !rgb && !trig;
+  bool dense = cw_ok && sm->dense_on && sm->walk_cw && sm->bw2 && !sm->bw3 && !sm->fuse_alloc && !rgb && !trig;
   long long dcap = 0;
   if (dense) {
     const double* W = sm->T_ws;
@@ -1947,10 +1947,14 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
       sm->dacc_blocks = 0;
       // accumulators, the trash region, then one touched flag per block
       const size_t bytes = (size_t)(dcap + kTrashBlocks) * kBlockVox * sizeof(unsigned long long) + (size_t)dcap;
-      cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&sm->dacc), bytes, st);
-      if (e != cudaSuccess) return e;
-      cudaMemsetAsync(sm->dacc, 0, bytes, st);
-      sm->dacc_blocks = dcap;
+      if (cudaMallocAsync(reinterpret_cast<void**>(&sm->dacc), bytes, st) == cudaSuccess) {
+        cudaMemsetAsync(sm->dacc, 0, bytes, st);
+        sm->dacc_blocks = dcap;
+      } else {                        // device memory short: this call takes the slot-list path instead
+        cudaGetLastError();
+        sm->dacc = nullptr;
+        dense = false;
+      }
     }
     dcap = sm->dacc_blocks;
   }

@@ -83,7 +83,7 @@ struct cvx_submap {
   bool fuse_alloc = false;    // constant weights: ALLOCATE inside walk_cw_kernel (measured 1.4x slower: off)
   // dense-window path (R19): block-major accumulators over the launch's block box, ALLOCATE after the walk
   bool dense_on = true;
-  long long dense_cap = 1ll << 20;          // blocks (4 GiB of u64 accumulators)
+  long long dense_cap = 1ll << 19;          // blocks (2 GiB of u64 accumulators; configs[1] / MAV boxes: <= 0.23 M)
   unsigned long long* dacc = nullptr;       // device [(dacc_blocks + kTrashBlocks) * 512], zero between folds
   long long dacc_blocks = 0;
   int* acc_dirty = nullptr;                 // device: a dense-eligible launch fell back to the pool accumulators
