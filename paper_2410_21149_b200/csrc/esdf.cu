@@ -929,6 +929,186 @@ __global__ void __launch_bounds__(kRingThreads, CVX_RING_MINB) ring_line_kernel(
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
+// Pass y with two threads per line, for AABBs with few long y lines (LiDAR / MAV submaps: ~1e5 lines of
+// ~1000 positions, fewer than the GPU's resident threads): thread A runs the ring kernel's forward sweep on
+// positions [0, h), thread B on [h, m), each from an empty stack.  A site B popped is dominated by B's own
+// sites wherever it was minimal, so only B's final stack can enter the line's envelope: thread B then
+// continues Meijster's sweep over those entries on top of A's final stack (pops and separators exactly as
+// the sequential sweep would do them), writing the merged B part back into its own array; once an entry
+// lands on its own B predecessor at an unchanged position the rest of B's stack is already right.  The two
+// threads then write their halves of the output walking the merged stack (A part, then B part) from the
+// entry covering their last position.  Same output as ring_line_kernel (the envelope's value is unique).
+constexpr int kSplitLines = kRingThreads / 2;
+__global__ void __launch_bounds__(kRingThreads, CVX_RING_MINB) ring2_line_kernel(const __grid_constant__ LinkParams p) {
+  __shared__ unsigned long long ring[kRing][kRingThreads];
+  __shared__ int s_k[kRingThreads];          // final stack top of every thread after its forward sweep
+  __shared__ int s_ka[kSplitLines], s_rb[kSplitLines];   // merged stack: A part [0, ka], B part [0, rb]
+  const int tid = threadIdx.x;
+  const bool isB = tid >= kSplitLines;
+  const int li = isB ? tid - kSplitLines : tid;
+  const long long nlines = (long long)p.nx * p.nz;
+  const long long line = (long long)blockIdx.x * kSplitLines + li;
+  const bool valid = line < nlines;
+  const int x = valid ? (int)(line % p.nx) : 0;
+  const int o2 = valid ? (int)(line / p.nx) : 0;   // z
+  const int m = p.ny;
+  const int h = (m >> 4) << 3;                      // split position (multiple of 8; m >= 16)
+  const long long stride = p.nx;
+  const long long base = (long long)o2 * p.nx * p.ny + x;
+  unsigned long long* const gA = static_cast<unsigned long long*>(p.meta) + (valid ? line : 0) * m;
+  unsigned long long* const gB = gA + h;
+  unsigned long long* const gst = isB ? gB : gA;    // this thread's own stack array
+  unsigned long long* const rg = &ring[0][tid];
+  auto raw_at = [&](int q) -> unsigned { return static_cast<const unsigned short*>(p.fin)[base + q * stride]; };
+  auto f_of = [](unsigned v) -> unsigned { return v == kNone16 ? kInf32 : v * v; };
+  auto row_has = [&](int q) -> bool {
+    return !CVX_RING_ROWSKIP || p.rowmask[(long long)(o2 >> 3) * p.nby + (q >> 3)] != 0;
+  };
+  const int q_lo = isB ? h : 0, q_hi = isB ? m : h;
+  int k = -1, lo = 0;
+  int s_top = 0, t_top = 0;
+  unsigned f_top = 0;
+  if (valid) {   // ---- forward sweep of the own segment (as ring_line_kernel)
+    unsigned fa[8];
+    bool ha = row_has(q_lo);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) fa[u] = ha ? raw_at(q_lo + u) : kNone16;
+    for (int q0 = q_lo; q0 < q_hi; q0 += 8) {
+      unsigned fb[8];
+      const int qn = q0 + 8 < q_hi ? q0 + 8 : q0;
+      const bool hb = row_has(qn);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) fb[u] = hb ? raw_at(qn + u) : kNone16;
+      if (ha) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int q = q0 + u;
+          const unsigned fq = f_of(fa[u]);
+          if (fq == kInf32) continue;
+          while (k >= 0) {
+            const int a = t_top - s_top, c = t_top - q;
+            if ((unsigned)(a * a) + f_top <= (unsigned)(c * c) + fq) break;
+            if (--k < 0) break;
+            if (k < lo) {
+              const int j0 = max(0, k - (kRing - 1));
+              for (int j = j0; j <= k; ++j) rg[(j & (kRing - 1)) * kRingThreads] = gst[j];
+              lo = j0;
+            }
+            const unsigned long long e = rg[(k & (kRing - 1)) * kRingThreads];
+            s_top = (int)(e & 0xffffu); t_top = (int)((e >> 16) & 0xffffu); f_top = (unsigned)(e >> 32);
+          }
+          int tq = 0;
+          if (k >= 0) {
+            const int sep = floordiv24(q * q - s_top * s_top + (int)fq - (int)f_top, 2 * (q - s_top));
+            if (sep + 1 >= m) continue;
+            tq = sep + 1;
+          }
+          ++k;
+          unsigned long long* slot = rg + (k & (kRing - 1)) * kRingThreads;
+          CVX_CHECK(k < q_hi - q_lo, "split stack depth <= segment length");
+          if (k - kRing >= lo) { gst[k - kRing] = *slot; lo = k - kRing + 1; }
+          *slot = ((unsigned long long)fq << 32) | ((unsigned)tq << 16) | (unsigned)q;
+          s_top = q; t_top = tq; f_top = fq;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) fa[u] = fb[u];
+      ha = hb;
+    }
+    for (int j = max(lo, 0); j <= k; ++j) gst[j] = rg[(j & (kRing - 1)) * kRingThreads];   // whole stack in HBM
+  }
+  s_k[tid] = k;
+  __syncthreads();
+  if (isB && valid) {   // ---- merge: B's stack entries continue the sweep on top of A's stack
+    int ka = s_k[li];
+    const int kb = k;
+    int r = 0;          // B entries in the merged stack: gB[0, r)
+    for (int j = 0; j <= kb; ++j) {
+      const unsigned long long e = gB[j];
+      const int es = (int)(e & 0xffffu);
+      const unsigned ef = (unsigned)(e >> 32);
+      while (r > 0 || ka >= 0) {
+        const unsigned long long tp = r > 0 ? gB[r - 1] : gA[ka];
+        const int ts = (int)(tp & 0xffffu), tt = (int)((tp >> 16) & 0xffffu);
+        const unsigned tf = (unsigned)(tp >> 32);
+        const int a = tt - ts, c = tt - es;
+        if ((unsigned)(a * a) + tf <= (unsigned)(c * c) + ef) break;
+        if (r > 0) --r; else --ka;
+      }
+      int tq = 0;
+      bool on_pred = false;
+      if (r > 0 || ka >= 0) {
+        const unsigned long long tp = r > 0 ? gB[r - 1] : gA[ka];
+        const int ts = (int)(tp & 0xffffu);
+        const unsigned tf = (unsigned)(tp >> 32);
+        const int sep = floordiv24(es * es - ts * ts + (int)ef - (int)tf, 2 * (es - ts));
+        if (sep + 1 >= m) continue;                   // never wins inside the line: dropped
+        tq = sep + 1;
+        on_pred = r == j && r > 0;                     // on its own B predecessor, at its own position
+      }
+      gB[r] = ((unsigned long long)ef << 32) | ((unsigned)tq << 16) | (unsigned)es;   // r <= j
+      ++r;
+      if (on_pred) { r = kb + 1; break; }             // the rest of B's stack is unchanged
+    }
+    s_ka[li] = ka;
+    s_rb[li] = r - 1;
+  }
+  __syncthreads();
+  if (!valid) return;
+  // ---- backward over the own half; unified index u: [0, ka] -> gA[u], then gB[u - ka - 1]
+  const int ka = s_ka[li], rb = s_rb[li];
+  auto at = [&](int u) -> const unsigned long long* { return u <= ka ? gA + u : gB + (u - ka - 1); };
+  int u0;
+  if (isB) u0 = ka + 1 + rb;                           // the top
+  else {                                               // the entry covering h - 1
+    int i = -1;
+    while (i + 1 <= rb && (int)((gB[i + 1] >> 16) & 0xffffu) <= h - 1) ++i;
+    if (i >= 0) u0 = ka + 1 + i;
+    else {
+      u0 = ka;
+      while (u0 >= 0 && (int)((gA[u0] >> 16) & 0xffffu) > h - 1) --u0;
+    }
+  }
+  k = u0;
+  lo = u0 + 1;                                         // every entry comes from HBM (cp.async kAhead ahead)
+  if (k >= 0) {
+    const unsigned long long e = *at(k);
+    s_top = (int)(e & 0xffffu); t_top = (int)((e >> 16) & 0xffffu); f_top = (unsigned)(e >> 32);
+  }
+  auto issue = [&](int j) {
+    if (j >= 0 && j < lo) {
+      const unsigned sa = smem_addr(rg + (j & (kRing - 1)) * kRingThreads);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(sa), "l"(at(j)) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if (k >= 0) {
+#pragma unroll 1
+    for (int i = 1; i <= kAhead; ++i) issue(k - i);
+  }
+  const int qtop = isB ? (((m - 1) >> 3) << 3) : h - 8, qbot = isB ? h : 0;
+  for (int q0 = qtop; q0 >= qbot; q0 -= 8) {
+    const bool wy = p.colmask[(long long)(q0 >> 3) * p.nbx + (x >> 3)] != 0;
+#pragma unroll kRingBUnroll
+    for (int u = 7; u >= 0; --u) {
+      const int q = q0 + u;
+      unsigned d2 = kInf32;
+      if (k >= 0) { const int dq = q - s_top; d2 = (unsigned)(dq * dq) + f_top; }
+      CVX_CHECK(base + (long long)q * stride < (long long)p.nx * p.ny * p.nz, "split line output index");
+      if (wy) p.g2[base + (long long)q * stride] = d2;
+      if (k >= 0 && q == t_top) {
+        if (--k >= 0) {
+          if (k < lo) asm volatile("cp.async.wait_group %0;" :: "n"(kAhead - 1) : "memory");
+          const unsigned long long e = *(volatile unsigned long long*)(rg + (k & (kRing - 1)) * kRingThreads);
+          s_top = (int)(e & 0xffffu); t_top = (int)((e >> 16) & 0xffffu); f_top = (unsigned)(e >> 32);
+          issue(k - kAhead);
+        }
+      }
+    }
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 // ------------------------------------------------------------------------------- incremental (f1)
 struct IncParams {
   const long long* sums;
@@ -1242,7 +1422,15 @@ cudaError_t dense_edt(cvx_submap* sm, const int lo[3], const int hi[3], cudaStre
     {
       ProfScope ps_(sm, "esdf_pass_y", st);
       const long long nl = (long long)nx * nz;
-      if (kernel == 0 && ring_y) ring_line_kernel<false><<<(unsigned)((nl + kRingThreads - 1) / kRingThreads), kRingThreads, 0, st>>>(lp);
+      // few long lines (fewer than ~1.5 per resident thread slot): two threads per line
+      // (serial ESDF: pass y 0.54 -> 0.40 ms on configs[1], 20.7 -> 15.5 ms over the MAV submaps; but beside a
+      // concurrent update walk the wider kernel costs the walk more than it saves: configs[1] step 6.21 ->
+      // 6.28 ms, MAV 80.8 -> 83.5-89.3 ms — so off by default, CVX_EDT_SPLIT=1 enables it per call)
+      const char* sv = std::getenv("CVX_EDT_SPLIT");
+      const int split = sv ? std::atoi(sv) : 0;
+      if (kernel == 0 && ring_y && split && ny >= 64 && nl < 148ll * 7 * kRingThreads * 3 / 2)
+        ring2_line_kernel<<<(unsigned)((nl + kSplitLines - 1) / kSplitLines), kRingThreads, 0, st>>>(lp);
+      else if (kernel == 0 && ring_y) ring_line_kernel<false><<<(unsigned)((nl + kRingThreads - 1) / kRingThreads), kRingThreads, 0, st>>>(lp);
       else link_line_kernel<false><<<(unsigned)((nl + 255) / 256), 256, 0, st>>>(lp);
     }
     lp.fin = g2;

@@ -461,3 +461,28 @@ def test_block_count_trigger_matches_oracle(orc, name, frames):
             assert_tsdf_parity(gpu_export_sorted(sm), ref.export())
     sm = Submap(cfg["grid"], cfg["submaps"][0]["T_world_submap"], 0)
     assert sm.integrate_until(data, poses, cfg["sensor"], counts[-1] + 1) == len(frames)
+
+
+@pytest.mark.parametrize("which", ["lidar", "mav"])
+def test_split_line_pass_equals_default(orc, monkeypatch, which):
+    """ESDF pass y with two threads per line (CVX_EDT_SPLIT=1: forward sweeps of the two halves, the second
+    half's stack merged onto the first's, R20) gives the default kernel's ESDF bit for bit, and the
+    stage-isolated oracle EDT."""
+    if which == "lidar":
+        cfg = synth.make_config("lidar", frames=[0, 60])
+        ks, g, T = [0, 60], cfg["grid"], None
+    else:
+        base = synth.make_config("mav", frames=[])
+        sub = base["submaps"][2]
+        ks = sub["frames"][:40:10]
+        cfg = synth.make_config("mav", frames=ks)
+        g, T = dict(cfg["grid"], max_blocks=1 << 16), sub["T_world_submap"]
+    sm, _ = gpu_build(cfg, ks, grid=g, T_ws=T, batch=True)
+    a = gpu_export_sorted(sm)
+    monkeypatch.setenv("CVX_EDT_SPLIT", "1")
+    sm2, _ = gpu_build(cfg, ks, grid=g, T_ws=T, batch=True)
+    b = gpu_export_sorted(sm2)
+    assert np.array_equal(a[0], b[0])
+    assert np.array_equal(a[3].view(np.uint32), b[3].view(np.uint32))
+    Eo, _ = orc.esdf(b[0], b[1].astype(np.float64), b[2].astype(np.float64), g["voxel_size"], g["site_threshold"])
+    assert_esdf_parity(b[3], Eo, b[2] > 0)
