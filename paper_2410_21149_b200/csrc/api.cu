@@ -129,6 +129,8 @@ void free_all(cvx_submap* sm) {
     if (B.staging) cudaFree(B.staging);
   }
   if (sm->side) cudaStreamDestroy(sm->side);
+  if (sm->wstream) cudaStreamDestroy(sm->wstream);
+  for (auto& e : sm->ev_w) if (e) cudaEventDestroy(e);
   if (sm->copy) cudaStreamDestroy(sm->copy);
   for (int b = 0; b < 2; ++b) {
     if (sm->ev_staged[b]) cudaEventDestroy(sm->ev_staged[b]);
@@ -188,6 +190,7 @@ cvx_status cvx_create_submap(const cvx_grid_config* cfg, const double* T_world_s
   if (const char* fa = std::getenv("CVX_FUSE_ALLOC")) sm->fuse_alloc = fa[0] != '0'; // tuning knob
   if (const char* lc = std::getenv("CVX_LIST_CAP")) sm->list_cap_limit = std::atoll(lc);  // test knob
   if (const char* dn = std::getenv("CVX_DENSE")) sm->dense_on = dn[0] != '0';         // R19 knob
+  if (const char* wp = std::getenv("CVX_WALK_PRIO")) sm->walk_prio = wp[0] != '0';      // scheduling knob
   if (const char* db = std::getenv("CVX_DENSE_BLOCKS"))                                 // R19 capacity knob
     sm->dense_cap = std::max(1ll, std::min(std::atoll(db), 1ll << 22));
   sm->cfg = *cfg;

@@ -2085,28 +2085,44 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     // ---- caller's stream: a4 UPDATE + a5 FOLD of launch k
     if (cw && pending + total > kMaxPackedRays) fold();
     cudaStreamWaitEvent(st, sm->ev_prepared[b], 0);
+    // CVX_WALK_PRIO: the update walk runs on a high-priority library stream (ordered after / before the
+    // caller's stream by events), so a concurrent ESDF of another submap does not take its SMs
+    cudaStream_t ws = st;
+    if (sm->walk_prio && !sm->serialize) {
+      if (!sm->wstream) {
+        int lo_p = 0, hi_p = 0;
+        cudaDeviceGetStreamPriorityRange(&lo_p, &hi_p);
+        cudaStreamCreateWithPriority(&sm->wstream, cudaStreamNonBlocking, hi_p);
+        cudaEventCreateWithFlags(&sm->ev_w[0], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&sm->ev_w[1], cudaEventDisableTiming);
+      }
+      ws = sm->wstream;
+      cudaEventRecord(sm->ev_w[0], st);
+      cudaStreamWaitEvent(ws, sm->ev_w[0], 0);
+    }
     {
-      ProfScope ps_(sm, "ray_walk_update", st);
+      ProfScope ps_(sm, "ray_walk_update", ws);
       const unsigned wblocks = (unsigned)((total + 127) / 128);   // 128-thread CTAs (measured best)
       if (cw && sm->aggregate && sm->walk_cw) {
-        if (rgb) { if (k32) walk_cw_kernel<true, true><<<wblocks, 128, 0, st>>>(wp); else walk_cw_kernel<false, true><<<wblocks, 128, 0, st>>>(wp); }
-        else if (fuse) { if (k32) walk_cw_kernel<true, false, true><<<wblocks, 128, 0, st>>>(wp); else walk_cw_kernel<false, false, true><<<wblocks, 128, 0, st>>>(wp); }
+        if (rgb) { if (k32) walk_cw_kernel<true, true><<<wblocks, 128, 0, ws>>>(wp); else walk_cw_kernel<false, true><<<wblocks, 128, 0, ws>>>(wp); }
+        else if (fuse) { if (k32) walk_cw_kernel<true, false, true><<<wblocks, 128, 0, ws>>>(wp); else walk_cw_kernel<false, false, true><<<wblocks, 128, 0, ws>>>(wp); }
         else {
-          if (dense) { if (k32) walk_dw_kernel<true><<<wblocks, 128, 0, st>>>(wp); else walk_dw_kernel<false><<<wblocks, 128, 0, st>>>(wp); }
+          if (dense) { if (k32) walk_dw_kernel<true><<<wblocks, 128, 0, ws>>>(wp); else walk_dw_kernel<false><<<wblocks, 128, 0, ws>>>(wp); }
           // (dense: runs only if this launch's box exceeds the dense buffer)
           const unsigned fwb = dense ? std::min(wblocks, 148u * 16u) : wblocks;
-          if (k32) walk_cw_kernel<true, false><<<fwb, 128, 0, st>>>(wp); else walk_cw_kernel<false, false><<<fwb, 128, 0, st>>>(wp);
+          if (k32) walk_cw_kernel<true, false><<<fwb, 128, 0, ws>>>(wp); else walk_cw_kernel<false, false><<<fwb, 128, 0, ws>>>(wp);
         }
       } else if (rgb) {
-        if (cw) { if (k32) walk_kernel<true, true, true, true><<<wblocks, 128, 0, st>>>(wp); else walk_kernel<true, true, false, true><<<wblocks, 128, 0, st>>>(wp); }
-        else { if (k32) walk_kernel<true, false, true, true><<<wblocks, 128, 0, st>>>(wp); else walk_kernel<true, false, false, true><<<wblocks, 128, 0, st>>>(wp); }
+        if (cw) { if (k32) walk_kernel<true, true, true, true><<<wblocks, 128, 0, ws>>>(wp); else walk_kernel<true, true, false, true><<<wblocks, 128, 0, ws>>>(wp); }
+        else { if (k32) walk_kernel<true, false, true, true><<<wblocks, 128, 0, ws>>>(wp); else walk_kernel<true, false, false, true><<<wblocks, 128, 0, ws>>>(wp); }
       } else if (sm->aggregate) {
-        if (cw) { if (k32) walk_kernel<true, true, true><<<wblocks, 128, 0, st>>>(wp); else walk_kernel<true, true, false><<<wblocks, 128, 0, st>>>(wp); }
-        else { if (k32) walk_kernel<true, false, true><<<wblocks, 128, 0, st>>>(wp); else walk_kernel<true, false, false><<<wblocks, 128, 0, st>>>(wp); }
+        if (cw) { if (k32) walk_kernel<true, true, true><<<wblocks, 128, 0, ws>>>(wp); else walk_kernel<true, true, false><<<wblocks, 128, 0, ws>>>(wp); }
+        else { if (k32) walk_kernel<true, false, true><<<wblocks, 128, 0, ws>>>(wp); else walk_kernel<true, false, false><<<wblocks, 128, 0, ws>>>(wp); }
       } else {
-        walk_kernel<false, false, false><<<wblocks, 128, 0, st>>>(wp);
+        walk_kernel<false, false, false><<<wblocks, 128, 0, ws>>>(wp);
       }
     }
+    if (ws != st) { cudaEventRecord(sm->ev_w[1], ws); cudaStreamWaitEvent(st, sm->ev_w[1], 0); }
     if (dense) {
       ProfScope ps_(sm, "dense_fold_allocate", st);
       dense_fold_kernel<<<148 * 8, 256, 0, st>>>(wp);

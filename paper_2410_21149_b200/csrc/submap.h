@@ -82,6 +82,9 @@ struct cvx_submap {
   long long list_cap_limit = 1ll << 62;   // test knob: cap on the per-ray slot-list buffer (full: walk hashes)
   bool fuse_alloc = false;    // constant weights: ALLOCATE inside walk_cw_kernel (measured 1.4x slower: off)
   // dense-window path (R19): block-major accumulators over the launch's block box, ALLOCATE after the walk
+  bool walk_prio = false;    // CVX_WALK_PRIO: update walks on a high-priority library stream
+  cudaStream_t wstream = nullptr;
+  cudaEvent_t ev_w[2] = {nullptr, nullptr};
   bool dense_on = true;
   long long dense_cap = 1ll << 19;          // blocks (2 GiB of u64 accumulators; configs[1] / MAV boxes: <= 0.23 M)
   unsigned long long* dacc = nullptr;       // device [(dacc_blocks + kTrashBlocks) * 512], zero between folds
