@@ -522,7 +522,7 @@ cvx_status cvx_sample_surface(cvx_submap* sm, const uint32_t* uniforms, int64_t 
   if (rc != CVX_OK) return rc;
   const int nb = c.n_blocks < sm->pool.max_blocks ? c.n_blocks : sm->pool.max_blocks;
   long long tot = 0;
-  cudaError_t e = cvx::launch_sample_surface(sm, nb, uniforms, m, out_xyz, out_weight, st, &tot);
+  cudaError_t e = cvx::launch_sample_surface(sm, nb, c.aabb_lo, c.aabb_hi, uniforms, m, out_xyz, out_weight, st, &tot);
   if (e != cudaSuccess) return cuda_fail(e, "sample_surface");
   if (total_weight) *total_weight = tot;
   return CVX_OK;

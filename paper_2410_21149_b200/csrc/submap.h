@@ -154,8 +154,8 @@ void release_esdf(cvx_submap* sm);   // frees the ESDF scratch, planes and incre
 cudaError_t launch_query(const cvx_submap* sm, const float* pts, int64_t m, float* out, uint8_t* status,
                          cudaStream_t st, float* grad = nullptr);
 // registration.cu
-cudaError_t launch_sample_surface(cvx_submap* sm, int n_blocks, const unsigned* uniforms, int64_t m, float* out_xyz,
-                                  float* out_w, cudaStream_t st, long long* total_weight);
+cudaError_t launch_sample_surface(cvx_submap* sm, int n_blocks, const int lo[3], const int hi[3], const unsigned* uniforms,
+                                  int64_t m, float* out_xyz, float* out_w, cudaStream_t st, long long* total_weight);
 cudaError_t launch_export(const cvx_submap* sm, int n_blocks, int32_t* bxyz, float* D, float* W, float* E,
                           cudaStream_t st);
 cudaError_t launch_import(cvx_submap* sm, const int32_t* bxyz, const float* D, const float* W, int64_t n,

@@ -48,3 +48,22 @@ def test_surface_sampling_parity(built, orc):
     assert tot == to > 0
     assert np.array_equal(xyz.cpu().numpy().view(np.uint32), xo.view(np.uint32))   # identical picks
     assert np.allclose(w.cpu().numpy(), wo)
+
+
+def test_surface_sampling_parity_lidar(orc):
+    """The same on a LiDAR subset (two configs[1] scans): the block grid spans ~1e5 cells, so the cell-weight
+    scan runs over many tiles (three-kernel exact integer scan, registration.cu)."""
+    cfg = synth.make_config("lidar", frames=[0, 60])
+    sm, _ = gpu_build(cfg, [0, 60], finalize=False)
+    b, D, W, _ = gpu_export_sorted(sm)
+    lo, hi = sm.aabb()
+    assert np.prod(np.asarray(hi) - np.asarray(lo) + 1) > 20000
+    g = cfg["grid"]
+    rng = np.random.default_rng(2)
+    u = rng.integers(0, 1 << 32, 20000, dtype=np.uint64).astype(np.uint32)
+    xyz, w, tot = sm.sample_surface(torch.from_numpy(u.view(np.int32)).cuda())
+    xo, wo, to = orc.sample_surface(b, D.astype(np.float64), W.astype(np.float64), g["site_threshold"],
+                                    g["voxel_size"], sm.T_ws, u)
+    assert tot == to > 0
+    assert np.array_equal(xyz.cpu().numpy().view(np.uint32), xo.view(np.uint32))
+    assert np.allclose(w.cpu().numpy(), wo)
