@@ -126,6 +126,7 @@ void free_all(cvx_submap* sm) {
     if (B.slot_lists) cudaFree(B.slot_lists);
     if (B.lcnt) cudaFree(B.lcnt);
     if (B.cta_box) cudaFree(B.cta_box);
+    if (B.cstat) cudaFree(B.cstat);
     if (B.staging) cudaFree(B.staging);
   }
   if (sm->side) cudaStreamDestroy(sm->side);

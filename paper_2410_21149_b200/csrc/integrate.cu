@@ -182,12 +182,20 @@ struct PrepParams {
   const unsigned char* rgb;   // nullable: per-point colour [total][3]
   int count_vox;    // add the raycast voxel counts to ctr->voxel_updates (0: projection mapping)
   int* box;         // nullable: per CTA {lo[3], hi[3]} block box of its rays (dense-window path, R19)
+  unsigned long long* cstat;   // nullable: per CTA look-back status (zeroed): rays claimed in CTA order
 };
 
 #ifndef CVX_PREP_MINB
 #define CVX_PREP_MINB 5   // 48 registers, 5 CTAs per SM: prepare 0.505 -> 0.467 ms against __launch_bounds__(256) (56 registers)
 #endif
-__global__ void __launch_bounds__(256, CVX_PREP_MINB) prepare_kernel(const __grid_constant__ PrepParams p) {
+#ifndef CVX_PREP_ORDERED
+#define CVX_PREP_ORDERED 0   // 1: rays claimed in CTA order (decoupled look-back) instead of atomic arrival order (walk -1.6 %, prepare +80 %: off)
+#endif
+#ifndef CVX_PREP_THREADS
+#define CVX_PREP_THREADS 256
+#endif
+constexpr int kPrepThreads = CVX_PREP_THREADS;
+__global__ void __launch_bounds__(kPrepThreads, CVX_PREP_MINB) prepare_kernel(const __grid_constant__ PrepParams p) {
   if (p.trig && *(volatile const int*)&p.trig[1]) return;   // block-count trigger fired: frame not taken
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
@@ -332,7 +340,30 @@ __global__ void __launch_bounds__(256, CVX_PREP_MINB) prepare_kernel(const __gri
         c[t] += x;
       }
     unsigned long long base = 0;
-    if (c[0] | c[1]) base = atomicAdd(reinterpret_cast<unsigned long long*>(p.lcnt), (c[1] << 32) | c[0]);
+    if (p.cstat) {
+      // single-pass decoupled look-back: the CTA's rays / slots are placed after those of every lower CTA,
+      // so the records keep the input order (consecutive patches stay adjacent for the walk's warps)
+      constexpr unsigned long long kAgg = 1ull << 62, kInc = 2ull << 62, kVal = (1ull << 62) - 1, kRayM = (1ull << 25) - 1;
+      const unsigned long long agg = (c[1] << 25) | c[0];        // slots : 37 | rays : 25
+      unsigned long long excl = 0;
+      if (blockIdx.x > 0) {
+        atomicExch(&p.cstat[blockIdx.x], kAgg | agg);
+        for (long long j = (long long)blockIdx.x - 1;;) {
+          const unsigned long long v = *(volatile unsigned long long*)&p.cstat[j];
+          if (v == 0ull) continue;                                // not yet published
+          excl += v & kVal;
+          if (v & kInc) break;
+          --j;
+        }
+      }
+      const unsigned long long inc = excl + agg;
+      atomicExch(&p.cstat[blockIdx.x], kInc | inc);
+      atomicMax(&p.lcnt[0], (int)(inc & kRayM));
+      atomicMax(&p.lcnt[1], (int)(inc >> 25));
+      base = ((excl >> 25) << 32) | (excl & kRayM);
+    } else if (c[0] | c[1]) {
+      base = atomicAdd(reinterpret_cast<unsigned long long*>(p.lcnt), (c[1] << 32) | c[0]);
+    }
     s_base = base;
     if (c[2]) atomicAdd(&p.ctr->rays_in, c[2]);
     if (c[0]) atomicAdd(&p.ctr->rays_used, c[0]);
@@ -1890,7 +1921,8 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
   // scratch growth is stream-ordered on the side stream, after the walk that last read the buffer
   const cudaStream_t gs = sm->serialize ? st : sm->side;
   for (int b = 0; b < 2; ++b) {
-    const bool need_grow = sm->buf[b].ray_cap < cap_rays || (sm->dense_on && sm->buf[b].cta_box_cap < 6 * ((cap_rays + 255) / 256)) || sm->buf[b].slot_cap < cap_rays * kSlotsPerRay + 1024 ||
+    const bool need_grow = sm->buf[b].ray_cap < cap_rays || (sm->dense_on && sm->buf[b].cta_box_cap < 6 * ((cap_rays + kPrepThreads - 1) / kPrepThreads)) ||
+                           (CVX_PREP_ORDERED && sm->buf[b].cstat_cap < (cap_rays + kPrepThreads - 1) / kPrepThreads) || sm->buf[b].slot_cap < cap_rays * kSlotsPerRay + 1024 ||
                            (rgb && sm->buf[b].rgbs_cap < cap_rays) || (sm->cfg.weighting != 0 && sm->buf[b].ws_cap < cap_rays) ||
                            (host_data && sm->buf[b].staging_cap < (long long)per * elems_per_frame);
     if (need_grow) {
@@ -1907,7 +1939,10 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     if (e == cudaSuccess) e = grow(reinterpret_cast<void**>(&sm->buf[b].slot_lists), &sm->buf[b].slot_cap,
                                    cap_rays * kSlotsPerRay + 1024, sizeof(int), gs);
     if (e == cudaSuccess && sm->dense_on)
-      e = grow(reinterpret_cast<void**>(&sm->buf[b].cta_box), &sm->buf[b].cta_box_cap, 6 * ((cap_rays + 255) / 256), sizeof(int), gs);
+      e = grow(reinterpret_cast<void**>(&sm->buf[b].cta_box), &sm->buf[b].cta_box_cap, 6 * ((cap_rays + kPrepThreads - 1) / kPrepThreads), sizeof(int), gs);
+    if (e == cudaSuccess && CVX_PREP_ORDERED)
+      e = grow(reinterpret_cast<void**>(&sm->buf[b].cstat), &sm->buf[b].cstat_cap, (cap_rays + kPrepThreads - 1) / kPrepThreads,
+               sizeof(unsigned long long), gs);
     if (e == cudaSuccess && host_data)
       e = grow(reinterpret_cast<void**>(&sm->buf[b].staging), &sm->buf[b].staging_cap, (long long)per * elems_per_frame,
                sizeof(float), gs);
@@ -2021,12 +2056,13 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
       compose_kernel<<<1, kMaxBatch, 0, side>>>(cp, B.frame_T);
     }
     cudaMemsetAsync(B.lcnt, 0, 4 * sizeof(int), side);
+    if (CVX_PREP_ORDERED) cudaMemsetAsync(B.cstat, 0, sizeof(unsigned long long) * (size_t)((total + kPrepThreads - 1) / kPrepThreads), side);
     if (dense) {   // box {lo[3], hi[3]} = {0x7f7f7f7f x3, 0x80808080 x3}: beyond any block coordinate (< 2^20)
       cudaMemsetAsync(B.lcnt + 8, 0x7f, 3 * sizeof(int), side);
       cudaMemsetAsync(B.lcnt + 11, 0x80, 3 * sizeof(int), side);
     }
     if (host_data && cstream != side) cudaStreamWaitEvent(side, sm->ev_staged[b], 0);
-    PrepParams pp;
+    PrepParams pp{};
     pp.data = chunk;
     pp.n_per_frame = n_per_frame; pp.total = total;
     pp.kind = sensor.kind; pp.width = sensor.width;
@@ -2046,11 +2082,12 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     pp.ws = sm->cfg.weighting != 0 ? B.ws : nullptr;
     pp.count_vox = 1;
     pp.box = dense ? B.cta_box : nullptr;
+    pp.cstat = CVX_PREP_ORDERED ? B.cstat : nullptr;
     {
       ProfScope ps_(sm, "ray_prepare", side);
-      prepare_kernel<<<blocks, 256, 0, side>>>(pp);
+      prepare_kernel<<<(unsigned)((total + kPrepThreads - 1) / kPrepThreads), kPrepThreads, 0, side>>>(pp);
     }
-    if (dense) box_reduce_kernel<<<32, 256, 0, side>>>(B.cta_box, (int)blocks, B.lcnt + 8);
+    if (dense) box_reduce_kernel<<<32, 256, 0, side>>>(B.cta_box, (int)((total + kPrepThreads - 1) / kPrepThreads), B.lcnt + 8);
     if (host_data && cstream != side) cudaEventRecord(sm->ev_stage_free[b], side);   // staging[b] consumed
     WalkParams wp{};
     wp.rays = (const RayRec*)B.rays; wp.ctr = sm->ctr; wp.hash = sm->hash; wp.pool = sm->pool;
@@ -2179,7 +2216,7 @@ cudaError_t launch_integrate_projective(cvx_submap* sm, const float* depth, int6
       const unsigned blocks = (unsigned)((total + 255) / 256);
       compose(f0, nf, B.frame_T);
       cudaMemsetAsync(B.lcnt, 0, 4 * sizeof(int), st);
-      PrepParams pp;
+      PrepParams pp{};
       pp.data = depth + (long long)f0 * n_per_frame;
       pp.n_per_frame = n_per_frame; pp.total = total;
       pp.kind = sensor.kind; pp.width = sensor.width;
@@ -2199,7 +2236,7 @@ cudaError_t launch_integrate_projective(cvx_submap* sm, const float* depth, int6
       pp.count_vox = 0;   // voxel_updates counts the projective updates instead
       {
         ProfScope ps_(sm, "ray_prepare", st);
-        prepare_kernel<<<blocks, 256, 0, st>>>(pp);
+        prepare_kernel<<<(unsigned)((total + kPrepThreads - 1) / kPrepThreads), kPrepThreads, 0, st>>>(pp);
       }
       WalkParams wp{};
       wp.rays = (const RayRec*)B.rays; wp.ctr = sm->ctr; wp.hash = sm->hash; wp.pool = sm->pool;

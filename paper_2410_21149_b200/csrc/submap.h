@@ -62,6 +62,8 @@ struct cvx_submap {
     int* lcnt = nullptr;        // device {n_rays, n_slots, -, -, 4 spare, box lo[3], hi[3]} of the launch
     int* cta_box = nullptr;     // device per-CTA block boxes of prepare_kernel (dense-window path, R19)
     int64_t cta_box_cap = 0;
+    unsigned long long* cstat = nullptr;   // device per-CTA look-back status of prepare_kernel
+    int64_t cstat_cap = 0;
     float* staging = nullptr;   // device copy of host frames (cvx_integrate_batch_host)
     int64_t staging_cap = 0;
   } buf[2];
