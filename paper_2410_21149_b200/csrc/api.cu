@@ -117,6 +117,7 @@ void free_all(cvx_submap* sm) {
   if (sm->ctr) cudaFree(sm->ctr);
   if (sm->acc_dirty) cudaFree(sm->acc_dirty);
   if (sm->dacc) cudaFree(sm->dacc);
+  if (sm->dcacc) cudaFree(sm->dcacc);
   if (sm->ctr_host) cudaFreeHost(sm->ctr_host);
   for (auto& B : sm->buf) {
     if (B.frame_T) cudaFree(B.frame_T);
@@ -192,6 +193,7 @@ cvx_status cvx_create_submap(const cvx_grid_config* cfg, const double* T_world_s
   if (const char* lc = std::getenv("CVX_LIST_CAP")) sm->list_cap_limit = std::atoll(lc);  // test knob
   if (const char* dn = std::getenv("CVX_DENSE")) sm->dense_on = dn[0] != '0';         // R19 knob
   if (const char* wp = std::getenv("CVX_WALK_PRIO")) sm->walk_prio = wp[0] != '0';      // scheduling knob
+  if (const char* dc = std::getenv("CVX_DENSE_COLOR")) sm->dense_color = dc[0] != '0';  // R19 knob (colour)
   if (const char* db = std::getenv("CVX_DENSE_BLOCKS"))                                 // R19 capacity knob
     sm->dense_cap = std::max(1ll, std::min(std::atoll(db), 1ll << 22));
   sm->cfg = *cfg;

@@ -420,6 +420,7 @@ struct WalkParams {
   const int* dbox;  // {lo[3], hi[3]} written by prepare_kernel
   long long dcap;   // capacity of dacc in blocks (excluding the trash region)
   unsigned char* dflag;   // per dense block: touched by the walk (cleared by dense_fold_kernel)
+  unsigned long long* dcacc;   // TSDF + Color: dense packed colour accumulators (2 per voxel), nullable
   int* acc_dirty;   // set when a dense-eligible launch falls back to the pool accumulators
 };
 
@@ -1376,7 +1377,7 @@ __device__ __forceinline__ void mark_block(unsigned char* flags, unsigned bi, bo
 #endif
 }
 
-template <bool k32>
+template <bool k32, bool kColor = false>
 __global__ void __launch_bounds__(128, CVX_DW_MINB) walk_dw_kernel(const __grid_constant__ WalkParams p) {
   using DT = typename std::conditional<k32, unsigned, unsigned long long>::type;
   using ST = typename std::conditional<k32, int, long long>::type;
@@ -1393,7 +1394,7 @@ __global__ void __launch_bounds__(128, CVX_DW_MINB) walk_dw_kernel(const __grid_
   DT D01 = 0, D02 = 0, D12 = 0, I0 = 0, I1 = 0, I2 = 0;
   long long S = 0, U0 = 0, U1 = 0, U2 = 0;
   int n = 0;
-  unsigned cexp = 0, addr = trash;
+  unsigned cexp = 0, addr = trash, rgb = 0;
   if (have) {
     const RayView r = load_ray(p, idx);
     long long R[3], AD[3];
@@ -1423,6 +1424,7 @@ __global__ void __launch_bounds__(128, CVX_DW_MINB) walk_dw_kernel(const __grid_
     S = r.S0 + (1ll << (kSdfF - 1)) + ((long long)p.tq << kSdfF);
     U0 = r.U[0]; U1 = r.U[1]; U2 = r.U[2];
     n = r.n_vox;
+    rgb = r.rgb;
     CVX_CHECK((va[0] >> 3) >= p.dbox[0] && (va[0] >> 3) <= p.dbox[3] && (va[1] >> 3) >= p.dbox[1] && (va[1] >> 3) <= p.dbox[4] &&
               (va[2] >> 3) >= p.dbox[2] && (va[2] >> 3) <= p.dbox[5], "ray start inside the launch's block box");
     const unsigned blk = (unsigned)((((va[2] >> 3) - p.dbox[2]) * nby + ((va[1] >> 3) - p.dbox[1])) * nbx + ((va[0] >> 3) - p.dbox[0]));
@@ -1439,8 +1441,11 @@ __global__ void __launch_bounds__(128, CVX_DW_MINB) walk_dw_kernel(const __grid_
   unsigned long long* const acc = p.dacc;
   int mfree = 0x7fffffff;
   const int K0 = k0, K1 = k1, K2 = k2;
+  const long long s_off = (1ll << (kSdfF - 1)) + ((long long)p.tq << kSdfF);
+  const long long band_lo = s_off - p.band, band_hi = s_off + p.band;   // colour band |S| < tau (R13)
   if (have) {
-    const long long thr = (long long)tq2 << kSdfF;
+    long long thr = (long long)tq2 << kSdfF;
+    if (kColor) thr = max(thr, band_hi);   // the free prefix never reaches the colour band
     const long long umax = max(U0, max(U1, U2));
     mfree = 0;
     if (S > thr && umax > 0) {
@@ -1506,6 +1511,12 @@ __global__ void __launch_bounds__(128, CVX_DW_MINB) walk_dw_kernel(const __grid_
       const unsigned len = run_len(stops & above_mask, lane);
       const unsigned long long val = ((unsigned long long)(len << (kCntShift - 32)) << 32) | (len * (unsigned)dpi);
       DW_RED(acc, addr, val, head & !parked);                  // ... and issues no reduction
+      if (kColor && S > band_lo && S < band_hi) {   // TSDF + Color: band updates carry the point's colour (R13)
+        const unsigned long long cr = rgb & 0xffu, cg = (rgb >> 8) & 0xffu, cb = (rgb >> 16) & 0xffu;
+        CVX_CHECK((long long)addr < (p.dcap + kTrashBlocks) * kBlockVox, "dense colour accumulator address");
+        atomicAdd(p.dcacc + 2ull * addr, (1ull << kCntShift) | cr);
+        atomicAdd(p.dcacc + 2ull * addr + 1, (cg << 32) | cb);
+      }
       if (it + 1 >= n) {   // that was the ray's last voxel: park
         addr = spot; k0 = 0x3fffffff; k1 = 0; k2 = 0; dx0 = 0; cexp = 1u; S = (long long)tq2 << (kSdfF + 1); U0 = 0;
         n = 0x7fffffff; ex0 = 0u; parked = true;
@@ -1651,6 +1662,23 @@ __global__ void __launch_bounds__(256) dense_fold_kernel(const __grid_constant__
         }
         src[e] = make_ulonglong2(0ull, 0ull);
       }
+      if (p.dcacc) {   // TSDF + Color: the block's packed colour accumulators (fold_color_kernel's arithmetic)
+        ulonglong2* csrc = reinterpret_cast<ulonglong2*>(p.dcacc) + (b0 + j) * kBlockVox;
+        longlong2* cs = reinterpret_cast<longlong2*>(p.pool.csum) + 2ll * (long long)(sl < 0 ? 0 : sl) * kBlockVox;
+        for (int vx = lane; vx < kBlockVox; vx += 32) {
+          const ulonglong2 cv = csrc[vx];
+          if ((cv.x | cv.y) == 0ull) continue;
+          if (sl >= 0) {
+            longlong2 a = cs[2 * vx], c2 = cs[2 * vx + 1];
+            a.x += (long long)(cv.x >> kCntShift) << 30;
+            a.y += (long long)(cv.x & ((1ull << kCntShift) - 1)) << 30;
+            c2.x += (long long)(cv.y >> 32) << 30;
+            c2.y += (long long)(cv.y & 0xffffffffull) << 30;
+            cs[2 * vx] = a; cs[2 * vx + 1] = c2;
+          }
+          csrc[vx] = make_ulonglong2(0ull, 0ull);
+        }
+      }
     }
   }
 }
@@ -1663,7 +1691,9 @@ __global__ void trigger_check_kernel(const Counters* ctr, int* trig, int frame) 
 
 // TSDF + Color (R13): fold the packed colour accumulators {n << 40 | sum r, sum g << 32 | sum b} (w = 1)
 // into the exact colour sums {sum w, sum w r, sum w g, sum w b} at 2^-30.
-__global__ void fold_color_kernel(const Counters* ctr, unsigned long long* cacc, long long* csum, int max_blocks) {
+__global__ void fold_color_kernel(const Counters* ctr, unsigned long long* cacc, long long* csum, int max_blocks,
+                                  const int* dirty) {
+  if (dirty && !*dirty) return;   // R19: every launch since the last fold ran in its dense window
   const int nb = min(ctr->n_blocks, max_blocks);
   const long long nv = (long long)nb * kBlockVox;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (long long)gridDim.x * blockDim.x) {
@@ -1957,7 +1987,8 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
   // accumulator buffer covers a conservative box of the call (balls of radius max_range + tau around the
   // frames' sensor origins), capped at dense_cap blocks; each launch uses the exact box of its rays
   // (prepare_kernel) and falls back to the slot-list path on the device if that box exceeds the buffer.
-  bool dense = cw_ok && sm->dense_on && sm->walk_cw && sm->bw2 && !sm->bw3 && !sm->fuse_alloc && !rgb && !trig;
+  bool dense = cw_ok && sm->dense_on && sm->walk_cw && sm->bw2 && !sm->bw3 && !sm->fuse_alloc && !trig &&
+               (!rgb || (sm->pool.csum && sm->dense_color));
   long long dcap = 0;
   if (dense) {
     const double* W = sm->T_ws;
@@ -1992,6 +2023,20 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
       }
     }
     dcap = sm->dacc_blocks;
+    if (dense && rgb && sm->dcacc_blocks < dcap) {   // TSDF + Color: dense colour accumulators, same index space
+      if (sm->dcacc) cudaFreeAsync(sm->dcacc, st);
+      sm->dcacc = nullptr;
+      sm->dcacc_blocks = 0;
+      const size_t cbytes = (size_t)(dcap + kTrashBlocks) * kBlockVox * 2 * sizeof(unsigned long long);
+      if (cudaMallocAsync(reinterpret_cast<void**>(&sm->dcacc), cbytes, st) == cudaSuccess) {
+        cudaMemsetAsync(sm->dcacc, 0, cbytes, st);
+        sm->dcacc_blocks = dcap;
+      } else {
+        cudaGetLastError();
+        sm->dcacc = nullptr;
+        dense = false;
+      }
+    }
   }
   long long pending = 0;                             // rays in the packed accumulators since the last fold
   auto fold = [&]() {
@@ -2001,11 +2046,12 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
       fold_kernel<<<148 * 8, 256, 0, st>>>(sm->ctr, sm->pool.acc, sm->pool.sums, sm->pool.max_blocks, tq, 30 - q,
                                            dense ? sm->acc_dirty : nullptr);
     }
-    if (dense) cudaMemsetAsync(sm->acc_dirty, 0, sizeof(int), st);
     if (rgb) {
       ProfScope ps_(sm, "fold_color", st);
-      fold_color_kernel<<<148 * 8, 256, 0, st>>>(sm->ctr, sm->pool.cacc, sm->pool.csum, sm->pool.max_blocks);
+      fold_color_kernel<<<148 * 8, 256, 0, st>>>(sm->ctr, sm->pool.cacc, sm->pool.csum, sm->pool.max_blocks,
+                                                 dense ? sm->acc_dirty : nullptr);
     }
+    if (dense) cudaMemsetAsync(sm->acc_dirty, 0, sizeof(int), st);   // after both folds read it
     pending = 0;
   };
   cudaEventRecord(sm->ev_entry, st);                 // the side stream starts after the caller's prior work
@@ -2100,6 +2146,7 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     wp.frame_T = B.frame_T; wp.rgbs = pp.rgbs; wp.ws = pp.ws; wp.frame_base = 0;
     wp.dacc = sm->dacc; wp.dbox = dense ? B.lcnt + 8 : nullptr; wp.dcap = dcap; wp.acc_dirty = sm->acc_dirty;
     wp.dflag = dense ? reinterpret_cast<unsigned char*>(sm->dacc + (dcap + kTrashBlocks) * kBlockVox) : nullptr;
+    wp.dcacc = dense && rgb ? sm->dcacc : nullptr;
     const bool cw = cw_ok && total <= launch_rays;
     // constant weights, no colour, no block-count trigger: ALLOCATE runs inside the update walk
     const bool fuse = sm->fuse_alloc && cw && sm->aggregate && sm->walk_cw && !rgb && !trig;
@@ -2141,7 +2188,11 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
       ProfScope ps_(sm, "ray_walk_update", ws);
       const unsigned wblocks = (unsigned)((total + 127) / 128);   // 128-thread CTAs (measured best)
       if (cw && sm->aggregate && sm->walk_cw) {
-        if (rgb) { if (k32) walk_cw_kernel<true, true><<<wblocks, 128, 0, ws>>>(wp); else walk_cw_kernel<false, true><<<wblocks, 128, 0, ws>>>(wp); }
+        if (rgb) {
+          if (dense) { if (k32) walk_dw_kernel<true, true><<<wblocks, 128, 0, ws>>>(wp); else walk_dw_kernel<false, true><<<wblocks, 128, 0, ws>>>(wp); }
+          const unsigned fwb = dense ? std::min(wblocks, 148u * 16u) : wblocks;   // dense: fallback only
+          if (k32) walk_cw_kernel<true, true><<<fwb, 128, 0, ws>>>(wp); else walk_cw_kernel<false, true><<<fwb, 128, 0, ws>>>(wp);
+        }
         else if (fuse) { if (k32) walk_cw_kernel<true, false, true><<<wblocks, 128, 0, ws>>>(wp); else walk_cw_kernel<false, false, true><<<wblocks, 128, 0, ws>>>(wp); }
         else {
           if (dense) { if (k32) walk_dw_kernel<true><<<wblocks, 128, 0, ws>>>(wp); else walk_dw_kernel<false><<<wblocks, 128, 0, ws>>>(wp); }

@@ -91,6 +91,9 @@ struct cvx_submap {
   long long dense_cap = 1ll << 19;          // blocks (2 GiB of u64 accumulators; configs[1] / MAV boxes: <= 0.23 M)
   unsigned long long* dacc = nullptr;       // device [(dacc_blocks + kTrashBlocks) * 512], zero between folds
   long long dacc_blocks = 0;
+  bool dense_color = true;                  // CVX_DENSE_COLOR: TSDF + Color through the dense window too
+  unsigned long long* dcacc = nullptr;      // device [(dcacc_blocks + kTrashBlocks) * 512][2] colour accumulators
+  long long dcacc_blocks = 0;
   int* acc_dirty = nullptr;                 // device: a dense-eligible launch fell back to the pool accumulators
 
   // ESDF scratch (grow-only, stream-ordered cudaMallocAsync on the calling stream)

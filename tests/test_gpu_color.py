@@ -138,3 +138,22 @@ def test_color_errors(tiny):
     smc.reset()
     smc.integrate(f["data"].to(dev), f["T_world_sensor"], tiny["sensor"])
     assert (smc.export_color()[1] == 0).all()
+
+
+@pytest.mark.parametrize("knob", ["CVX_DENSE_COLOR=0", "CVX_DENSE_BLOCKS=64"])
+def test_dense_window_color_equals_slot_list_path(monkeypatch, knob):
+    """TSDF + Color through the dense window (R19: colour accumulators in the same block-major index space,
+    folded with the touched blocks) equals the slot-list colour path bit for bit — host-selected
+    (CVX_DENSE_COLOR=0) and the device-side fallback (a 64-block window, smaller than the launch's box)."""
+    frames = [0, 100]
+    cfg = synth.make_config("lidar", frames=frames, color=True)
+    a = _gpu(cfg, frames, batch=True)
+    k, v = knob.split("=")
+    monkeypatch.setenv(k, v)
+    b = _gpu(cfg, frames, batch=True)
+    ea, eb = gpu_export_sorted(a), gpu_export_sorted(b)
+    assert np.array_equal(ea[0], eb[0])
+    assert np.array_equal(ea[1].view(np.uint32), eb[1].view(np.uint32))
+    ra, ca = _gpu_color_sorted(a)
+    rb, cb = _gpu_color_sorted(b)
+    assert np.array_equal(ca.view(np.uint32), cb.view(np.uint32)) and np.array_equal(ra.view(np.uint32), rb.view(np.uint32))
