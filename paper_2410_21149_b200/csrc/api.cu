@@ -75,6 +75,8 @@ cvx_status check_sensor(const cvx_sensor_model* s, int64_t n_per_frame) {
 // synchronising calls (get_stats / get_block_count / get_aabb / packed_size) pass whole_device and wait for
 // the whole device first, so work on non-blocking streams (e.g. torch's pool streams) is included.
 cvx_status read_counters(const cvx_submap* sm, cudaStream_t st, cvx::Counters* out, bool whole_device = false) {
+  // a fold deferred by the last integrate call changes the block count / AABB: apply it first (R19)
+  if (cudaError_t fe = cvx::flush_fold(const_cast<cvx_submap*>(sm), st)) return cuda_fail(fe, "deferred fold");
   if (whole_device) {
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return cuda_fail(e, "synchronising before the counter read");
@@ -139,6 +141,7 @@ void free_all(cvx_submap* sm) {
     if (sm->ev_stage_free[b]) cudaEventDestroy(sm->ev_stage_free[b]);
   }
   if (sm->ev_entry) cudaEventDestroy(sm->ev_entry);
+  if (sm->ev_walked) cudaEventDestroy(sm->ev_walked);
   for (int b = 0; b < 2; ++b) {
     if (sm->ev_prepared[b]) cudaEventDestroy(sm->ev_prepared[b]);
     if (sm->ev_free[b]) cudaEventDestroy(sm->ev_free[b]);
@@ -194,6 +197,7 @@ cvx_status cvx_create_submap(const cvx_grid_config* cfg, const double* T_world_s
   if (const char* dn = std::getenv("CVX_DENSE")) sm->dense_on = dn[0] != '0';         // R19 knob
   if (const char* wp = std::getenv("CVX_WALK_PRIO")) sm->walk_prio = wp[0] != '0';      // scheduling knob
   if (const char* dc = std::getenv("CVX_DENSE_COLOR")) sm->dense_color = dc[0] != '0';  // R19 knob (colour)
+  if (const char* df = std::getenv("CVX_DEFER_FOLD")) sm->defer_fold = df[0] != '0';   // R19 knob (deferred fold)
   if (const char* db = std::getenv("CVX_DENSE_BLOCKS"))                                 // R19 capacity knob
     sm->dense_cap = std::max(1ll, std::min(std::atoll(db), 1ll << 22));
   sm->cfg = *cfg;
@@ -218,6 +222,7 @@ cvx_status cvx_create_submap(const cvx_grid_config* cfg, const double* T_world_s
       (e = cudaMalloc(&sm->buf[1].frame_T, sizeof(double) * 16 * cvx::kMaxBatch)) != cudaSuccess ||
       (e = cudaMalloc(&sm->buf[0].lcnt, 64)) != cudaSuccess || (e = cudaMalloc(&sm->buf[1].lcnt, 64)) != cudaSuccess ||
       (e = cudaMalloc(&sm->acc_dirty, sizeof(int))) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&sm->ev_walked, cudaEventDisableTiming)) != cudaSuccess ||
       (e = cudaStreamCreateWithFlags(&sm->side, cudaStreamNonBlocking)) != cudaSuccess ||
       (e = cudaEventCreateWithFlags(&sm->ev_entry, cudaEventDisableTiming)) != cudaSuccess ||
       (e = cudaEventCreateWithFlags(&sm->ev_prepared[0], cudaEventDisableTiming)) != cudaSuccess ||
@@ -494,7 +499,8 @@ cvx_status cvx_query_distance(const cvx_submap* sm, const float* pts, int64_t m,
   if (m < 0) return fail(CVX_E_INVALID, "m < 0");
   if (m > 0 && (!pts || !out || !status)) return fail(CVX_E_INVALID, "NULL buffer");
   DeviceGuard g(sm->device);
-  cudaError_t e = cvx::launch_query(sm, pts, m, out, status, (cudaStream_t)stream);
+  cudaError_t e = cvx::flush_fold(const_cast<cvx_submap*>(sm), (cudaStream_t)stream);
+  if (e == cudaSuccess) e = cvx::launch_query(sm, pts, m, out, status, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "query_distance");
   return CVX_OK;
 }
@@ -507,7 +513,8 @@ cvx_status cvx_query_distance_gradient(const cvx_submap* sm, const float* pts, i
   if (m < 0) return fail(CVX_E_INVALID, "m < 0");
   if (m > 0 && (!pts || !out || !grad || !status)) return fail(CVX_E_INVALID, "NULL buffer");
   DeviceGuard g(sm->device);
-  cudaError_t e = cvx::launch_query(sm, pts, m, out, status, (cudaStream_t)stream, grad);
+  cudaError_t e = cvx::flush_fold(const_cast<cvx_submap*>(sm), (cudaStream_t)stream);
+  if (e == cudaSuccess) e = cvx::launch_query(sm, pts, m, out, status, (cudaStream_t)stream, grad);
   if (e != cudaSuccess) return cuda_fail(e, "query_distance_gradient");
   return CVX_OK;
 }
@@ -557,7 +564,8 @@ cvx_status cvx_import_tsdf_blocks(cvx_submap* sm, const int32_t* bxyz, const flo
   if (n < 0) return fail(CVX_E_INVALID, "n < 0");
   if (n > 0 && (!bxyz || !D || !W)) return fail(CVX_E_INVALID, "NULL buffer");
   DeviceGuard g(sm->device);
-  cudaError_t e = cvx::launch_import(sm, bxyz, D, W, n, (cudaStream_t)stream);
+  cudaError_t e = cvx::flush_fold(sm, (cudaStream_t)stream);
+  if (e == cudaSuccess) e = cvx::launch_import(sm, bxyz, D, W, n, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "import_tsdf_blocks");
   return CVX_OK;
 }

@@ -1882,7 +1882,29 @@ __global__ void reset_counters_kernel(Counters* ctr) {
 
 }  // namespace
 
+// R19: apply a dense fold deferred by the last integrate call (ALLOCATE + FOLD of its last launch) on `st`,
+// after that call's walk.  Every call that reads or changes the submap's state runs it first.
+cudaError_t flush_fold(cvx_submap* sm, cudaStream_t st) {
+  if (!sm->fold_pending) return cudaSuccess;
+  sm->fold_pending = false;
+  cudaStreamWaitEvent(st, sm->ev_walked, 0);
+  const int q = packed_q(sm->cfg.truncation);
+  WalkParams wp{};
+  wp.hash = sm->hash; wp.pool = sm->pool; wp.ctr = sm->ctr;
+  wp.q = q; wp.tq = (int)std::llround(std::ldexp(sm->cfg.truncation, q));
+  wp.dacc = sm->dacc; wp.dbox = sm->buf[sm->fold_buf].lcnt + 8; wp.dcap = sm->fold_dcap;
+  wp.dflag = reinterpret_cast<unsigned char*>(sm->dacc + (sm->fold_dcap + kTrashBlocks) * kBlockVox);
+  wp.dcacc = sm->fold_color ? sm->dcacc : nullptr;
+  {
+    ProfScope ps_(sm, "dense_fold_allocate", st);
+    dense_fold_kernel<<<148 * 8, 256, 0, st>>>(wp);
+  }
+  cudaEventRecord(sm->ev_free[sm->fold_buf], st);   // the buffer's box may be reused after the fold
+  return cudaGetLastError();
+}
+
 cudaError_t launch_reset(cvx_submap* sm, cudaStream_t st) {
+  if (cudaError_t fe = flush_fold(sm, st)) return fe;   // leaves the dense window zero
   {
     ProfScope ps_(sm, "reset_zero_blocks", st);
     zero_blocks_kernel<<<148 * 8, 256, 0, st>>>(sm->ctr, sm->pool.sums, sm->pool.acc, sm->pool.max_blocks);
@@ -1926,6 +1948,7 @@ static cudaError_t grow(void** ptr, int64_t* cap, int64_t need, size_t elem, cud
 cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_frame, int n_frames,
                              const double* T_world_sensor, const cvx_sensor_model& sensor, cudaStream_t st,
                              bool host_data, int* trig, const unsigned char* rgb) {
+  if (cudaError_t fe = flush_fold(sm, st)) return fe;   // the previous call's deferred fold first
   if (n_per_frame <= 0 || n_frames <= 0) return cudaSuccess;
   // pipeline side stream (a1-a3 of launch k+1 under the walk of launch k); the caller's stream itself
   // when the submap is in serialised profiling mode
@@ -2075,7 +2098,9 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     // run under whatever the caller's stream is still doing (e.g. the previous submap's walk)
   }
   int f0 = 0;
-  for (const int nf : plan) {
+  for (size_t li = 0; li < plan.size(); ++li) {
+    const int nf = plan[li];
+    const bool last_launch = li + 1 == plan.size();
     const long long total = (long long)nf * n_per_frame;
     const int b = sm->next_buf;
     sm->next_buf ^= 1;
@@ -2211,7 +2236,12 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
       }
     }
     if (ws != st) { cudaEventRecord(sm->ev_w[1], ws); cudaStreamWaitEvent(st, sm->ev_w[1], 0); }
-    if (dense) {
+    if (dense && last_launch && sm->defer_fold) {
+      // the call's last dense fold is deferred to the next call that reads or changes the submap (flush_fold):
+      // a caller that integrates the next submap meanwhile overlaps this fold with that submap's walk
+      cudaEventRecord(sm->ev_walked, st);
+      sm->fold_pending = true; sm->fold_buf = b; sm->fold_dcap = dcap; sm->fold_color = rgb != nullptr;
+    } else if (dense) {
       ProfScope ps_(sm, "dense_fold_allocate", st);
       dense_fold_kernel<<<148 * 8, 256, 0, st>>>(wp);
     }
@@ -2232,6 +2262,7 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
 cudaError_t launch_integrate_projective(cvx_submap* sm, const float* depth, int64_t n_per_frame, int n_frames,
                                         const double* T_world_sensor, const cvx_sensor_model& sensor,
                                         cudaStream_t st) {
+  if (cudaError_t fe = flush_fold(sm, st)) return fe;
   if (n_per_frame <= 0 || n_frames <= 0) return cudaSuccess;
   const int lim = (int)std::max<long long>(1, std::min<long long>(kMaxBatch, kLaunchRays / n_per_frame));
   cvx_submap::Buf& B = sm->buf[0];

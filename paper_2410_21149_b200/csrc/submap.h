@@ -92,6 +92,12 @@ struct cvx_submap {
   unsigned long long* dacc = nullptr;       // device [(dacc_blocks + kTrashBlocks) * 512], zero between folds
   long long dacc_blocks = 0;
   bool dense_color = true;                  // CVX_DENSE_COLOR: TSDF + Color through the dense window too
+  bool defer_fold = false;                  // CVX_DEFER_FOLD=1: the call's last dense fold runs at the next access (measured slower)
+  bool fold_pending = false;                // a deferred fold waits (flush_fold)
+  int fold_buf = 0;                         //   its launch buffer (box in buf[fold_buf].lcnt + 8)
+  long long fold_dcap = 0;
+  bool fold_color = false;
+  cudaEvent_t ev_walked = nullptr;          //   after that launch's walk
   unsigned long long* dcacc = nullptr;      // device [(dcacc_blocks + kTrashBlocks) * 512][2] colour accumulators
   long long dcacc_blocks = 0;
   int* acc_dirty = nullptr;                 // device: a dense-eligible launch fell back to the pool accumulators
@@ -143,6 +149,7 @@ constexpr int kSlotsPerRay = 40; // average block-slot list capacity per ray (ov
 
 // integrate.cu
 cudaError_t launch_reset(cvx_submap* sm, cudaStream_t st);
+cudaError_t flush_fold(cvx_submap* sm, cudaStream_t st);   // deferred dense fold (R19), if any
 cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_frame, int n_frames,
                              const double* T_world_sensor, const cvx_sensor_model& sensor, cudaStream_t st,
                              bool host_data, int* trig = nullptr, const unsigned char* rgb = nullptr);
