@@ -399,6 +399,9 @@ __global__ void __launch_bounds__(kPrepThreads, CVX_PREP_MINB) prepare_kernel(co
   }
 }
 
+#ifndef CVX_RAY_LDCS
+#define CVX_RAY_LDCS 0   // 1: evict-first loads of the ray records in the walk (measured neutral)
+#endif
 struct WalkParams {
   const RayRec* rays;
   const double* frame_T;   // compose_kernel records of the launch's frames (ray origins)
@@ -433,7 +436,18 @@ __device__ __forceinline__ bool dense_dims(const int* box, long long cap, int& n
 }
 
 __device__ __forceinline__ RayView load_ray(const WalkParams& p, int idx) {
+#if CVX_RAY_LDCS
+  // ray records are read once: streaming (evict-first) loads keep them from evicting the walk's hot
+  // accumulator lines in L2
+  RayRec r;
+  {
+    const int4* src = reinterpret_cast<const int4*>(p.rays + idx);
+    int4* dst = reinterpret_cast<int4*>(&r);
+    dst[0] = __ldcs(src); dst[1] = __ldcs(src + 1); dst[2] = __ldcs(src + 2);
+  }
+#else
   const RayRec r = p.rays[idx];
+#endif
   RayView v;
   v.frame = (int)(r.S0f & ((1ll << kFrameBits) - 1));
   const double* T = p.frame_T + kFrameRec * v.frame;
