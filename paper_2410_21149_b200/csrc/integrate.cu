@@ -169,6 +169,8 @@ struct PrepParams {
   double sdf_scale;   // 2^(q + kSdfF)
   double rs;          // RN(1 / s) (fast correctly rounded divisions by s, div_rn)
   double r_npf, r_width, r_pcols;   // RN(1 / n_per_frame), RN(1 / width), RN(1 / (width / patch cols))
+  int sec_cols, nframes;            // sector-major ray order (organised sensors): patch columns per sector, 0 = off
+  double r_secpat, r_frmpat, r_seccols;   // RN(1 / patches per sector), RN(1 / patches per (sector, frame)), RN(1 / sec_cols)
   int weighting, carve;
   int height;
   const double* frame_T;
@@ -188,6 +190,9 @@ struct PrepParams {
 #ifndef CVX_PREP_MINB
 #define CVX_PREP_MINB 5   // 48 registers, 5 CTAs per SM: prepare 0.505 -> 0.467 ms against __launch_bounds__(256) (56 registers)
 #endif
+#ifndef CVX_SECTOR_COLS
+#define CVX_SECTOR_COLS 0    // > 0: sector-major ray order, patch columns per sector (measured slower: concurrent warps collide on the same voxels)
+#endif
 #ifndef CVX_PREP_ORDERED
 #define CVX_PREP_ORDERED 0   // 1: rays claimed in CTA order (decoupled look-back) instead of atomic arrival order (walk -1.6 %, prepare +80 %: off)
 #endif
@@ -204,11 +209,25 @@ __global__ void __launch_bounds__(kPrepThreads, CVX_PREP_MINB) prepare_kernel(co
   unsigned f_used = 0;
   if (idx < p.total) {
     // (index arithmetic in 32 bits: a launch holds < 2^31 rays; divisions by multiplication, udiv_fast)
-    const unsigned f = udiv_fast((unsigned)idx, (unsigned)p.n_per_frame, p.r_npf);
-    f_used = f;
+    unsigned f = udiv_fast((unsigned)idx, (unsigned)p.n_per_frame, p.r_npf);
     unsigned i = (unsigned)idx - f * (unsigned)p.n_per_frame;
     constexpr int PR = CVX_PATCH_ROWS, PC = 32 / CVX_PATCH_ROWS;
-    if (p.kind != 0 && p.width > 0 && p.height > 0 && p.width % PC == 0 && p.height % PR == 0) {
+    if (p.sec_cols > 0) {
+      // sector-major order: azimuth sector s of every frame of the launch, then the next sector — the walk's
+      // warps in flight then touch one sector's voxels (nearly the same for consecutive scans), a smaller L2
+      // working set for their reductions.  Inside a (sector, frame): patch rows x sector patch columns.
+      const unsigned P = (unsigned)idx >> 5, l = (unsigned)idx & 31u;
+      const unsigned S = (unsigned)p.sec_cols, prows = (unsigned)p.height / PR;
+      const unsigned PF = prows * S, PS = PF * (unsigned)p.nframes;
+      const unsigned sec = udiv_fast(P, PS, p.r_secpat);
+      const unsigned rem = P - sec * PS;
+      f = udiv_fast(rem, PF, p.r_frmpat);
+      const unsigned rem2 = rem - f * PF;
+      const unsigned prow = udiv_fast(rem2, S, p.r_seccols);
+      const unsigned pcol = sec * S + (rem2 - prow * S);
+      const unsigned rr = l / PC, cc = (rr & 1) ? PC - 1 - (l % PC) : (l % PC);
+      i = (prow * PR + rr) * (unsigned)p.width + pcol * PC + cc;
+    } else if (p.kind != 0 && p.width > 0 && p.height > 0 && p.width % PC == 0 && p.height % PR == 0) {
       // organised sensor: warp = PR rows x PC columns patch (spatially coherent rays per warp)
       const unsigned pt = i >> 5, l = i & 31, pcols = (unsigned)p.width / PC;
       const unsigned rr = l / PC, cc = (rr & 1) ? PC - 1 - (l % PC) : (l % PC);   // serpentine: lane l+1 neighbours lane l
@@ -216,6 +235,7 @@ __global__ void __launch_bounds__(kPrepThreads, CVX_PREP_MINB) prepare_kernel(co
       const unsigned row = prow * PR + rr, col = (pt - prow * pcols) * PC + cc;
       i = row * (unsigned)p.width + col;
     }
+    f_used = f;
     const long long src = f * p.n_per_frame + i;
     const double* T = p.frame_T + kFrameRec * f;
     double pc[3];
@@ -2158,6 +2178,17 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
     pp.sdf_scale = std::ldexp(1.0, q + kSdfF);
     set_divisors(pp, sensor);
     pp.height = sensor.height;
+    {
+      constexpr int PR = CVX_PATCH_ROWS, PC = 32 / CVX_PATCH_ROWS;
+      const int S = CVX_SECTOR_COLS;
+      const bool org = sensor.kind != 0 && sensor.width > 0 && sensor.height > 0 && sensor.width % PC == 0 &&
+                       sensor.height % PR == 0 && n_per_frame == (long long)sensor.width * sensor.height;
+      if (S > 0 && org && (sensor.width / PC) % (S > 0 ? S : 1) == 0 && dense) {
+        const double PF = (double)(sensor.height / PR) * S;
+        pp.sec_cols = S; pp.nframes = nf;
+        pp.r_frmpat = 1.0 / PF; pp.r_secpat = 1.0 / (PF * nf); pp.r_seccols = 1.0 / S;
+      }
+    }
     pp.frame_T = B.frame_T; pp.rays = (RayRec*)B.rays; pp.ctr = sm->ctr; pp.lcnt = B.lcnt;
     // one spare entry: walk_cw_kernel prefetches the entry after a ray's last block unconditionally
     pp.list_cap = (int)std::min<long long>(std::min<long long>(B.slot_cap - 1, sm->list_cap_limit), 0x7fffffffll);
