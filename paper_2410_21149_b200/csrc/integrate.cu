@@ -2186,7 +2186,7 @@ cudaError_t launch_integrate(cvx_submap* sm, const float* data, int64_t n_per_fr
       if (S > 0 && org && (sensor.width / PC) % (S > 0 ? S : 1) == 0 && dense) {
         const double PF = (double)(sensor.height / PR) * S;
         pp.sec_cols = S; pp.nframes = nf;
-        pp.r_frmpat = 1.0 / PF; pp.r_secpat = 1.0 / (PF * nf); pp.r_seccols = 1.0 / S;
+        pp.r_frmpat = 1.0 / PF; pp.r_secpat = 1.0 / (PF * nf); pp.r_seccols = 1.0 / (double)(S > 0 ? S : 1);
       }
     }
     pp.frame_T = B.frame_T; pp.rays = (RayRec*)B.rays; pp.ctr = sm->ctr; pp.lcnt = B.lcnt;
